@@ -1,0 +1,230 @@
+/*
+ * rr_realloc.h — C ABI of the B200 parameter-reallocation library
+ * (paper_2406_14088_b200/librrealloc.so).
+ *
+ * The reference (arXiv 2406.14088, ReaL) exposes this path only as the C++
+ * `rlplan` namespace (proj/include/rlplan/{common,model_arith,cluster}.hpp) plus the SPEC-declared
+ * realloc module; its runtime executes plans with NCCL
+ * broadcasts. This header is the flat, exception-free
+ * boundary a foreign caller (Python ctypes, cgo, JNI, the upstream runtime's
+ * C++ model worker) binds instead. Every entry point names the reference
+ * interface it replaces. Plain pointers and sizes only; no torch or CUDA
+ * types appear in the signatures (streams are passed as `void*` holding a
+ * cudaStream_t, NULL = legacy default stream).
+ *
+ * Errors: every function returns rr_status; on failure rr_last_error()
+ * returns a thread-local message. RR_EINVAL carries the text of the
+ * reference's ValidationError (common.hpp:22-25).
+ *
+ * Threading: planning functions are pure and reentrant.
+ * A plan is immutable once created and may be read concurrently. An
+ * executor is bound to one CUDA device and one set of buffers; launches are
+ * asynchronous and ordered on the caller's stream.
+ */
+#ifndef RR_REALLOC_H_
+#define RR_REALLOC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RR_ABI_VERSION 1
+
+typedef enum {
+  RR_OK = 0,
+  RR_EINVAL = 1,       /* ValidationError or bad argument */
+  RR_ECUDA = 2,        /* CUDA runtime/driver error */
+  RR_ENOMEM = 3,       /* allocation failed */
+  RR_EUNSUPPORTED = 4, /* feature absent on this device (e.g. multicast) */
+  RR_ETIMEOUT = 5,     /* cross-GPU barrier did not complete */
+  RR_ERANGE = 6        /* caller buffer too small; *needed says how large */
+} rr_status;
+
+/* ---- vocabulary (reference model_arith.hpp:13-35, cluster.hpp:14-41) ---- */
+
+typedef struct {
+  const char* name; /* may be NULL */
+  int64_t hidden_size;
+  int64_t intermediate_size;
+  int64_t num_layers;
+  int64_t num_attention_heads;
+  int64_t num_kv_heads;
+  int64_t vocab_size;
+  int64_t max_position_embeddings;
+  int64_t param_bytes;
+  int64_t grad_bytes;
+  int64_t optimizer_bytes_per_param;
+  int32_t has_output_head;
+} rr_model;
+
+typedef struct {
+  int32_t n_nodes;
+  int32_t gpus_per_node;
+  int64_t mem_per_device;
+  double intra_node_bw;
+  double inter_node_bw;
+  double host_to_device_bw;
+} rr_cluster;
+
+typedef struct {
+  int32_t node_offset;
+  int32_t node_count;
+  int32_t gpu_offset;
+  int32_t gpu_count;
+} rr_mesh;
+
+/* qkv_layout: 0 separate, 1 concat [Q;K;V], 2 Megatron grouped.
+ * gate_up_layout: 0 separate, 1 concat [G;U]. (DESIGN.md §3 G4) */
+typedef struct {
+  rr_mesh mesh;
+  int32_t dp, tp, pp, n_microbatches;
+  int32_t qkv_layout;
+  int32_t gate_up_layout;
+} rr_placement;
+
+typedef struct { /* SPEC.md:547-549; layers -1 and L are embed / final+head */
+  int64_t layer_start;
+  int64_t layer_end;
+  int32_t tp_rank;
+  int32_t tp_degree;
+  int32_t replicated;
+} rr_shard;
+
+typedef struct {
+  int32_t src;
+  int32_t n_dst;
+  const int32_t* dst; /* valid for the plan's lifetime */
+  rr_shard payload;
+  int64_t bytes;
+} rr_op;
+
+typedef struct rr_plan rr_plan;
+typedef struct rr_exec rr_exec;
+typedef struct rr_barrier rr_barrier;
+
+const char* rr_last_error(void);
+int rr_abi_version(void);
+
+/* ---- model-arith (reference model_arith.hpp:37-72) ---- */
+rr_status rr_model_validate(const rr_model* m);                                 /* ModelSpec::validate, model_arith.hpp:31 */
+rr_status rr_param_count(const rr_model* m, int include_output_embedding, int64_t* out); /* model_arith.hpp:42 */
+rr_status rr_natural_param_count(const rr_model* m, int64_t* out);              /* model_arith.hpp:46 */
+rr_status rr_flops(const rr_model* m, int backward, int64_t tokens, int64_t context_len, double* out); /* model_arith.hpp:54 */
+rr_status rr_layer_flops_fwd(const rr_model* m, int64_t tokens, int64_t context_len, double* out);     /* model_arith.hpp:57 */
+rr_status rr_kv_cache_bytes(const rr_model* m, int64_t batch, int64_t seq_len, int64_t* out);          /* model_arith.hpp:60 */
+rr_status rr_logits_bytes(int64_t vocab, int64_t batch, int64_t ctx_len, int64_t elem_bytes, int64_t* out); /* model_arith.hpp:63 */
+rr_status rr_static_param_bytes(const rr_model* m, int64_t* params, int64_t* grads, int64_t* optimizer); /* model_arith.hpp:72 */
+
+/* ---- cluster-topo (reference cluster.hpp:14-63) ---- */
+rr_status rr_cluster_validate(const rr_cluster* c);                             /* ClusterSpec::validate, cluster.hpp:23 */
+rr_status rr_validate_mesh(const rr_mesh* m, const rr_cluster* c);               /* cluster.hpp:45 */
+rr_status rr_mesh_devices(const rr_mesh* m, const rr_cluster* c, int32_t* out, int cap, int* n); /* DeviceMesh::devices, cluster.hpp:38 */
+rr_status rr_mesh_contains(const rr_mesh* m, const rr_cluster* c, int32_t device, int* out);      /* DeviceMesh::contains, cluster.hpp:40 */
+rr_status rr_enumerate_meshes(const rr_cluster* c, rr_mesh* out, int cap, int* n);             /* cluster.hpp:49 */
+rr_status rr_overlap(const rr_mesh* a, const rr_mesh* b, const rr_cluster* c, int* out);        /* cluster.hpp:51 */
+rr_status rr_link_bandwidth(const rr_cluster* c, int32_t a, int32_t b, double* out);            /* cluster.hpp:55 */
+rr_status rr_mesh_to_string(const rr_mesh* m, const rr_cluster* c, char* buf, size_t cap, size_t* needed); /* cluster.hpp:62 */
+rr_status rr_mesh_from_string(const char* text, const rr_cluster* c, rr_mesh* out);            /* cluster.hpp:63 */
+
+/* ---- realloc planning ---- */
+rr_status rr_stage_layer_map(int64_t num_layers, int pp, int64_t* starts, int64_t* ends);
+rr_status rr_validate_placement(const rr_model* m, const rr_placement* p, const rr_cluster* c);
+/* policy: 0 = SPEC tie-break (lowest id), 1 = balanced egress. */
+rr_status rr_plan_create(const rr_model* m, const rr_placement* src, const rr_placement* dst,
+                         const rr_cluster* c, int policy, rr_plan** out);                     /* plan_param_realloc */
+void rr_plan_destroy(rr_plan* plan);
+rr_status rr_plan_totals(const rr_plan* plan, int64_t* total_bytes, double* est_time);
+rr_status rr_plan_num_ops(const rr_plan* plan, int local, int* n);
+rr_status rr_plan_get_op(const rr_plan* plan, int local, int index, rr_op* out);
+rr_status rr_plan_to_json(const rr_plan* plan, char* buf, size_t cap, size_t* needed);        /* realloc-plan */
+/* side 0 = source placement, 1 = destination placement. 0 bytes if the
+ * device is not part of that placement. */
+rr_status rr_plan_shard_bytes(const rr_plan* plan, int side, int32_t device, int64_t* bytes);
+/* Per-device traffic of the lowered plan (bytes): over links in/out, and
+ * copied locally (src and dst on the same device). */
+rr_status rr_plan_device_traffic(const rr_plan* plan, int32_t device, int64_t* wire_in,
+                                 int64_t* wire_out, int64_t* local);
+rr_status rr_plan_num_rects(const rr_plan* plan, int64_t* n);
+/* Shard layout block table for (side, device): 6 int64 per block
+ * {tensor, r0, r1, c0, c1, offset}. */
+rr_status rr_plan_layout(const rr_plan* plan, int side, int32_t device, int64_t* out, int64_t cap_blocks,
+                         int64_t* n_blocks);
+
+/* Lowered plan inspection (host only): op i of the merged (remote + local)
+ * list has source *src, destinations dst[0..*n_dst) (cap 64) and *n_rects
+ * copy rectangles, 6 int64 each {src_off, dst_off, row_bytes, src_pitch,
+ * dst_pitch, rows}; pass rects = NULL to query *n_rects. */
+rr_status rr_plan_num_lowered(const rr_plan* plan, int* n);
+rr_status rr_plan_get_lowered(const rr_plan* plan, int index, int32_t* src, int32_t* dst, int* n_dst,
+                              int64_t* rects, int64_t cap_rects, int64_t* n_rects);
+/* Work an executor with this `local` set and mode would do (host only, no
+ * CUDA): bytes read from sources and bytes stored to destinations. */
+rr_status rr_plan_work(const rr_plan* plan, int n_local, const int32_t* local, int mode,
+                       int64_t* bytes_read, int64_t* bytes_written);
+
+/* ---- device memory and peer mapping (plumbing) ---- */
+rr_status rr_device_count(int* n);
+rr_status rr_device_alloc(int cuda_device, size_t bytes, void** out);
+rr_status rr_device_free(void* ptr);
+rr_status rr_host_alloc(size_t bytes, void** out); /* pinned */
+rr_status rr_host_free(void* ptr);
+/* kind: 0 host->device, 1 device->host, 2 device->device. */
+rr_status rr_memcpy(void* dst, const void* src, size_t bytes, int kind, void* stream, int synchronous);
+rr_status rr_memset(void* dst, int value, size_t bytes, void* stream);
+rr_status rr_stream_sync(void* stream);
+rr_status rr_ipc_handle(void* device_ptr, void* handle64);            /* 64-byte cudaIpcMemHandle */
+rr_status rr_ipc_open(int cuda_device, const void* handle64, void** out);
+rr_status rr_ipc_close(void* ptr);
+rr_status rr_enable_peer(int cuda_device, int peer_device);
+
+/* ---- execution: the B200 replacement of the upstream NCCL-broadcast
+ *      executor ----
+ *
+ * src_bufs / dst_bufs are indexed by global DeviceId (n_devices entries,
+ * NULL where unused) and must be addressable from `cuda_device` (local
+ * allocations, or IPC-opened / peer-enabled pointers). `local` lists the
+ * plan devices whose SMs this executor drives (the virtual devices hosted on
+ * cuda_device).
+ * mode 0 = PUSH: a local source reads its shard once and stores every
+ *          destination copy (local relayout + NVLink peer stores, K1/K2).
+ * mode 1 = PULL: a local destination loads from the (possibly remote)
+ *          source and stores locally.
+ * chunk_bytes: work-item granularity (0 = default 256 KiB). */
+rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices,
+                         void* const* src_bufs, void* const* dst_bufs, int n_local,
+                         const int32_t* local, int mode, int64_t chunk_bytes, rr_exec** out);
+/* ctas = 0 picks 148 x resident CTAs. */
+rr_status rr_exec_launch(rr_exec* ex, void* stream, int ctas);
+/* items, bytes moved per launch (sum over destinations), bytes read. */
+rr_status rr_exec_stats(const rr_exec* ex, int64_t* items, int64_t* bytes_written, int64_t* bytes_read);
+void rr_exec_destroy(rr_exec* ex);
+
+/* ---- deterministic weights (test/bench infrastructure) ----
+ * Fill or check a device's shard under one side of a plan with
+ * bf16 value = hash(seed, tensor_id, logical_index). */
+rr_status rr_fill_shard(const rr_plan* plan, int side, int32_t device, void* buf, uint64_t seed,
+                        void* stream);
+/* Synchronous; *mismatches = number of differing elements, *first = buffer
+ * element index of the first difference (or -1). */
+rr_status rr_verify_shard(const rr_plan* plan, int side, int32_t device, const void* buf,
+                          uint64_t seed, void* stream, int64_t* mismatches, int64_t* first);
+/* Host-side reference of the value function (for KATs). */
+uint16_t rr_weight_value(uint64_t seed, int64_t tensor_id, int64_t logical_index);
+
+/* ---- cross-GPU barrier for one-process-per-GPU execution ----
+ * flags[p] = rank p's flag array (world uint32), mapped into this process. */
+rr_status rr_barrier_create(int cuda_device, int rank, int world, void* const* flags,
+                            rr_barrier** out);
+rr_status rr_barrier_launch(rr_barrier* b, void* stream);
+/* Nonzero *timed_out if any launch gave up waiting (bounded spin). */
+rr_status rr_barrier_status(rr_barrier* b, int* timed_out);
+void rr_barrier_destroy(rr_barrier* b);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RR_REALLOC_H_ */

@@ -1,0 +1,831 @@
+// C ABI (include/rr_realloc.h) over the rlplan C++ library and the sm_100a
+// kernels. No exception crosses this boundary: ValidationError -> RR_EINVAL
+// with the reference's message (reference common.hpp:22-25), CUDA failures
+// -> RR_ECUDA, allocation failures -> RR_ENOMEM.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "rlplan/realloc.hpp"
+#include "rr_internal.hpp"
+#include "rr_realloc.h"
+
+using namespace rlplan;
+
+namespace {
+
+thread_local std::string g_error;
+
+struct StatusError {
+  rr_status status;
+  std::string message;
+};
+
+[[noreturn]] void raise(rr_status s, const std::string& msg) { throw StatusError{s, msg}; }
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) raise(RR_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void check_cuda(int e, const char* what) { check_cuda(static_cast<cudaError_t>(e), what); }
+
+template <class F>
+rr_status guarded(F&& f) {
+  try {
+    f();
+    return RR_OK;
+  } catch (const StatusError& e) {
+    g_error = e.message;
+    return e.status;
+  } catch (const ValidationError& e) {
+    g_error = e.what();
+    return RR_EINVAL;
+  } catch (const std::bad_alloc&) {
+    g_error = "out of host memory";
+    return RR_ENOMEM;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return RR_EINVAL;
+  }
+}
+
+void need(bool ok, const char* what) {
+  if (!ok) raise(RR_EINVAL, what);
+}
+
+ModelSpec to_model(const rr_model* m) {
+  need(m != nullptr, "null model");
+  ModelSpec s;
+  s.name = m->name ? m->name : "";
+  s.hidden_size = m->hidden_size;
+  s.intermediate_size = m->intermediate_size;
+  s.num_layers = m->num_layers;
+  s.num_attention_heads = m->num_attention_heads;
+  s.num_kv_heads = m->num_kv_heads;
+  s.vocab_size = m->vocab_size;
+  s.max_position_embeddings = m->max_position_embeddings;
+  s.param_bytes = m->param_bytes;
+  s.grad_bytes = m->grad_bytes;
+  s.optimizer_bytes_per_param = m->optimizer_bytes_per_param;
+  s.has_output_head = m->has_output_head != 0;
+  return s;
+}
+
+ClusterSpec to_cluster(const rr_cluster* c) {
+  need(c != nullptr, "null cluster");
+  ClusterSpec s;
+  s.n_nodes = c->n_nodes;
+  s.gpus_per_node = c->gpus_per_node;
+  s.mem_per_device = c->mem_per_device;
+  s.intra_node_bw = c->intra_node_bw;
+  s.inter_node_bw = c->inter_node_bw;
+  s.host_to_device_bw = c->host_to_device_bw;
+  return s;
+}
+
+DeviceMesh to_mesh(const rr_mesh* m) {
+  need(m != nullptr, "null mesh");
+  return DeviceMesh{m->node_offset, m->node_count, m->gpu_offset, m->gpu_count};
+}
+
+rr_mesh from_mesh(const DeviceMesh& m) {
+  return rr_mesh{m.node_offset, m.node_count, m.gpu_offset, m.gpu_count};
+}
+
+Placement to_placement(const rr_placement* p) {
+  need(p != nullptr, "null placement");
+  Placement out;
+  out.mesh = to_mesh(&p->mesh);
+  out.strategy = ParallelStrategy{p->dp, p->tp, p->pp, p->n_microbatches};
+  need(p->qkv_layout >= 0 && p->qkv_layout <= 2, "qkv_layout must be 0, 1 or 2");
+  need(p->gate_up_layout >= 0 && p->gate_up_layout <= 1, "gate_up_layout must be 0 or 1");
+  out.qkv = static_cast<QkvLayout>(p->qkv_layout);
+  out.gate_up = static_cast<GateUpLayout>(p->gate_up_layout);
+  return out;
+}
+
+rr_shard to_shard(const ShardDescriptor& d) {
+  return rr_shard{d.layer_start, d.layer_end, d.tp_rank, d.tp_degree, d.replicated ? 1 : 0};
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Plan object
+// ---------------------------------------------------------------------------
+
+struct rr_plan {
+  ModelSpec model;
+  Placement src, dst;
+  ClusterSpec cluster;
+  ReallocPlan plan;
+  std::vector<std::vector<int32_t>> remote_dst, local_dst;  // int32 copies for rr_op
+  std::vector<LoweredOp> lowered;
+  std::map<std::pair<int, DeviceId>, ShardLayout> layouts;
+  std::mutex mu;  // guards lazily built layouts
+
+  const ShardLayout& layout(int side, DeviceId d) {
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_pair(side, d);
+    auto it = layouts.find(key);
+    if (it == layouts.end())
+      it = layouts.emplace(key, shard_layout(model, side ? dst : src, cluster, d)).first;
+    return it->second;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Executor object
+// ---------------------------------------------------------------------------
+
+struct rr_exec {
+  int cuda_device = 0;
+  rr::CopyItem* d_items = nullptr;
+  int n_items = 0;
+  int fence_sys = 0;
+  int default_ctas = 0;
+  int64_t bytes_written = 0, bytes_read = 0;
+};
+
+struct rr_barrier {
+  int cuda_device = 0;
+  int rank = 0, world = 0;
+  uint32_t epoch = 0;
+  uint32_t** d_flags = nullptr;
+  int* d_timed_out = nullptr;
+};
+
+// Definitions take C linkage from the declarations in rr_realloc.h.
+
+const char* rr_last_error(void) { return g_error.c_str(); }
+int rr_abi_version(void) { return RR_ABI_VERSION; }
+
+// ---- model-arith ----------------------------------------------------------
+
+rr_status rr_model_validate(const rr_model* m) {
+  return guarded([&] { to_model(m).validate(); });
+}
+rr_status rr_param_count(const rr_model* m, int include, int64_t* out) {
+  return guarded([&] { *out = param_count(to_model(m), include != 0); });
+}
+rr_status rr_natural_param_count(const rr_model* m, int64_t* out) {
+  return guarded([&] { *out = natural_param_count(to_model(m)); });
+}
+rr_status rr_flops(const rr_model* m, int backward, int64_t tokens, int64_t ctx, double* out) {
+  return guarded([&] { *out = flops(to_model(m), backward ? Phase::Backward : Phase::Forward, tokens, ctx); });
+}
+rr_status rr_layer_flops_fwd(const rr_model* m, int64_t tokens, int64_t ctx, double* out) {
+  return guarded([&] { *out = layer_flops_fwd(to_model(m), tokens, ctx); });
+}
+rr_status rr_kv_cache_bytes(const rr_model* m, int64_t batch, int64_t seq, int64_t* out) {
+  return guarded([&] { *out = kv_cache_bytes(to_model(m), batch, seq); });
+}
+rr_status rr_logits_bytes(int64_t vocab, int64_t batch, int64_t ctx, int64_t elem, int64_t* out) {
+  return guarded([&] { *out = logits_bytes(vocab, batch, ctx, elem); });
+}
+rr_status rr_static_param_bytes(const rr_model* m, int64_t* params, int64_t* grads, int64_t* opt) {
+  return guarded([&] {
+    const auto s = static_param_bytes(to_model(m));
+    *params = s.params;
+    *grads = s.grads;
+    *opt = s.optimizer;
+  });
+}
+
+// ---- cluster-topo -----------------------------------------------------------
+
+rr_status rr_cluster_validate(const rr_cluster* c) {
+  return guarded([&] { to_cluster(c).validate(); });
+}
+rr_status rr_validate_mesh(const rr_mesh* m, const rr_cluster* c) {
+  return guarded([&] { validate_mesh(to_mesh(m), to_cluster(c)); });
+}
+rr_status rr_mesh_devices(const rr_mesh* m, const rr_cluster* c, int32_t* out, int cap, int* n) {
+  return guarded([&] {
+    const auto d = to_mesh(m).devices(to_cluster(c));
+    *n = static_cast<int>(d.size());
+    if (static_cast<int>(d.size()) > cap) raise(RR_ERANGE, "rr_mesh_devices: buffer too small");
+    std::copy(d.begin(), d.end(), out);
+  });
+}
+rr_status rr_mesh_contains(const rr_mesh* m, const rr_cluster* c, int32_t device, int* out) {
+  return guarded([&] { *out = to_mesh(m).contains(to_cluster(c), device) ? 1 : 0; });
+}
+rr_status rr_enumerate_meshes(const rr_cluster* c, rr_mesh* out, int cap, int* n) {
+  return guarded([&] {
+    const auto all = enumerate_meshes(to_cluster(c));
+    *n = static_cast<int>(all.size());
+    if (static_cast<int>(all.size()) > cap) raise(RR_ERANGE, "rr_enumerate_meshes: buffer too small");
+    for (size_t i = 0; i < all.size(); ++i) out[i] = from_mesh(all[i]);
+  });
+}
+rr_status rr_overlap(const rr_mesh* a, const rr_mesh* b, const rr_cluster* c, int* out) {
+  return guarded([&] { *out = overlap(to_mesh(a), to_mesh(b), to_cluster(c)) ? 1 : 0; });
+}
+rr_status rr_link_bandwidth(const rr_cluster* c, int32_t a, int32_t b, double* out) {
+  return guarded([&] { *out = link_bandwidth(to_cluster(c), a, b); });
+}
+rr_status rr_mesh_to_string(const rr_mesh* m, const rr_cluster* c, char* buf, size_t cap, size_t* needed) {
+  return guarded([&] {
+    const std::string s = mesh_to_string(to_mesh(m), to_cluster(c));
+    *needed = s.size() + 1;
+    if (cap < s.size() + 1) raise(RR_ERANGE, "rr_mesh_to_string: buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+rr_status rr_mesh_from_string(const char* text, const rr_cluster* c, rr_mesh* out) {
+  return guarded([&] {
+    need(text != nullptr, "null mesh string");
+    *out = from_mesh(mesh_from_string(text, to_cluster(c)));
+  });
+}
+
+// ---- realloc planning -------------------------------------------------------
+
+rr_status rr_stage_layer_map(int64_t num_layers, int pp, int64_t* starts, int64_t* ends) {
+  return guarded([&] {
+    const auto st = stage_layer_map(num_layers, pp);
+    for (size_t i = 0; i < st.size(); ++i) {
+      starts[i] = st[i].first;
+      ends[i] = st[i].second;
+    }
+  });
+}
+
+rr_status rr_validate_placement(const rr_model* m, const rr_placement* p, const rr_cluster* c) {
+  return guarded([&] { validate_placement(to_model(m), to_placement(p), to_cluster(c)); });
+}
+
+rr_status rr_plan_create(const rr_model* m, const rr_placement* src, const rr_placement* dst,
+                         const rr_cluster* c, int policy, rr_plan** out) {
+  return guarded([&] {
+    need(out != nullptr, "null output");
+    need(policy == 0 || policy == 1, "policy must be 0 (spec) or 1 (balanced)");
+    auto p = std::make_unique<rr_plan>();
+    p->model = to_model(m);
+    p->src = to_placement(src);
+    p->dst = to_placement(dst);
+    p->cluster = to_cluster(c);
+    p->plan = plan_param_realloc(p->model, p->src, p->dst, p->cluster, static_cast<SourcePolicy>(policy));
+    for (const auto& op : p->plan.ops) p->remote_dst.emplace_back(op.dst.begin(), op.dst.end());
+    for (const auto& op : p->plan.local_ops) p->local_dst.emplace_back(op.dst.begin(), op.dst.end());
+    p->lowered = lower_plan(p->model, p->src, p->dst, p->cluster, p->plan);
+    *out = p.release();
+  });
+}
+
+void rr_plan_destroy(rr_plan* plan) { delete plan; }
+
+rr_status rr_plan_totals(const rr_plan* plan, int64_t* total_bytes, double* est_time) {
+  return guarded([&] {
+    need(plan != nullptr, "null plan");
+    *total_bytes = plan->plan.total_bytes;
+    *est_time = plan->plan.est_time;
+  });
+}
+
+rr_status rr_plan_num_ops(const rr_plan* plan, int local, int* n) {
+  return guarded([&] {
+    need(plan != nullptr, "null plan");
+    *n = static_cast<int>(local ? plan->plan.local_ops.size() : plan->plan.ops.size());
+  });
+}
+
+rr_status rr_plan_get_op(const rr_plan* plan, int local, int index, rr_op* out) {
+  return guarded([&] {
+    need(plan != nullptr, "null plan");
+    const auto& list = local ? plan->plan.local_ops : plan->plan.ops;
+    const auto& dsts = local ? plan->local_dst : plan->remote_dst;
+    need(index >= 0 && index < static_cast<int>(list.size()), "op index out of range");
+    const auto& op = list[static_cast<size_t>(index)];
+    out->src = op.src;
+    out->n_dst = static_cast<int32_t>(op.dst.size());
+    out->dst = dsts[static_cast<size_t>(index)].data();
+    out->payload = to_shard(op.payload);
+    out->bytes = op.bytes;
+  });
+}
+
+rr_status rr_plan_to_json(const rr_plan* plan, char* buf, size_t cap, size_t* needed) {
+  return guarded([&] {
+    need(plan != nullptr, "null plan");
+    const std::string s = plan_to_json(plan->plan, plan->model, plan->src, plan->dst, plan->cluster);
+    *needed = s.size() + 1;
+    if (cap < s.size() + 1) raise(RR_ERANGE, "rr_plan_to_json: buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+rr_status rr_plan_shard_bytes(const rr_plan* plan, int side, int32_t device, int64_t* bytes) {
+  return guarded([&] {
+    need(plan != nullptr, "null plan");
+    *bytes = const_cast<rr_plan*>(plan)->layout(side, device).bytes;
+  });
+}
+
+rr_status rr_plan_device_traffic(const rr_plan* plan, int32_t device, int64_t* wire_in,
+                                 int64_t* wire_out, int64_t* local) {
+  return guarded([&] {
+    need(plan != nullptr, "null plan");
+    int64_t in = 0, out = 0, loc = 0;
+    for (const auto& op : plan->lowered) {
+      int64_t bytes = 0;
+      for (const auto& r : op.rects) bytes += r.row_bytes * r.rows;
+      for (DeviceId d : op.dst) {
+        if (d == op.src) {
+          if (d == device) loc += bytes;
+        } else {
+          if (d == device) in += bytes;
+          if (op.src == device) out += bytes;
+        }
+      }
+    }
+    *wire_in = in;
+    *wire_out = out;
+    *local = loc;
+  });
+}
+
+rr_status rr_plan_num_rects(const rr_plan* plan, int64_t* n) {
+  return guarded([&] {
+    need(plan != nullptr, "null plan");
+    int64_t k = 0;
+    for (const auto& op : plan->lowered) k += static_cast<int64_t>(op.rects.size());
+    *n = k;
+  });
+}
+
+rr_status rr_plan_layout(const rr_plan* plan, int side, int32_t device, int64_t* out,
+                         int64_t cap_blocks, int64_t* n_blocks) {
+  return guarded([&] {
+    need(plan != nullptr, "null plan");
+    const auto& lay = const_cast<rr_plan*>(plan)->layout(side, device);
+    *n_blocks = static_cast<int64_t>(lay.blocks.size());
+    if (cap_blocks < *n_blocks) raise(RR_ERANGE, "rr_plan_layout: buffer too small");
+    for (size_t i = 0; i < lay.blocks.size(); ++i) {
+      const auto& b = lay.blocks[i];
+      int64_t* o = out + 6 * i;
+      o[0] = b.tensor;
+      o[1] = b.r0;
+      o[2] = b.r1;
+      o[3] = b.c0;
+      o[4] = b.c1;
+      o[5] = b.offset;
+    }
+  });
+}
+
+rr_status rr_plan_num_lowered(const rr_plan* plan, int* n) {
+  return guarded([&] {
+    need(plan != nullptr, "null plan");
+    *n = static_cast<int>(plan->lowered.size());
+  });
+}
+
+rr_status rr_plan_get_lowered(const rr_plan* plan, int index, int32_t* src, int32_t* dst, int* n_dst,
+                              int64_t* rects, int64_t cap_rects, int64_t* n_rects) {
+  return guarded([&] {
+    need(plan != nullptr, "null plan");
+    need(index >= 0 && index < static_cast<int>(plan->lowered.size()), "lowered op index out of range");
+    const auto& op = plan->lowered[static_cast<size_t>(index)];
+    need(op.dst.size() <= 64, "more than 64 destinations");
+    *src = op.src;
+    *n_dst = static_cast<int>(op.dst.size());
+    std::copy(op.dst.begin(), op.dst.end(), dst);
+    *n_rects = static_cast<int64_t>(op.rects.size());
+    if (!rects) return;
+    if (cap_rects < *n_rects) raise(RR_ERANGE, "rr_plan_get_lowered: rect buffer too small");
+    for (size_t i = 0; i < op.rects.size(); ++i) {
+      const auto& r = op.rects[i];
+      int64_t* o = rects + 6 * i;
+      o[0] = r.src_off;
+      o[1] = r.dst_off;
+      o[2] = r.row_bytes;
+      o[3] = r.src_pitch;
+      o[4] = r.dst_pitch;
+      o[5] = r.rows;
+    }
+  });
+}
+
+rr_status rr_plan_work(const rr_plan* plan, int n_local, const int32_t* local, int mode, int64_t* bytes_read,
+                       int64_t* bytes_written) {
+  return guarded([&] {
+    need(plan != nullptr, "null plan");
+    need(mode == 0 || mode == 1, "mode must be 0 (push) or 1 (pull)");
+    auto is_local = [&](DeviceId d) { return std::find(local, local + n_local, d) != local + n_local; };
+    int64_t rd = 0, wr = 0;
+    for (const auto& op : plan->lowered) {
+      int64_t bytes = 0;
+      for (const auto& r : op.rects) bytes += r.row_bytes * r.rows;
+      int64_t targets = 0;
+      if (mode == 0) {
+        if (!is_local(op.src)) continue;
+        targets = static_cast<int64_t>(op.dst.size());
+      } else {
+        for (DeviceId d : op.dst) targets += is_local(d) ? 1 : 0;
+        if (!targets) continue;
+      }
+      // One read per group of kMaxFan destinations (see rr_exec_create).
+      rd += bytes * ((targets + rr::kMaxFan - 1) / rr::kMaxFan);
+      wr += bytes * targets;
+    }
+    *bytes_read = rd;
+    *bytes_written = wr;
+  });
+}
+
+// ---- device memory and peer mapping ----------------------------------------
+
+rr_status rr_device_count(int* n) {
+  return guarded([&] {
+    int k = 0;
+    const cudaError_t e = cudaGetDeviceCount(&k);
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+      cudaGetLastError();
+      k = 0;
+    } else {
+      check_cuda(e, "cudaGetDeviceCount");
+    }
+    *n = k;
+  });
+}
+
+rr_status rr_device_alloc(int cuda_device, size_t bytes, void** out) {
+  return guarded([&] {
+    check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
+    const cudaError_t e = cudaMalloc(out, bytes ? bytes : 256);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      raise(RR_ENOMEM, "cudaMalloc: out of device memory");
+    }
+    check_cuda(e, "cudaMalloc");
+  });
+}
+
+rr_status rr_device_free(void* ptr) {
+  return guarded([&] { check_cuda(cudaFree(ptr), "cudaFree"); });
+}
+
+rr_status rr_host_alloc(size_t bytes, void** out) {
+  return guarded([&] {
+    const cudaError_t e = cudaMallocHost(out, bytes ? bytes : 256);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      raise(RR_ENOMEM, "cudaMallocHost: out of pinned memory");
+    }
+    check_cuda(e, "cudaMallocHost");
+  });
+}
+
+rr_status rr_host_free(void* ptr) {
+  return guarded([&] { check_cuda(cudaFreeHost(ptr), "cudaFreeHost"); });
+}
+
+rr_status rr_memcpy(void* dst, const void* src, size_t bytes, int kind, void* stream, int synchronous) {
+  return guarded([&] {
+    static const cudaMemcpyKind kinds[] = {cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost,
+                                           cudaMemcpyDeviceToDevice};
+    need(kind >= 0 && kind <= 2, "memcpy kind must be 0, 1 or 2");
+    auto s = static_cast<cudaStream_t>(stream);
+    check_cuda(cudaMemcpyAsync(dst, src, bytes, kinds[kind], s), "cudaMemcpyAsync");
+    if (synchronous) check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  });
+}
+
+rr_status rr_memset(void* dst, int value, size_t bytes, void* stream) {
+  return guarded([&] {
+    check_cuda(cudaMemsetAsync(dst, value, bytes, static_cast<cudaStream_t>(stream)), "cudaMemsetAsync");
+  });
+}
+
+rr_status rr_stream_sync(void* stream) {
+  return guarded([&] {
+    check_cuda(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "cudaStreamSynchronize");
+  });
+}
+
+rr_status rr_ipc_handle(void* device_ptr, void* handle64) {
+  return guarded([&] {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    check_cuda(cudaIpcGetMemHandle(&h, device_ptr), "cudaIpcGetMemHandle");
+    std::memcpy(handle64, &h, sizeof(h));
+  });
+}
+
+rr_status rr_ipc_open(int cuda_device, const void* handle64, void** out) {
+  return guarded([&] {
+    check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    check_cuda(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  });
+}
+
+rr_status rr_ipc_close(void* ptr) {
+  return guarded([&] { check_cuda(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle"); });
+}
+
+rr_status rr_enable_peer(int cuda_device, int peer_device) {
+  return guarded([&] {
+    int ok = 0;
+    check_cuda(cudaDeviceCanAccessPeer(&ok, cuda_device, peer_device), "cudaDeviceCanAccessPeer");
+    if (!ok) raise(RR_EUNSUPPORTED, "peer access not supported between these devices");
+    check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+      cudaGetLastError();
+      return;
+    }
+    check_cuda(e, "cudaDeviceEnablePeerAccess");
+  });
+}
+
+// ---- execution ----------------------------------------------------------------
+
+namespace {
+
+struct Builder {
+  std::vector<std::vector<rr::CopyItem>> streams;  // one item stream per (op, dst group)
+  int64_t written = 0, read = 0;
+
+  // Chunk one rectangle for (src base, dst bases) into items.
+  void add_rect(std::vector<rr::CopyItem>& out, uint64_t src, const std::vector<uint64_t>& dsts,
+                const CopyRect& r, int64_t chunk) {
+    const bool vec = ((src | r.src_off | r.dst_off | r.row_bytes | r.src_pitch | r.dst_pitch) & 15) == 0 &&
+                     std::all_of(dsts.begin(), dsts.end(), [](uint64_t d) { return (d & 15) == 0; });
+    const int64_t unit = vec ? 16 : 2;
+    const int64_t cap_units = std::min<int64_t>(chunk / unit, rr::kMaxItemUnits);
+    const int64_t row_units = r.row_bytes / unit;
+    const int64_t sp = r.src_pitch / unit, dp = r.dst_pitch / unit;
+    auto emit = [&](int64_t row0, int64_t col0, int64_t rows, int64_t cols) {
+      rr::CopyItem it;
+      std::memset(&it, 0, sizeof(it));
+      it.src = src + static_cast<uint64_t>(r.src_off + (row0 * sp + col0) * unit);
+      for (size_t j = 0; j < dsts.size(); ++j)
+        it.dst[j] = dsts[j] + static_cast<uint64_t>(r.dst_off + (row0 * dp + col0) * unit);
+      it.ndst = static_cast<uint16_t>(dsts.size());
+      it.vec = vec ? 1 : 0;
+      it.row_units = static_cast<uint32_t>(cols);
+      it.nrows = static_cast<uint32_t>(rows);
+      it.src_pitch = static_cast<uint32_t>(rows > 1 ? sp : cols);
+      it.dst_pitch = static_cast<uint32_t>(rows > 1 ? dp : cols);
+      it.inv_row = 1.0f / static_cast<float>(cols);
+      if (rows > 1 && ((rows - 1) * dp + cols >= (int64_t{1} << 32) || (rows - 1) * sp + cols >= (int64_t{1} << 32)))
+        raise(RR_EINVAL, "copy item spans more than 2^32 units");
+      out.push_back(it);
+      const int64_t bytes = rows * cols * unit;
+      read += bytes;
+      written += bytes * static_cast<int64_t>(dsts.size());
+    };
+    if (row_units <= cap_units) {
+      const int64_t rows_per = std::max<int64_t>(1, cap_units / std::max<int64_t>(row_units, 1));
+      for (int64_t r0 = 0; r0 < r.rows; r0 += rows_per) emit(r0, 0, std::min(rows_per, r.rows - r0), row_units);
+    } else {
+      for (int64_t row = 0; row < r.rows; ++row)
+        for (int64_t c0 = 0; c0 < row_units; c0 += cap_units) emit(row, c0, 1, std::min(cap_units, row_units - c0));
+    }
+  }
+};
+
+}  // namespace
+
+rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, void* const* src_bufs,
+                         void* const* dst_bufs, int n_local, const int32_t* local, int mode,
+                         int64_t chunk_bytes, rr_exec** out) {
+  return guarded([&] {
+    need(plan != nullptr && out != nullptr, "null plan/output");
+    need(mode == 0 || mode == 1, "mode must be 0 (push) or 1 (pull)");
+    need(n_devices >= plan->cluster.device_count(), "buffer tables must cover every cluster device");
+    if (chunk_bytes <= 0) chunk_bytes = 256 << 10;
+    need(chunk_bytes >= 16, "chunk_bytes too small");
+    std::vector<bool> is_local(static_cast<size_t>(n_devices), false);
+    for (int i = 0; i < n_local; ++i) {
+      need(local[i] >= 0 && local[i] < n_devices, "local device out of range");
+      is_local[static_cast<size_t>(local[i])] = true;
+    }
+    auto addr = [&](void* const* bufs, DeviceId d, const char* what) {
+      void* p = bufs[d];
+      if (!p) raise(RR_EINVAL, std::string("missing ") + what + " buffer for device " + std::to_string(d));
+      return reinterpret_cast<uint64_t>(p);
+    };
+    Builder b;
+    bool remote = false;
+    for (const auto& op : plan->lowered) {
+      std::vector<DeviceId> targets;
+      if (mode == 0) {
+        if (!is_local[static_cast<size_t>(op.src)]) continue;
+        targets = op.dst;
+      } else {
+        for (DeviceId d : op.dst)
+          if (is_local[static_cast<size_t>(d)]) targets.push_back(d);
+        if (targets.empty()) continue;
+      }
+      const uint64_t s = addr(src_bufs, op.src, "source");
+      for (size_t g = 0; g < targets.size(); g += rr::kMaxFan) {
+        std::vector<uint64_t> dsts;
+        for (size_t j = g; j < std::min(targets.size(), g + rr::kMaxFan); ++j) {
+          dsts.push_back(addr(dst_bufs, targets[j], "destination"));
+          if (!is_local[static_cast<size_t>(targets[j])]) remote = true;
+        }
+        b.streams.emplace_back();
+        for (const auto& r : op.rects) {
+          // Same-address copies (identical placement and buffers) are no-ops.
+          if (dsts.size() == 1 && s + r.src_off == dsts[0] + r.dst_off) continue;
+          b.add_rect(b.streams.back(), s, dsts, r, chunk_bytes);
+        }
+      }
+    }
+    // Interleave the per-op streams round-robin so concurrently running CTAs
+    // spread their stores over many destinations (NVLink ingress balance).
+    std::vector<rr::CopyItem> items;
+    size_t total = 0;
+    for (const auto& s : b.streams) total += s.size();
+    items.reserve(total);
+    for (size_t k = 0; items.size() < total; ++k)
+      for (const auto& s : b.streams)
+        if (k < s.size()) items.push_back(s[k]);
+    need(items.size() < (size_t{1} << 31), "too many copy items");
+
+    auto ex = std::make_unique<rr_exec>();
+    ex->cuda_device = cuda_device;
+    ex->n_items = static_cast<int>(items.size());
+    ex->fence_sys = remote ? 1 : 0;
+    ex->bytes_written = b.written;
+    ex->bytes_read = b.read;
+    check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
+    int per_sm = 0, sms = 0;
+    check_cuda(rr::copy_max_ctas(&per_sm, &sms), "occupancy query");
+    ex->default_ctas = std::max(1, per_sm) * sms;
+    if (!items.empty()) {
+      const size_t bytes = items.size() * sizeof(rr::CopyItem);
+      check_cuda(cudaMalloc(&ex->d_items, bytes), "cudaMalloc(items)");
+      check_cuda(cudaMemcpy(ex->d_items, items.data(), bytes, cudaMemcpyHostToDevice), "upload items");
+    }
+    *out = ex.release();
+  });
+}
+
+rr_status rr_exec_launch(rr_exec* ex, void* stream, int ctas) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+    check_cuda(rr::launch_copy(ex->d_items, ex->n_items, ctas > 0 ? ctas : ex->default_ctas,
+                               ex->fence_sys, stream),
+               "rr_copy_kernel launch");
+  });
+}
+
+rr_status rr_exec_stats(const rr_exec* ex, int64_t* items, int64_t* written, int64_t* read) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    *items = ex->n_items;
+    *written = ex->bytes_written;
+    *read = ex->bytes_read;
+  });
+}
+
+void rr_exec_destroy(rr_exec* ex) {
+  if (!ex) return;
+  if (ex->d_items) {
+    cudaSetDevice(ex->cuda_device);
+    cudaFree(ex->d_items);
+  }
+  delete ex;
+}
+
+// ---- deterministic weights ----------------------------------------------------
+
+namespace {
+
+std::vector<rr::FillItem> fill_items(const ShardLayout& lay, const ModelSpec& m, uint64_t base) {
+  const auto inv = tensor_inventory(m);
+  constexpr uint32_t kChunk = 1u << 16;
+  std::vector<rr::FillItem> items;
+  for (const auto& b : lay.blocks) {
+    const uint64_t n = static_cast<uint64_t>((b.r1 - b.r0) * (b.c1 - b.c0));
+    if (n >= (uint64_t{1} << 32)) raise(RR_EINVAL, "layout block larger than 2^32 elements");
+    for (uint64_t e = 0; e < n; e += kChunk) {
+      rr::FillItem it;
+      it.base = base + static_cast<uint64_t>(b.offset);
+      it.r0 = static_cast<uint64_t>(b.r0);
+      it.c0 = static_cast<uint64_t>(b.c0);
+      it.full_cols = static_cast<uint64_t>(inv[static_cast<size_t>(b.tensor)].cols);
+      it.cols = static_cast<uint32_t>(b.c1 - b.c0);
+      it.tensor = static_cast<uint32_t>(b.tensor);
+      it.elem0 = static_cast<uint32_t>(e);
+      it.n = static_cast<uint32_t>(std::min<uint64_t>(kChunk, n - e));
+      items.push_back(it);
+    }
+  }
+  return items;
+}
+
+template <class T>
+struct DeviceArray {
+  T* ptr = nullptr;
+  explicit DeviceArray(const std::vector<T>& host) {
+    if (host.empty()) return;
+    check_cuda(cudaMalloc(&ptr, host.size() * sizeof(T)), "cudaMalloc(items)");
+    check_cuda(cudaMemcpy(ptr, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice), "upload items");
+  }
+  ~DeviceArray() {
+    if (ptr) cudaFree(ptr);
+  }
+};
+
+}  // namespace
+
+rr_status rr_fill_shard(const rr_plan* plan, int side, int32_t device, void* buf, uint64_t seed, void* stream) {
+  return guarded([&] {
+    need(plan != nullptr && buf != nullptr, "null plan/buffer");
+    const auto& lay = const_cast<rr_plan*>(plan)->layout(side, device);
+    const auto items = fill_items(lay, plan->model, reinterpret_cast<uint64_t>(buf));
+    DeviceArray<rr::FillItem> d(items);
+    auto s = static_cast<cudaStream_t>(stream);
+    check_cuda(rr::launch_fill(d.ptr, static_cast<int>(items.size()), seed, s), "rr_fill_kernel launch");
+    check_cuda(cudaStreamSynchronize(s), "fill sync");
+  });
+}
+
+rr_status rr_verify_shard(const rr_plan* plan, int side, int32_t device, const void* buf, uint64_t seed,
+                          void* stream, int64_t* mismatches, int64_t* first) {
+  return guarded([&] {
+    need(plan != nullptr && buf != nullptr, "null plan/buffer");
+    const auto& lay = const_cast<rr_plan*>(plan)->layout(side, device);
+    const uint64_t base = reinterpret_cast<uint64_t>(buf);
+    const auto items = fill_items(lay, plan->model, base);
+    DeviceArray<rr::FillItem> d(items);
+    const std::vector<unsigned long long> init = {0ull, ~0ull};
+    DeviceArray<unsigned long long> counters(init);
+    auto s = static_cast<cudaStream_t>(stream);
+    check_cuda(rr::launch_verify(d.ptr, static_cast<int>(items.size()), seed, counters.ptr, base, s),
+               "rr_verify_kernel launch");
+    unsigned long long host[2];
+    check_cuda(cudaMemcpyAsync(host, counters.ptr, sizeof(host), cudaMemcpyDeviceToHost, s), "verify readback");
+    check_cuda(cudaStreamSynchronize(s), "verify sync");
+    *mismatches = static_cast<int64_t>(host[0]);
+    *first = host[0] ? static_cast<int64_t>(host[1]) : -1;
+  });
+}
+
+uint16_t rr_weight_value(uint64_t seed, int64_t tensor_id, int64_t logical_index) {
+  return rr::weight_value(seed, static_cast<uint64_t>(tensor_id), static_cast<uint64_t>(logical_index));
+}
+
+// ---- barrier -------------------------------------------------------------------
+
+rr_status rr_barrier_create(int cuda_device, int rank, int world, void* const* flags, rr_barrier** out) {
+  return guarded([&] {
+    need(world >= 1 && world <= 32 && rank >= 0 && rank < world, "bad rank/world");
+    auto b = std::make_unique<rr_barrier>();
+    b->cuda_device = cuda_device;
+    b->rank = rank;
+    b->world = world;
+    check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
+    std::vector<uint32_t*> host(static_cast<size_t>(world));
+    for (int p = 0; p < world; ++p) {
+      need(flags[p] != nullptr, "missing flag buffer");
+      host[static_cast<size_t>(p)] = static_cast<uint32_t*>(flags[p]);
+    }
+    check_cuda(cudaMalloc(&b->d_flags, host.size() * sizeof(uint32_t*)), "cudaMalloc(flags)");
+    check_cuda(cudaMemcpy(b->d_flags, host.data(), host.size() * sizeof(uint32_t*), cudaMemcpyHostToDevice),
+               "upload flags");
+    check_cuda(cudaMalloc(&b->d_timed_out, sizeof(int)), "cudaMalloc(timeout)");
+    check_cuda(cudaMemset(b->d_timed_out, 0, sizeof(int)), "cudaMemset(timeout)");
+    *out = b.release();
+  });
+}
+
+rr_status rr_barrier_launch(rr_barrier* b, void* stream) {
+  return guarded([&] {
+    need(b != nullptr, "null barrier");
+    check_cuda(cudaSetDevice(b->cuda_device), "cudaSetDevice");
+    ++b->epoch;
+    check_cuda(rr::launch_barrier(b->d_flags, b->rank, b->world, b->epoch, b->d_timed_out, stream),
+               "rr_barrier_kernel launch");
+  });
+}
+
+rr_status rr_barrier_status(rr_barrier* b, int* timed_out) {
+  return guarded([&] {
+    need(b != nullptr, "null barrier");
+    check_cuda(cudaSetDevice(b->cuda_device), "cudaSetDevice");
+    check_cuda(cudaMemcpy(timed_out, b->d_timed_out, sizeof(int), cudaMemcpyDeviceToHost), "barrier status");
+  });
+}
+
+void rr_barrier_destroy(rr_barrier* b) {
+  if (!b) return;
+  cudaSetDevice(b->cuda_device);
+  cudaFree(b->d_flags);
+  cudaFree(b->d_timed_out);
+  delete b;
+}

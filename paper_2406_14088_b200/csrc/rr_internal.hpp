@@ -1,0 +1,72 @@
+// Internal device-side structures shared by capi.cpp and kernels.cu.
+#pragma once
+
+#include <cstdint>
+
+namespace rr {
+
+// Maximum destinations one work item stores to (fan-out of a broadcast op
+// that is executed by one source read). Larger fan-outs are split.
+constexpr int kMaxFan = 8;
+
+// Hard cap on units per work item so that the float row/col split in the
+// copy kernel stays exact (see rr_copy_kernel).
+constexpr uint32_t kMaxItemUnits = 1u << 20;
+
+// One chunk of a 2D copy: `nrows` rows of `row_units` units; unit = 16 bytes
+// when vec != 0, else 2 bytes (one bf16). Source read once, stored to every
+// dst[0..ndst).
+struct alignas(16) CopyItem {
+  uint64_t src;
+  uint64_t dst[kMaxFan];
+  uint32_t row_units;
+  uint32_t nrows;
+  uint32_t src_pitch;  // units
+  uint32_t dst_pitch;  // units
+  float inv_row;       // 1.0f / row_units
+  uint16_t ndst;
+  uint16_t vec;
+  uint32_t pad[2];
+};
+static_assert(sizeof(CopyItem) % 16 == 0, "CopyItem must be a multiple of 16 bytes");
+
+// A run of elements of one layout block for hash fill / verify.
+struct alignas(16) FillItem {
+  uint64_t base;       // address of the block's first element
+  uint64_t r0;         // logical row of the block's first row
+  uint64_t c0;         // logical column of the block's first column
+  uint64_t full_cols;  // logical tensor width
+  uint32_t cols;       // block width (elements)
+  uint32_t tensor;
+  uint32_t elem0;      // first element (within the block) of this item
+  uint32_t n;          // elements in this item
+};
+
+// splitmix64 finaliser: the weight value function of DESIGN.md §4.
+__host__ __device__ inline uint64_t mix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// bf16 bits: random sign, exponent in [2^-10, 2^-3], random 7-bit mantissa
+// (never NaN/Inf/denormal).
+__host__ __device__ inline uint16_t weight_value(uint64_t seed, uint64_t tensor, uint64_t idx) {
+  const uint64_t h = mix64(seed ^ (tensor << 40) ^ idx);
+  const uint32_t sign = static_cast<uint32_t>(h >> 63);
+  const uint32_t expo = 117u + static_cast<uint32_t>((h >> 8) & 7u);
+  const uint32_t mant = static_cast<uint32_t>(h & 0x7fu);
+  return static_cast<uint16_t>((sign << 15) | (expo << 7) | mant);
+}
+
+// Host-callable launchers (kernels.cu). All return a cudaError_t as int.
+int launch_copy(const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream);
+int copy_max_ctas(int* ctas_per_sm, int* sms);
+int launch_fill(const FillItem* items, int n_items, uint64_t seed, void* stream);
+int launch_verify(const FillItem* items, int n_items, uint64_t seed, unsigned long long* counters,
+                  uint64_t buf_base, void* stream);
+int launch_barrier(uint32_t* const* flags, int rank, int world, uint32_t epoch, int* timed_out,
+                   void* stream);
+
+}  // namespace rr

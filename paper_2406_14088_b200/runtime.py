@@ -1,0 +1,321 @@
+"""Device-side execution of a ReallocPlan on B200s (through librrealloc.so).
+
+This is the B200 replacement of the upstream model worker's
+"Redistributing Parameters" step: there, sources NCCL-
+broadcast TP partitions to destinations; here every source GPU runs one
+sm_100a kernel that gathers its slices and stores them straight into the
+destination shards — locally through HBM, remotely through NVLink peer
+stores — with no pack/unpack pass.
+
+Two deployment shapes:
+
+* ``VirtualCluster`` — all plan devices hosted on one CUDA device (the
+  1-GPU local-relayout configuration and the single-GPU parity tests).
+* ``RankRealloc`` — one process per GPU (torchrun), each hosting a
+  contiguous block of plan devices; destination shards are exchanged as
+  CUDA IPC handles through ``torch.distributed`` and a flag barrier over
+  peer memory orders the phases.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Dict, Iterable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from ._lib import check, lib
+from .rlplan import ReallocPlan
+
+PUSH, PULL = 0, 1
+SRC, DST = 0, 1
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    """Accept None, an int cudaStream_t, or a torch.cuda.Stream."""
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return int(stream.cuda_stream)
+
+
+def device_count() -> int:
+    n = ctypes.c_int()
+    check(lib.rr_device_count(ctypes.byref(n)))
+    return n.value
+
+
+class DeviceBuffer:
+    """A cudaMalloc allocation owned by the library (IPC-exportable)."""
+
+    def __init__(self, cuda_device: int, nbytes: int):
+        self.cuda_device, self.nbytes = cuda_device, nbytes
+        p = ctypes.c_void_p()
+        check(lib.rr_device_alloc(cuda_device, max(nbytes, 256), ctypes.byref(p)))
+        self.ptr: int = p.value
+
+    def zero(self, stream=None) -> None:
+        check(lib.rr_memset(self.ptr, 0, max(self.nbytes, 256), _stream_ptr(stream)))
+
+    def ipc_handle(self) -> bytes:
+        h = ctypes.create_string_buffer(64)
+        check(lib.rr_ipc_handle(self.ptr, h))
+        return h.raw
+
+    def to_host(self) -> np.ndarray:
+        out = np.empty(self.nbytes // 2, dtype=np.uint16)
+        if self.nbytes:
+            check(lib.rr_memcpy(out.ctypes.data, self.ptr, self.nbytes, 1, None, 1))
+        return out
+
+    def from_host(self, arr: np.ndarray) -> None:
+        arr = np.ascontiguousarray(arr)
+        assert arr.nbytes <= max(self.nbytes, 256)
+        check(lib.rr_memcpy(self.ptr, arr.ctypes.data, arr.nbytes, 0, None, 1))
+
+    def free(self) -> None:
+        if self.ptr:
+            lib.rr_device_free(self.ptr)
+            self.ptr = 0
+
+
+class HostBuffer:
+    """Pinned host memory (for the end-to-end host->device leg)."""
+
+    def __init__(self, nbytes: int):
+        self.nbytes = nbytes
+        p = ctypes.c_void_p()
+        check(lib.rr_host_alloc(max(nbytes, 256), ctypes.byref(p)))
+        self.ptr: int = p.value
+
+    def array(self) -> np.ndarray:
+        buf = (ctypes.c_uint16 * (self.nbytes // 2)).from_address(self.ptr)
+        return np.ctypeslib.as_array(buf)
+
+    def free(self) -> None:
+        if self.ptr:
+            lib.rr_host_free(self.ptr)
+            self.ptr = 0
+
+
+def memcpy_async(dst: int, src: int, nbytes: int, kind: int, stream=None) -> None:
+    """kind 0 host->device, 1 device->host, 2 device->device."""
+    check(lib.rr_memcpy(dst, src, nbytes, kind, _stream_ptr(stream), 0))
+
+
+def stream_sync(stream=None) -> None:
+    check(lib.rr_stream_sync(_stream_ptr(stream)))
+
+
+def fill_shard(plan: ReallocPlan, side: int, device: int, ptr: int, seed: int, stream=None) -> None:
+    check(lib.rr_fill_shard(plan.handle, side, device, ptr, seed, _stream_ptr(stream)))
+
+
+def verify_shard(plan: ReallocPlan, side: int, device: int, ptr: int, seed: int,
+                 stream=None) -> Tuple[int, int]:
+    """(mismatching elements, first mismatching element index or -1)."""
+    bad, first = ctypes.c_int64(), ctypes.c_int64()
+    check(lib.rr_verify_shard(plan.handle, side, device, ptr, seed, _stream_ptr(stream),
+                              ctypes.byref(bad), ctypes.byref(first)))
+    return bad.value, first.value
+
+
+def weight_value(seed: int, tensor: int, index: int) -> int:
+    return lib.rr_weight_value(seed, tensor, index)
+
+
+class Executor:
+    """A plan bound to buffers on one CUDA device (rr_exec_create)."""
+
+    def __init__(self, plan: ReallocPlan, cuda_device: int, src_ptrs: Dict[int, int], dst_ptrs: Dict[int, int],
+                 local: Iterable[int], mode: int = PUSH, chunk_bytes: int = 0):
+        n = plan.cluster.device_count()
+        self.plan = plan
+        sp, dp = (ctypes.c_void_p * n)(), (ctypes.c_void_p * n)()
+        for d, p in src_ptrs.items():
+            sp[d] = p
+        for d, p in dst_ptrs.items():
+            dp[d] = p
+        loc = list(local)
+        arr = (ctypes.c_int32 * max(1, len(loc)))(*loc)
+        h = ctypes.c_void_p()
+        check(lib.rr_exec_create(plan.handle, cuda_device, n, sp, dp, len(loc), arr, mode, chunk_bytes,
+                                 ctypes.byref(h)))
+        self._h = h
+        it, w, r = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(lib.rr_exec_stats(h, ctypes.byref(it), ctypes.byref(w), ctypes.byref(r)))
+        self.items, self.bytes_written, self.bytes_read = it.value, w.value, r.value
+
+    def launch(self, stream=None, ctas: int = 0) -> None:
+        check(lib.rr_exec_launch(self._h, _stream_ptr(stream), ctas))
+
+    def close(self) -> None:
+        if self._h and self._h.value:
+            lib.rr_exec_destroy(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        self.close()
+
+
+class VirtualCluster:
+    """Every device of a plan hosted on one CUDA device.
+
+    Allocates the source shards of the plan's source placement and the
+    destination shards of its destination placement, each zeroed (padding
+    bytes are therefore deterministic)."""
+
+    def __init__(self, plan: ReallocPlan, cuda_device: int = 0):
+        self.plan, self.cuda_device = plan, cuda_device
+        self.src: Dict[int, DeviceBuffer] = {}
+        self.dst: Dict[int, DeviceBuffer] = {}
+        for d in plan.devices(SRC):
+            self.src[d] = DeviceBuffer(cuda_device, plan.shard_bytes(SRC, d))
+            self.src[d].zero()
+        for d in plan.devices(DST):
+            self.dst[d] = DeviceBuffer(cuda_device, plan.shard_bytes(DST, d))
+            self.dst[d].zero()
+        stream_sync()
+
+    def fill_sources(self, seed: int) -> None:
+        for d, b in self.src.items():
+            fill_shard(self.plan, SRC, d, b.ptr, seed)
+
+    def executor(self, mode: int = PUSH, chunk_bytes: int = 0) -> Executor:
+        devs = sorted(set(self.src) | set(self.dst))
+        return Executor(self.plan, self.cuda_device, {d: b.ptr for d, b in self.src.items()},
+                        {d: b.ptr for d, b in self.dst.items()}, devs, mode, chunk_bytes)
+
+    def verify_destinations(self, seed: int) -> Dict[int, Tuple[int, int]]:
+        return {d: verify_shard(self.plan, DST, d, b.ptr, seed) for d, b in self.dst.items()}
+
+    def free(self) -> None:
+        for b in list(self.src.values()) + list(self.dst.values()):
+            b.free()
+
+
+class Barrier:
+    """Cross-GPU barrier for one-process-per-GPU runs (rr_barrier_*).
+
+    Each rank owns a `world`-entry uint32 flag array; rank r's launch stores
+    the epoch into every peer's slot r (st.release.sys) and waits until all
+    its own slots reach the epoch (ld.acquire.sys, bounded spin)."""
+
+    def __init__(self, cuda_device: int, rank: int, world: int, flag_ptrs: Sequence[int]):
+        arr = (ctypes.c_void_p * world)(*flag_ptrs)
+        h = ctypes.c_void_p()
+        check(lib.rr_barrier_create(cuda_device, rank, world, arr, ctypes.byref(h)))
+        self._h = h
+
+    def launch(self, stream=None) -> None:
+        check(lib.rr_barrier_launch(self._h, _stream_ptr(stream)))
+
+    def timed_out(self) -> bool:
+        out = ctypes.c_int()
+        check(lib.rr_barrier_status(self._h, ctypes.byref(out)))
+        return bool(out.value)
+
+    def close(self) -> None:
+        if self._h and self._h.value:
+            lib.rr_barrier_destroy(self._h)
+            self._h = ctypes.c_void_p(0)
+
+
+def open_ipc(cuda_device: int, handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    check(lib.rr_ipc_open(cuda_device, handle, ctypes.byref(p)))
+    return p.value
+
+
+def close_ipc(ptr: int) -> None:
+    lib.rr_ipc_close(ptr)
+
+
+def hosted_devices(n_plan_devices: int, rank: int, world: int) -> List[int]:
+    """Contiguous block of plan devices hosted by `rank` (world | n)."""
+    if n_plan_devices % world:
+        raise ValueError(f"{world} ranks cannot evenly host {n_plan_devices} plan devices")
+    k = n_plan_devices // world
+    return list(range(rank * k, (rank + 1) * k))
+
+
+class RankRealloc:
+    """One rank of a one-process-per-GPU reallocation.
+
+    ``plans`` is a sequence of phases (e.g. train->gen, then gen->train); all
+    use the same cluster devices. Each phase gets its own executor; phase i's
+    destination shards must be phase i+1's source shards when chained, which
+    the caller expresses through ``shards``: a dict name -> (plan index, side)
+    telling which buffers to allocate, and ``bind``: per phase the (src name,
+    dst name). Buffers of remote hosts are mapped through CUDA IPC; a barrier
+    runs after every phase so the next phase reads completed shards.
+    """
+
+    def __init__(self, plans: Sequence[ReallocPlan], shards: Dict[str, Tuple[int, int]],
+                 bind: Sequence[Tuple[str, str]], rank: int, world: int, cuda_device: int, group=None,
+                 mode: int = PUSH):
+        self.plans, self.rank, self.world, self.cuda_device = list(plans), rank, world, cuda_device
+        n = plans[0].cluster.device_count()
+        self.local = hosted_devices(n, rank, world)
+        self.owner = {d: d // (n // world) for d in range(n)}
+        self.buffers: Dict[str, Dict[int, DeviceBuffer]] = {}
+        for name, (pi, side) in shards.items():
+            p = self.plans[pi]
+            bufs = {}
+            for d in p.devices(side):
+                if d in self.local:
+                    bufs[d] = DeviceBuffer(cuda_device, p.shard_bytes(side, d))
+                    bufs[d].zero()
+            self.buffers[name] = bufs
+        stream_sync()
+        # Exchange IPC handles of every local shard (and the barrier flags).
+        self.flags = DeviceBuffer(cuda_device, 4 * max(world, 64))
+        self.flags.zero()
+        stream_sync()
+        mine: dict = {}
+        if world > 1:
+            mine = {name: {d: b.ipc_handle() for d, b in bufs.items()} for name, bufs in self.buffers.items()}
+            mine["__flags__"] = {rank: self.flags.ipc_handle()}
+        gathered: List[dict] = [None] * world  # type: ignore
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_gather_object(gathered, mine, group=group)
+        else:
+            gathered[0] = mine
+        self.ptrs: Dict[str, Dict[int, int]] = {name: {d: b.ptr for d, b in bufs.items()}
+                                                 for name, bufs in self.buffers.items()}
+        self._opened: List[int] = []
+        flag_ptrs = [0] * world
+        flag_ptrs[rank] = self.flags.ptr
+        for r, table in enumerate(gathered):
+            if r == rank:
+                continue
+            for name, handles in table.items():
+                for d, h in handles.items():
+                    p = open_ipc(cuda_device, h)
+                    self._opened.append(p)
+                    if name == "__flags__":
+                        flag_ptrs[r] = p
+                    else:
+                        self.ptrs[name][d] = p
+        self.barrier = Barrier(cuda_device, rank, world, flag_ptrs)
+        self.executors: List[Executor] = []
+        for pi, (sname, dname) in enumerate(bind):
+            self.executors.append(Executor(self.plans[pi], cuda_device, self.ptrs[sname], self.ptrs[dname],
+                                           self.local, mode))
+
+    def run_phase(self, i: int, stream=None, ctas: int = 0) -> None:
+        self.executors[i].launch(stream, ctas)
+        if self.world > 1:
+            self.barrier.launch(stream)
+
+    def close(self) -> None:
+        for e in self.executors:
+            e.close()
+        self.barrier.close()
+        for p in self._opened:
+            close_ipc(p)
+        for bufs in self.buffers.values():
+            for b in bufs.values():
+                b.free()
+        self.flags.free()

@@ -1,0 +1,75 @@
+"""Named reallocation workloads: the BASELINE.json configs as placements.
+
+Each workload is a list of phases (src placement -> dst placement) over the
+same plan devices; a bench "step" runs every phase once. Placements are
+written (pp, dp, tp) as in BASELINE.json.
+"""
+from __future__ import annotations
+
+import dataclasses
+from dataclasses import dataclass
+from typing import Dict, List, Tuple
+
+from .rlplan import (BALANCED, GATE_UP_CONCAT, GATE_UP_SEPARATE, MODELS, QKV_CONCAT, QKV_GROUPED,
+                     QKV_SEPARATE, ClusterSpec, DeviceMesh, ModelSpec, ParallelStrategy, Placement,
+                     b200_cluster)
+
+
+def layout(devices: int, pp: int, dp: int, tp: int, qkv: int = QKV_SEPARATE,
+           gate_up: int = GATE_UP_SEPARATE) -> Placement:
+    return Placement(DeviceMesh(0, 1, 0, devices), ParallelStrategy(dp=dp, tp=tp, pp=pp), qkv, gate_up)
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    description: str
+    model: ModelSpec
+    devices: int                      # plan devices (hosted on 1..devices GPUs)
+    phases: Tuple[Tuple[Placement, Placement], ...]
+
+    def cluster(self) -> ClusterSpec:
+        return b200_cluster(self.devices)
+
+
+def _pp(p: Placement) -> str:
+    s = p.strategy
+    return f"(pp{s.pp},dp{s.dp},tp{s.tp})"
+
+
+def _make(name: str, model: str, devices: int, src: Placement, dst: Placement, back: bool,
+          desc: str) -> Workload:
+    phases = ((src, dst), (dst, src)) if back else ((src, dst),)
+    return Workload(name, desc, MODELS[model], devices, phases)
+
+
+WORKLOADS: Dict[str, Workload] = {}
+
+
+def _register(w: Workload) -> None:
+    WORKLOADS[w.name] = w
+
+
+# BASELINE.json configs[0]: the CPU oracle case.
+_register(_make("tiny_tp2_to_dp2", "tiny", 2, layout(2, 1, 1, 2), layout(2, 1, 2, 1), False,
+                "tiny LLaMA (4L, h256) (pp1,dp1,tp2)->(pp1,dp2,tp1) on 2 devices"))
+# BASELINE.json configs[1]: actor train layout -> generation layout and back.
+_register(_make("llama7b_tp8_dp8_roundtrip", "llama7b", 8, layout(8, 1, 1, 8), layout(8, 1, 8, 1), True,
+                "LLaMA-7B bf16 train (pp1,dp1,tp8) -> gen (pp1,dp8,tp1) and back, 8 plan devices"))
+# BASELINE.json configs[2]: pipeline-stage remap.
+_register(_make("llama13b_pp2tp4_to_dp2tp4", "llama13b", 8, layout(8, 2, 1, 4), layout(8, 1, 2, 4), False,
+                "LLaMA-13B bf16 (pp2,dp1,tp4)->(pp1,dp2,tp4)"))
+# BASELINE.json configs[3]: critic with Megatron-grouped QKV / fused gate-up -> concat layouts.
+_register(_make("llama34b_critic_pp4tp2_to_tp8", "llama34b_critic", 8,
+                layout(8, 4, 1, 2, QKV_GROUPED, GATE_UP_CONCAT), layout(8, 1, 1, 8, QKV_CONCAT, GATE_UP_CONCAT),
+                False, "LLaMA-34B critic bf16 (pp4,dp1,tp2)->(pp1,dp1,tp8), fused QKV/gate-up reinterleave"))
+# BASELINE.json configs[4]: full-box 70B.
+_register(_make("llama70b_pp2tp4_to_tp8", "llama70b", 8, layout(8, 2, 1, 4), layout(8, 1, 1, 8), False,
+                "LLaMA-70B bf16 (pp2,dp1,tp4)->(pp1,dp1,tp8)"))
+
+
+def truncated(w: Workload, layers: int) -> Workload:
+    """Same shapes and layouts with fewer decoder layers (bounded samples)."""
+    m = dataclasses.replace(w.model, num_layers=layers)
+    return Workload(f"{w.name}[{layers}L]", w.description + f", truncated to {layers} layers", m, w.devices,
+                    w.phases)

@@ -1,0 +1,63 @@
+"""Shared test helpers: placements for the BASELINE configs, op conversion,
+and a numpy emulation of the product's lowered copy rectangles."""
+from __future__ import annotations
+
+import dataclasses
+from typing import Dict, List, Optional, Tuple
+
+import numpy as np
+
+from paper_2406_14088_b200.rlplan import (MODELS, DeviceMesh, ParallelStrategy, Placement, b200_cluster)
+
+
+def mesh(gpus: int, offset: int = 0) -> DeviceMesh:
+    return DeviceMesh(0, 1, offset, gpus)
+
+
+def placement(gpus: int, pp: int, dp: int, tp: int, offset: int = 0, qkv: int = 0, gate_up: int = 0) -> Placement:
+    """(pp, dp, tp) order as written in BASELINE.json configs."""
+    return Placement(mesh(gpus, offset), ParallelStrategy(dp=dp, tp=tp, pp=pp), qkv, gate_up)
+
+
+def op_tuple(op) -> tuple:
+    p = op.payload
+    return (op.src, tuple(op.dst), (p.layer_start, p.layer_end, p.tp_rank, p.tp_degree, p.replicated), op.bytes)
+
+
+def scaled(name: str, layers: Optional[int] = None, vocab: Optional[int] = None):
+    m = MODELS[name]
+    kw = {}
+    if layers is not None:
+        kw["num_layers"] = layers
+    if vocab is not None:
+        kw["vocab_size"] = vocab
+    return dataclasses.replace(m, **kw) if kw else m
+
+
+# BASELINE.json configs (pp, dp, tp) -> (pp, dp, tp), with layouts.
+BASELINE_CONFIGS = {
+    "tiny_tp2_to_dp2": ("tiny", 2, (1, 1, 2, 0, 0), (1, 2, 1, 0, 0)),
+    "7b_tp8_to_dp8": ("llama7b", 8, (1, 1, 8, 0, 0), (1, 8, 1, 0, 0)),
+    "7b_dp8_to_tp8": ("llama7b", 8, (1, 8, 1, 0, 0), (1, 1, 8, 0, 0)),
+    "13b_pp2tp4_to_dp2tp4": ("llama13b", 8, (2, 1, 4, 0, 0), (1, 2, 4, 0, 0)),
+    "34b_pp4tp2_to_tp8_fused": ("llama34b_critic", 8, (4, 1, 2, 2, 1), (1, 1, 8, 1, 1)),
+    "70b_pp2tp4_to_tp8": ("llama70b", 8, (2, 1, 4, 0, 0), (1, 1, 8, 0, 0)),
+}
+
+
+def config_placements(key: str):
+    name, gpus, s, d = BASELINE_CONFIGS[key]
+    src = placement(gpus, s[0], s[1], s[2], qkv=s[3], gate_up=s[4])
+    dst = placement(gpus, d[0], d[1], d[2], qkv=d[3], gate_up=d[4])
+    return MODELS[name], src, dst, b200_cluster(gpus)
+
+
+def emulate_lowered(plan, src_bufs: Dict[int, np.ndarray], dst_bufs: Dict[int, np.ndarray]) -> None:
+    """Apply the product's lowered rectangles with numpy (uint8 views)."""
+    for s, dsts, rects in plan.lowered():
+        sb = src_bufs[s].view(np.uint8)
+        for d in dsts:
+            db = dst_bufs[d].view(np.uint8)
+            for (so, do, rb, sp, dp, rows) in rects:
+                for r in range(rows):
+                    db[do + r * dp: do + r * dp + rb] = sb[so + r * sp: so + r * sp + rb]
