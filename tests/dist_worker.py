@@ -1,0 +1,98 @@
+"""Multi-process GPU parity worker (launched by tests/test_multigpu.py via
+torchrun, one process per GPU). Each rank hosts a contiguous block of the 8
+plan devices; destination shards of remote ranks are reached through CUDA
+IPC and written by NVLink peer stores. Every rank compares its hosted
+destination shards with the CPU oracle and the results are all-reduced."""
+from __future__ import annotations
+
+import dataclasses
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from _helpers import placement  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from paper_2406_14088_b200 import runtime as R  # noqa: E402
+from paper_2406_14088_b200.rlplan import BALANCED, MODELS, b200_cluster, plan_param_realloc  # noqa: E402
+from paper_2406_14088_b200.workloads import WORKLOADS  # noqa: E402
+
+TINY_GQA = dataclasses.replace(MODELS["tiny"], name="tiny_gqa", hidden_size=512, num_attention_heads=16,
+                               num_kv_heads=8, intermediate_size=1024)
+
+CASES = [
+    ((1, 1, 8, 0, 0), (1, 8, 1, 0, 0)),
+    ((4, 1, 2, 2, 1), (1, 1, 8, 1, 1)),
+    ((2, 1, 4, 0, 0), (1, 1, 8, 0, 0)),
+    ((2, 1, 4, 0, 0), (1, 2, 4, 0, 0)),
+    ((1, 8, 1, 2, 1), (4, 1, 2, 0, 0)),
+]
+
+
+def main() -> int:
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = b200_cluster(8)
+    failures = []
+    for mode in (R.PUSH, R.PULL):
+        for sp, dp in CASES:
+            src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
+            dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
+            plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
+            rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
+                               mode=mode)
+            for d, b in rr.buffers["a"].items():
+                R.fill_shard(plan, R.SRC, d, b.ptr, 21)
+            torch.cuda.synchronize()
+            dist.barrier()
+            rr.run_phase(0)
+            torch.cuda.synchronize()
+            if rr.barrier.timed_out():
+                failures.append(f"{sp}->{dp} mode {mode}: barrier timed out")
+            for d, b in rr.buffers["b"].items():
+                got = b.to_host()
+                want = O.fill(TINY_GQA, dst, c, d, 21)
+                if not np.array_equal(got, want):
+                    failures.append(f"{sp}->{dp} mode {mode}: device {d} differs in "
+                                    f"{int(np.count_nonzero(got != want))} elements")
+            dist.barrier()
+            rr.close()
+    if os.environ.get("RR_FULL_7B") == "1":
+        w = WORKLOADS["llama7b_tp8_dp8_roundtrip"]
+        plans = [plan_param_realloc(w.model, s, d, c, BALANCED) for (s, d) in w.phases]
+        rr = R.RankRealloc(plans, {"train": (0, R.SRC), "gen": (0, R.DST)}, [("train", "gen"), ("gen", "train")],
+                           rank, world, local)
+        for d, b in rr.buffers["train"].items():
+            R.fill_shard(plans[0], R.SRC, d, b.ptr, 4)
+        torch.cuda.synchronize()
+        dist.barrier()
+        for _ in range(2):
+            rr.run_phase(0)
+            rr.run_phase(1)
+        torch.cuda.synchronize()
+        for name, p in (("gen", plans[0]), ("train", plans[1])):
+            for d, b in rr.buffers[name].items():
+                bad, first = R.verify_shard(p, R.DST, d, b.ptr, 4)
+                if bad:
+                    failures.append(f"7B {name} shard {d}: {bad} mismatches (first {first})")
+        dist.barrier()
+        rr.close()
+    flag = torch.tensor([len(failures)], device="cuda")
+    dist.all_reduce(flag)
+    for f in failures:
+        print(f"rank {rank}: {f}", flush=True)
+    if rank == 0:
+        print(f"dist_worker world={world}: {'OK' if flag.item() == 0 else 'FAILED'}", flush=True)
+    dist.destroy_process_group()
+    return 0 if flag.item() == 0 else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

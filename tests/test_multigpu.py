@@ -1,0 +1,37 @@
+"""One process per GPU (torchrun): NVLink peer-store / peer-load reallocation
+across real GPUs, bit-exact against the CPU oracle (tests/dist_worker.py)."""
+from __future__ import annotations
+
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _torchrun(n: int, env_extra=None, timeout=900):
+    env = dict(os.environ)
+    env.update(env_extra or {})
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "dist_worker.py")]
+    return subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_cross_gpu_bitexact(n_gpus, world):
+    if n_gpus < world:
+        pytest.skip(f"needs {world} GPUs, have {n_gpus}")
+    r = _torchrun(world, {"RR_FULL_7B": "1"})
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    assert f"dist_worker world={world}: OK" in r.stdout
