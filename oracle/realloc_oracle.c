@@ -106,7 +106,16 @@ static int rank_of(const orc_placement* p, const orc_cluster* c, int d, int* pp,
   return -1;
 }
 
-static int placement_ok(const orc_model* m, const orc_placement* p) {
+/* Mesh shape rules of reference cluster.cpp:43-61, placement rules of
+ * SPEC.md:261/268 and the layout codes of DESIGN.md §3. */
+static int placement_ok(const orc_model* m, const orc_placement* p, const orc_cluster* c) {
+  const int M = c->gpus_per_node;
+  if (p->node_count < 1 || p->gpu_count < 1 || p->node_offset < 0 || p->gpu_offset < 0) return 0;
+  if (p->node_offset + p->node_count > c->n_nodes || p->gpu_offset + p->gpu_count > M) return 0;
+  if (p->gpu_count == M ? p->gpu_offset != 0
+                        : (p->node_count != 1 || M % p->gpu_count || p->gpu_offset % p->gpu_count))
+    return 0;
+  if (p->qkv_layout < 0 || p->qkv_layout > 2 || p->gate_up_layout < 0 || p->gate_up_layout > 1) return 0;
   if (p->dp < 1 || p->tp < 1 || p->pp < 1) return 0;
   if (p->dp * p->tp * p->pp != mesh_size(p)) return 0;
   if (p->pp > m->layers || (p->tp & (p->tp - 1)) || m->heads % p->tp) return 0;
@@ -188,7 +197,7 @@ static int cmp_int(const void* a, const void* b) { return *(const int*)a - *(con
 int orc_plan(const orc_model* m, const orc_placement* src, const orc_placement* dst,
              const orc_cluster* c, int policy, orc_op* ops, int cap, int* n_ops, orc_op* local,
              int cap_local, int* n_local, int64_t* total_bytes, double* est_time) {
-  if (!placement_ok(m, src) || !placement_ok(m, dst)) return -1;
+  if (!placement_ok(m, src, c) || !placement_ok(m, dst, c)) return -1;
   const int G = (int)(src->tp / gcd64(src->tp, dst->tp) * dst->tp);
   for (int64_t id = 0; id < n_tensors(m); ++id) {
     const tensor_shape s = shape_of(m, id);
