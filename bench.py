@@ -188,6 +188,9 @@ def run_b200(args) -> None:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     w = WORKLOADS[args.workload]
+    if args.layers:
+        from paper_2406_14088_b200.workloads import truncated
+        w = truncated(w, args.layers)
     c = w.cluster()
     policy = BALANCED if args.policy == "balanced" else SPEC
     plans = [plan_param_realloc(w.model, s, d, c, policy) for (s, d) in w.phases]
@@ -202,7 +205,8 @@ def run_b200(args) -> None:
         src_name = "train" if i == 0 else bind[-1][1]
         bind.append((src_name, dst_name))
     mode = R.PUSH if args.mode == "push" else R.PULL
-    rr = R.RankRealloc(plans, shards, bind, rank, world, local_rank, mode=mode)
+    kernel = R.DEFAULT_KERNEL if args.kernel < 0 else args.kernel
+    rr = R.RankRealloc(plans, shards, bind, rank, world, local_rank, mode=mode, kernel=kernel)
     stream = torch.cuda.current_stream()
     seed = 1
     for d, b in rr.buffers["train"].items():
@@ -401,13 +405,15 @@ def profile_traffic(workload: str):
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", default="llama7b_tp8_dp8_roundtrip")
     ap.add_argument("--policy", choices=["balanced", "spec"], default="balanced")
     ap.add_argument("--mode", choices=["push", "pull"], default="push")
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--layers", type=int, default=0, help="truncate the model (profiling only)")
+    ap.add_argument("--kernel", type=int, default=-1, help="copy engine: 0 LDG/STG, 1..5 TMA bulk (-1 default)")
     ap.add_argument("--cpu-layers", type=int, default=2)
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=3)

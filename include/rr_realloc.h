@@ -198,6 +198,10 @@ rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices,
                          const int32_t* local, int mode, int64_t chunk_bytes, rr_exec** out);
 /* ctas = 0 picks 148 x resident CTAs. */
 rr_status rr_exec_launch(rr_exec* ex, void* stream, int ctas);
+/* Copy engine: 0 = vectorised LDG/STG kernel; 1..5 = TMA bulk-copy ring
+ * (cp.async.bulk through shared memory; 2-byte-aligned items still take the
+ * LDG/STG kernel). */
+rr_status rr_exec_set_kernel(rr_exec* ex, int kernel);
 /* items, bytes moved per launch (sum over destinations), bytes read. */
 rr_status rr_exec_stats(const rr_exec* ex, int64_t* items, int64_t* bytes_written, int64_t* bytes_read);
 void rr_exec_destroy(rr_exec* ex);

@@ -103,6 +103,7 @@ _SIGNATURES = {
     "rr_exec_create": (c_int, [_P, c_int, c_int, POINTER(_P), POINTER(_P), c_int, POINTER(c_int32), c_int,
                                c_int64, POINTER(_P)]),
     "rr_exec_launch": (c_int, [_P, _P, c_int]),
+    "rr_exec_set_kernel": (c_int, [_P, c_int]),
     "rr_exec_stats": (c_int, [_P, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
     "rr_exec_destroy": (None, [_P]),
     "rr_fill_shard": (c_int, [_P, c_int, c_int32, _P, c_uint64, _P]),

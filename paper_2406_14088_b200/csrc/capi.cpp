@@ -146,10 +146,16 @@ struct rr_plan {
 
 struct rr_exec {
   int cuda_device = 0;
-  rr::CopyItem* d_items = nullptr;
+  rr::CopyItem* d_items = nullptr;  // 16-byte (vec) items first, then 2-byte items
   int n_items = 0;
+  int n_vec = 0;
   int fence_sys = 0;
   int default_ctas = 0;
+  // 0 = LDG/STG rr_copy_kernel, 1..kBulkVariants = TMA bulk ring. Default:
+  // variant 1 (4 x 16 KiB stages, 3 CTAs/SM), the fastest in the r01 sweep.
+  int kernel = 1;
+  int bulk_ctas = 0;
+  unsigned int* d_sched = nullptr;  // dynamic work counter (see retire_cta)
   int64_t bytes_written = 0, bytes_read = 0;
 };
 
@@ -645,18 +651,25 @@ rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, vo
     }
     // Interleave the per-op streams round-robin so concurrently running CTAs
     // spread their stores over many destinations (NVLink ingress balance).
-    std::vector<rr::CopyItem> items;
+    // 16-byte items first (both kernels), then 2-byte items (LDG/STG only).
+    std::vector<rr::CopyItem> items, elem_items;
     size_t total = 0;
     for (const auto& s : b.streams) total += s.size();
     items.reserve(total);
-    for (size_t k = 0; items.size() < total; ++k)
+    for (size_t k = 0, seen = 0; seen < total; ++k)
       for (const auto& s : b.streams)
-        if (k < s.size()) items.push_back(s[k]);
+        if (k < s.size()) {
+          (s[k].vec ? items : elem_items).push_back(s[k]);
+          ++seen;
+        }
+    const size_t n_vec = items.size();
+    items.insert(items.end(), elem_items.begin(), elem_items.end());
     need(items.size() < (size_t{1} << 31), "too many copy items");
 
     auto ex = std::make_unique<rr_exec>();
     ex->cuda_device = cuda_device;
     ex->n_items = static_cast<int>(items.size());
+    ex->n_vec = static_cast<int>(n_vec);
     ex->fence_sys = remote ? 1 : 0;
     ex->bytes_written = b.written;
     ex->bytes_read = b.read;
@@ -669,6 +682,9 @@ rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, vo
       check_cuda(cudaMalloc(&ex->d_items, bytes), "cudaMalloc(items)");
       check_cuda(cudaMemcpy(ex->d_items, items.data(), bytes, cudaMemcpyHostToDevice), "upload items");
     }
+    check_cuda(cudaMalloc(&ex->d_sched, 2 * sizeof(unsigned int)), "cudaMalloc(sched)");
+    check_cuda(cudaMemset(ex->d_sched, 0, 2 * sizeof(unsigned int)), "cudaMemset(sched)");
+    check_cuda(rr::launch_bulk(1, nullptr, 0, 0, 0, nullptr, &ex->bulk_ctas, nullptr), "bulk occupancy");
     *out = ex.release();
   });
 }
@@ -677,9 +693,31 @@ rr_status rr_exec_launch(rr_exec* ex, void* stream, int ctas) {
   return guarded([&] {
     need(ex != nullptr, "null executor");
     check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
-    check_cuda(rr::launch_copy(ex->d_items, ex->n_items, ctas > 0 ? ctas : ex->default_ctas,
-                               ex->fence_sys, stream),
-               "rr_copy_kernel launch");
+    if (ex->kernel == 0) {
+      check_cuda(rr::launch_copy(ex->d_items, ex->n_items, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys,
+                                 stream, ex->d_sched),
+                 "rr_copy_kernel launch");
+      return;
+    }
+    check_cuda(rr::launch_bulk(ex->kernel, ex->d_items, ex->n_vec, ctas > 0 ? ctas : ex->bulk_ctas,
+                               ex->fence_sys, stream, nullptr, ex->d_sched),
+               "rr_bulk_kernel launch");
+    if (ex->n_items > ex->n_vec)
+      check_cuda(rr::launch_copy(ex->d_items + ex->n_vec, ex->n_items - ex->n_vec, ex->default_ctas,
+                                 ex->fence_sys, stream, ex->d_sched),
+                 "rr_copy_kernel launch (2-byte items)");
+  });
+}
+
+rr_status rr_exec_set_kernel(rr_exec* ex, int kernel) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    need(kernel >= 0 && kernel <= rr::kBulkVariants, "unknown copy kernel");
+    ex->kernel = kernel;
+    if (kernel > 0) {
+      check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+      check_cuda(rr::launch_bulk(kernel, nullptr, 0, 0, 0, nullptr, &ex->bulk_ctas, nullptr), "bulk occupancy");
+    }
   });
 }
 
@@ -694,10 +732,9 @@ rr_status rr_exec_stats(const rr_exec* ex, int64_t* items, int64_t* written, int
 
 void rr_exec_destroy(rr_exec* ex) {
   if (!ex) return;
-  if (ex->d_items) {
-    cudaSetDevice(ex->cuda_device);
-    cudaFree(ex->d_items);
-  }
+  cudaSetDevice(ex->cuda_device);
+  if (ex->d_items) cudaFree(ex->d_items);
+  if (ex->d_sched) cudaFree(ex->d_sched);
   delete ex;
 }
 

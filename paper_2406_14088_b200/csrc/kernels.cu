@@ -90,12 +90,29 @@ __device__ __forceinline__ void copy_elem_item(const CopyItem& it, const uint64_
   }
 }
 
+// Dynamic work distribution: sched[0] is the next item, sched[1] counts
+// CTAs that ran out of work; the last one resets both for the next launch.
+__device__ __forceinline__ int grab_item(unsigned int* sched) { return static_cast<int>(atomicAdd(sched, 1u)); }
+
+__device__ __forceinline__ void retire_cta(unsigned int* sched) {
+  __threadfence();
+  if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
+    atomicExch(sched, 0u);
+    atomicExch(sched + 1, 0u);
+  }
+}
+
 __global__ void __launch_bounds__(kCopyThreads) rr_copy_kernel(const CopyItem* __restrict__ items,
-                                                               int n_items, int fence_sys) {
+                                                               int n_items, int fence_sys, unsigned int* sched) {
   __shared__ CopyItem sh;
+  __shared__ int cur;
   constexpr int kWords = sizeof(CopyItem) / 16;
-  for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+  for (;;) {
     __syncthreads();
+    if (threadIdx.x == 0) cur = grab_item(sched);
+    __syncthreads();
+    const int i = cur;
+    if (i >= n_items) break;
     if (threadIdx.x < kWords)
       reinterpret_cast<int4*>(&sh)[threadIdx.x] = reinterpret_cast<const int4*>(items + i)[threadIdx.x];
     __syncthreads();
@@ -116,6 +133,204 @@ __global__ void __launch_bounds__(kCopyThreads) rr_copy_kernel(const CopyItem* _
   // Peer stores must be visible system-wide before a later barrier releases
   // them to the destination GPU.
   if (fence_sys) __threadfence_system();
+  if (threadIdx.x == 0) retire_cta(sched);
+}
+
+// ---------------------------------------------------------------------------
+// rr_bulk_kernel: the same work items, moved by the TMA engine. One elected
+// thread per CTA streams pieces of each item through a ring of shared-memory
+// stages: cp.async.bulk global->shared completes on a per-stage mbarrier,
+// then one cp.async.bulk shared->global per destination (per row when the
+// destination is strided) drains the stage. No data passes through
+// registers, so one thread keeps ~S stages of loads and stores in flight.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// L2 policies for the bulk copies: 0 = default, otherwise a createpolicy value.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar,
+                                          uint64_t policy) {
+  if (policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_addr(smem_dst)),
+        "l"(gmem_src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(smem_dst)),
+        "l"(gmem_src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void bulk_store(void* gmem_dst, const void* smem_src, uint32_t bytes, uint64_t policy) {
+  if (policy) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gmem_dst),
+                 "r"(smem_addr(smem_src)), "r"(bytes), "l"(policy)
+                 : "memory");
+  } else {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst),
+                 "r"(smem_addr(smem_src)), "r"(bytes)
+                 : "memory");
+  }
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// One piece = up to `rows` rows of `row_bytes` (all 16-byte multiples).
+struct Piece {
+  uint64_t src;
+  uint32_t rows, row_bytes, src_pitch, dst_pitch;  // bytes
+  uint64_t dst_off;                                 // byte offset added to every dst base
+  int item;
+};
+
+// Walks this CTA's items (blockIdx.x, +gridDim.x, ...) in pieces of at most
+// `cap` bytes.
+struct PieceCursor {
+  int item;
+  uint32_t row, col;  // next row; next column byte offset inside the row
+};
+
+__device__ __forceinline__ bool next_piece(const CopyItem* __restrict__ items, int n_items, PieceCursor& c,
+                                           uint32_t cap, Piece& p, unsigned int* sched) {
+  while (c.item < n_items) {
+    const CopyItem& it = items[c.item];
+    const uint32_t row_bytes = it.row_units * 16u;
+    const uint32_t sp = it.src_pitch * 16u, dp = it.dst_pitch * 16u;
+    if (c.row < it.nrows) {
+      p.item = c.item;
+      if (row_bytes <= cap) {
+        const uint32_t rows = min(it.nrows - c.row, max(1u, cap / row_bytes));
+        p.src = it.src + static_cast<uint64_t>(c.row) * sp;
+        p.dst_off = static_cast<uint64_t>(c.row) * dp;
+        p.rows = rows;
+        p.row_bytes = row_bytes;
+        c.row += rows;
+      } else {
+        const uint32_t cols = min(row_bytes - c.col, cap);
+        p.src = it.src + static_cast<uint64_t>(c.row) * sp + c.col;
+        p.dst_off = static_cast<uint64_t>(c.row) * dp + c.col;
+        p.rows = 1;
+        p.row_bytes = cols;
+        c.col += cols;
+        if (c.col >= row_bytes) {
+          c.col = 0;
+          ++c.row;
+        }
+      }
+      p.src_pitch = sp;
+      p.dst_pitch = dp;
+      return true;
+    }
+    c.item = grab_item(sched);
+    c.row = c.col = 0;
+  }
+  return false;
+}
+
+// HINT bit 0: source reads evict-first in L2; bit 1: destination writes evict-first.
+template <int S, int STAGE, int HINT>
+__global__ void __launch_bounds__(32) rr_bulk_kernel(const CopyItem* __restrict__ items, int n_items,
+                                                     int fence_sys, unsigned int* sched) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[S];
+  __shared__ Piece meta[S];
+  if (threadIdx.x != 0) return;
+  const uint64_t ld_policy = (HINT & 1) ? policy_evict_first() : 0;
+  const uint64_t st_policy = (HINT & 2) ? policy_evict_first() : 0;
+  for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+
+  PieceCursor ld{grab_item(sched), 0, 0};
+  Piece p;
+  auto issue_load = [&](int s) {
+    meta[s] = p;
+    const uint32_t bytes = p.rows * p.row_bytes;
+    mbar_expect_tx(&full[s], bytes);
+    uint8_t* buf = ring + s * STAGE;
+    if (p.rows == 1 || p.src_pitch == p.row_bytes) {
+      bulk_load(buf, reinterpret_cast<const void*>(p.src), bytes, &full[s], ld_policy);
+    } else {
+      for (uint32_t r = 0; r < p.rows; ++r)
+        bulk_load(buf + r * p.row_bytes, reinterpret_cast<const void*>(p.src + static_cast<uint64_t>(r) * p.src_pitch),
+                  p.row_bytes, &full[s], ld_policy);
+    }
+  };
+
+  int issued = 0;
+  while (issued < S && next_piece(items, n_items, ld, STAGE, p, sched)) {
+    issue_load(issued);
+    ++issued;
+  }
+  for (int done = 0; done < issued; ++done) {
+    const int s = done % S;
+    mbar_wait(&full[s], (done / S) & 1);
+    const Piece q = meta[s];
+    const CopyItem& it = items[q.item];
+    const uint8_t* buf = ring + s * STAGE;
+    const int ndst = it.ndst;
+    for (int j = 0; j < ndst; ++j) {
+      uint8_t* dst = reinterpret_cast<uint8_t*>(it.dst[j]) + q.dst_off;
+      if (q.rows == 1 || q.dst_pitch == q.row_bytes) {
+        bulk_store(dst, buf, q.rows * q.row_bytes, st_policy);
+      } else {
+        for (uint32_t r = 0; r < q.rows; ++r)
+          bulk_store(dst + static_cast<uint64_t>(r) * q.dst_pitch, buf + r * q.row_bytes, q.row_bytes, st_policy);
+      }
+    }
+    bulk_commit();
+    if (done >= 1) {
+      // Everything but the group just committed has finished reading its
+      // stage: refill the stage drained in the previous iteration.
+      bulk_wait_read<1>();
+      if (next_piece(items, n_items, ld, STAGE, p, sched)) {
+        issue_load((done - 1) % S);
+        ++issued;
+      }
+    }
+  }
+  bulk_wait_all();
+  if (fence_sys) __threadfence_system();
+  retire_cta(sched);
 }
 
 __global__ void rr_fill_kernel(const FillItem* __restrict__ items, int n_items, uint64_t seed) {
@@ -195,11 +410,55 @@ int copy_max_ctas(int* ctas_per_sm, int* sms) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, rr_copy_kernel, kCopyThreads, 0);
 }
 
-int launch_copy(const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream) {
+int launch_copy(const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream, unsigned int* sched) {
   if (n_items <= 0) return cudaSuccess;
   if (ctas > n_items) ctas = n_items;
-  rr_copy_kernel<<<ctas, kCopyThreads, 0, static_cast<cudaStream_t>(stream)>>>(items, n_items, fence_sys);
+  rr_copy_kernel<<<ctas, kCopyThreads, 0, static_cast<cudaStream_t>(stream)>>>(items, n_items, fence_sys,
+                                                                                sched);
   return cudaGetLastError();
+}
+
+namespace {
+
+template <int S, int STAGE, int HINT = 0>
+int launch_bulk_t(const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream, int* max_ctas,
+                  unsigned int* sched) {
+  constexpr int kSmem = S * STAGE;
+  cudaError_t e = cudaFuncSetAttribute(rr_bulk_kernel<S, STAGE, HINT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  if (e != cudaSuccess) return e;
+  if (max_ctas) {
+    int dev = 0, sms = 0, per_sm = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rr_bulk_kernel<S, STAGE, HINT>, 32, kSmem);
+    if (e != cudaSuccess) return e;
+    *max_ctas = per_sm * sms;
+    return cudaSuccess;
+  }
+  if (n_items <= 0) return cudaSuccess;
+  if (ctas > n_items) ctas = n_items;
+  rr_bulk_kernel<S, STAGE, HINT><<<ctas, 32, kSmem, static_cast<cudaStream_t>(stream)>>>(items, n_items, fence_sys,
+                                                                                        sched);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int launch_bulk(int variant, const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream,
+                int* max_ctas, unsigned int* sched) {
+  switch (variant) {
+    case 1: return launch_bulk_t<4, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 2: return launch_bulk_t<8, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 3: return launch_bulk_t<4, 32768>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 4: return launch_bulk_t<6, 32768>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 5: return launch_bulk_t<3, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 6: return launch_bulk_t<4, 32768, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 7: return launch_bulk_t<4, 32768, 2>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 8: return launch_bulk_t<4, 32768, 3>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 9: return launch_bulk_t<3, 32768, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 10: return launch_bulk_t<3, 65536, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 int launch_fill(const FillItem* items, int n_items, uint64_t seed, void* stream) {

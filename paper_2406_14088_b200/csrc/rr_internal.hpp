@@ -61,8 +61,14 @@ __host__ __device__ inline uint16_t weight_value(uint64_t seed, uint64_t tensor,
 }
 
 // Host-callable launchers (kernels.cu). All return a cudaError_t as int.
-int launch_copy(const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream);
+// sched: 2 device uints, zero before the first launch (kernels reset them).
+int launch_copy(const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream, unsigned int* sched);
 int copy_max_ctas(int* ctas_per_sm, int* sms);
+// TMA bulk variant (1..kBulkVariants = stage ring shapes / L2 hints); items must all be vec items.
+// With max_ctas != NULL only reports the resident-CTA capacity.
+int launch_bulk(int variant, const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream,
+                int* max_ctas, unsigned int* sched);
+constexpr int kBulkVariants = 10;
 int launch_fill(const FillItem* items, int n_items, uint64_t seed, void* stream);
 int launch_verify(const FillItem* items, int n_items, uint64_t seed, unsigned long long* counters,
                   uint64_t buf_base, void* stream);

@@ -28,6 +28,9 @@ from .rlplan import ReallocPlan
 
 PUSH, PULL = 0, 1
 SRC, DST = 0, 1
+# Copy engine used unless a caller picks one (rr_exec_set_kernel): the TMA
+# bulk ring, 4 x 16 KiB stages, 3 CTAs per SM (profiles/r01_sweep_kernels.txt).
+DEFAULT_KERNEL = 1
 
 
 def _stream_ptr(stream) -> Optional[int]:
@@ -149,6 +152,10 @@ class Executor:
     def launch(self, stream=None, ctas: int = 0) -> None:
         check(lib.rr_exec_launch(self._h, _stream_ptr(stream), ctas))
 
+    def set_kernel(self, kernel: int) -> None:
+        """0 = LDG/STG kernel, 1..5 = TMA bulk-copy ring variants."""
+        check(lib.rr_exec_set_kernel(self._h, kernel))
+
     def close(self) -> None:
         if self._h and self._h.value:
             lib.rr_exec_destroy(self._h)
@@ -181,10 +188,12 @@ class VirtualCluster:
         for d, b in self.src.items():
             fill_shard(self.plan, SRC, d, b.ptr, seed)
 
-    def executor(self, mode: int = PUSH, chunk_bytes: int = 0) -> Executor:
+    def executor(self, mode: int = PUSH, chunk_bytes: int = 0, kernel: int = DEFAULT_KERNEL) -> Executor:
         devs = sorted(set(self.src) | set(self.dst))
-        return Executor(self.plan, self.cuda_device, {d: b.ptr for d, b in self.src.items()},
-                        {d: b.ptr for d, b in self.dst.items()}, devs, mode, chunk_bytes)
+        ex = Executor(self.plan, self.cuda_device, {d: b.ptr for d, b in self.src.items()},
+                      {d: b.ptr for d, b in self.dst.items()}, devs, mode, chunk_bytes)
+        ex.set_kernel(kernel)
+        return ex
 
     def verify_destinations(self, seed: int) -> Dict[int, Tuple[int, int]]:
         return {d: verify_shard(self.plan, DST, d, b.ptr, seed) for d, b in self.dst.items()}
@@ -253,7 +262,7 @@ class RankRealloc:
 
     def __init__(self, plans: Sequence[ReallocPlan], shards: Dict[str, Tuple[int, int]],
                  bind: Sequence[Tuple[str, str]], rank: int, world: int, cuda_device: int, group=None,
-                 mode: int = PUSH):
+                 mode: int = PUSH, kernel: int = DEFAULT_KERNEL):
         self.plans, self.rank, self.world, self.cuda_device = list(plans), rank, world, cuda_device
         n = plans[0].cluster.device_count()
         self.local = hosted_devices(n, rank, world)
@@ -303,6 +312,11 @@ class RankRealloc:
         for pi, (sname, dname) in enumerate(bind):
             self.executors.append(Executor(self.plans[pi], cuda_device, self.ptrs[sname], self.ptrs[dname],
                                            self.local, mode))
+            self.executors[-1].set_kernel(kernel)
+
+    def set_kernel(self, kernel: int) -> None:
+        for e in self.executors:
+            e.set_kernel(kernel)
 
     def run_phase(self, i: int, stream=None, ctas: int = 0) -> None:
         self.executors[i].launch(stream, ctas)

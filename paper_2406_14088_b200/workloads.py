@@ -68,6 +68,13 @@ _register(_make("llama70b_pp2tp4_to_tp8", "llama70b", 8, layout(8, 2, 1, 4), lay
                 "LLaMA-70B bf16 (pp2,dp1,tp4)->(pp1,dp1,tp8)"))
 
 
+# Parameter sync of a whole replica to a DP group (disjoint =
+# parameter sync): every op is a contiguous one-to-many broadcast.
+_register(Workload("llama7b_replicate_to_dp8", "LLaMA-7B bf16 (pp1,dp1,tp1) on device 0 -> (pp1,dp8,tp1)",
+                   MODELS["llama7b"], 8,
+                   ((Placement(DeviceMesh(0, 1, 0, 1), ParallelStrategy()), layout(8, 1, 8, 1)),)))
+
+
 def truncated(w: Workload, layers: int) -> Workload:
     """Same shapes and layouts with fewer decoder layers (bounded samples)."""
     m = dataclasses.replace(w.model, num_layers=layers)

@@ -25,7 +25,7 @@ TINY_GQA = dataclasses.replace(MODELS["tiny"], name="tiny_gqa", hidden_size=512,
                                num_kv_heads=8, intermediate_size=1024)
 
 
-def run_virtual(model, src, dst, cluster, policy=BALANCED, mode=R.PUSH, chunk=0, seed=11):
+def run_virtual(model, src, dst, cluster, policy=BALANCED, mode=R.PUSH, chunk=0, seed=11, kernel=0):
     plan = plan_param_realloc(model, src, dst, cluster, policy)
     vc = R.VirtualCluster(plan, 0)
     try:
@@ -33,7 +33,7 @@ def run_virtual(model, src, dst, cluster, policy=BALANCED, mode=R.PUSH, chunk=0,
         # the GPU fill is the oracle's value function, byte for byte
         for d, b in vc.src.items():
             assert np.array_equal(b.to_host(), O.fill(model, src, cluster, d, seed)), f"fill differs on {d}"
-        ex = vc.executor(mode, chunk)
+        ex = vc.executor(mode, chunk, kernel)
         ex.launch()
         R.stream_sync()
         got = {d: b.to_host() for d, b in vc.dst.items()}
@@ -87,22 +87,24 @@ def test_tiny_baseline_config_bitexact(need_gpu):
     ((2, 1, 4, 0, 0), (1, 1, 8, 0, 0)),   # 70B-style pp2 tp4 -> tp8
 ])
 @pytest.mark.parametrize("mode", [R.PUSH, R.PULL])
-def test_reinterleave_bitexact(need_gpu, sp, dp, mode):
+@pytest.mark.parametrize("kernel", [0, 1, 2, 3, 4, 5])
+def test_reinterleave_bitexact(need_gpu, sp, dp, mode, kernel):
     c = b200_cluster(8)
     src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
     dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
     # a small chunk forces row- and column-splitting of the copy items
-    _plan, got = run_virtual(TINY_GQA, src, dst, c, BALANCED, mode, chunk=4096)
+    _plan, got = run_virtual(TINY_GQA, src, dst, c, BALANCED, mode, chunk=4096, kernel=kernel)
     assert_same(got, expected(TINY_GQA, src, dst, c))
 
 
-def test_spec_tiny_unaligned_elements(need_gpu):
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_spec_tiny_unaligned_elements(need_gpu, kernel):
     """SPEC.md:47 tiny spec (h=4): 8-byte rows take the 2-byte element path."""
     m = MODELS["spec_tiny"]
     c = b200_cluster(2)
     src = placement(2, 1, 2, 1)
     dst = placement(2, 1, 1, 2)
-    _plan, got = run_virtual(m, src, dst, c, SPEC)
+    _plan, got = run_virtual(m, src, dst, c, SPEC, kernel=kernel)
     assert_same(got, expected(m, src, dst, c))
 
 
@@ -111,8 +113,9 @@ def test_disjoint_meshes_bitexact(need_gpu):
     c = b200_cluster(8)
     src = placement(4, 1, 4, 1, offset=0)
     dst = placement(4, 1, 1, 4, offset=4)
-    _plan, got = run_virtual(TINY_GQA, src, dst, c, BALANCED)
-    assert_same(got, expected(TINY_GQA, src, dst, c))
+    for kernel in (0, 3):
+        _plan, got = run_virtual(TINY_GQA, src, dst, c, BALANCED, kernel=kernel)
+        assert_same(got, expected(TINY_GQA, src, dst, c))
 
 
 def test_7b_train_gen_roundtrip_full_size(need_gpu):
