@@ -216,6 +216,8 @@ def run_b200(args) -> None:
         dist.barrier()
 
     def step(ev=None):
+        # Same sequence as RankRealloc.run_phase, with events around the
+        # direct-copy kernel of each phase (the dominant launch).
         for i in range(len(plans)):
             if ev is not None:
                 ev[i][0].record(stream)
@@ -224,6 +226,9 @@ def run_b200(args) -> None:
                 ev[i][1].record(stream)
             if world > 1:
                 rr.barrier.launch(stream)
+                if rr.has_fanout[i]:
+                    rr.executors[i].launch_fanout(stream, args.ctas)
+                    rr.barrier.launch(stream)
 
     for _ in range(args.warmup):
         step()
@@ -249,24 +254,13 @@ def run_b200(args) -> None:
                 for i in range(len(plans))]
     timed_out = rr.barrier.timed_out() if world > 1 else False
 
-    # Whole-job bytes: every rank's executor work (sum), delivered = written.
-    written = sum(e.bytes_written for e in rr.executors)
-    read = sum(e.bytes_read for e in rr.executors)
-    wire_in = wire_out = 0
-    for p in plans:
-        for d in rr.local:
-            i_, o_, _l = p.device_traffic(d)
-            # transfers between plan devices hosted on the same GPU are local HBM copies
-            wire_in += i_
-            wire_out += o_
-    local_set = set(rr.local)
-    for p in plans:
-        for s, dsts, rects in p.lowered():
-            b = sum(r[2] * r[5] for r in rects)
-            for d in dsts:
-                if d != s and s in local_set and d in local_set:
-                    wire_in -= b
-                    wire_out -= b
+    # Whole-job bytes: every rank's executor work (sum), delivered = written
+    # (direct copies plus in-host fan-out); link bytes per GPU from the
+    # executors' host-level accounting.
+    written = sum(e.bytes_written + e.fanout_written for e in rr.executors)
+    read = sum(e.bytes_read + e.fanout_read for e in rr.executors)
+    wire_in = sum(e.wire_in for e in rr.executors)
+    wire_out = sum(e.wire_out for e in rr.executors)
     # Dominant phase (longest) roofline on this rank.
     dom = max(range(len(plans)), key=lambda i: phase_ms[i])
     dom_bytes = rr.executors[dom].bytes_read + rr.executors[dom].bytes_written
@@ -380,7 +374,8 @@ def run_b200(args) -> None:
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * len(plans) * (2 if world > 1 else 1),
+            "gpu_launches": args.steps * sum(1 + (1 + 2 * rr.has_fanout[i] if world > 1 else 0)
+                                             for i in range(len(plans))),
             "clocks": clock_info,
             "verified": verified,
         }

@@ -160,10 +160,12 @@ rr_status rr_plan_layout(const rr_plan* plan, int side, int32_t device, int64_t*
 rr_status rr_plan_num_lowered(const rr_plan* plan, int* n);
 rr_status rr_plan_get_lowered(const rr_plan* plan, int index, int32_t* src, int32_t* dst, int* n_dst,
                               int64_t* rects, int64_t cap_rects, int64_t* n_rects);
-/* Work an executor with this `local` set and mode would do (host only, no
- * CUDA): bytes read from sources and bytes stored to destinations. */
-rr_status rr_plan_work(const rr_plan* plan, int n_local, const int32_t* local, int mode,
-                       int64_t* bytes_read, int64_t* bytes_written);
+/* Work an executor driving `local` (with `host_of`, see rr_exec_create)
+ * would do, host only, no CUDA. out6 = {phase-0 bytes read, phase-0 bytes
+ * written, phase-1 bytes read, phase-1 bytes written, bytes entering this
+ * host over links, bytes leaving it}. */
+rr_status rr_plan_work(const rr_plan* plan, int n_local, const int32_t* local, const int32_t* host_of,
+                       int mode, int64_t* out6);
 
 /* ---- device memory and peer mapping (plumbing) ---- */
 rr_status rr_device_count(int* n);
@@ -186,8 +188,12 @@ rr_status rr_enable_peer(int cuda_device, int peer_device);
  * src_bufs / dst_bufs are indexed by global DeviceId (n_devices entries,
  * NULL where unused) and must be addressable from `cuda_device` (local
  * allocations, or IPC-opened / peer-enabled pointers). `local` lists the
- * plan devices whose SMs this executor drives (the virtual devices hosted on
- * cuda_device).
+ * plan devices whose SMs this executor drives (the plan devices hosted on
+ * cuda_device). host_of[d] (NULL = every non-local device is its own host)
+ * names the GPU hosting plan device d: a payload bound for several devices
+ * of one remote host crosses NVLink once, into the lowest-id one (phase 0),
+ * and that host replicates it locally (phase 1, rr_exec_launch_fanout,
+ * after a cross-GPU barrier).
  * mode 0 = PUSH: a local source reads its shard once and stores every
  *          destination copy (local relayout + NVLink peer stores, K1/K2).
  * mode 1 = PULL: a local destination loads from the (possibly remote)
@@ -195,15 +201,21 @@ rr_status rr_enable_peer(int cuda_device, int peer_device);
  * chunk_bytes: work-item granularity (0 = default 256 KiB). */
 rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices,
                          void* const* src_bufs, void* const* dst_bufs, int n_local,
-                         const int32_t* local, int mode, int64_t chunk_bytes, rr_exec** out);
-/* ctas = 0 picks 148 x resident CTAs. */
+                         const int32_t* local, const int32_t* host_of, int mode, int64_t chunk_bytes,
+                         rr_exec** out);
+/* Phase 0 (all direct copies). ctas = 0 picks the resident-CTA capacity. */
 rr_status rr_exec_launch(rr_exec* ex, void* stream, int ctas);
-/* Copy engine: 0 = vectorised LDG/STG kernel; 1..5 = TMA bulk-copy ring
- * (cp.async.bulk through shared memory; 2-byte-aligned items still take the
- * LDG/STG kernel). */
+/* Phase 1 (in-host fan-out from leader replicas); no-op when empty. */
+rr_status rr_exec_launch_fanout(rr_exec* ex, void* stream, int ctas);
+/* Copy engine: 0 = vectorised LDG/STG kernel; 1..10 = TMA bulk-copy ring
+ * variants (cp.async.bulk through shared-memory stages; default 1).
+ * 2-byte-aligned items always take the LDG/STG kernel. */
 rr_status rr_exec_set_kernel(rr_exec* ex, int kernel);
-/* items, bytes moved per launch (sum over destinations), bytes read. */
-rr_status rr_exec_stats(const rr_exec* ex, int64_t* items, int64_t* bytes_written, int64_t* bytes_read);
+/* Per phase: items, bytes stored (sum over destinations), bytes read. */
+rr_status rr_exec_stats(const rr_exec* ex, int phase, int64_t* items, int64_t* bytes_written,
+                        int64_t* bytes_read);
+/* Bytes entering / leaving this executor's host over links per launch. */
+rr_status rr_exec_wire(const rr_exec* ex, int64_t* wire_in, int64_t* wire_out);
 void rr_exec_destroy(rr_exec* ex);
 
 /* ---- deterministic weights (test/bench infrastructure) ----

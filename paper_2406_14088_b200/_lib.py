@@ -87,7 +87,7 @@ _SIGNATURES = {
     "rr_plan_num_lowered": (c_int, [_P, POINTER(c_int)]),
     "rr_plan_get_lowered": (c_int, [_P, c_int, POINTER(c_int32), POINTER(c_int32), POINTER(c_int),
                                     POINTER(c_int64), c_int64, POINTER(c_int64)]),
-    "rr_plan_work": (c_int, [_P, c_int, POINTER(c_int32), c_int, POINTER(c_int64), POINTER(c_int64)]),
+    "rr_plan_work": (c_int, [_P, c_int, POINTER(c_int32), POINTER(c_int32), c_int, POINTER(c_int64)]),
     "rr_device_count": (c_int, [POINTER(c_int)]),
     "rr_device_alloc": (c_int, [c_int, c_size_t, POINTER(_P)]),
     "rr_device_free": (c_int, [_P]),
@@ -100,11 +100,13 @@ _SIGNATURES = {
     "rr_ipc_open": (c_int, [c_int, _P, POINTER(_P)]),
     "rr_ipc_close": (c_int, [_P]),
     "rr_enable_peer": (c_int, [c_int, c_int]),
-    "rr_exec_create": (c_int, [_P, c_int, c_int, POINTER(_P), POINTER(_P), c_int, POINTER(c_int32), c_int,
-                               c_int64, POINTER(_P)]),
+    "rr_exec_create": (c_int, [_P, c_int, c_int, POINTER(_P), POINTER(_P), c_int, POINTER(c_int32),
+                               POINTER(c_int32), c_int, c_int64, POINTER(_P)]),
     "rr_exec_launch": (c_int, [_P, _P, c_int]),
+    "rr_exec_launch_fanout": (c_int, [_P, _P, c_int]),
+    "rr_exec_wire": (c_int, [_P, POINTER(c_int64), POINTER(c_int64)]),
     "rr_exec_set_kernel": (c_int, [_P, c_int]),
-    "rr_exec_stats": (c_int, [_P, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
+    "rr_exec_stats": (c_int, [_P, c_int, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
     "rr_exec_destroy": (None, [_P]),
     "rr_fill_shard": (c_int, [_P, c_int, c_int32, _P, c_uint64, _P]),
     "rr_verify_shard": (c_int, [_P, c_int, c_int32, _P, c_uint64, _P, POINTER(c_int64), POINTER(c_int64)]),

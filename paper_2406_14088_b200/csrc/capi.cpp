@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "rlplan/realloc.hpp"
+#include "exec_plan.hpp"
 #include "rr_internal.hpp"
 #include "rr_realloc.h"
 
@@ -145,10 +146,13 @@ struct rr_plan {
 // ---------------------------------------------------------------------------
 
 struct rr_exec {
+  struct Phase {
+    rr::CopyItem* d = nullptr;  // 16-byte (vec) items first, then 2-byte items
+    int n = 0, n_vec = 0;
+    int64_t read = 0, written = 0;
+  };
   int cuda_device = 0;
-  rr::CopyItem* d_items = nullptr;  // 16-byte (vec) items first, then 2-byte items
-  int n_items = 0;
-  int n_vec = 0;
+  Phase phase[2];  // [0] direct copies, [1] in-host fan-out from leader replicas
   int fence_sys = 0;
   int default_ctas = 0;
   // 0 = LDG/STG rr_copy_kernel, 1..kBulkVariants = TMA bulk ring. Default:
@@ -156,7 +160,7 @@ struct rr_exec {
   int kernel = 1;
   int bulk_ctas = 0;
   unsigned int* d_sched = nullptr;  // dynamic work counter (see retire_cta)
-  int64_t bytes_written = 0, bytes_read = 0;
+  int64_t wire_in = 0, wire_out = 0;  // bytes crossing into / out of this host
 };
 
 struct rr_barrier {
@@ -420,33 +424,6 @@ rr_status rr_plan_get_lowered(const rr_plan* plan, int index, int32_t* src, int3
   });
 }
 
-rr_status rr_plan_work(const rr_plan* plan, int n_local, const int32_t* local, int mode, int64_t* bytes_read,
-                       int64_t* bytes_written) {
-  return guarded([&] {
-    need(plan != nullptr, "null plan");
-    need(mode == 0 || mode == 1, "mode must be 0 (push) or 1 (pull)");
-    auto is_local = [&](DeviceId d) { return std::find(local, local + n_local, d) != local + n_local; };
-    int64_t rd = 0, wr = 0;
-    for (const auto& op : plan->lowered) {
-      int64_t bytes = 0;
-      for (const auto& r : op.rects) bytes += r.row_bytes * r.rows;
-      int64_t targets = 0;
-      if (mode == 0) {
-        if (!is_local(op.src)) continue;
-        targets = static_cast<int64_t>(op.dst.size());
-      } else {
-        for (DeviceId d : op.dst) targets += is_local(d) ? 1 : 0;
-        if (!targets) continue;
-      }
-      // One read per group of kMaxFan destinations (see rr_exec_create).
-      rd += bytes * ((targets + rr::kMaxFan - 1) / rr::kMaxFan);
-      wr += bytes * targets;
-    }
-    *bytes_read = rd;
-    *bytes_written = wr;
-  });
-}
-
 // ---- device memory and peer mapping ----------------------------------------
 
 rr_status rr_device_count(int* n) {
@@ -558,133 +535,113 @@ rr_status rr_enable_peer(int cuda_device, int peer_device) {
 
 namespace {
 
-struct Builder {
-  std::vector<std::vector<rr::CopyItem>> streams;  // one item stream per (op, dst group)
-  int64_t written = 0, read = 0;
-
-  // Chunk one rectangle for (src base, dst bases) into items.
-  void add_rect(std::vector<rr::CopyItem>& out, uint64_t src, const std::vector<uint64_t>& dsts,
-                const CopyRect& r, int64_t chunk) {
-    const bool vec = ((src | r.src_off | r.dst_off | r.row_bytes | r.src_pitch | r.dst_pitch) & 15) == 0 &&
-                     std::all_of(dsts.begin(), dsts.end(), [](uint64_t d) { return (d & 15) == 0; });
-    const int64_t unit = vec ? 16 : 2;
-    const int64_t cap_units = std::min<int64_t>(chunk / unit, rr::kMaxItemUnits);
-    const int64_t row_units = r.row_bytes / unit;
-    const int64_t sp = r.src_pitch / unit, dp = r.dst_pitch / unit;
-    auto emit = [&](int64_t row0, int64_t col0, int64_t rows, int64_t cols) {
-      rr::CopyItem it;
-      std::memset(&it, 0, sizeof(it));
-      it.src = src + static_cast<uint64_t>(r.src_off + (row0 * sp + col0) * unit);
-      for (size_t j = 0; j < dsts.size(); ++j)
-        it.dst[j] = dsts[j] + static_cast<uint64_t>(r.dst_off + (row0 * dp + col0) * unit);
-      it.ndst = static_cast<uint16_t>(dsts.size());
-      it.vec = vec ? 1 : 0;
-      it.row_units = static_cast<uint32_t>(cols);
-      it.nrows = static_cast<uint32_t>(rows);
-      it.src_pitch = static_cast<uint32_t>(rows > 1 ? sp : cols);
-      it.dst_pitch = static_cast<uint32_t>(rows > 1 ? dp : cols);
-      it.inv_row = 1.0f / static_cast<float>(cols);
-      if (rows > 1 && ((rows - 1) * dp + cols >= (int64_t{1} << 32) || (rows - 1) * sp + cols >= (int64_t{1} << 32)))
-        raise(RR_EINVAL, "copy item spans more than 2^32 units");
-      out.push_back(it);
-      const int64_t bytes = rows * cols * unit;
-      read += bytes;
-      written += bytes * static_cast<int64_t>(dsts.size());
-    };
-    if (row_units <= cap_units) {
-      const int64_t rows_per = std::max<int64_t>(1, cap_units / std::max<int64_t>(row_units, 1));
-      for (int64_t r0 = 0; r0 < r.rows; r0 += rows_per) emit(r0, 0, std::min(rows_per, r.rows - r0), row_units);
-    } else {
-      for (int64_t row = 0; row < r.rows; ++row)
-        for (int64_t c0 = 0; c0 < row_units; c0 += cap_units) emit(row, c0, 1, std::min(cap_units, row_units - c0));
+// Host map for an executor: `local` plan devices form this host; without an
+// explicit table every other device is its own host.
+rr::HostMap host_map(const rr_plan* plan, int n_local, const int32_t* local, const int32_t* host_of) {
+  const int n = plan->cluster.device_count();
+  rr::HostMap hm;
+  hm.host.resize(static_cast<size_t>(n));
+  if (host_of) {
+    for (int d = 0; d < n; ++d) hm.host[static_cast<size_t>(d)] = host_of[d];
+    need(n_local > 0, "host_of needs at least one local device");
+    need(local[0] >= 0 && local[0] < n, "local device out of range");
+    hm.me = host_of[local[0]];
+    for (int i = 0; i < n_local; ++i) {
+      need(local[i] >= 0 && local[i] < n, "local device out of range");
+      need(host_of[local[i]] == hm.me, "local devices must share one host");
     }
+    return hm;
   }
-};
+  hm.hierarchical = false;
+  for (int d = 0; d < n; ++d) hm.host[static_cast<size_t>(d)] = n + d;  // distinct remote hosts
+  hm.me = -1;
+  for (int i = 0; i < n_local; ++i) {
+    need(local[i] >= 0 && local[i] < n, "local device out of range");
+    hm.host[static_cast<size_t>(local[i])] = hm.me;
+  }
+  return hm;
+}
+
+void upload(const rr::ItemSet& set, rr_exec::Phase& ph) {
+  ph.n = static_cast<int>(set.items.size());
+  ph.n_vec = set.n_vec;
+  ph.read = set.read;
+  ph.written = set.written;
+  if (set.items.empty()) return;
+  const size_t bytes = set.items.size() * sizeof(rr::CopyItem);
+  check_cuda(cudaMalloc(&ph.d, bytes), "cudaMalloc(items)");
+  check_cuda(cudaMemcpy(ph.d, set.items.data(), bytes, cudaMemcpyHostToDevice), "upload items");
+}
+
+void launch_phase(rr_exec* ex, const rr_exec::Phase& ph, void* stream, int ctas) {
+  check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+  if (ph.n == 0) return;
+  if (ex->kernel == 0) {
+    check_cuda(rr::launch_copy(ph.d, ph.n, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys, stream, ex->d_sched),
+               "rr_copy_kernel launch");
+    return;
+  }
+  if (ph.n_vec > 0)
+    check_cuda(rr::launch_bulk(ex->kernel, ph.d, ph.n_vec, ctas > 0 ? ctas : ex->bulk_ctas, ex->fence_sys, stream,
+                               nullptr, ex->d_sched),
+               "rr_bulk_kernel launch");
+  if (ph.n > ph.n_vec)
+    check_cuda(rr::launch_copy(ph.d + ph.n_vec, ph.n - ph.n_vec, ex->default_ctas, ex->fence_sys, stream,
+                               ex->d_sched),
+               "rr_copy_kernel launch (2-byte items)");
+}
 
 }  // namespace
 
+rr_status rr_plan_work(const rr_plan* plan, int n_local, const int32_t* local, const int32_t* host_of, int mode,
+                       int64_t* out6) {
+  return guarded([&] {
+    need(plan != nullptr && out6 != nullptr, "null plan/output");
+    need(mode == 0 || mode == 1, "mode must be 0 (push) or 1 (pull)");
+    const rr::HostMap hm = host_map(plan, n_local, local, host_of);
+    const auto jobs = rr::build_jobs(plan->lowered, hm, mode);
+    const auto a = rr::build_items(jobs, 0, hm, nullptr, nullptr, int64_t{1} << 30);
+    const auto b = rr::build_items(jobs, 1, hm, nullptr, nullptr, int64_t{1} << 30);
+    out6[0] = a.read;
+    out6[1] = a.written;
+    out6[2] = b.read;
+    out6[3] = b.written;
+    rr::host_wire_bytes(plan->lowered, hm, &out6[4], &out6[5]);
+  });
+}
+
 rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, void* const* src_bufs,
-                         void* const* dst_bufs, int n_local, const int32_t* local, int mode,
-                         int64_t chunk_bytes, rr_exec** out) {
+                         void* const* dst_bufs, int n_local, const int32_t* local, const int32_t* host_of,
+                         int mode, int64_t chunk_bytes, rr_exec** out) {
   return guarded([&] {
     need(plan != nullptr && out != nullptr, "null plan/output");
     need(mode == 0 || mode == 1, "mode must be 0 (push) or 1 (pull)");
     need(n_devices >= plan->cluster.device_count(), "buffer tables must cover every cluster device");
     if (chunk_bytes <= 0) chunk_bytes = 256 << 10;
     need(chunk_bytes >= 16, "chunk_bytes too small");
-    std::vector<bool> is_local(static_cast<size_t>(n_devices), false);
-    for (int i = 0; i < n_local; ++i) {
-      need(local[i] >= 0 && local[i] < n_devices, "local device out of range");
-      is_local[static_cast<size_t>(local[i])] = true;
-    }
-    auto addr = [&](void* const* bufs, DeviceId d, const char* what) {
-      void* p = bufs[d];
-      if (!p) raise(RR_EINVAL, std::string("missing ") + what + " buffer for device " + std::to_string(d));
-      return reinterpret_cast<uint64_t>(p);
-    };
-    Builder b;
-    bool remote = false;
-    for (const auto& op : plan->lowered) {
-      std::vector<DeviceId> targets;
-      if (mode == 0) {
-        if (!is_local[static_cast<size_t>(op.src)]) continue;
-        targets = op.dst;
-      } else {
-        for (DeviceId d : op.dst)
-          if (is_local[static_cast<size_t>(d)]) targets.push_back(d);
-        if (targets.empty()) continue;
-      }
-      const uint64_t s = addr(src_bufs, op.src, "source");
-      for (size_t g = 0; g < targets.size(); g += rr::kMaxFan) {
-        std::vector<uint64_t> dsts;
-        for (size_t j = g; j < std::min(targets.size(), g + rr::kMaxFan); ++j) {
-          dsts.push_back(addr(dst_bufs, targets[j], "destination"));
-          if (!is_local[static_cast<size_t>(targets[j])]) remote = true;
-        }
-        b.streams.emplace_back();
-        for (const auto& r : op.rects) {
-          // Same-address copies (identical placement and buffers) are no-ops.
-          if (dsts.size() == 1 && s + r.src_off == dsts[0] + r.dst_off) continue;
-          b.add_rect(b.streams.back(), s, dsts, r, chunk_bytes);
-        }
-      }
-    }
-    // Interleave the per-op streams round-robin so concurrently running CTAs
-    // spread their stores over many destinations (NVLink ingress balance).
-    // 16-byte items first (both kernels), then 2-byte items (LDG/STG only).
-    std::vector<rr::CopyItem> items, elem_items;
-    size_t total = 0;
-    for (const auto& s : b.streams) total += s.size();
-    items.reserve(total);
-    for (size_t k = 0, seen = 0; seen < total; ++k)
-      for (const auto& s : b.streams)
-        if (k < s.size()) {
-          (s[k].vec ? items : elem_items).push_back(s[k]);
-          ++seen;
-        }
-    const size_t n_vec = items.size();
-    items.insert(items.end(), elem_items.begin(), elem_items.end());
-    need(items.size() < (size_t{1} << 31), "too many copy items");
+    const rr::HostMap hm = host_map(plan, n_local, local, host_of);
+    const auto jobs = rr::build_jobs(plan->lowered, hm, mode);
+    const auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes);
+    const auto b = rr::build_items(jobs, 1, hm, src_bufs, dst_bufs, chunk_bytes);
 
     auto ex = std::make_unique<rr_exec>();
     ex->cuda_device = cuda_device;
-    ex->n_items = static_cast<int>(items.size());
-    ex->n_vec = static_cast<int>(n_vec);
-    ex->fence_sys = remote ? 1 : 0;
-    ex->bytes_written = b.written;
-    ex->bytes_read = b.read;
+    // Remote accesses (peer stores, or peer loads in pull mode) must be
+    // visible system-wide before the following barrier releases them.
+    int64_t win = 0, wout = 0;
+    rr::host_wire_bytes(plan->lowered, hm, &win, &wout);
+    ex->fence_sys = (a.remote_stores || win || wout) ? 1 : 0;
+    ex->wire_in = win;
+    ex->wire_out = wout;
     check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
     int per_sm = 0, sms = 0;
     check_cuda(rr::copy_max_ctas(&per_sm, &sms), "occupancy query");
     ex->default_ctas = std::max(1, per_sm) * sms;
-    if (!items.empty()) {
-      const size_t bytes = items.size() * sizeof(rr::CopyItem);
-      check_cuda(cudaMalloc(&ex->d_items, bytes), "cudaMalloc(items)");
-      check_cuda(cudaMemcpy(ex->d_items, items.data(), bytes, cudaMemcpyHostToDevice), "upload items");
-    }
+    upload(a, ex->phase[0]);
+    upload(b, ex->phase[1]);
     check_cuda(cudaMalloc(&ex->d_sched, 2 * sizeof(unsigned int)), "cudaMalloc(sched)");
     check_cuda(cudaMemset(ex->d_sched, 0, 2 * sizeof(unsigned int)), "cudaMemset(sched)");
-    check_cuda(rr::launch_bulk(1, nullptr, 0, 0, 0, nullptr, &ex->bulk_ctas, nullptr), "bulk occupancy");
+    check_cuda(rr::launch_bulk(ex->kernel, nullptr, 0, 0, 0, nullptr, &ex->bulk_ctas, nullptr), "bulk occupancy");
     *out = ex.release();
   });
 }
@@ -692,20 +649,14 @@ rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, vo
 rr_status rr_exec_launch(rr_exec* ex, void* stream, int ctas) {
   return guarded([&] {
     need(ex != nullptr, "null executor");
-    check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
-    if (ex->kernel == 0) {
-      check_cuda(rr::launch_copy(ex->d_items, ex->n_items, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys,
-                                 stream, ex->d_sched),
-                 "rr_copy_kernel launch");
-      return;
-    }
-    check_cuda(rr::launch_bulk(ex->kernel, ex->d_items, ex->n_vec, ctas > 0 ? ctas : ex->bulk_ctas,
-                               ex->fence_sys, stream, nullptr, ex->d_sched),
-               "rr_bulk_kernel launch");
-    if (ex->n_items > ex->n_vec)
-      check_cuda(rr::launch_copy(ex->d_items + ex->n_vec, ex->n_items - ex->n_vec, ex->default_ctas,
-                                 ex->fence_sys, stream, ex->d_sched),
-                 "rr_copy_kernel launch (2-byte items)");
+    launch_phase(ex, ex->phase[0], stream, ctas);
+  });
+}
+
+rr_status rr_exec_launch_fanout(rr_exec* ex, void* stream, int ctas) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    launch_phase(ex, ex->phase[1], stream, ctas);
   });
 }
 
@@ -721,19 +672,30 @@ rr_status rr_exec_set_kernel(rr_exec* ex, int kernel) {
   });
 }
 
-rr_status rr_exec_stats(const rr_exec* ex, int64_t* items, int64_t* written, int64_t* read) {
+rr_status rr_exec_stats(const rr_exec* ex, int phase, int64_t* items, int64_t* written, int64_t* read) {
   return guarded([&] {
     need(ex != nullptr, "null executor");
-    *items = ex->n_items;
-    *written = ex->bytes_written;
-    *read = ex->bytes_read;
+    need(phase == 0 || phase == 1, "phase must be 0 or 1");
+    const auto& ph = ex->phase[phase];
+    *items = ph.n;
+    *written = ph.written;
+    *read = ph.read;
+  });
+}
+
+rr_status rr_exec_wire(const rr_exec* ex, int64_t* wire_in, int64_t* wire_out) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    *wire_in = ex->wire_in;
+    *wire_out = ex->wire_out;
   });
 }
 
 void rr_exec_destroy(rr_exec* ex) {
   if (!ex) return;
   cudaSetDevice(ex->cuda_device);
-  if (ex->d_items) cudaFree(ex->d_items);
+  for (auto& ph : ex->phase)
+    if (ph.d) cudaFree(ph.d);
   if (ex->d_sched) cudaFree(ex->d_sched);
   delete ex;
 }

@@ -1,0 +1,59 @@
+// Host-side construction of executor work: which device reads what and
+// stores where, in which phase, for one executing host. Shared by
+// rr_exec_create (real pointers, device items) and rr_plan_work (byte
+// accounting only, no CUDA).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "rlplan/realloc.hpp"
+#include "rr_internal.hpp"
+
+namespace rr {
+
+// Phase A: every copy that reads a real source shard. A destination host
+// with several plan devices of one op receives the payload once, into its
+// lowest-id device (the leader); a host that holds the source writes all of
+// its own destinations directly.
+// Phase B (after a cross-host barrier): the host copies leader regions into
+// the other local destinations of that op — one NVLink crossing per host
+// instead of one per destination device (hierarchical broadcast).
+struct Job {
+  int phase = 0;
+  rlplan::DeviceId src = -1;       // device whose buffer is read
+  bool src_is_dst_buffer = false;  // phase B: the leader's destination shard
+  std::vector<rlplan::DeviceId> dsts;
+  const rlplan::LoweredOp* op = nullptr;
+};
+
+struct HostMap {
+  std::vector<int> host;     // host id per plan device
+  int me = 0;                // executing host
+  bool hierarchical = true;  // false: flat delivery, every destination served directly
+};
+
+// mode 0 = push (source host executes phase A), 1 = pull (destination host).
+std::vector<Job> build_jobs(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm, int mode);
+
+// Bytes that cross from/to host `me` (each payload crosses once per
+// destination host).
+void host_wire_bytes(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm, int64_t* in, int64_t* out);
+
+int64_t rect_bytes(const rlplan::CopyRect& r);
+
+// Items of one phase, chunked and interleaved across jobs; 16-byte items
+// first, then 2-byte items.
+struct ItemSet {
+  std::vector<CopyItem> items;
+  int n_vec = 0;
+  int64_t read = 0, written = 0;
+  bool remote_stores = false;  // some destination is on another host
+};
+
+// Resolve jobs of `phase` into items. src_bufs/dst_bufs are indexed by plan
+// device; nullptr tables mean "accounting only" (addresses left at offsets).
+ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, void* const* src_bufs,
+                    void* const* dst_bufs, int64_t chunk_bytes);
+
+}  // namespace rr

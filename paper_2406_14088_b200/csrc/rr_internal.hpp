@@ -1,6 +1,8 @@
 // Internal device-side structures shared by capi.cpp and kernels.cu.
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdint>
 
 namespace rr {

@@ -352,12 +352,17 @@ class ReallocPlan:
                         [tuple(rects[6 * k: 6 * k + 6]) for k in range(nr.value)]))
         return out
 
-    def work(self, local: Sequence[int], mode: int = 0) -> Tuple[int, int]:
-        """(bytes read, bytes written) an executor driving `local` would move."""
+    def work(self, local: Sequence[int], mode: int = 0, host_of: Optional[Sequence[int]] = None) -> Dict[str, int]:
+        """Bytes an executor driving `local` would move (host only): phase 0
+        (direct) and phase 1 (in-host fan-out) reads/writes, and bytes
+        entering / leaving its host over links."""
         arr = (ctypes.c_int32 * max(1, len(local)))(*local)
-        r, w = ctypes.c_int64(), ctypes.c_int64()
-        check(lib.rr_plan_work(self._h, len(local), arr, mode, ctypes.byref(r), ctypes.byref(w)))
-        return r.value, w.value
+        n = self.cluster.device_count()
+        hosts = (ctypes.c_int32 * n)(*host_of) if host_of is not None else None
+        out = (ctypes.c_int64 * 6)()
+        check(lib.rr_plan_work(self._h, len(local), arr, hosts, mode, out))
+        keys = ("read", "written", "fanout_read", "fanout_written", "wire_in", "wire_out")
+        return dict(zip(keys, out))
 
     def devices(self, side: int) -> List[int]:
         p = self.src if side == 0 else self.dst

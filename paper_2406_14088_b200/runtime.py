@@ -128,10 +128,15 @@ def weight_value(seed: int, tensor: int, index: int) -> int:
 
 
 class Executor:
-    """A plan bound to buffers on one CUDA device (rr_exec_create)."""
+    """A plan bound to buffers on one CUDA device (rr_exec_create).
+
+    ``host_of`` (plan device -> GPU) enables hierarchical delivery: a payload
+    for several plan devices of one remote GPU crosses NVLink once (phase 0)
+    and that GPU replicates it locally (phase 1, ``launch_fanout``)."""
 
     def __init__(self, plan: ReallocPlan, cuda_device: int, src_ptrs: Dict[int, int], dst_ptrs: Dict[int, int],
-                 local: Iterable[int], mode: int = PUSH, chunk_bytes: int = 0):
+                 local: Iterable[int], mode: int = PUSH, chunk_bytes: int = 0,
+                 host_of: Optional[Sequence[int]] = None):
         n = plan.cluster.device_count()
         self.plan = plan
         sp, dp = (ctypes.c_void_p * n)(), (ctypes.c_void_p * n)()
@@ -141,19 +146,31 @@ class Executor:
             dp[d] = p
         loc = list(local)
         arr = (ctypes.c_int32 * max(1, len(loc)))(*loc)
+        hosts = (ctypes.c_int32 * n)(*host_of) if host_of is not None else None
         h = ctypes.c_void_p()
-        check(lib.rr_exec_create(plan.handle, cuda_device, n, sp, dp, len(loc), arr, mode, chunk_bytes,
+        check(lib.rr_exec_create(plan.handle, cuda_device, n, sp, dp, len(loc), arr, hosts, mode, chunk_bytes,
                                  ctypes.byref(h)))
         self._h = h
+        self.items, self.bytes_written, self.bytes_read = self.stats(0)
+        self.fanout_items, self.fanout_written, self.fanout_read = self.stats(1)
+        wi, wo = ctypes.c_int64(), ctypes.c_int64()
+        check(lib.rr_exec_wire(h, ctypes.byref(wi), ctypes.byref(wo)))
+        self.wire_in, self.wire_out = wi.value, wo.value
+
+    def stats(self, phase: int) -> Tuple[int, int, int]:
+        """(items, bytes stored, bytes read) of phase 0 (direct) or 1 (fan-out)."""
         it, w, r = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
-        check(lib.rr_exec_stats(h, ctypes.byref(it), ctypes.byref(w), ctypes.byref(r)))
-        self.items, self.bytes_written, self.bytes_read = it.value, w.value, r.value
+        check(lib.rr_exec_stats(self._h, phase, ctypes.byref(it), ctypes.byref(w), ctypes.byref(r)))
+        return it.value, w.value, r.value
 
     def launch(self, stream=None, ctas: int = 0) -> None:
         check(lib.rr_exec_launch(self._h, _stream_ptr(stream), ctas))
 
+    def launch_fanout(self, stream=None, ctas: int = 0) -> None:
+        check(lib.rr_exec_launch_fanout(self._h, _stream_ptr(stream), ctas))
+
     def set_kernel(self, kernel: int) -> None:
-        """0 = LDG/STG kernel, 1..5 = TMA bulk-copy ring variants."""
+        """0 = LDG/STG kernel, 1..10 = TMA bulk-copy ring variants."""
         check(lib.rr_exec_set_kernel(self._h, kernel))
 
     def close(self) -> None:
@@ -262,7 +279,7 @@ class RankRealloc:
 
     def __init__(self, plans: Sequence[ReallocPlan], shards: Dict[str, Tuple[int, int]],
                  bind: Sequence[Tuple[str, str]], rank: int, world: int, cuda_device: int, group=None,
-                 mode: int = PUSH, kernel: int = DEFAULT_KERNEL):
+                 mode: int = PUSH, kernel: int = DEFAULT_KERNEL, hierarchical: bool = True):
         self.plans, self.rank, self.world, self.cuda_device = list(plans), rank, world, cuda_device
         n = plans[0].cluster.device_count()
         self.local = hosted_devices(n, rank, world)
@@ -308,20 +325,35 @@ class RankRealloc:
                     else:
                         self.ptrs[name][d] = p
         self.barrier = Barrier(cuda_device, rank, world, flag_ptrs)
+        host_of = [self.owner[d] for d in range(n)]
         self.executors: List[Executor] = []
         for pi, (sname, dname) in enumerate(bind):
             self.executors.append(Executor(self.plans[pi], cuda_device, self.ptrs[sname], self.ptrs[dname],
-                                           self.local, mode))
+                                           self.local, mode, host_of=host_of if hierarchical else None))
             self.executors[-1].set_kernel(kernel)
+        # Every rank must run the same barrier sequence: a phase has a fan-out
+        # step if any rank has fan-out work in it.
+        counts = [e.fanout_items for e in self.executors]
+        if world > 1:
+            import torch.distributed as dist
+            allc: List[list] = [None] * world  # type: ignore
+            dist.all_gather_object(allc, counts, group=group)
+            counts = [sum(c[i] for c in allc) for i in range(len(counts))]
+        self.has_fanout = [c > 0 for c in counts]
 
     def set_kernel(self, kernel: int) -> None:
         for e in self.executors:
             e.set_kernel(kernel)
 
     def run_phase(self, i: int, stream=None, ctas: int = 0) -> None:
+        """Phase i: direct copies, barrier, then (if any rank has some) the
+        in-host fan-out from leader replicas and another barrier."""
         self.executors[i].launch(stream, ctas)
         if self.world > 1:
             self.barrier.launch(stream)
+            if self.has_fanout[i]:
+                self.executors[i].launch_fanout(stream, ctas)
+                self.barrier.launch(stream)
 
     def close(self) -> None:
         for e in self.executors:

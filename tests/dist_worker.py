@@ -41,13 +41,14 @@ def main() -> int:
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = b200_cluster(8)
     failures = []
-    for mode in (R.PUSH, R.PULL):
+    combos = [(m, k, h) for m in (R.PUSH, R.PULL) for k in (0, 1) for h in (True, False)]
+    for mode, kernel, hier in combos:
         for sp, dp in CASES:
             src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
             dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
             plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
             rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
-                               mode=mode)
+                               mode=mode, kernel=kernel, hierarchical=hier)
             for d, b in rr.buffers["a"].items():
                 R.fill_shard(plan, R.SRC, d, b.ptr, 21)
             torch.cuda.synchronize()
@@ -55,12 +56,12 @@ def main() -> int:
             rr.run_phase(0)
             torch.cuda.synchronize()
             if rr.barrier.timed_out():
-                failures.append(f"{sp}->{dp} mode {mode}: barrier timed out")
+                failures.append(f"{sp}->{dp} mode {mode} kernel {kernel} hier {hier}: barrier timed out")
             for d, b in rr.buffers["b"].items():
                 got = b.to_host()
                 want = O.fill(TINY_GQA, dst, c, d, 21)
                 if not np.array_equal(got, want):
-                    failures.append(f"{sp}->{dp} mode {mode}: device {d} differs in "
+                    failures.append(f"{sp}->{dp} mode {mode} kernel {kernel} hier {hier}: device {d} differs in "
                                     f"{int(np.count_nonzero(got != want))} elements")
             dist.barrier()
             rr.close()

@@ -38,15 +38,21 @@ def _worker(rank, world, port, out_dir):
         js = json.dumps(plan.to_json(), sort_keys=True)
         plans = [None] * world
         dist.all_gather_object(plans, js)
-        local = hosted_devices(c.device_count(), rank, world)
-        work = {mode: plan.work(local, mode) for mode in (0, 1)}
+        n = c.device_count()
+        local = hosted_devices(n, rank, world)
+        host_of = [d // (n // world) for d in range(n)]
+        work = {f"{mode}{h}": plan.work(local, mode, host_of if h else None) for mode in (0, 1) for h in (0, 1)}
         works = [None] * world
         dist.all_gather_object(works, work)
-        total_written = plan.work(list(range(c.device_count())), 0)[1]
-        result[key] = {"same_plan": all(p == js for p in plans),
-                       "push_written": sum(w[0][1] for w in works),
-                       "pull_written": sum(w[1][1] for w in works),
-                       "total": total_written}
+        total_written = plan.work(list(range(n)), 0)["written"]
+        entry = {"same_plan": all(p == js for p in plans), "total": total_written}
+        for k in work:
+            entry[f"written_{k}"] = sum(w[k]["written"] + w[k]["fanout_written"] for w in works)
+            entry[f"wire_in_{k}"] = sum(w[k]["wire_in"] for w in works)
+            entry[f"wire_out_{k}"] = sum(w[k]["wire_out"] for w in works)
+        # hierarchical delivery never sends more over links than flat delivery
+        entry["hier_saves"] = all(w["01"]["wire_in"] <= w["00"]["wire_in"] for w in works)
+        result[key] = entry
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
         json.dump(result, f)
     dist.barrier()
@@ -60,8 +66,11 @@ def test_ranks_agree_and_partition_covers_plan(tmp_path, world):
         res = json.load(open(tmp_path / f"rank{r}.json"))
         for key, v in res.items():
             assert v["same_plan"], key
-            assert v["push_written"] == v["total"], key
-            assert v["pull_written"] == v["total"], key
+            assert v["hier_saves"], key
+            for k in ("00", "01", "10", "11"):
+                # every destination byte is stored exactly once across ranks and phases
+                assert v[f"written_{k}"] == v["total"], (key, k)
+                assert v[f"wire_in_{k}"] == v[f"wire_out_{k}"], (key, k)
 
 
 def test_hosted_devices_blocks():

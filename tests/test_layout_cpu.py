@@ -130,7 +130,8 @@ def test_lowering_is_compact():
     m, src, dst, c = config_placements("7b_tp8_to_dp8")
     plan = P.plan_param_realloc(m, src, dst, c, BALANCED)
     assert plan.num_rects() < 4000
-    read, written = plan.work(list(range(8)), 0)
+    w = plan.work(list(range(8)), 0)
+    read, written = w["read"], w["written"]
     # one read of each source slice, eight stores (seven replicas + own); the
     # replicated norms are taken by every replica from itself
     assert read < written / 7.9
