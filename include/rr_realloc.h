@@ -218,6 +218,38 @@ rr_status rr_exec_stats(const rr_exec* ex, int phase, int64_t* items, int64_t* b
 rr_status rr_exec_wire(const rr_exec* ex, int64_t* wire_in, int64_t* wire_out);
 void rr_exec_destroy(rr_exec* ex);
 
+/* Executor options (superset of rr_exec_create's arguments).
+ * mc_bufs[d] (NULL table = no multicast): the NVLS multicast address whose
+ * member buffers are the destination shards of one plan device per host
+ * (rr_mcast_bind). A payload whose destination hosts are exactly that
+ * group is stored once through multimem.st and replicated by the NVSwitch
+ * (push mode, K3) instead of one peer store per host. */
+typedef struct {
+  int32_t mode;               /* 0 push, 1 pull */
+  int64_t chunk_bytes;        /* 0 = 256 KiB */
+  const int32_t* host_of;     /* NULL = flat delivery */
+  void* const* mc_bufs;       /* NULL = no multicast */
+} rr_exec_options;
+rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices, void* const* src_bufs,
+                            void* const* dst_bufs, int n_local, const int32_t* local,
+                            const rr_exec_options* options, rr_exec** out);
+
+/* ---- NVLS multicast objects (K3), one process per GPU ----
+ * root: rr_mcast_create -> POSIX fd + padded size (share the fd with the
+ * other ranks, e.g. SCM_RIGHTS); others: rr_mcast_import(fd); then, after
+ * every rank has created/imported (a barrier), each rank rr_mcast_bind:
+ * local physical memory bound into the object, mapped twice — a unicast
+ * address (ordinary loads/stores on this GPU) and the multicast address
+ * (multimem stores reach every member). */
+typedef struct rr_mcast rr_mcast;
+rr_status rr_mcast_supported(int cuda_device, int* supported);
+rr_status rr_mcast_create(int cuda_device, size_t bytes, int n_devices, int* fd_out, size_t* size_out,
+                          rr_mcast** out);
+rr_status rr_mcast_import(int cuda_device, int fd, size_t size, int n_devices, rr_mcast** out);
+rr_status rr_mcast_bind(rr_mcast* m, void** unicast_ptr, void** multicast_ptr);
+rr_status rr_mcast_size(const rr_mcast* m, size_t* size);
+void rr_mcast_destroy(rr_mcast* m);
+
 /* ---- deterministic weights (test/bench infrastructure) ----
  * Fill or check a device's shard under one side of a plan with
  * bf16 value = hash(seed, tensor_id, logical_index). */

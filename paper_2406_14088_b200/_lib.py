@@ -50,8 +50,21 @@ class RrOp(Structure):
                 ("bytes", c_int64)]
 
 
+class RrExecOptions(Structure):
+    _fields_ = [("mode", c_int32), ("chunk_bytes", c_int64), ("host_of", POINTER(c_int32)),
+                ("mc_bufs", POINTER(c_void_p))]
+
+
 _P = c_void_p
 _SIGNATURES = {
+    "rr_exec_create_ex": (c_int, [_P, c_int, c_int, POINTER(_P), POINTER(_P), c_int, POINTER(c_int32),
+                                  POINTER(RrExecOptions), POINTER(_P)]),
+    "rr_mcast_supported": (c_int, [c_int, POINTER(c_int)]),
+    "rr_mcast_create": (c_int, [c_int, c_size_t, c_int, POINTER(c_int), POINTER(c_size_t), POINTER(_P)]),
+    "rr_mcast_import": (c_int, [c_int, c_int, c_size_t, c_int, POINTER(_P)]),
+    "rr_mcast_bind": (c_int, [_P, POINTER(_P), POINTER(_P)]),
+    "rr_mcast_size": (c_int, [_P, POINTER(c_size_t)]),
+    "rr_mcast_destroy": (None, [_P]),
     "rr_last_error": (c_char_p, []),
     "rr_abi_version": (c_int, []),
     "rr_model_validate": (c_int, [POINTER(RrModel)]),

@@ -171,6 +171,10 @@ struct rr_barrier {
   int* d_timed_out = nullptr;
 };
 
+namespace rr {
+void set_last_error(const std::string& msg) { g_error = msg; }
+}  // namespace rr
+
 // Definitions take C linkage from the declarations in rr_realloc.h.
 
 const char* rr_last_error(void) { return g_error.c_str(); }
@@ -613,13 +617,32 @@ rr_status rr_plan_work(const rr_plan* plan, int n_local, const int32_t* local, c
 rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, void* const* src_bufs,
                          void* const* dst_bufs, int n_local, const int32_t* local, const int32_t* host_of,
                          int mode, int64_t chunk_bytes, rr_exec** out) {
+  rr_exec_options opt;
+  opt.mode = mode;
+  opt.chunk_bytes = chunk_bytes;
+  opt.host_of = host_of;
+  opt.mc_bufs = nullptr;
+  return rr_exec_create_ex(plan, cuda_device, n_devices, src_bufs, dst_bufs, n_local, local, &opt, out);
+}
+
+rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices, void* const* src_bufs,
+                            void* const* dst_bufs, int n_local, const int32_t* local,
+                            const rr_exec_options* options, rr_exec** out) {
   return guarded([&] {
-    need(plan != nullptr && out != nullptr, "null plan/output");
+    need(plan != nullptr && out != nullptr && options != nullptr, "null plan/options/output");
+    const int mode = options->mode;
+    int64_t chunk_bytes = options->chunk_bytes;
     need(mode == 0 || mode == 1, "mode must be 0 (push) or 1 (pull)");
     need(n_devices >= plan->cluster.device_count(), "buffer tables must cover every cluster device");
     if (chunk_bytes <= 0) chunk_bytes = 256 << 10;
     need(chunk_bytes >= 16, "chunk_bytes too small");
-    const rr::HostMap hm = host_map(plan, n_local, local, host_of);
+    rr::HostMap hm = host_map(plan, n_local, local, options->host_of);
+    if (options->mc_bufs) {
+      need(options->host_of != nullptr, "multicast needs a host_of table");
+      need(mode == 0, "multicast is a push-mode path");
+      hm.mc.resize(hm.host.size());
+      for (size_t d = 0; d < hm.mc.size(); ++d) hm.mc[d] = reinterpret_cast<uint64_t>(options->mc_bufs[d]);
+    }
     const auto jobs = rr::build_jobs(plan->lowered, hm, mode);
     const auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes);
     const auto b = rr::build_items(jobs, 1, hm, src_bufs, dst_bufs, chunk_bytes);

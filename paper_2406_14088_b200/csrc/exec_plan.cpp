@@ -33,6 +33,23 @@ std::map<int, std::vector<DeviceId>> by_host(const LoweredOp& op, const HostMap&
   return g;
 }
 
+// An op can be multicast when the leaders of its destination hosts are
+// exactly the members of one multicast group (the switch writes every
+// member, so a strict subset would clobber a non-destination).
+bool multicast_target(const std::map<int, std::vector<DeviceId>>& groups, const HostMap& hm, uint64_t* base) {
+  if (hm.mc.empty() || !hm.hierarchical) return false;
+  uint64_t v = 0;
+  for (const auto& kv : groups) {
+    const uint64_t m = hm.mc[static_cast<size_t>(kv.second.front())];
+    if (m == 0 || (v != 0 && m != v)) return false;
+    v = m;
+  }
+  const size_t members = static_cast<size_t>(std::count(hm.mc.begin(), hm.mc.end(), v));
+  if (members != groups.size()) return false;
+  *base = v;
+  return true;
+}
+
 }  // namespace
 
 std::vector<Job> build_jobs(const std::vector<LoweredOp>& ops, const HostMap& hm, int mode) {
@@ -55,7 +72,20 @@ std::vector<Job> build_jobs(const std::vector<LoweredOp>& ops, const HostMap& hm
     const int hs = hm.host[static_cast<size_t>(op.src)];
     const auto groups = by_host(op, hm);
     const auto mine = groups.find(hm.me);
-    if (mode == 0) {  // push: the source host drives phase A
+    uint64_t mc_base = 0;
+    if (mode == 0 && hs == hm.me && multicast_target(groups, hm, &mc_base)) {
+      // One multimem store reaches every host's leader (our own included);
+      // our other local destinations are stored directly from the same read.
+      Job j;
+      j.phase = 0;
+      j.src = op.src;
+      j.op = &op;
+      j.multicast = true;
+      j.mc_base = mc_base;
+      j.dsts.push_back(groups.begin()->second.front());
+      if (mine != groups.end()) j.dsts.insert(j.dsts.end(), mine->second.begin() + 1, mine->second.end());
+      jobs.push_back(std::move(j));
+    } else if (mode == 0) {  // push: the source host drives phase A
       if (hs == hm.me) {
         for (const auto& [h, list] : groups) {
           Job j;
@@ -95,12 +125,18 @@ void host_wire_bytes(const std::vector<LoweredOp>& ops, const HostMap& hm, int64
   for (const auto& op : ops) {
     const int hs = hm.host[static_cast<size_t>(op.src)];
     const int64_t b = op_bytes(op);
-    for (const auto& [h, list] : by_host(op, hm)) {
+    const auto groups = by_host(op, hm);
+    uint64_t mc_base = 0;
+    const bool mc = multicast_target(groups, hm, &mc_base);
+    bool sent = false;
+    for (const auto& [h, list] : groups) {
       if (h == hs) continue;
-      // hierarchical: once per destination host; flat: once per destination device
+      // hierarchical: once per destination host; flat: once per destination
+      // device; multicast: leaves the source once, enters every host once
       const int64_t copies = hm.hierarchical ? 1 : static_cast<int64_t>(list.size());
       if (h == hm.me) i += b * copies;
-      if (hs == hm.me) o += b * copies;
+      if (hs == hm.me && !(mc && sent)) o += b * copies;
+      sent = true;
     }
   }
   *in = i;
@@ -111,10 +147,11 @@ namespace {
 
 // Chunk one rectangle for (src base, dst bases) into items.
 void add_rect(std::vector<CopyItem>& out, ItemSet& acc, uint64_t src, const std::vector<uint64_t>& dsts,
-              const CopyRect& r, int64_t chunk) {
+              const CopyRect& r, int64_t chunk, bool mc0) {
   const bool vec = ((src | static_cast<uint64_t>(r.src_off | r.dst_off | r.row_bytes | r.src_pitch | r.dst_pitch)) &
                     15) == 0 &&
                    std::all_of(dsts.begin(), dsts.end(), [](uint64_t d) { return (d & 15) == 0; });
+  if (mc0 && !vec) throw rlplan::ValidationError("multicast copies must be 16-byte aligned");
   const int64_t unit = vec ? 16 : 2;
   const int64_t cap_units = std::min<int64_t>(chunk / unit, kMaxItemUnits);
   const int64_t row_units = r.row_bytes / unit;
@@ -126,7 +163,7 @@ void add_rect(std::vector<CopyItem>& out, ItemSet& acc, uint64_t src, const std:
     for (size_t j = 0; j < dsts.size(); ++j)
       it.dst[j] = dsts[j] + static_cast<uint64_t>(r.dst_off + (row0 * dp + col0) * unit);
     it.ndst = static_cast<uint16_t>(dsts.size());
-    it.vec = vec ? 1 : 0;
+    it.vec = static_cast<uint16_t>((vec ? kItemVec : 0) | (mc0 ? kItemMulticast0 : 0));
     it.row_units = static_cast<uint32_t>(cols);
     it.nrows = static_cast<uint32_t>(rows);
     it.src_pitch = static_cast<uint32_t>(rows > 1 ? sp : cols);
@@ -168,7 +205,13 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
                                            : base_of(src_bufs, j.src, "source");
     for (size_t g = 0; g < j.dsts.size(); g += kMaxFan) {
       std::vector<uint64_t> dsts;
+      const bool mc0 = j.multicast && g == 0;
       for (size_t k = g; k < std::min(j.dsts.size(), g + kMaxFan); ++k) {
+        if (mc0 && k == 0) {
+          dsts.push_back(accounting ? 0 : j.mc_base);
+          acc.remote_stores = true;
+          continue;
+        }
         dsts.push_back(base_of(dst_bufs, j.dsts[k], "destination"));
         if (hm.host[static_cast<size_t>(j.dsts[k])] != hm.me) acc.remote_stores = true;
       }
@@ -179,9 +222,10 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
           r.src_pitch = r.dst_pitch;
         }
         // Same-address copies (identical placement and buffers) are no-ops.
-        if (!accounting && dsts.size() == 1 && s + static_cast<uint64_t>(r.src_off) == dsts[0] + static_cast<uint64_t>(r.dst_off))
+        if (!accounting && !mc0 && dsts.size() == 1 &&
+            s + static_cast<uint64_t>(r.src_off) == dsts[0] + static_cast<uint64_t>(r.dst_off))
           continue;
-        add_rect(streams.back(), acc, s, dsts, r, chunk_bytes);
+        add_rect(streams.back(), acc, s, dsts, r, chunk_bytes, mc0);
       }
     }
   }
@@ -194,7 +238,8 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
   for (size_t k = 0, seen = 0; seen < total; ++k)
     for (const auto& st : streams)
       if (k < st.size()) {
-        (st[k].vec ? acc.items : elem).push_back(st[k]);
+        // TMA-eligible (16-byte, no multicast) first; the rest takes the LDG/STG kernel
+        (st[k].vec == kItemVec ? acc.items : elem).push_back(st[k]);
         ++seen;
       }
   acc.n_vec = static_cast<int>(acc.items.size());

@@ -25,12 +25,17 @@ struct Job {
   bool src_is_dst_buffer = false;  // phase B: the leader's destination shard
   std::vector<rlplan::DeviceId> dsts;
   const rlplan::LoweredOp* op = nullptr;
+  // dsts[0] stands for every member of an NVLS multicast group: stored once
+  // through mc_base (multimem.st), replicated by the switch.
+  bool multicast = false;
+  uint64_t mc_base = 0;
 };
 
 struct HostMap {
   std::vector<int> host;     // host id per plan device
   int me = 0;                // executing host
   bool hierarchical = true;  // false: flat delivery, every destination served directly
+  std::vector<uint64_t> mc;  // per plan device: multicast address of its group (0 = none)
 };
 
 // mode 0 = push (source host executes phase A), 1 = pull (destination host).

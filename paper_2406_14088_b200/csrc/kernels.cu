@@ -34,6 +34,14 @@ __device__ __forceinline__ void st_vec(int4* p, const int4& v) {
                : "memory");
 }
 
+// NVLS multicast store: the NVSwitch replicates it into every member buffer.
+// A plain bit move (.f32 is only the element type the v4 form requires).
+__device__ __forceinline__ void st_multimem(int4* p, const int4& v) {
+  asm volatile("multimem.st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
 // Split a flat unit index into (row, col). The float estimate is exact for
 // idx < 2^20 (kMaxItemUnits); the two fix-ups make it robust regardless.
 __device__ __forceinline__ void split_index(uint32_t idx, uint32_t row_units, float inv,
@@ -52,7 +60,7 @@ __device__ __forceinline__ void split_index(uint32_t idx, uint32_t row_units, fl
 
 // `dsts` points at the shared-memory copy of the item's destination table.
 __device__ __forceinline__ void copy_vec_item(const CopyItem& it, const uint64_t* dsts, int ndst,
-                                              uint32_t total) {
+                                              uint32_t total, bool mc0) {
   const int4* __restrict__ src = reinterpret_cast<const int4*>(it.src);
   const uint32_t step = kCopyThreads * kCopyUnroll;
   for (uint32_t base = 0; base < total; base += step) {
@@ -69,7 +77,15 @@ __device__ __forceinline__ void copy_vec_item(const CopyItem& it, const uint64_t
         doff[u] = row * it.dst_pitch + col;  // < 2^32 units: checked on the host
       }
     }
-    for (int j = 0; j < ndst; ++j) {
+    int j = 0;
+    if (mc0) {  // one store through the multicast address reaches every group member
+      int4* dst = reinterpret_cast<int4*>(dsts[0]);
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u)
+        if (doff[u] != 0xffffffffu) st_multimem(dst + doff[u], v[u]);
+      j = 1;
+    }
+    for (; j < ndst; ++j) {
       int4* dst = reinterpret_cast<int4*>(dsts[j]);
 #pragma unroll
       for (int u = 0; u < kCopyUnroll; ++u)
@@ -125,8 +141,8 @@ __global__ void __launch_bounds__(kCopyThreads) rr_copy_kernel(const CopyItem* _
     it.inv_row = sh.inv_row;
     const int ndst = sh.ndst;
     const uint32_t total = it.row_units * it.nrows;
-    if (sh.vec)
-      copy_vec_item(it, sh.dst, ndst, total);
+    if (sh.vec & kItemVec)
+      copy_vec_item(it, sh.dst, ndst, total, (sh.vec & kItemMulticast0) != 0);
     else
       copy_elem_item(it, sh.dst, ndst, total);
   }

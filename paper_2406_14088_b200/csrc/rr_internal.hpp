@@ -4,8 +4,12 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 
 namespace rr {
+
+// Thread-local message returned by rr_last_error() (defined in capi.cpp).
+void set_last_error(const std::string& msg);
 
 // Maximum destinations one work item stores to (fan-out of a broadcast op
 // that is executed by one source read). Larger fan-outs are split.
@@ -15,9 +19,13 @@ constexpr int kMaxFan = 8;
 // copy kernel stays exact (see rr_copy_kernel).
 constexpr uint32_t kMaxItemUnits = 1u << 20;
 
+// CopyItem::vec flags.
+constexpr uint16_t kItemVec = 1;         // 16-byte units (else 2-byte units)
+constexpr uint16_t kItemMulticast0 = 2;  // dst[0] is an NVLS multicast address
+
 // One chunk of a 2D copy: `nrows` rows of `row_units` units; unit = 16 bytes
-// when vec != 0, else 2 bytes (one bf16). Source read once, stored to every
-// dst[0..ndst).
+// when vec has kItemVec, else 2 bytes (one bf16). Source read once, stored to
+// every dst[0..ndst).
 struct alignas(16) CopyItem {
   uint64_t src;
   uint64_t dst[kMaxFan];

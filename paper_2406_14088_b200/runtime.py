@@ -23,7 +23,7 @@ from typing import Dict, Iterable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from ._lib import check, lib
+from ._lib import RrExecOptions, check, lib
 from .rlplan import ReallocPlan
 
 PUSH, PULL = 0, 1
@@ -136,7 +136,7 @@ class Executor:
 
     def __init__(self, plan: ReallocPlan, cuda_device: int, src_ptrs: Dict[int, int], dst_ptrs: Dict[int, int],
                  local: Iterable[int], mode: int = PUSH, chunk_bytes: int = 0,
-                 host_of: Optional[Sequence[int]] = None):
+                 host_of: Optional[Sequence[int]] = None, mc_ptrs: Optional[Dict[int, int]] = None):
         n = plan.cluster.device_count()
         self.plan = plan
         sp, dp = (ctypes.c_void_p * n)(), (ctypes.c_void_p * n)()
@@ -147,9 +147,15 @@ class Executor:
         loc = list(local)
         arr = (ctypes.c_int32 * max(1, len(loc)))(*loc)
         hosts = (ctypes.c_int32 * n)(*host_of) if host_of is not None else None
+        mcs = None
+        if mc_ptrs:
+            mcs = (ctypes.c_void_p * n)()
+            for d, p in mc_ptrs.items():
+                mcs[d] = p
+        opt = RrExecOptions(mode, chunk_bytes, hosts, mcs)
         h = ctypes.c_void_p()
-        check(lib.rr_exec_create(plan.handle, cuda_device, n, sp, dp, len(loc), arr, hosts, mode, chunk_bytes,
-                                 ctypes.byref(h)))
+        check(lib.rr_exec_create_ex(plan.handle, cuda_device, n, sp, dp, len(loc), arr, ctypes.byref(opt),
+                                    ctypes.byref(h)))
         self._h = h
         self.items, self.bytes_written, self.bytes_read = self.stats(0)
         self.fanout_items, self.fanout_written, self.fanout_read = self.stats(1)
@@ -265,6 +271,94 @@ def hosted_devices(n_plan_devices: int, rank: int, world: int) -> List[int]:
     return list(range(rank * k, (rank + 1) * k))
 
 
+def multicast_supported(cuda_device: int = 0) -> bool:
+    out = ctypes.c_int()
+    check(lib.rr_mcast_supported(cuda_device, ctypes.byref(out)))
+    return bool(out.value)
+
+
+_MC_COUNTER = [0]
+
+
+def _share_fd(fd: int, rank: int, world: int, tag: str, group=None) -> int:
+    """Pass rank 0's file descriptor to every rank (SCM_RIGHTS over an
+    abstract AF_UNIX socket; all ranks are on one host)."""
+    import socket
+
+    import torch.distributed as dist
+    name = "\0" + tag
+    if rank == 0:
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(name)
+        srv.listen(world)
+        dist.barrier(group=group)
+        for _ in range(world - 1):
+            conn, _ = srv.accept()
+            socket.send_fds(conn, [b"fd"], [fd])
+            conn.close()
+        srv.close()
+        dist.barrier(group=group)
+        return fd
+    dist.barrier(group=group)
+    s = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    s.connect(name)
+    _msg, fds, _flags, _addr = socket.recv_fds(s, 16, 1)
+    s.close()
+    dist.barrier(group=group)
+    return fds[0]
+
+
+class MulticastBuffer:
+    """One rank's member buffer of an NVLS multicast object (rr_mcast_*).
+
+    Collective over the process group: rank 0 creates the object, the others
+    import it through its file descriptor, every rank adds its GPU, then
+    (after a barrier) binds local memory. ``ptr`` is the ordinary (unicast)
+    address of this rank's member; ``mc_ptr`` the multicast address through
+    which one store reaches every member."""
+
+    def __init__(self, cuda_device: int, nbytes: int, rank: int, world: int, group=None):
+        import os
+
+        import torch.distributed as dist
+        self.cuda_device, self.nbytes = cuda_device, nbytes
+        h = ctypes.c_void_p()
+        meta = [None]
+        if rank == 0:
+            fd, size = ctypes.c_int(), ctypes.c_size_t()
+            check(lib.rr_mcast_create(cuda_device, max(nbytes, 256), world, ctypes.byref(fd), ctypes.byref(size),
+                                      ctypes.byref(h)))
+            _MC_COUNTER[0] += 1
+            meta = [(fd.value, size.value, f"rr-mcast-{os.getpid()}-{_MC_COUNTER[0]}")]
+        dist.broadcast_object_list(meta, src=0, group=group)
+        fd0, size, tag = meta[0]
+        fd_local = _share_fd(fd0 if rank == 0 else -1, rank, world, tag, group)
+        if rank != 0:
+            check(lib.rr_mcast_import(cuda_device, fd_local, size, world, ctypes.byref(h)))
+            os.close(fd_local)
+        self._h = h
+        dist.barrier(group=group)  # every GPU added before anyone binds memory
+        uc, mc = ctypes.c_void_p(), ctypes.c_void_p()
+        check(lib.rr_mcast_bind(h, ctypes.byref(uc), ctypes.byref(mc)))
+        dist.barrier(group=group)
+        self.ptr, self.mc_ptr, self.padded = uc.value, mc.value, size
+
+    def zero(self, stream=None) -> None:
+        check(lib.rr_memset(self.ptr, 0, self.padded, _stream_ptr(stream)))
+
+    def to_host(self) -> np.ndarray:
+        out = np.empty(self.nbytes // 2, dtype=np.uint16)
+        if self.nbytes:
+            check(lib.rr_memcpy(out.ctypes.data, self.ptr, self.nbytes, 1, None, 1))
+        return out
+
+    def free(self) -> None:
+        if self._h and self._h.value:
+            lib.rr_mcast_destroy(self._h)
+            self._h = ctypes.c_void_p(0)
+            self.ptr = 0
+
+
 class RankRealloc:
     """One rank of a one-process-per-GPU reallocation.
 
@@ -279,19 +373,45 @@ class RankRealloc:
 
     def __init__(self, plans: Sequence[ReallocPlan], shards: Dict[str, Tuple[int, int]],
                  bind: Sequence[Tuple[str, str]], rank: int, world: int, cuda_device: int, group=None,
-                 mode: int = PUSH, kernel: int = DEFAULT_KERNEL, hierarchical: bool = True):
+                 mode: int = PUSH, kernel: int = DEFAULT_KERNEL, hierarchical: bool = True,
+                 multicast: Sequence[str] = ()):
+        """``multicast`` names shard sets whose per-GPU leader shards (the
+        lowest-id plan device of the set on each GPU) are members of one NVLS
+        multicast object: a payload bound for every GPU is then stored once
+        (K3) instead of once per GPU (needs world > 1, push mode,
+        hierarchical delivery)."""
         self.plans, self.rank, self.world, self.cuda_device = list(plans), rank, world, cuda_device
         n = plans[0].cluster.device_count()
         self.local = hosted_devices(n, rank, world)
         self.owner = {d: d // (n // world) for d in range(n)}
-        self.buffers: Dict[str, Dict[int, DeviceBuffer]] = {}
+        if multicast and (world < 2 or mode != PUSH or not hierarchical):
+            raise ValueError("multicast needs world > 1, push mode and hierarchical delivery")
+        self.buffers: Dict[str, Dict[int, object]] = {}
+        self.mc_tables: Dict[str, Dict[int, int]] = {}
+        mc_leaders: Dict[str, int] = {}
         for name, (pi, side) in shards.items():
             p = self.plans[pi]
             bufs = {}
-            for d in p.devices(side):
-                if d in self.local:
-                    bufs[d] = DeviceBuffer(cuda_device, p.shard_bytes(side, d))
-                    bufs[d].zero()
+            mine = [d for d in p.devices(side) if d in self.local]
+            if name in multicast:
+                if not mine:
+                    raise ValueError(f"multicast set {name!r}: rank {rank} hosts none of its devices")
+                import torch.distributed as dist
+                leader = min(mine)
+                sizes: List[int] = [None] * world  # type: ignore
+                dist.all_gather_object(sizes, p.shard_bytes(side, leader), group=group)
+                if len(set(sizes)) != 1:
+                    raise ValueError(f"multicast set {name!r}: leader shards differ in size {sizes}")
+                bufs[leader] = MulticastBuffer(cuda_device, sizes[0], rank, world, group)
+                bufs[leader].zero()
+                mc_leaders[name] = leader
+                leaders = [min(d for d in p.devices(side) if d in hosted_devices(n, r, world)) for r in range(world)]
+                self.mc_tables[name] = {d: bufs[leader].mc_ptr for d in leaders}
+            for d in mine:
+                if d in bufs:
+                    continue
+                bufs[d] = DeviceBuffer(cuda_device, p.shard_bytes(side, d))
+                bufs[d].zero()
             self.buffers[name] = bufs
         stream_sync()
         # Exchange IPC handles of every local shard (and the barrier flags).
@@ -300,7 +420,10 @@ class RankRealloc:
         stream_sync()
         mine: dict = {}
         if world > 1:
-            mine = {name: {d: b.ipc_handle() for d, b in bufs.items()} for name, bufs in self.buffers.items()}
+            # multicast members are VMM allocations: reached through the
+            # multicast address, not through CUDA IPC
+            mine = {name: {d: b.ipc_handle() for d, b in bufs.items() if mc_leaders.get(name) != d}
+                    for name, bufs in self.buffers.items()}
             mine["__flags__"] = {rank: self.flags.ipc_handle()}
         gathered: List[dict] = [None] * world  # type: ignore
         if world > 1:
@@ -329,7 +452,8 @@ class RankRealloc:
         self.executors: List[Executor] = []
         for pi, (sname, dname) in enumerate(bind):
             self.executors.append(Executor(self.plans[pi], cuda_device, self.ptrs[sname], self.ptrs[dname],
-                                           self.local, mode, host_of=host_of if hierarchical else None))
+                                           self.local, mode, host_of=host_of if hierarchical else None,
+                                           mc_ptrs=self.mc_tables.get(dname)))
             self.executors[-1].set_kernel(kernel)
         # Every rank must run the same barrier sequence: a phase has a fan-out
         # step if any rank has fan-out work in it.
@@ -356,6 +480,10 @@ class RankRealloc:
                 self.barrier.launch(stream)
 
     def close(self) -> None:
+        stream_sync()
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()  # no rank may still be storing into shared buffers
         for e in self.executors:
             e.close()
         self.barrier.close()

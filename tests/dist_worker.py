@@ -20,7 +20,8 @@ import torch.distributed as dist  # noqa: E402
 from _helpers import placement  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 from paper_2406_14088_b200 import runtime as R  # noqa: E402
-from paper_2406_14088_b200.rlplan import BALANCED, MODELS, b200_cluster, plan_param_realloc  # noqa: E402
+from paper_2406_14088_b200.rlplan import (BALANCED, MODELS, DeviceMesh, ParallelStrategy, Placement,  # noqa: E402
+                                          b200_cluster, plan_param_realloc)
 from paper_2406_14088_b200.workloads import WORKLOADS  # noqa: E402
 
 TINY_GQA = dataclasses.replace(MODELS["tiny"], name="tiny_gqa", hidden_size=512, num_attention_heads=16,
@@ -65,6 +66,32 @@ def main() -> int:
                                     f"{int(np.count_nonzero(got != want))} elements")
             dist.barrier()
             rr.close()
+    # NVLS multicast (K3): one-to-many payloads stored once through multimem.st.
+    if R.multicast_supported(local):
+        mc_cases = [
+            (Placement(DeviceMesh(0, 1, 0, 1), ParallelStrategy()), placement(8, 1, 8, 1)),  # replicate from dev 0
+            (placement(8, 1, 1, 8), placement(8, 1, 8, 1)),                                  # tp8 -> dp8
+        ]
+        for src, dst in mc_cases:
+            plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
+            rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
+                               multicast=["b"])
+            uses_mc = sum(e.stats(0)[0] for e in rr.executors) > 0
+            for d, b in rr.buffers["a"].items():
+                R.fill_shard(plan, R.SRC, d, b.ptr, 23)
+            torch.cuda.synchronize()
+            dist.barrier()
+            rr.run_phase(0)
+            torch.cuda.synchronize()
+            for d, b in rr.buffers["b"].items():
+                got = b.to_host()
+                want = O.fill(TINY_GQA, dst, c, d, 23)
+                if not np.array_equal(got, want):
+                    failures.append(f"multicast {src.strategy}->{dst.strategy}: device {d} differs in "
+                                    f"{int(np.count_nonzero(got != want))} elements (items {uses_mc})")
+            rr.close()
+    elif rank == 0:
+        print("dist_worker: NVLS multicast not supported, skipped", flush=True)
     if os.environ.get("RR_FULL_7B") == "1":
         w = WORKLOADS["llama7b_tp8_dp8_roundtrip"]
         plans = [plan_param_realloc(w.model, s, d, c, BALANCED) for (s, d) in w.phases]
