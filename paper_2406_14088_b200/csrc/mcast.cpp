@@ -202,6 +202,9 @@ rr_status rr_mcast_bind(rr_mcast* m, void** unicast_ptr, void** multicast_ptr) {
     prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     prop.location.id = m->cuda_device;
+    // Binding requires the member memory to carry the multicast object's
+    // handle type (tools/mc_probe.cu: without it cuMulticastBindMem fails).
+    prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     cu(driver().memCreate(&m->mem, m->size, &prop, 0), "cuMemCreate");
     cu(driver().mcBindMem(m->mc, 0, m->mem, 0, m->size, 0), "cuMulticastBindMem");
     m->bound = true;
