@@ -205,7 +205,7 @@ def run_b200(args) -> None:
         src_name = "train" if i == 0 else bind[-1][1]
         bind.append((src_name, dst_name))
     mode = R.PULL if args.mode == "pull" else R.PUSH
-    multicast = [bind[0][1]] if args.mode == "mc" else []
+    multicast = [bind[0][1]] if args.mode == "mc" else ("auto" if args.mode == "auto" else [])
     kernel = R.DEFAULT_KERNEL if args.kernel < 0 else args.kernel
     rr = R.RankRealloc(plans, shards, bind, rank, world, local_rank, mode=mode, kernel=kernel,
                        multicast=multicast)
@@ -370,7 +370,8 @@ def run_b200(args) -> None:
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": w.name, "description": w.description, "plan_devices": w.devices,
                        "plan_devices_per_gpu": w.devices // world, "phases": len(plans),
-                       "policy": args.policy, "mode": args.mode,
+                       "policy": args.policy, "mode": args.mode, "multicast_sets": rr.multicast,
+                       "copy_kernel": kname,
                        "l2": "inputs larger than L2 (multi-GB shards); no flush needed",
                        "weights": "hash-initialised bf16 (seed 1), verified after timing"},
             "phase_ms": [round(float(x), 4) for x in ph_ms_all.max(axis=0)],
@@ -410,8 +411,9 @@ def main() -> None:
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", default="llama7b_tp8_dp8_roundtrip")
     ap.add_argument("--policy", choices=["balanced", "spec"], default="balanced")
-    ap.add_argument("--mode", choices=["push", "pull", "mc"], default="push",
-                    help="mc = push with NVLS multicast for the first phase's destination (N > 1)")
+    ap.add_argument("--mode", choices=["auto", "push", "pull", "mc"], default="auto",
+                    help="push = SM peer stores; mc = push with NVLS multicast for the first phase's "
+                         "destination (N > 1); auto = push, multicast where it lowers the link bottleneck")
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--layers", type=int, default=0, help="truncate the model (profiling only)")
     ap.add_argument("--kernel", type=int, default=-1, help="copy engine: 0 LDG/STG, 1..5 TMA bulk (-1 default)")

@@ -589,10 +589,10 @@ void launch_phase(rr_exec* ex, const rr_exec::Phase& ph, void* stream, int ctas)
     check_cuda(rr::launch_bulk(ex->kernel, ph.d, ph.n_vec, ctas > 0 ? ctas : ex->bulk_ctas, ex->fence_sys, stream,
                                nullptr, ex->d_sched),
                "rr_bulk_kernel launch");
-  if (ph.n > ph.n_vec)
-    check_cuda(rr::launch_copy(ph.d + ph.n_vec, ph.n - ph.n_vec, ex->default_ctas, ex->fence_sys, stream,
-                               ex->d_sched),
-               "rr_copy_kernel launch (2-byte items)");
+  if (ph.n > ph.n_vec)  // multicast and 2-byte items
+    check_cuda(rr::launch_copy(ph.d + ph.n_vec, ph.n - ph.n_vec, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys,
+                               stream, ex->d_sched),
+               "rr_copy_kernel launch (multicast / 2-byte items)");
 }
 
 }  // namespace

@@ -271,6 +271,30 @@ def hosted_devices(n_plan_devices: int, rank: int, world: int) -> List[int]:
     return list(range(rank * k, (rank + 1) * k))
 
 
+def link_bottleneck(plan: ReallocPlan, host_of: Sequence[int], multicast: bool) -> int:
+    """Estimated bottleneck link bytes of a GPU (max over hosts of max(egress,
+    ingress)) for hierarchical push delivery, with or without NVLS multicast
+    of payloads that reach every host (the switch also loops the source's own
+    copy back, so multicast adds ingress at the source)."""
+    hosts = set(host_of)
+    egress = {h: 0 for h in hosts}
+    ingress = {h: 0 for h in hosts}
+    for s, dsts, rects in plan.lowered():
+        b = sum(r[2] * r[5] for r in rects)
+        hs = host_of[s]
+        dst_hosts = {host_of[d] for d in dsts}
+        remote = dst_hosts - {hs}
+        if multicast and dst_hosts == hosts and remote:
+            egress[hs] += b
+            for h in dst_hosts:
+                ingress[h] += b
+        else:
+            egress[hs] += b * len(remote)
+            for h in remote:
+                ingress[h] += b
+    return max(max(egress[h], ingress[h]) for h in hosts)
+
+
 def multicast_supported(cuda_device: int = 0) -> bool:
     out = ctypes.c_int()
     check(lib.rr_mcast_supported(cuda_device, ctypes.byref(out)))
@@ -384,6 +408,18 @@ class RankRealloc:
         n = plans[0].cluster.device_count()
         self.local = hosted_devices(n, rank, world)
         self.owner = {d: d // (n // world) for d in range(n)}
+        if multicast == "auto":
+            # Multicast a phase's destination set only where it lowers the
+            # estimated link bottleneck by >10% (one source feeding many GPUs;
+            # not all-gather patterns, where every GPU is ingress-bound).
+            multicast = []
+            if world > 1 and mode == PUSH and hierarchical and multicast_supported(cuda_device):
+                host_of = [self.owner[d] for d in range(n)]
+                for pi, (_sname, dname) in enumerate(bind):
+                    p = self.plans[pi]
+                    if link_bottleneck(p, host_of, True) < 0.9 * link_bottleneck(p, host_of, False):
+                        multicast.append(dname)
+        self.multicast = list(multicast)
         if multicast and (world < 2 or mode != PUSH or not hierarchical):
             raise ValueError("multicast needs world > 1, push mode and hierarchical delivery")
         self.buffers: Dict[str, Dict[int, object]] = {}
