@@ -119,6 +119,20 @@ ReallocPlan plan_param_realloc(const ModelSpec& model, const Placement& src, con
                                const ClusterSpec& cluster,
                                SourcePolicy policy = SourcePolicy::Spec);
 
+// data produced by one function call and consumed by the
+// next. "Model function calls produce disjoint data partitions along the DP
+// dimension, while replicating the data along the TP dimension":
+// the same greedy broadcast algorithm with TP and DP exchanged. Payloads
+// are slice tp_rank of tp_degree = lcm(dp_producer, dp_consumer) of the data
+// (layer range [0, 0)). PP, like TP, is a replica axis for data: every
+// device of a DP group holds (producer) or needs (consumer) that group's
+// data, so identical placements give an empty plan (DESIGN.md
+// §3 G13). ValidationError on invalid placements or when the data does not
+// split into lcm(dp) equal 2-byte-aligned slices.
+ReallocPlan plan_data_transfer(const Placement& producer, const Placement& consumer,
+                               Bytes data_bytes_per_dp_shard, const ClusterSpec& cluster,
+                               SourcePolicy policy = SourcePolicy::Spec);
+
 // Bytes of one payload.
 Bytes payload_bytes(const ModelSpec& model, const ShardDescriptor& payload);
 
@@ -209,5 +223,21 @@ struct LoweredOp {
 std::vector<LoweredOp> lower_plan(const ModelSpec& model, const Placement& src,
                                   const Placement& dst, const ClusterSpec& cluster,
                                   const ReallocPlan& plan);
+
+// ---------------------------------------------------------------------------
+// Inter-call data (plan_data_transfer) layout and lowering.
+// ---------------------------------------------------------------------------
+
+// Tensor id of the (1-D, bf16-element) data a data-transfer plan moves.
+constexpr int kDataTensor = 0x7fff0000;
+
+// Data held (producer) or needed (consumer) by a device: its DP group's
+// elements, one block [0,1) x [first, last) of kDataTensor at offset 0.
+ShardLayout data_layout(const Placement& p, const ClusterSpec& cluster, DeviceId d, Bytes total_bytes,
+                        bool producer);
+
+// Data-transfer ops lowered to 1-D copy rectangles.
+std::vector<LoweredOp> lower_data_plan(const Placement& producer, const Placement& consumer,
+                                       const ClusterSpec& cluster, Bytes total_bytes, const ReallocPlan& plan);
 
 }  // namespace rlplan

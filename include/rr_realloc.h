@@ -135,6 +135,13 @@ rr_status rr_validate_placement(const rr_model* m, const rr_placement* p, const 
 /* policy: 0 = SPEC tie-break (lowest id), 1 = balanced egress. */
 rr_status rr_plan_create(const rr_model* m, const rr_placement* src, const rr_placement* dst,
                          const rr_cluster* c, int policy, rr_plan** out);                     /* plan_param_realloc */
+/* plan_data_transfer: inter-call data, DP-partitioned on
+ * the producer's last stage, re-sliced at lcm(dp) for every consumer device.
+ * The resulting plan executes like a parameter plan (rr_exec_*); its shard
+ * layout is one 1-D bf16 block per device (tensor id 0x7fff0000). */
+rr_status rr_plan_create_data(const rr_placement* producer, const rr_placement* consumer,
+                              const rr_cluster* c, int64_t data_bytes_per_dp_shard, int policy,
+                              rr_plan** out);
 void rr_plan_destroy(rr_plan* plan);
 rr_status rr_plan_totals(const rr_plan* plan, int64_t* total_bytes, double* est_time);
 rr_status rr_plan_num_ops(const rr_plan* plan, int local, int* n);

@@ -328,3 +328,84 @@ class Reference:
         out = (c_int * 4)()
         rc = self.lib.ref_mesh_from_string(nodes, gpus, text.encode(), out)
         return (None, self.error()) if rc else (tuple(out), None)
+
+
+# ---- inter-call data transfer --------------------------------
+
+DATA_TENSOR = 0x7fff0000
+_lib.orc_plan_data.argtypes = [POINTER(OrcPlacement), POINTER(OrcPlacement), POINTER(OrcCluster), c_int, c_int64,
+                               POINTER(OrcOp), c_int, POINTER(c_int), POINTER(OrcOp), c_int, POINTER(c_int),
+                               POINTER(c_int64), POINTER(c_double)]
+_lib.orc_data_shard_bytes.restype = c_int64
+_lib.orc_data_shard_bytes.argtypes = [POINTER(OrcPlacement), POINTER(OrcCluster), c_int, c_int, c_int64]
+_lib.orc_data_fill.argtypes = [POINTER(OrcPlacement), POINTER(OrcCluster), c_int, c_int, c_int64, c_uint64, c_void_p]
+_lib.orc_data_execute.argtypes = [POINTER(OrcPlacement), POINTER(OrcPlacement), POINTER(OrcCluster), c_int64,
+                                  POINTER(OrcOp), c_int, POINTER(c_void_p), POINTER(c_void_p)]
+
+
+def plan_data(producer, consumer, cluster, data_bytes_per_dp_shard: int, policy: int = 0):
+    cap = 1 << 12
+    ops, loc = (OrcOp * cap)(), (OrcOp * cap)()
+    n, nl = c_int(), c_int()
+    tb, et = c_int64(), c_double()
+    rc = _lib.orc_plan_data(ctypes.byref(_placement(producer)), ctypes.byref(_placement(consumer)),
+                            ctypes.byref(_cluster(cluster)), policy, data_bytes_per_dp_shard, ops, cap,
+                            ctypes.byref(n), loc, cap, ctypes.byref(nl), ctypes.byref(tb), ctypes.byref(et))
+    if rc:
+        return None
+    return ([_op_tuple(ops[i]) for i in range(n.value)], [_op_tuple(loc[i]) for i in range(nl.value)],
+            tb.value, et.value)
+
+
+def data_shard_bytes(placement, cluster, dev: int, producer: bool, total_bytes: int) -> int:
+    return _lib.orc_data_shard_bytes(ctypes.byref(_placement(placement)), ctypes.byref(_cluster(cluster)), dev,
+                                     int(producer), total_bytes)
+
+
+def data_fill(placement, cluster, dev: int, producer: bool, total_bytes: int, seed: int) -> np.ndarray:
+    n = data_shard_bytes(placement, cluster, dev, producer, total_bytes)
+    buf = np.zeros(n // 2, dtype=np.uint16)
+    if n:
+        assert _lib.orc_data_fill(ctypes.byref(_placement(placement)), ctypes.byref(_cluster(cluster)), dev,
+                                  int(producer), total_bytes, seed, buf.ctypes.data) == 0
+    return buf
+
+
+def data_execute(producer, consumer, cluster, total_bytes: int, ops, src_bufs, dst_bufs) -> None:
+    n = cluster.n_nodes * cluster.gpus_per_node
+    sp, dp = (c_void_p * n)(), (c_void_p * n)()
+    for i in range(n):
+        sp[i] = src_bufs[i].ctypes.data if src_bufs[i] is not None else None
+        dp[i] = dst_bufs[i].ctypes.data if dst_bufs[i] is not None else None
+    arr = _ops_array(ops)
+    assert _lib.orc_data_execute(ctypes.byref(_placement(producer)), ctypes.byref(_placement(consumer)),
+                                 ctypes.byref(_cluster(cluster)), total_bytes, arr, len(ops), sp, dp) == 0
+
+
+def replay_data(producer, consumer, cluster, data_bytes_per_dp_shard: int, ops, local_ops):
+    """SPEC.md:586 replay: each consumer device ends with exactly its DP
+    group's slices; every source (right DP rank) holds what it sends."""
+    G = int(np.lcm(producer.strategy.dp, consumer.strategy.dp))
+
+    def ranks(p):
+        devs = _mesh_devices(p, cluster)
+        s = p.strategy
+        return {d: (i // (s.tp * s.dp), (i // s.tp) % s.dp) for i, d in enumerate(devs)}
+    pr, cr = ranks(producer), ranks(consumer)
+    got = {d: [] for d in cr}
+    for (s, dsts, (lo, hi, k, slices, rep), _b) in list(ops) + list(local_ops):
+        if slices != G or rep or s not in pr:
+            return f"bad payload from {s}"
+        pp_r, dp_r = pr[s]
+        if k // (G // producer.strategy.dp) != dp_r:
+            return f"source {s} does not hold slice {k}"
+        for d in dsts:
+            if d not in got:
+                return f"{d} is not a consumer"
+            got[d].append(k)
+    per = G // consumer.strategy.dp
+    for d, ks in got.items():
+        want = list(range(cr[d][1] * per, (cr[d][1] + 1) * per))
+        if sorted(ks) != want:
+            return f"consumer {d} got {sorted(ks)} want {want}"
+    return None

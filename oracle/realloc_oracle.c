@@ -108,16 +108,20 @@ static int rank_of(const orc_placement* p, const orc_cluster* c, int d, int* pp,
 
 /* Mesh shape rules of reference cluster.cpp:43-61, placement rules of
  * SPEC.md:261/268 and the layout codes of DESIGN.md §3. */
-static int placement_ok(const orc_model* m, const orc_placement* p, const orc_cluster* c) {
+static int mesh_ok(const orc_placement* p, const orc_cluster* c) {
   const int M = c->gpus_per_node;
   if (p->node_count < 1 || p->gpu_count < 1 || p->node_offset < 0 || p->gpu_offset < 0) return 0;
   if (p->node_offset + p->node_count > c->n_nodes || p->gpu_offset + p->gpu_count > M) return 0;
   if (p->gpu_count == M ? p->gpu_offset != 0
                         : (p->node_count != 1 || M % p->gpu_count || p->gpu_offset % p->gpu_count))
     return 0;
-  if (p->qkv_layout < 0 || p->qkv_layout > 2 || p->gate_up_layout < 0 || p->gate_up_layout > 1) return 0;
   if (p->dp < 1 || p->tp < 1 || p->pp < 1) return 0;
-  if (p->dp * p->tp * p->pp != mesh_size(p)) return 0;
+  return p->dp * p->tp * p->pp == mesh_size(p);
+}
+
+static int placement_ok(const orc_model* m, const orc_placement* p, const orc_cluster* c) {
+  if (!mesh_ok(p, c)) return 0;
+  if (p->qkv_layout < 0 || p->qkv_layout > 2 || p->gate_up_layout < 0 || p->gate_up_layout > 1) return 0;
   if (p->pp > m->layers || (p->tp & (p->tp - 1)) || m->heads % p->tp) return 0;
   if (p->qkv_layout == 2 && m->kv_heads % p->tp) return 0;
   return 1;
@@ -539,5 +543,102 @@ int orc_execute(const orc_model* m, const orc_placement* src, const orc_placemen
   }
   free(x.s_lay);
   free(x.d_lay);
+  return 0;
+}
+
+/* ---- inter-call data transfer: SPEC.md:578-586, PAPER.md:522 ------------- */
+
+/* Data placements need only a valid mesh and dp*tp*pp == mesh size. */
+static int strategy_ok(const orc_placement* p, const orc_cluster* c) { return mesh_ok(p, c); }
+
+int orc_plan_data(const orc_placement* prod, const orc_placement* cons, const orc_cluster* c, int policy,
+                  int64_t per_shard, orc_op* ops, int cap, int* n_ops, orc_op* local, int cap_local,
+                  int* n_local, int64_t* total_bytes, double* est_time) {
+  if (!strategy_ok(prod, c) || !strategy_ok(cons, c) || per_shard <= 0) return -1;
+  const int G = (int)(prod->dp / gcd64(prod->dp, cons->dp) * cons->dp);
+  const int64_t total = per_shard * prod->dp;
+  if (total % (2 * G)) return -1;
+  const int64_t slice = total / G;
+  const int n_dev = c->n_nodes * c->gpus_per_node;
+  int64_t* egress = calloc((size_t)n_dev, sizeof(int64_t));
+  int holders[64];
+  op_list R = {ops, cap, 0}, Lc = {local, cap_local, 0};
+  int rc = 0;
+  /* consumers in ascending device order == (pp, dp, tp) rank order */
+  for (int i = 0; i < mesh_size(cons) && !rc; ++i) {
+    const int d = mesh_device(cons, c, i);
+    const int dp_r = (i / cons->tp) % cons->dp;
+    for (int k = dp_r * (G / cons->dp); k < (dp_r + 1) * (G / cons->dp) && !rc; ++k) {
+      int nh = 0; /* PP and TP are both replica axes of a DP group's data */
+      for (int s = 0; s < prod->pp; ++s)
+        for (int t = 0; t < prod->tp; ++t) holders[nh++] = device_at(prod, c, s, k / (G / prod->dp), t);
+      qsort(holders, (size_t)nh, sizeof(int), cmp_int);
+      const int s = pick_source(c, holders, nh, d, policy, egress, slice);
+      rc = add_need(s == d ? &Lc : &R, s, d, 0, 0, k, G, 0, slice);
+    }
+  }
+  if (rc) { free(egress); return -1; }
+  double* busy = calloc((size_t)n_dev, sizeof(double));
+  int64_t tb = 0;
+  for (int i = 0; i < R.n; ++i) {
+    double bw = INFINITY;
+    for (int k = 0; k < R.list[i].n_dst; ++k) {
+      const double b = bandwidth(c, R.list[i].src, R.list[i].dst[k]);
+      if (b < bw) bw = b;
+    }
+    busy[R.list[i].src] += (double)R.list[i].bytes / bw;
+    tb += R.list[i].bytes * R.list[i].n_dst;
+  }
+  double est = 0;
+  for (int d = 0; d < n_dev; ++d) if (busy[d] > est) est = busy[d];
+  free(busy);
+  free(egress);
+  *n_ops = R.n;
+  *n_local = Lc.n;
+  *total_bytes = tb;
+  *est_time = est;
+  return 0;
+}
+
+/* First element and element count of a device's data, or -1. */
+static int64_t data_range(const orc_placement* p, const orc_cluster* c, int dev, int producer, int64_t total,
+                          int64_t* first) {
+  int pr, dr, tr;
+  if (rank_of(p, c, dev, &pr, &dr, &tr)) return -1;
+  (void)producer; /* producers and consumers hold their DP group's data */
+  const int64_t per = total / 2 / p->dp;
+  *first = dr * per;
+  return per;
+}
+
+int64_t orc_data_shard_bytes(const orc_placement* p, const orc_cluster* c, int dev, int producer, int64_t total) {
+  int64_t first;
+  const int64_t n = data_range(p, c, dev, producer, total, &first);
+  return n < 0 ? 0 : align256(n * 2);
+}
+
+int orc_data_fill(const orc_placement* p, const orc_cluster* c, int dev, int producer, int64_t total,
+                  uint64_t seed, uint16_t* buf) {
+  int64_t first;
+  const int64_t n = data_range(p, c, dev, producer, total, &first);
+  if (n < 0) return -1;
+  for (int64_t e = 0; e < n; ++e) buf[e] = orc_value(seed, ORC_DATA_TENSOR, first + e);
+  return 0;
+}
+
+int orc_data_execute(const orc_placement* prod, const orc_placement* cons, const orc_cluster* c, int64_t total,
+                     const orc_op* ops, int n_ops, void* const* src_bufs, void* const* dst_bufs) {
+  const int64_t elems = total / 2;
+  for (int o = 0; o < n_ops; ++o) {
+    const orc_op* op = &ops[o];
+    const int64_t s0 = op->slice * elems / op->slices, s1 = (op->slice + 1) * elems / op->slices;
+    int64_t sf, df;
+    if (data_range(prod, c, op->src, 1, total, &sf) < 0) return -1;
+    for (int k = 0; k < op->n_dst; ++k) {
+      if (data_range(cons, c, op->dst[k], 0, total, &df) < 0) return -1;
+      memcpy((uint16_t*)dst_bufs[op->dst[k]] + (s0 - df), (const uint16_t*)src_bufs[op->src] + (s0 - sf),
+             (size_t)(s1 - s0) * 2);
+    }
+  }
   return 0;
 }

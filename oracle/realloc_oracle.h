@@ -79,6 +79,24 @@ int orc_execute(const orc_model* m, const orc_placement* src, const orc_placemen
                 const orc_cluster* c, const orc_op* ops, int n_ops, void* const* src_bufs,
                 void* const* dst_bufs, int threads);
 
+/* ---- inter-call data transfer: SPEC.md:578-586, PAPER.md:522 ----
+ * DP indexes disjoint data slices (finest common slicing lcm(dp)), TP and PP
+ * index replicas: every device of a DP group holds (producer) or needs
+ * (consumer) that group's slices, so identical placements move nothing
+ * (SPEC.md:584). Data elements are bf16 words of tensor id ORC_DATA_TENSOR. */
+#define ORC_DATA_TENSOR 0x7fff0000
+int orc_plan_data(const orc_placement* producer, const orc_placement* consumer, const orc_cluster* c,
+                  int policy, int64_t data_bytes_per_dp_shard, orc_op* ops, int cap, int* n_ops,
+                  orc_op* local, int cap_local, int* n_local, int64_t* total_bytes, double* est_time);
+/* Bytes of a device's data buffer (0 if it holds/needs none). */
+int64_t orc_data_shard_bytes(const orc_placement* p, const orc_cluster* c, int dev, int producer,
+                             int64_t total_bytes);
+int orc_data_fill(const orc_placement* p, const orc_cluster* c, int dev, int producer, int64_t total_bytes,
+                  uint64_t seed, uint16_t* buf);
+int orc_data_execute(const orc_placement* producer, const orc_placement* consumer, const orc_cluster* c,
+                     int64_t total_bytes, const orc_op* ops, int n_ops, void* const* src_bufs,
+                     void* const* dst_bufs);
+
 #ifdef __cplusplus
 }
 #endif

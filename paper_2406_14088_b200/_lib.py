@@ -89,6 +89,8 @@ _SIGNATURES = {
     "rr_plan_create": (c_int, [POINTER(RrModel), POINTER(RrPlacement), POINTER(RrPlacement), POINTER(RrCluster),
                                c_int, POINTER(_P)]),
     "rr_plan_destroy": (None, [_P]),
+    "rr_plan_create_data": (c_int, [POINTER(RrPlacement), POINTER(RrPlacement), POINTER(RrCluster), c_int64, c_int,
+                                    POINTER(_P)]),
     "rr_plan_totals": (c_int, [_P, POINTER(c_int64), POINTER(c_double)]),
     "rr_plan_num_ops": (c_int, [_P, c_int, POINTER(c_int)]),
     "rr_plan_get_op": (c_int, [_P, c_int, c_int, POINTER(RrOp)]),

@@ -130,14 +130,30 @@ struct rr_plan {
   std::vector<LoweredOp> lowered;
   std::map<std::pair<int, DeviceId>, ShardLayout> layouts;
   std::mutex mu;  // guards lazily built layouts
+  bool data = false;     // inter-call data transfer plan (plan_data_transfer)
+  Bytes data_total = 0;  // its total data bytes
 
   const ShardLayout& layout(int side, DeviceId d) {
     std::lock_guard<std::mutex> lock(mu);
     auto key = std::make_pair(side, d);
     auto it = layouts.find(key);
-    if (it == layouts.end())
-      it = layouts.emplace(key, shard_layout(model, side ? dst : src, cluster, d)).first;
+    if (it == layouts.end()) {
+      ShardLayout lay = data ? data_layout(side ? dst : src, cluster, d, data_total, side == 0)
+                             : shard_layout(model, side ? dst : src, cluster, d);
+      it = layouts.emplace(key, std::move(lay)).first;
+    }
     return it->second;
+  }
+
+  // Logical width of a tensor (for the weight value function's index).
+  std::vector<Count> tensor_cols() const {
+    std::vector<Count> cols;
+    if (!data)
+      for (const auto& t : tensor_inventory(model)) cols.push_back(t.cols);
+    return cols;
+  }
+  Count cols_of(const std::vector<Count>& cols, int tensor) const {
+    return tensor == kDataTensor ? data_total / 2 : cols.at(static_cast<size_t>(tensor));
   }
 };
 
@@ -290,6 +306,27 @@ rr_status rr_plan_create(const rr_model* m, const rr_placement* src, const rr_pl
     for (const auto& op : p->plan.ops) p->remote_dst.emplace_back(op.dst.begin(), op.dst.end());
     for (const auto& op : p->plan.local_ops) p->local_dst.emplace_back(op.dst.begin(), op.dst.end());
     p->lowered = lower_plan(p->model, p->src, p->dst, p->cluster, p->plan);
+    *out = p.release();
+  });
+}
+
+rr_status rr_plan_create_data(const rr_placement* producer, const rr_placement* consumer, const rr_cluster* c,
+                              int64_t data_bytes_per_dp_shard, int policy, rr_plan** out) {
+  return guarded([&] {
+    need(out != nullptr, "null output");
+    need(policy == 0 || policy == 1, "policy must be 0 (spec) or 1 (balanced)");
+    auto p = std::make_unique<rr_plan>();
+    p->model.name = "data";
+    p->src = to_placement(producer);
+    p->dst = to_placement(consumer);
+    p->cluster = to_cluster(c);
+    p->data = true;
+    p->plan = plan_data_transfer(p->src, p->dst, data_bytes_per_dp_shard, p->cluster,
+                                 static_cast<SourcePolicy>(policy));
+    p->data_total = data_bytes_per_dp_shard * p->src.strategy.dp;
+    for (const auto& op : p->plan.ops) p->remote_dst.emplace_back(op.dst.begin(), op.dst.end());
+    for (const auto& op : p->plan.local_ops) p->local_dst.emplace_back(op.dst.begin(), op.dst.end());
+    p->lowered = lower_data_plan(p->src, p->dst, p->cluster, p->data_total, p->plan);
     *out = p.release();
   });
 }
@@ -727,8 +764,8 @@ void rr_exec_destroy(rr_exec* ex) {
 
 namespace {
 
-std::vector<rr::FillItem> fill_items(const ShardLayout& lay, const ModelSpec& m, uint64_t base) {
-  const auto inv = tensor_inventory(m);
+std::vector<rr::FillItem> fill_items(const ShardLayout& lay, const rr_plan& plan, uint64_t base) {
+  const auto cols = plan.tensor_cols();
   constexpr uint32_t kChunk = 1u << 16;
   std::vector<rr::FillItem> items;
   for (const auto& b : lay.blocks) {
@@ -739,7 +776,7 @@ std::vector<rr::FillItem> fill_items(const ShardLayout& lay, const ModelSpec& m,
       it.base = base + static_cast<uint64_t>(b.offset);
       it.r0 = static_cast<uint64_t>(b.r0);
       it.c0 = static_cast<uint64_t>(b.c0);
-      it.full_cols = static_cast<uint64_t>(inv[static_cast<size_t>(b.tensor)].cols);
+      it.full_cols = static_cast<uint64_t>(plan.cols_of(cols, b.tensor));
       it.cols = static_cast<uint32_t>(b.c1 - b.c0);
       it.tensor = static_cast<uint32_t>(b.tensor);
       it.elem0 = static_cast<uint32_t>(e);
@@ -769,7 +806,7 @@ rr_status rr_fill_shard(const rr_plan* plan, int side, int32_t device, void* buf
   return guarded([&] {
     need(plan != nullptr && buf != nullptr, "null plan/buffer");
     const auto& lay = const_cast<rr_plan*>(plan)->layout(side, device);
-    const auto items = fill_items(lay, plan->model, reinterpret_cast<uint64_t>(buf));
+    const auto items = fill_items(lay, *plan, reinterpret_cast<uint64_t>(buf));
     DeviceArray<rr::FillItem> d(items);
     auto s = static_cast<cudaStream_t>(stream);
     check_cuda(rr::launch_fill(d.ptr, static_cast<int>(items.size()), seed, s), "rr_fill_kernel launch");
@@ -783,7 +820,7 @@ rr_status rr_verify_shard(const rr_plan* plan, int side, int32_t device, const v
     need(plan != nullptr && buf != nullptr, "null plan/buffer");
     const auto& lay = const_cast<rr_plan*>(plan)->layout(side, device);
     const uint64_t base = reinterpret_cast<uint64_t>(buf);
-    const auto items = fill_items(lay, plan->model, base);
+    const auto items = fill_items(lay, *plan, base);
     DeviceArray<rr::FillItem> d(items);
     const std::vector<unsigned long long> init = {0ull, ~0ull};
     DeviceArray<unsigned long long> counters(init);

@@ -22,7 +22,7 @@ __all__ = [
     "flops", "layer_flops_fwd", "kv_cache_bytes", "logits_bytes", "static_param_bytes",
     "validate_mesh", "enumerate_meshes", "overlap", "link_bandwidth", "local_bandwidth",
     "mesh_to_string", "mesh_from_string", "stage_layer_map", "validate_placement",
-    "plan_param_realloc", "is_power_of_two", "ceil_div", "MODELS", "b200_cluster",
+    "plan_param_realloc", "plan_data_transfer", "is_power_of_two", "ceil_div", "MODELS", "b200_cluster",
     "QKV_SEPARATE", "QKV_CONCAT", "QKV_GROUPED", "GATE_UP_SEPARATE", "GATE_UP_CONCAT",
     "SPEC", "BALANCED",
 ]
@@ -373,6 +373,20 @@ class ReallocPlan:
         if h is not None and h.value:
             lib.rr_plan_destroy(h)
             self._h = ctypes.c_void_p(0)
+
+
+def plan_data_transfer(producer: Placement, consumer: Placement, data_bytes_per_dp_shard: int,
+                       cluster: ClusterSpec, policy: int = SPEC) -> ReallocPlan:
+    """the realloc algorithm with TP and DP exchanged. Payloads
+    are slices (tp_rank of tp_degree = lcm(dp)) of the data; the producer's
+    outputs live on its last pipeline stage, every consumer device of a DP
+    group needs that group's slices (DESIGN.md §3 G13)."""
+    h = ctypes.c_void_p()
+    check(lib.rr_plan_create_data(ctypes.byref(producer._c()), ctypes.byref(consumer._c()),
+                                  ctypes.byref(cluster._c()), data_bytes_per_dp_shard, policy, ctypes.byref(h)))
+    plan = ReallocPlan(h.value, None, producer, consumer, cluster, policy)
+    plan.data_total = data_bytes_per_dp_shard * producer.strategy.dp
+    return plan
 
 
 def plan_param_realloc(model: ModelSpec, src: Placement, dst: Placement, cluster: ClusterSpec,
