@@ -1,0 +1,81 @@
+"""Measured B200 cost model of a reallocation.
+
+The reference's simulator gives a param_realloc node the SPEC estimate
+``est_time = max over sources of sum(bytes / bandwidth)`` (SPEC.md:572,
+SPEC.md:420-428). This module replaces that with the time this executor
+actually takes on B200, from the same lowered work the kernels run:
+
+* per GPU, HBM bytes (every copy reads its source once and writes each
+  local destination; hierarchical fan-out included) at the measured
+  effective copy bandwidth of the TMA bulk kernel;
+* per GPU, link bytes in and out at the measured NVLink rate of the peer
+  store path (or the multicast rate for multicast payloads);
+* phases serialise, GPUs run in parallel: time = max over GPUs of
+  max(HBM time, link time) per phase, plus a fixed launch/barrier cost.
+
+Constants are the r01 measurements (profiles/).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, Optional, Sequence
+
+from .rlplan import ReallocPlan
+
+
+@dataclass(frozen=True)
+class B200Profile:
+    hbm_copy_gbs: float = 6340.0        # read+write bytes/s of rr_bulk_kernel (7B tp8->dp8 forward, 1 GPU)
+    nvlink_push_gbs: float = 708.0      # per GPU per direction, SM peer stores (2/4 GPUs, all-to-all)
+    nvlink_mc_gbs: float = 565.0        # per receiving GPU, NVLS multimem.st (4 GPUs)
+    launch_us: float = 8.0              # kernel launch + dynamic-scheduler tail
+    barrier_us: float = 12.0            # cross-GPU flag barrier
+
+
+def estimate_seconds(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
+                     profile: B200Profile = B200Profile(), multicast: bool = False) -> Dict[str, float]:
+    """Estimated execution time of `plan` with plan device d hosted on GPU
+    host_of[d] (default: one GPU per plan device)."""
+    n = plan.cluster.device_count()
+    host = list(host_of) if host_of is not None else list(range(n))
+    hosts = sorted(set(host))
+    hbm = {h: 0 for h in hosts}
+    fan = {h: 0 for h in hosts}
+    egress = {h: 0 for h in hosts}
+    ingress = {h: 0 for h in hosts}
+    mc_in = {h: 0 for h in hosts}
+    for s, dsts, rects in plan.lowered():
+        b = sum(r[2] * r[5] for r in rects)
+        hs = host[s]
+        groups: Dict[int, list] = {}
+        for d in dsts:
+            groups.setdefault(host[d], []).append(d)
+        local = groups.get(hs, [])
+        hbm[hs] += b * (1 + len(local))      # one read, one write per local destination
+        remote = [h for h in groups if h != hs]
+        use_mc = multicast and set(groups) == set(hosts) and len(remote) > 0
+        if use_mc:
+            egress[hs] += b
+            for h in groups:
+                mc_in[h] += b
+        else:
+            egress[hs] += b * len(remote)
+            for h in remote:
+                ingress[h] += b
+        for h in remote:
+            extra = len(groups[h]) - 1       # hierarchical fan-out inside host h
+            hbm[h] += b                      # the leader replica is written once
+            fan[h] += b * (1 + extra) if extra else 0  # read the leader, write the others
+    t_phase0 = max(max(hbm[h] / (profile.hbm_copy_gbs * 1e9),
+                       max(egress[h], ingress[h]) / (profile.nvlink_push_gbs * 1e9) +
+                       mc_in[h] / (profile.nvlink_mc_gbs * 1e9)) for h in hosts)
+    t_phase1 = max(fan[h] / (profile.hbm_copy_gbs * 1e9) for h in hosts)
+    multi = len(hosts) > 1
+    fixed = profile.launch_us * 1e-6 * (2 if t_phase1 > 0 else 1)
+    if multi:
+        fixed += profile.barrier_us * 1e-6 * (2 if t_phase1 > 0 else 1)
+    total = t_phase0 + t_phase1 + fixed
+    return {"seconds": total, "phase0_s": t_phase0, "fanout_s": t_phase1,
+            "spec_est_time_s": plan.est_time,
+            "max_link_bytes": max(max(egress[h], ingress[h]) + mc_in[h] for h in hosts),
+            "max_hbm_bytes": max(hbm[h] for h in hosts)}

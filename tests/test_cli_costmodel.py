@@ -1,0 +1,84 @@
+"""realloc-plan / data-plan CLI and the
+measured B200 cost model (costmodel.py) against the round-1 measurements."""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from paper_2406_14088_b200 import cli, costmodel
+from paper_2406_14088_b200.rlplan import BALANCED, plan_param_realloc
+from paper_2406_14088_b200.workloads import WORKLOADS
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+EXAMPLE = os.path.join(ROOT, "examples", "llama7b_train_to_gen.json")
+
+
+def run(*args):
+    return subprocess.run([sys.executable, "-m", "paper_2406_14088_b200", *args], cwd=ROOT, capture_output=True,
+                          text=True)
+
+
+def test_realloc_plan_cli_emits_plan_json(tmp_path):
+    out = tmp_path / "plan.json"
+    r = run("realloc-plan", EXAMPLE, "-o", str(out))
+    assert r.returncode == 0, r.stderr
+    plan = json.load(open(out))
+    assert len(plan["ops"]) == 8 and plan["total_bytes"] == 112419930112
+    for op in plan["ops"]:
+        assert {"src", "dst", "layer_range", "slice_index", "bytes"} <= set(op)
+    assert plan["b200_estimate"]["seconds"] > plan["est_time"]
+
+
+def test_identical_src_dst_gives_empty_op_list(tmp_path):
+    """SPEC.md:649."""
+    cfg = json.load(open(EXAMPLE))
+    cfg["dst"] = cfg["src"]
+    p = tmp_path / "same.json"
+    p.write_text(json.dumps(cfg))
+    r = run("realloc-plan", str(p))
+    assert r.returncode == 0 and json.loads(r.stdout)["ops"] == []
+
+
+@pytest.mark.parametrize("edit,path", [
+    (lambda c: c["src"].update(mesh="trainer01:gpu[1-2]"), "$.src.mesh"),
+    (lambda c: c["dst"].update(dp=4), "$: Placement: dp*tp*pp must equal the mesh size"),
+    (lambda c: c.update(model="llama99b"), "$.model: unknown preset"),
+    (lambda c: c.update(schema=2), "$.schema"),
+    (lambda c: c["cluster"].pop("n_nodes"), "$.cluster.n_nodes: missing"),
+])
+def test_config_errors_name_the_path(tmp_path, edit, path):
+    """exit code != 0, diagnostics name the offending path."""
+    cfg = json.load(open(EXAMPLE))
+    edit(cfg)
+    p = tmp_path / "bad.json"
+    p.write_text(json.dumps(cfg))
+    r = run("realloc-plan", str(p))
+    assert r.returncode == 1 and path in r.stderr, r.stderr
+
+
+def test_data_plan_cli(tmp_path):
+    cfg = json.load(open(EXAMPLE))
+    cfg["src"] = {"mesh": "trainer01:gpu[0-1]", "dp": 2, "tp": 1, "pp": 1}
+    cfg["dst"] = {"mesh": "trainer01:gpu[0-3]", "dp": 1, "tp": 4, "pp": 1}
+    cfg["data_bytes_per_dp_shard"] = 1 << 20
+    p = tmp_path / "data.json"
+    p.write_text(json.dumps(cfg))
+    out = cli.build(json.load(open(p)), data=True)
+    assert out["total_bytes"] == 2 * (1 << 20) // 2 * 2 + 2 * (2 << 20)  # 2 holders x half + 2 empty x full
+
+
+@pytest.mark.parametrize("gpus,measured_ms,tol", [
+    (1, 22.79, 0.05),   # r01 forward phase, 1 GPU (HBM-bound)
+    (2, 11.31, 0.05),   # r01 forward phase 0, 2 GPUs (NVLink-bound)
+    (4, 17.03, 0.05),   # r01 forward phase 0, 4 GPUs
+])
+def test_cost_model_matches_round1_measurements(gpus, measured_ms, tol):
+    w = WORKLOADS["llama7b_tp8_dp8_roundtrip"]
+    plan = plan_param_realloc(w.model, *w.phases[0], w.cluster(), BALANCED)
+    host_of = [d // (8 // gpus) for d in range(8)]
+    est = costmodel.estimate_seconds(plan, host_of)
+    assert est["phase0_s"] * 1e3 == pytest.approx(measured_ms, rel=tol)
