@@ -308,10 +308,16 @@ def run_b200(args) -> None:
         d2h = sample * len(res_host)
         torch.cuda.synchronize()
 
+        copy_stream = torch.cuda.Stream()
+        host_ptrs = {d: hb.ptr for d, hb in host.items()}
+
         def e2e_step():
-            for d, b in rr.buffers["train"].items():
-                R.memcpy_async(b.ptr, host[d].ptr, b.nbytes, 0, stream)
-            step()
+            # Phase 0 onloads its sources from pinned host memory, H2D chunks
+            # overlapped with the copy kernels (RankRealloc.run_phase_onload);
+            # then the remaining phases as in the device-resident step.
+            rr.run_phase_onload(0, host_ptrs, copy_stream, stream, args.ctas)
+            for i in range(1, len(plans)):
+                rr.run_phase(i, stream, args.ctas)
             for d, b in rr.buffers[res_name].items():
                 R.memcpy_async(res_host[d].ptr, b.ptr, min(sample, b.nbytes), 1, stream)
             R.stream_sync(stream)

@@ -221,6 +221,16 @@ rr_status rr_exec_set_kernel(rr_exec* ex, int kernel);
 /* Per phase: items, bytes stored (sum over destinations), bytes read. */
 rr_status rr_exec_stats(const rr_exec* ex, int phase, int64_t* items, int64_t* bytes_written,
                         int64_t* bytes_read);
+/* Onload of parked parameters pipelined with the reallocation (PAPER.md:514:
+ * host<->device copies on an additional stream). enable: the local source
+ * shards src_devices[i] are onloaded (their first src_bytes[i] bytes) in
+ * chunk_bytes pieces, in this order; phase-0 copies are regrouped by the
+ * last chunk they read. launch: H2D copies on copy_stream from
+ * host_bufs[device] (pinned) into the executor's source buffers, each
+ * phase-0 segment launched on `stream` as soon as its chunk has landed. */
+rr_status rr_exec_enable_onload(rr_exec* ex, int n_src, const int32_t* src_devices, const int64_t* src_bytes,
+                                int64_t chunk_bytes);
+rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_stream, void* stream, int ctas);
 /* Bytes entering / leaving this executor's host over links per launch. */
 rr_status rr_exec_wire(const rr_exec* ex, int64_t* wire_in, int64_t* wire_out);
 void rr_exec_destroy(rr_exec* ex);

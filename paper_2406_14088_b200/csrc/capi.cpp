@@ -177,6 +177,23 @@ struct rr_exec {
   int bulk_ctas = 0;
   unsigned int* d_sched = nullptr;  // dynamic work counter (see retire_cta)
   int64_t wire_in = 0, wire_out = 0;  // bytes crossing into / out of this host
+
+  // Onload pipelining (rr_exec_enable_onload): phase-0 items regrouped into
+  // segments by the last host->device chunk they read; segment s may start
+  // once chunk s has landed.
+  rr::ItemSet phase0_host;             // items + provenance as built
+  std::vector<void*> src_bases;        // source buffer per plan device
+  struct Segment {
+    int offset = 0, n = 0, n_vec = 0;
+  };
+  std::vector<Segment> segments;       // [0] = no dependency, [1 + c] waits for chunk c
+  rr::CopyItem* d_onload = nullptr;
+  struct Chunk {
+    int32_t device;
+    int64_t offset, bytes;
+  };
+  std::vector<Chunk> chunks;
+  std::vector<cudaEvent_t> events;
 };
 
 struct rr_barrier {
@@ -699,6 +716,9 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
     ex->default_ctas = std::max(1, per_sm) * sms;
     upload(a, ex->phase[0]);
     upload(b, ex->phase[1]);
+    ex->phase0_host = a;
+    ex->src_bases.assign(static_cast<size_t>(n_devices), nullptr);
+    for (int d = 0; d < n_devices; ++d) ex->src_bases[static_cast<size_t>(d)] = src_bufs ? src_bufs[d] : nullptr;
     check_cuda(cudaMalloc(&ex->d_sched, 2 * sizeof(unsigned int)), "cudaMalloc(sched)");
     check_cuda(cudaMemset(ex->d_sched, 0, 2 * sizeof(unsigned int)), "cudaMemset(sched)");
     check_cuda(rr::launch_bulk(ex->kernel, nullptr, 0, 0, 0, nullptr, &ex->bulk_ctas, nullptr), "bulk occupancy");
@@ -751,12 +771,109 @@ rr_status rr_exec_wire(const rr_exec* ex, int64_t* wire_in, int64_t* wire_out) {
   });
 }
 
+rr_status rr_exec_enable_onload(rr_exec* ex, int n_src, const int32_t* src_devices, const int64_t* src_bytes,
+                                 int64_t chunk_bytes) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    need(n_src >= 0 && chunk_bytes >= 4096, "bad onload arguments");
+    check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+    for (auto e : ex->events) cudaEventDestroy(e);
+    ex->events.clear();
+    ex->chunks.clear();
+    std::map<DeviceId, int> first_chunk;
+    for (int i = 0; i < n_src; ++i) {
+      need(src_devices[i] >= 0 && src_devices[i] < static_cast<int>(ex->src_bases.size()), "onload device range");
+      need(ex->src_bases[static_cast<size_t>(src_devices[i])] != nullptr, "onload device has no source buffer");
+      first_chunk[src_devices[i]] = static_cast<int>(ex->chunks.size());
+      for (int64_t off = 0; off < src_bytes[i]; off += chunk_bytes)
+        ex->chunks.push_back({src_devices[i], off, std::min(chunk_bytes, src_bytes[i] - off)});
+    }
+    // Segment of each item: 0 = independent of the onload, 1 + c = needs chunk c.
+    const rr::ItemSet& a = ex->phase0_host;
+    const size_t n = a.items.size(), C = ex->chunks.size();
+    std::vector<std::vector<int>> seg_vec(C + 1), seg_other(C + 1);
+    for (size_t i = 0; i < n; ++i) {
+      int seg = 0;
+      const auto it = first_chunk.find(a.src_dev[i]);
+      if (it != first_chunk.end() && !a.src_is_dst[i]) {
+        const DeviceId d = a.src_dev[i];
+        int64_t total = 0;
+        for (int k = 0; k < n_src; ++k)
+          if (src_devices[k] == d) total = src_bytes[k];
+        need(a.src_end[i] <= total, "an item reads beyond the onloaded bytes of its source");
+        seg = 1 + it->second + static_cast<int>((a.src_end[i] - 1) / chunk_bytes);
+      }
+      (static_cast<int>(i) < a.n_vec ? seg_vec : seg_other)[static_cast<size_t>(seg)].push_back(static_cast<int>(i));
+    }
+    std::vector<rr::CopyItem> ordered;
+    ordered.reserve(n);
+    ex->segments.assign(C + 1, {});
+    for (size_t s = 0; s <= C; ++s) {
+      auto& sg = ex->segments[s];
+      sg.offset = static_cast<int>(ordered.size());
+      for (int i : seg_vec[s]) ordered.push_back(a.items[static_cast<size_t>(i)]);
+      sg.n_vec = static_cast<int>(seg_vec[s].size());
+      for (int i : seg_other[s]) ordered.push_back(a.items[static_cast<size_t>(i)]);
+      sg.n = static_cast<int>(ordered.size()) - sg.offset;
+    }
+    if (ex->d_onload) cudaFree(ex->d_onload);
+    ex->d_onload = nullptr;
+    if (!ordered.empty()) {
+      check_cuda(cudaMalloc(&ex->d_onload, ordered.size() * sizeof(rr::CopyItem)), "cudaMalloc(onload items)");
+      check_cuda(cudaMemcpy(ex->d_onload, ordered.data(), ordered.size() * sizeof(rr::CopyItem),
+                            cudaMemcpyHostToDevice),
+                 "upload onload items");
+    }
+    ex->events.resize(C);
+    for (auto& e : ex->events) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+  });
+}
+
+rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_stream, void* stream, int ctas) {
+  return guarded([&] {
+    need(ex != nullptr && host_bufs != nullptr, "null executor/host buffers");
+    need(!ex->segments.empty(), "rr_exec_enable_onload has not been called");
+    check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+    auto cs = static_cast<cudaStream_t>(copy_stream);
+    auto ks = static_cast<cudaStream_t>(stream);
+    // The copy stream must not overwrite sources still read by an earlier
+    // launch on the compute stream.
+    cudaEvent_t ready;
+    check_cuda(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "cudaEventCreate");
+    check_cuda(cudaEventRecord(ready, ks), "cudaEventRecord");
+    check_cuda(cudaStreamWaitEvent(cs, ready, 0), "cudaStreamWaitEvent");
+    cudaEventDestroy(ready);
+    for (size_t c = 0; c < ex->chunks.size(); ++c) {
+      const auto& ch = ex->chunks[c];
+      const void* h = host_bufs[ch.device];
+      need(h != nullptr, "missing host buffer for an onloaded device");
+      char* dst = static_cast<char*>(ex->src_bases[static_cast<size_t>(ch.device)]) + ch.offset;
+      check_cuda(cudaMemcpyAsync(dst, static_cast<const char*>(h) + ch.offset, static_cast<size_t>(ch.bytes),
+                                 cudaMemcpyHostToDevice, cs),
+                 "onload cudaMemcpyAsync");
+      check_cuda(cudaEventRecord(ex->events[c], cs), "cudaEventRecord");
+    }
+    for (size_t s = 0; s < ex->segments.size(); ++s) {
+      if (s > 0) check_cuda(cudaStreamWaitEvent(ks, ex->events[s - 1], 0), "cudaStreamWaitEvent");
+      const auto& sg = ex->segments[s];
+      if (sg.n == 0) continue;
+      rr_exec::Phase ph;
+      ph.d = ex->d_onload + sg.offset;
+      ph.n = sg.n;
+      ph.n_vec = sg.n_vec;
+      launch_phase(ex, ph, stream, ctas);
+    }
+  });
+}
+
 void rr_exec_destroy(rr_exec* ex) {
   if (!ex) return;
   cudaSetDevice(ex->cuda_device);
   for (auto& ph : ex->phase)
     if (ph.d) cudaFree(ph.d);
   if (ex->d_sched) cudaFree(ex->d_sched);
+  if (ex->d_onload) cudaFree(ex->d_onload);
+  for (auto e : ex->events) cudaEventDestroy(e);
   delete ex;
 }
 

@@ -145,9 +145,17 @@ void host_wire_bytes(const std::vector<LoweredOp>& ops, const HostMap& hm, int64
 
 namespace {
 
+// An item plus where it reads from (for onload pipelining).
+struct Tagged {
+  CopyItem it;
+  DeviceId src_dev;
+  int64_t src_end;
+  bool src_is_dst;
+};
+
 // Chunk one rectangle for (src base, dst bases) into items.
-void add_rect(std::vector<CopyItem>& out, ItemSet& acc, uint64_t src, const std::vector<uint64_t>& dsts,
-              const CopyRect& r, int64_t chunk, bool mc0) {
+void add_rect(std::vector<Tagged>& out, ItemSet& acc, uint64_t src, const std::vector<uint64_t>& dsts,
+              const CopyRect& r, int64_t chunk, bool mc0, DeviceId src_dev, bool src_is_dst) {
   const bool vec = ((src | static_cast<uint64_t>(r.src_off | r.dst_off | r.row_bytes | r.src_pitch | r.dst_pitch)) &
                     15) == 0 &&
                    std::all_of(dsts.begin(), dsts.end(), [](uint64_t d) { return (d & 15) == 0; });
@@ -159,7 +167,8 @@ void add_rect(std::vector<CopyItem>& out, ItemSet& acc, uint64_t src, const std:
   auto emit = [&](int64_t row0, int64_t col0, int64_t rows, int64_t cols) {
     CopyItem it;
     std::memset(&it, 0, sizeof(it));
-    it.src = src + static_cast<uint64_t>(r.src_off + (row0 * sp + col0) * unit);
+    const int64_t src_begin = r.src_off + (row0 * sp + col0) * unit;
+    it.src = src + static_cast<uint64_t>(src_begin);
     for (size_t j = 0; j < dsts.size(); ++j)
       it.dst[j] = dsts[j] + static_cast<uint64_t>(r.dst_off + (row0 * dp + col0) * unit);
     it.ndst = static_cast<uint16_t>(dsts.size());
@@ -171,7 +180,7 @@ void add_rect(std::vector<CopyItem>& out, ItemSet& acc, uint64_t src, const std:
     it.inv_row = 1.0f / static_cast<float>(cols);
     if (rows > 1 && ((rows - 1) * dp + cols >= (int64_t{1} << 32) || (rows - 1) * sp + cols >= (int64_t{1} << 32)))
       throw rlplan::ValidationError("copy item spans more than 2^32 units");
-    out.push_back(it);
+    out.push_back({it, src_dev, src_begin + ((rows - 1) * sp + cols) * unit, src_is_dst});
     const int64_t bytes = rows * cols * unit;
     acc.read += bytes;
     acc.written += bytes * static_cast<int64_t>(dsts.size());
@@ -197,7 +206,7 @@ uint64_t base_of(void* const* bufs, DeviceId d, const char* what) {
 ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, void* const* src_bufs,
                     void* const* dst_bufs, int64_t chunk_bytes) {
   ItemSet acc;
-  std::vector<std::vector<CopyItem>> streams;
+  std::vector<std::vector<Tagged>> streams;
   const bool accounting = src_bufs == nullptr;
   for (const auto& j : jobs) {
     if (j.phase != phase) continue;
@@ -225,26 +234,33 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
         if (!accounting && !mc0 && dsts.size() == 1 &&
             s + static_cast<uint64_t>(r.src_off) == dsts[0] + static_cast<uint64_t>(r.dst_off))
           continue;
-        add_rect(streams.back(), acc, s, dsts, r, chunk_bytes, mc0);
+        add_rect(streams.back(), acc, s, dsts, r, chunk_bytes, mc0, j.src, j.src_is_dst_buffer);
       }
     }
   }
   // Interleave the per-job streams round-robin so concurrently running CTAs
   // spread their stores over many destinations (NVLink ingress balance).
-  std::vector<CopyItem> elem;
+  // TMA-eligible items (16-byte, no multicast) first; the rest take the
+  // LDG/STG kernel.
+  std::vector<const Tagged*> vec_items, other;
   size_t total = 0;
   for (const auto& st : streams) total += st.size();
-  acc.items.reserve(total);
   for (size_t k = 0, seen = 0; seen < total; ++k)
     for (const auto& st : streams)
       if (k < st.size()) {
-        // TMA-eligible (16-byte, no multicast) first; the rest takes the LDG/STG kernel
-        (st[k].vec == kItemVec ? acc.items : elem).push_back(st[k]);
+        (st[k].it.vec == kItemVec ? vec_items : other).push_back(&st[k]);
         ++seen;
       }
-  acc.n_vec = static_cast<int>(acc.items.size());
-  acc.items.insert(acc.items.end(), elem.begin(), elem.end());
-  if (acc.items.size() >= (size_t{1} << 31)) throw rlplan::ValidationError("too many copy items");
+  acc.n_vec = static_cast<int>(vec_items.size());
+  vec_items.insert(vec_items.end(), other.begin(), other.end());
+  if (vec_items.size() >= (size_t{1} << 31)) throw rlplan::ValidationError("too many copy items");
+  acc.items.reserve(vec_items.size());
+  for (const Tagged* t : vec_items) {
+    acc.items.push_back(t->it);
+    acc.src_dev.push_back(t->src_dev);
+    acc.src_end.push_back(t->src_end);
+    acc.src_is_dst.push_back(t->src_is_dst);
+  }
   return acc;
 }
 

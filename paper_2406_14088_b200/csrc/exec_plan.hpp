@@ -54,6 +54,11 @@ struct ItemSet {
   int n_vec = 0;
   int64_t read = 0, written = 0;
   bool remote_stores = false;  // some destination is on another host
+  // Per item (same order): the device whose buffer it reads and one past the
+  // last source byte it reads (onload pipelining, rr_exec_enable_onload).
+  std::vector<rlplan::DeviceId> src_dev;
+  std::vector<int64_t> src_end;
+  std::vector<bool> src_is_dst;  // reads a destination (leader) buffer
 };
 
 // Resolve jobs of `phase` into items. src_bufs/dst_bufs are indexed by plan

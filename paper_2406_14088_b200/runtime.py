@@ -175,6 +175,23 @@ class Executor:
     def launch_fanout(self, stream=None, ctas: int = 0) -> None:
         check(lib.rr_exec_launch_fanout(self._h, _stream_ptr(stream), ctas))
 
+    def enable_onload(self, src_bytes: Dict[int, int], chunk_bytes: int = 256 << 20) -> None:
+        """Prepare onload pipelining: the local source shards {device: bytes}
+        are copied host->device in chunk_bytes pieces (in device order)."""
+        devs = sorted(src_bytes)
+        arr = (ctypes.c_int32 * max(1, len(devs)))(*devs)
+        sizes = (ctypes.c_int64 * max(1, len(devs)))(*[src_bytes[d] for d in devs])
+        check(lib.rr_exec_enable_onload(self._h, len(devs), arr, sizes, chunk_bytes))
+
+    def launch_onload(self, host_ptrs: Dict[int, int], copy_stream, stream=None, ctas: int = 0) -> None:
+        """Phase 0 with its sources onloaded from pinned host memory on
+        ``copy_stream``; each copy segment starts as soon as its chunk lands."""
+        n = self.plan.cluster.device_count()
+        hp = (ctypes.c_void_p * n)()
+        for d, p in host_ptrs.items():
+            hp[d] = p
+        check(lib.rr_exec_launch_onload(self._h, hp, _stream_ptr(copy_stream), _stream_ptr(stream), ctas))
+
     def set_kernel(self, kernel: int) -> None:
         """0 = LDG/STG kernel, 1..10 = TMA bulk-copy ring variants."""
         check(lib.rr_exec_set_kernel(self._h, kernel))
@@ -484,6 +501,7 @@ class RankRealloc:
                     else:
                         self.ptrs[name][d] = p
         self.barrier = Barrier(cuda_device, rank, world, flag_ptrs)
+        self.bind = list(bind)
         host_of = [self.owner[d] for d in range(n)]
         self.executors: List[Executor] = []
         for pi, (sname, dname) in enumerate(bind):
@@ -509,11 +527,28 @@ class RankRealloc:
         """Phase i: direct copies, barrier, then (if any rank has some) the
         in-host fan-out from leader replicas and another barrier."""
         self.executors[i].launch(stream, ctas)
+        self._finish_phase(i, stream, ctas)
+
+    def _finish_phase(self, i: int, stream, ctas: int) -> None:
         if self.world > 1:
             self.barrier.launch(stream)
             if self.has_fanout[i]:
                 self.executors[i].launch_fanout(stream, ctas)
                 self.barrier.launch(stream)
+
+    def run_phase_onload(self, i: int, host_ptrs: Dict[int, int], copy_stream, stream=None, ctas: int = 0,
+                         chunk_bytes: int = 256 << 20) -> None:
+        """Phase i with its local source shards onloaded from pinned host
+        memory (host_ptrs: device -> pointer), H2D chunks overlapped with the
+        copy kernels."""
+        e = self.executors[i]
+        sname = self.bind[i][0]
+        key = (i, chunk_bytes)
+        if getattr(self, "_onload_key", {}).get(i) != key:
+            e.enable_onload({d: b.nbytes for d, b in self.buffers[sname].items()}, chunk_bytes)
+            self._onload_key = {**getattr(self, "_onload_key", {}), i: key}
+        e.launch_onload(host_ptrs, copy_stream, stream, ctas)
+        self._finish_phase(i, stream, ctas)
 
     def close(self) -> None:
         stream_sync()

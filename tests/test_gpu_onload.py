@@ -1,0 +1,53 @@
+"""Onload of parked parameters pipelined with the reallocation (
+SURVEY.md §8(f) rank 2): source shards come from pinned host memory in
+chunks on a side stream, copy segments start as their chunk lands. Results
+are bit-exact against the CPU oracle."""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+from _helpers import placement
+from oracle import oracle as O
+from paper_2406_14088_b200 import runtime as R
+from paper_2406_14088_b200.rlplan import BALANCED, MODELS, b200_cluster, plan_param_realloc
+
+pytestmark = pytest.mark.gpu
+
+TINY_GQA = dataclasses.replace(MODELS["tiny"], name="tiny_gqa", hidden_size=512, num_attention_heads=16,
+                               num_kv_heads=8, intermediate_size=1024)
+
+
+@pytest.mark.parametrize("sp,dp", [((1, 1, 8, 0, 0), (1, 8, 1, 0, 0)), ((4, 1, 2, 2, 1), (1, 1, 8, 1, 1))])
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_onload_pipeline_bitexact(need_gpu, sp, dp, kernel):
+    import torch
+    c = b200_cluster(8)
+    src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
+    dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
+    plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
+    vc = R.VirtualCluster(plan, 0)
+    hosts = {}
+    try:
+        for d, b in vc.src.items():   # parked parameters: pinned host copies of the source shards
+            hb = R.HostBuffer(b.nbytes)
+            hb.array()[:] = O.fill(TINY_GQA, src, c, d, 31)
+            hosts[d] = hb
+            b.zero()
+        ex = vc.executor(R.PUSH, 4096, kernel)
+        ex.enable_onload({d: b.nbytes for d, b in vc.src.items()}, chunk_bytes=64 << 10)
+        copy = torch.cuda.Stream()
+        for _ in range(2):  # re-launchable
+            for b in vc.dst.values():
+                b.zero()
+            ex.launch_onload({d: h.ptr for d, h in hosts.items()}, copy, torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            for d, b in vc.dst.items():
+                assert np.array_equal(b.to_host(), O.fill(TINY_GQA, dst, c, d, 31)), d
+        ex.close()
+    finally:
+        vc.free()
+        for h in hosts.values():
+            h.free()
