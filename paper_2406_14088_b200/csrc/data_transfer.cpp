@@ -128,7 +128,8 @@ std::vector<LoweredOp> lower_data_plan(const Placement& prod, const Placement& c
     for (DeviceId d : lo.dst)  // one DP group: identical element ranges
       if (data_layout(cons, cluster, d, total_bytes, false).blocks.at(0).c0 != bd.c0)
         throw ValidationError("lower_data_plan: destinations of one op differ in geometry");
-    if (s0 < bs.c0 || s1 > bs.c1 || s0 < bd.c0 || s1 > bd.c1)
+    if (s0 < bs.c0 || s1 > bs.c1 || s0 < bd.c0 || s1 > bd.c1 || (s1 - bs.c0) * 2 > src.bytes ||
+        (s1 - bd.c0) * 2 > dst.bytes)
       throw ValidationError("lower_data_plan: slice outside a shard");
     CopyRect r;
     r.src_off = (s0 - bs.c0) * 2;

@@ -323,6 +323,15 @@ std::vector<LoweredOp> lower_plan(const ModelSpec& m, const Placement& src, cons
       if (covered != (want.r1 - want.r0) * (want.c1 - want.c0))
         throw ValidationError("lower_plan: source/destination layouts do not cover the payload");
     }
+    // Bounds: every rectangle lies inside both shards (compute-sanitizer is
+    // unavailable on the GPU pool, so out-of-bounds copies are ruled out here).
+    const Bytes s_bytes = s_lay[lo.src].bytes, d_bytes = d_lay[lo.dst.front()].bytes;
+    for (const auto& r : lo.rects) {
+      const Bytes s_end = r.src_off + (r.rows - 1) * r.src_pitch + r.row_bytes;
+      const Bytes d_end = r.dst_off + (r.rows - 1) * r.dst_pitch + r.row_bytes;
+      if (r.src_off < 0 || r.dst_off < 0 || r.rows < 1 || r.row_bytes < 1 || s_end > s_bytes || d_end > d_bytes)
+        throw ValidationError("lower_plan: copy rectangle outside a shard");
+    }
   }
   return out;
 }
