@@ -205,10 +205,13 @@ def run_b200(args) -> None:
         src_name = "train" if i == 0 else bind[-1][1]
         bind.append((src_name, dst_name))
     mode = R.PULL if args.mode == "pull" else R.PUSH
-    multicast = [bind[0][1]] if args.mode == "mc" else ("auto" if args.mode == "auto" else [])
+    # auto: peer stores, plus the pipelined relay where it lowers the link
+    # bottleneck (single source feeding many GPUs); mc: NVLS multicast instead.
+    multicast = [bind[0][1]] if args.mode == "mc" else []
+    relay = {"auto": "auto", "relay": True}.get(args.mode, False)
     kernel = R.DEFAULT_KERNEL if args.kernel < 0 else args.kernel
     rr = R.RankRealloc(plans, shards, bind, rank, world, local_rank, mode=mode, kernel=kernel,
-                       multicast=multicast)
+                       multicast=multicast, relay=relay)
     stream = torch.cuda.current_stream()
     seed = 1
     for d, b in rr.buffers["train"].items():
@@ -254,7 +257,7 @@ def run_b200(args) -> None:
     ms = t0.elapsed_time(t1) / args.steps
     phase_ms = [sum(evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(args.steps)) / args.steps
                 for i in range(len(plans))]
-    timed_out = rr.barrier.timed_out() if world > 1 else False
+    timed_out = (rr.barrier.timed_out() or rr.relay_timeouts() > 0) if world > 1 else False
 
     # Whole-job bytes: every rank's executor work (sum), delivered = written
     # (direct copies plus in-host fan-out); link bytes per GPU from the
@@ -377,6 +380,7 @@ def run_b200(args) -> None:
             "config": {"workload": w.name, "description": w.description, "plan_devices": w.devices,
                        "plan_devices_per_gpu": w.devices // world, "phases": len(plans),
                        "policy": args.policy, "mode": args.mode, "multicast_sets": rr.multicast,
+                       "relay_phases": rr.relay_phases,
                        "copy_kernel": kname,
                        "l2": "inputs larger than L2 (multi-GB shards); no flush needed",
                        "weights": "hash-initialised bf16 (seed 1), verified after timing"},
@@ -417,9 +421,10 @@ def main() -> None:
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", default="llama7b_tp8_dp8_roundtrip")
     ap.add_argument("--policy", choices=["balanced", "spec"], default="balanced")
-    ap.add_argument("--mode", choices=["auto", "push", "pull", "mc"], default="auto",
-                    help="push = SM peer stores; mc = push with NVLS multicast for the first phase's "
-                         "destination (N > 1); auto = push, multicast where it lowers the link bottleneck")
+    ap.add_argument("--mode", choices=["auto", "push", "pull", "mc", "relay"], default="auto",
+                    help="push = SM peer stores; relay = push + pipelined relay for payloads reaching >= 2 "
+                         "other GPUs; mc = push + NVLS multicast for the first phase's destination (N > 1); "
+                         "auto = push, relay where it lowers the link bottleneck")
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--layers", type=int, default=0, help="truncate the model (profiling only)")
     ap.add_argument("--kernel", type=int, default=-1, help="copy engine: 0 LDG/STG, 1..5 TMA bulk (-1 default)")

@@ -246,7 +246,18 @@ typedef struct {
   int64_t chunk_bytes;        /* 0 = 256 KiB */
   const int32_t* host_of;     /* NULL = flat delivery */
   void* const* mc_bufs;       /* NULL = no multicast */
+  /* Pipelined relay (push, hierarchical): relay_flags[d] = the uint32 flag
+   * array (rr_plan_relay_slots entries, zeroed once, mapped here) of plan
+   * device d's host. A payload reaching >= 2 other hosts then travels
+   * source -> host 1 -> host 2 ... chunk by chunk, each host forwarding and
+   * fanning out locally as chunks land. NULL = no relay. */
+  void* const* relay_flags;
 } rr_exec_options;
+/* Length of the relay flag array for this host map and chunk size
+ * (identical on every rank). */
+rr_status rr_plan_relay_slots(const rr_plan* plan, const int32_t* host_of, int64_t chunk_bytes, int64_t* slots);
+/* Relay waits that timed out (bounded spins) since the executor was created. */
+rr_status rr_exec_relay_timeouts(rr_exec* ex, int64_t* timeouts);
 rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices, void* const* src_bufs,
                             void* const* dst_bufs, int n_local, const int32_t* local,
                             const rr_exec_options* options, rr_exec** out);

@@ -177,6 +177,7 @@ struct rr_exec {
   int bulk_ctas = 0;
   unsigned int* d_sched = nullptr;  // dynamic work counter (see retire_cta)
   int64_t wire_in = 0, wire_out = 0;  // bytes crossing into / out of this host
+  uint32_t epoch = 0;                 // relay flag epoch, advanced by every phase-0 launch
 
   // Onload pipelining (rr_exec_enable_onload): phase-0 items regrouped into
   // segments by the last host->device chunk they read; segment s may start
@@ -635,18 +636,21 @@ void launch_phase(rr_exec* ex, const rr_exec::Phase& ph, void* stream, int ctas)
   check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
   if (ph.n == 0) return;
   if (ex->kernel == 0) {
-    check_cuda(rr::launch_copy(ph.d, ph.n, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys, stream, ex->d_sched),
+    check_cuda(rr::launch_copy(ph.d, ph.n, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys, stream, ex->d_sched,
+                               ex->epoch),
                "rr_copy_kernel launch");
     return;
   }
+  // Relay, multicast and 2-byte items take the LDG/STG kernel, launched
+  // first so relay chains start immediately; then the TMA bulk kernel.
+  if (ph.n > ph.n_vec)
+    check_cuda(rr::launch_copy(ph.d + ph.n_vec, ph.n - ph.n_vec, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys,
+                               stream, ex->d_sched, ex->epoch),
+               "rr_copy_kernel launch (relay / multicast / 2-byte items)");
   if (ph.n_vec > 0)
     check_cuda(rr::launch_bulk(ex->kernel, ph.d, ph.n_vec, ctas > 0 ? ctas : ex->bulk_ctas, ex->fence_sys, stream,
                                nullptr, ex->d_sched),
                "rr_bulk_kernel launch");
-  if (ph.n > ph.n_vec)  // multicast and 2-byte items
-    check_cuda(rr::launch_copy(ph.d + ph.n_vec, ph.n - ph.n_vec, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys,
-                               stream, ex->d_sched),
-               "rr_copy_kernel launch (multicast / 2-byte items)");
 }
 
 }  // namespace
@@ -697,6 +701,13 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       hm.mc.resize(hm.host.size());
       for (size_t d = 0; d < hm.mc.size(); ++d) hm.mc[d] = reinterpret_cast<uint64_t>(options->mc_bufs[d]);
     }
+    hm.relay_chunk = chunk_bytes;
+    if (options->relay_flags) {
+      need(options->host_of != nullptr && mode == 0, "relay needs a host_of table and push mode");
+      hm.relay_flags.resize(hm.host.size());
+      for (size_t d = 0; d < hm.relay_flags.size(); ++d)
+        hm.relay_flags[d] = reinterpret_cast<uint64_t>(options->relay_flags[d]);
+    }
     const auto jobs = rr::build_jobs(plan->lowered, hm, mode);
     const auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes);
     const auto b = rr::build_items(jobs, 1, hm, src_bufs, dst_bufs, chunk_bytes);
@@ -719,8 +730,8 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
     ex->phase0_host = a;
     ex->src_bases.assign(static_cast<size_t>(n_devices), nullptr);
     for (int d = 0; d < n_devices; ++d) ex->src_bases[static_cast<size_t>(d)] = src_bufs ? src_bufs[d] : nullptr;
-    check_cuda(cudaMalloc(&ex->d_sched, 2 * sizeof(unsigned int)), "cudaMalloc(sched)");
-    check_cuda(cudaMemset(ex->d_sched, 0, 2 * sizeof(unsigned int)), "cudaMemset(sched)");
+    check_cuda(cudaMalloc(&ex->d_sched, 4 * sizeof(unsigned int)), "cudaMalloc(sched)");
+    check_cuda(cudaMemset(ex->d_sched, 0, 4 * sizeof(unsigned int)), "cudaMemset(sched)");
     check_cuda(rr::launch_bulk(ex->kernel, nullptr, 0, 0, 0, nullptr, &ex->bulk_ctas, nullptr), "bulk occupancy");
     *out = ex.release();
   });
@@ -729,7 +740,28 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
 rr_status rr_exec_launch(rr_exec* ex, void* stream, int ctas) {
   return guarded([&] {
     need(ex != nullptr, "null executor");
+    ++ex->epoch;  // every rank launches phase 0 the same number of times
     launch_phase(ex, ex->phase[0], stream, ctas);
+  });
+}
+
+rr_status rr_exec_relay_timeouts(rr_exec* ex, int64_t* timeouts) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+    unsigned int h[4];
+    check_cuda(cudaMemcpy(h, ex->d_sched, sizeof(h), cudaMemcpyDeviceToHost), "read relay status");
+    *timeouts = h[2];
+  });
+}
+
+rr_status rr_plan_relay_slots(const rr_plan* plan, const int32_t* host_of, int64_t chunk_bytes, int64_t* slots) {
+  return guarded([&] {
+    need(plan != nullptr && host_of != nullptr, "null plan/host table");
+    rr::HostMap hm;
+    for (int d = 0; d < plan->cluster.device_count(); ++d) hm.host.push_back(host_of[d]);
+    hm.relay_chunk = chunk_bytes > 0 ? chunk_bytes : (256 << 10);
+    *slots = rr::relay_slots(plan->lowered, hm);
   });
 }
 
@@ -834,6 +866,7 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
     need(ex != nullptr && host_bufs != nullptr, "null executor/host buffers");
     need(!ex->segments.empty(), "rr_exec_enable_onload has not been called");
     check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+    ++ex->epoch;  // a phase-0 launch like rr_exec_launch
     auto cs = static_cast<cudaStream_t>(copy_stream);
     auto ks = static_cast<cudaStream_t>(stream);
     // The copy stream must not overwrite sources still read by an earlier

@@ -50,7 +50,59 @@ bool multicast_target(const std::map<int, std::vector<DeviceId>>& groups, const 
   return true;
 }
 
+// Pieces add_rect cuts a 16-byte-unit rectangle into (the same rule).
+int64_t pieces_of(const CopyRect& r, int64_t chunk) {
+  const int64_t cap_units = std::min<int64_t>(chunk / 16, kMaxItemUnits);
+  const int64_t row_units = r.row_bytes / 16;
+  if (row_units <= cap_units) {
+    const int64_t rows_per = std::max<int64_t>(1, cap_units / std::max<int64_t>(row_units, 1));
+    return (r.rows + rows_per - 1) / rows_per;
+  }
+  return r.rows * ((row_units + cap_units - 1) / cap_units);
+}
+
+// Remote destination hosts in ring order after the source host.
+std::vector<int> relay_chain(const std::map<int, std::vector<DeviceId>>& groups, int hs) {
+  std::vector<int> chain;
+  int span = 1;
+  for (const auto& kv : groups) span = std::max(span, std::abs(kv.first - hs) + 1);
+  for (const auto& kv : groups)
+    if (kv.first != hs) chain.push_back(kv.first);
+  std::sort(chain.begin(), chain.end(), [&](int a, int b) {
+    return ((a - hs) % span + span) % span < ((b - hs) % span + span) % span;
+  });
+  return chain;
+}
+
+// Relay pays off when a payload reaches >= 2 other hosts (it caps every
+// host's egress at one copy). Needs 16-byte geometry on both sides (the
+// source and the forwarders cut identical pieces) and small fan-outs.
+bool relay_eligible(const LoweredOp& op, const std::map<int, std::vector<DeviceId>>& groups, const HostMap& hm) {
+  if (!hm.hierarchical) return false;
+  const int hs = hm.host[static_cast<size_t>(op.src)];
+  uint64_t mc = 0;
+  if (multicast_target(groups, hm, &mc)) return false;
+  int remote = 0;
+  for (const auto& kv : groups) {
+    if (kv.first != hs) ++remote;
+    if (static_cast<int>(kv.second.size()) + 1 > kMaxFan) return false;
+  }
+  if (remote < 2) return false;
+  for (const auto& r : op.rects)
+    if (((r.src_off | r.dst_off | r.row_bytes | r.src_pitch | r.dst_pitch) & 15) != 0) return false;
+  return true;
+}
+
 }  // namespace
+
+int64_t relay_slots(const std::vector<LoweredOp>& ops, const HostMap& hm) {
+  int64_t n = 0;
+  for (const auto& op : ops) {
+    if (!relay_eligible(op, by_host(op, hm), hm)) continue;
+    for (const auto& r : op.rects) n += pieces_of(r, hm.relay_chunk);
+  }
+  return n;
+}
 
 std::vector<Job> build_jobs(const std::vector<LoweredOp>& ops, const HostMap& hm, int mode) {
   std::vector<Job> jobs;
@@ -68,10 +120,45 @@ std::vector<Job> build_jobs(const std::vector<LoweredOp>& ops, const HostMap& hm
     }
     return jobs;
   }
+  int64_t relay_next_slot = 0;  // slots are numbered identically on every rank
   for (const auto& op : ops) {
     const int hs = hm.host[static_cast<size_t>(op.src)];
     const auto groups = by_host(op, hm);
     const auto mine = groups.find(hm.me);
+    if (mode == 0 && !hm.relay_flags.empty() && relay_eligible(op, groups, hm)) {
+      // Pipelined relay: source -> c1 -> c2 -> ... (ring order); each host
+      // forwards every chunk as soon as it lands and fans it out locally in
+      // the same pass, so no host sends more than one copy.
+      const int64_t base = relay_next_slot;
+      for (const auto& r : op.rects) relay_next_slot += pieces_of(r, hm.relay_chunk);
+      const std::vector<int> chain = relay_chain(groups, hs);
+      auto leader = [&](int h) { return groups.at(h).front(); };
+      if (hs == hm.me) {
+        Job j;
+        j.src = op.src;
+        j.op = &op;
+        j.dsts.push_back(leader(chain.front()));
+        if (mine != groups.end()) j.dsts.insert(j.dsts.end(), mine->second.begin(), mine->second.end());
+        j.relay_signal = true;
+        j.relay_base = base;
+        jobs.push_back(std::move(j));
+      } else if (mine != groups.end()) {
+        const size_t pos = static_cast<size_t>(std::find(chain.begin(), chain.end(), hm.me) - chain.begin());
+        Job j;
+        j.src = mine->second.front();
+        j.src_is_dst_buffer = true;
+        j.op = &op;
+        if (pos + 1 < chain.size()) {
+          j.dsts.push_back(leader(chain[pos + 1]));
+          j.relay_signal = true;
+        }
+        j.dsts.insert(j.dsts.end(), mine->second.begin() + 1, mine->second.end());
+        j.relay_wait = true;
+        j.relay_base = base;
+        if (!j.dsts.empty()) jobs.push_back(std::move(j));
+      }
+      continue;
+    }
     uint64_t mc_base = 0;
     if (mode == 0 && hs == hm.me && multicast_target(groups, hm, &mc_base)) {
       // One multimem store reaches every host's leader (our own included);
@@ -126,6 +213,17 @@ void host_wire_bytes(const std::vector<LoweredOp>& ops, const HostMap& hm, int64
     const int hs = hm.host[static_cast<size_t>(op.src)];
     const int64_t b = op_bytes(op);
     const auto groups = by_host(op, hm);
+    if (!hm.relay_flags.empty() && relay_eligible(op, groups, hm)) {
+      // relay: every chain host receives one copy; all but the last send one
+      const std::vector<int> chain = relay_chain(groups, hs);
+      if (hs == hm.me) o += b;
+      const auto at = std::find(chain.begin(), chain.end(), hm.me);
+      if (at != chain.end()) {
+        i += b;
+        if (at + 1 != chain.end()) o += b;
+      }
+      continue;
+    }
     uint64_t mc_base = 0;
     const bool mc = multicast_target(groups, hm, &mc_base);
     bool sent = false;
@@ -154,8 +252,16 @@ struct Tagged {
 };
 
 // Chunk one rectangle for (src base, dst bases) into items.
+// Relay flags of the items a rectangle is cut into: item k waits on
+// wait_base + 4*slot and/or signals signal_base + 4*slot, slot = (*slot)++.
+struct RelayTags {
+  uint64_t wait_base = 0, signal_base = 0;
+  int64_t* slot = nullptr;
+};
+
 void add_rect(std::vector<Tagged>& out, ItemSet& acc, uint64_t src, const std::vector<uint64_t>& dsts,
-              const CopyRect& r, int64_t chunk, bool mc0, DeviceId src_dev, bool src_is_dst) {
+              const CopyRect& r, int64_t chunk, bool mc0, DeviceId src_dev, bool src_is_dst,
+              RelayTags relay = {}) {
   const bool vec = ((src | static_cast<uint64_t>(r.src_off | r.dst_off | r.row_bytes | r.src_pitch | r.dst_pitch)) &
                     15) == 0 &&
                    std::all_of(dsts.begin(), dsts.end(), [](uint64_t d) { return (d & 15) == 0; });
@@ -180,6 +286,11 @@ void add_rect(std::vector<Tagged>& out, ItemSet& acc, uint64_t src, const std::v
     it.inv_row = 1.0f / static_cast<float>(cols);
     if (rows > 1 && ((rows - 1) * dp + cols >= (int64_t{1} << 32) || (rows - 1) * sp + cols >= (int64_t{1} << 32)))
       throw rlplan::ValidationError("copy item spans more than 2^32 units");
+    if (relay.slot) {
+      const uint64_t off = 4u * static_cast<uint64_t>((*relay.slot)++);
+      if (relay.wait_base) it.wait_flag = relay.wait_base + off;
+      if (relay.signal_base) it.signal_flag = relay.signal_base + off;
+    }
     out.push_back({it, src_dev, src_begin + ((rows - 1) * sp + cols) * unit, src_is_dst});
     const int64_t bytes = rows * cols * unit;
     acc.read += bytes;
@@ -225,15 +336,30 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
         if (hm.host[static_cast<size_t>(j.dsts[k])] != hm.me) acc.remote_stores = true;
       }
       streams.emplace_back();
+      int64_t relay_slot = j.relay_base;
+      if ((j.relay_wait || j.relay_signal) && j.dsts.size() > static_cast<size_t>(kMaxFan))
+        throw rlplan::ValidationError("relay job with more than kMaxFan destinations");
       for (CopyRect r : j.op->rects) {
         if (j.src_is_dst_buffer) {  // fan-out reads the leader's copy: destination geometry
           r.src_off = r.dst_off;
           r.src_pitch = r.dst_pitch;
         }
         // Same-address copies (identical placement and buffers) are no-ops.
-        if (!accounting && !mc0 && dsts.size() == 1 &&
+        if (!accounting && !mc0 && !j.relay_wait && !j.relay_signal && dsts.size() == 1 &&
             s + static_cast<uint64_t>(r.src_off) == dsts[0] + static_cast<uint64_t>(r.dst_off))
           continue;
+        if (j.relay_wait || j.relay_signal) {
+          // relay pieces are cut at the slot granularity every rank agrees on
+          const auto flags = [&](DeviceId d) {
+            return accounting ? uint64_t{0} : hm.relay_flags.at(static_cast<size_t>(d));
+          };
+          RelayTags tags;
+          tags.wait_base = j.relay_wait ? flags(j.src) : 0;
+          tags.signal_base = j.relay_signal ? flags(j.dsts.front()) : 0;
+          tags.slot = &relay_slot;
+          add_rect(streams.back(), acc, s, dsts, r, hm.relay_chunk, mc0, j.src, j.src_is_dst_buffer, tags);
+          continue;
+        }
         add_rect(streams.back(), acc, s, dsts, r, chunk_bytes, mc0, j.src, j.src_is_dst_buffer);
       }
     }
@@ -248,7 +374,8 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
   for (size_t k = 0, seen = 0; seen < total; ++k)
     for (const auto& st : streams)
       if (k < st.size()) {
-        (st[k].it.vec == kItemVec ? vec_items : other).push_back(&st[k]);
+        const bool tma = st[k].it.vec == kItemVec && !st[k].it.wait_flag && !st[k].it.signal_flag;
+        (tma ? vec_items : other).push_back(&st[k]);
         ++seen;
       }
   acc.n_vec = static_cast<int>(vec_items.size());

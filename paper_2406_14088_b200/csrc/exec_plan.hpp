@@ -29,6 +29,13 @@ struct Job {
   // through mc_base (multimem.st), replicated by the switch.
   bool multicast = false;
   uint64_t mc_base = 0;
+  // Pipelined relay: item k of this job is relay slot relay_base + k. With
+  // relay_wait the job reads this host's leader copy only after the previous
+  // host of the chain flagged that slot; with relay_signal dsts[0] is the
+  // next host's leader, flagged after each item.
+  bool relay_wait = false;
+  bool relay_signal = false;
+  int64_t relay_base = 0;
 };
 
 struct HostMap {
@@ -36,7 +43,14 @@ struct HostMap {
   int me = 0;                // executing host
   bool hierarchical = true;  // false: flat delivery, every destination served directly
   std::vector<uint64_t> mc;  // per plan device: multicast address of its group (0 = none)
+  // Pipelined relay for payloads reaching >= 2 other hosts: per plan device,
+  // the (locally mapped) relay flag array of its host; empty = no relay.
+  std::vector<uint64_t> relay_flags;
+  int64_t relay_chunk = 256 << 10;
 };
+
+// Relay slots a plan needs (flag array length, identical on every rank).
+int64_t relay_slots(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm);
 
 // mode 0 = push (source host executes phase A), 1 = pull (destination host).
 std::vector<Job> build_jobs(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm, int mode);

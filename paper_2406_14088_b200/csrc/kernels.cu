@@ -28,6 +28,33 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
   return v;
 }
 
+// L2-coherent load (bypasses L1): for relay sources that another GPU writes
+// while this kernel runs (the .nc path above would be unsafe there).
+__device__ __forceinline__ int4 ld_coherent(const int4* p) {
+  int4 v;
+  asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Relay wait: spin (acquire, system scope, bounded) until *flag >= epoch.
+// Returns false on timeout (the caller counts it instead of hanging the GPU).
+__device__ __forceinline__ bool wait_flag_geq(const uint32_t* flag, uint32_t epoch) {
+  const uint64_t t0 = global_ns();
+  while (true) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (static_cast<int32_t>(v - epoch) >= 0) return true;
+    if (global_ns() - t0 > 20000000000ull) return false;
+    __nanosleep(32);
+  }
+}
+
 __device__ __forceinline__ void st_vec(int4* p, const int4& v) {
   asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)
@@ -60,7 +87,7 @@ __device__ __forceinline__ void split_index(uint32_t idx, uint32_t row_units, fl
 
 // `dsts` points at the shared-memory copy of the item's destination table.
 __device__ __forceinline__ void copy_vec_item(const CopyItem& it, const uint64_t* dsts, int ndst,
-                                              uint32_t total, bool mc0) {
+                                              uint32_t total, bool mc0, bool coherent) {
   const int4* __restrict__ src = reinterpret_cast<const int4*>(it.src);
   const uint32_t step = kCopyThreads * kCopyUnroll;
   for (uint32_t base = 0; base < total; base += step) {
@@ -73,7 +100,8 @@ __device__ __forceinline__ void copy_vec_item(const CopyItem& it, const uint64_t
       if (idx < total) {
         uint32_t row, col;
         split_index(idx, it.row_units, it.inv_row, row, col);
-        v[u] = ld_stream(src + static_cast<size_t>(row) * it.src_pitch + col);
+        const int4* p = src + static_cast<size_t>(row) * it.src_pitch + col;
+        v[u] = coherent ? ld_coherent(p) : ld_stream(p);
         doff[u] = row * it.dst_pitch + col;  // < 2^32 units: checked on the host
       }
     }
@@ -118,8 +146,9 @@ __device__ __forceinline__ void retire_cta(unsigned int* sched) {
   }
 }
 
-__global__ void __launch_bounds__(kCopyThreads) rr_copy_kernel(const CopyItem* __restrict__ items,
-                                                               int n_items, int fence_sys, unsigned int* sched) {
+// sched[2] counts relay waits that timed out (reported by rr_exec_status).
+__global__ void __launch_bounds__(kCopyThreads) rr_copy_kernel(const CopyItem* __restrict__ items, int n_items,
+                                                               int fence_sys, unsigned int* sched, uint32_t epoch) {
   __shared__ CopyItem sh;
   __shared__ int cur;
   constexpr int kWords = sizeof(CopyItem) / 16;
@@ -132,6 +161,11 @@ __global__ void __launch_bounds__(kCopyThreads) rr_copy_kernel(const CopyItem* _
     if (threadIdx.x < kWords)
       reinterpret_cast<int4*>(&sh)[threadIdx.x] = reinterpret_cast<const int4*>(items + i)[threadIdx.x];
     __syncthreads();
+    if (sh.wait_flag) {  // relay: the previous GPU of the chain must have delivered this chunk
+      if (threadIdx.x == 0 && !wait_flag_geq(reinterpret_cast<const uint32_t*>(sh.wait_flag), epoch))
+        atomicAdd(sched + 2, 1u);
+      __syncthreads();
+    }
     CopyItem it;  // scalar fields only; the dst table stays in shared memory
     it.src = sh.src;
     it.row_units = sh.row_units;
@@ -142,9 +176,16 @@ __global__ void __launch_bounds__(kCopyThreads) rr_copy_kernel(const CopyItem* _
     const int ndst = sh.ndst;
     const uint32_t total = it.row_units * it.nrows;
     if (sh.vec & kItemVec)
-      copy_vec_item(it, sh.dst, ndst, total, (sh.vec & kItemMulticast0) != 0);
+      copy_vec_item(it, sh.dst, ndst, total, (sh.vec & kItemMulticast0) != 0, sh.wait_flag != 0);
     else
       copy_elem_item(it, sh.dst, ndst, total);
+    if (sh.signal_flag) {  // relay: release this chunk to the next GPU of the chain
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sh.signal_flag), "r"(epoch) : "memory");
+      }
+    }
   }
   // Peer stores must be visible system-wide before a later barrier releases
   // them to the destination GPU.
@@ -386,12 +427,6 @@ __global__ void rr_verify_kernel(const FillItem* __restrict__ items, int n_items
   }
 }
 
-__device__ __forceinline__ uint64_t global_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
 __global__ void rr_barrier_kernel(uint32_t* const* __restrict__ flags, int rank, int world,
                                   uint32_t epoch, int* timed_out) {
   const int p = threadIdx.x;
@@ -426,11 +461,12 @@ int copy_max_ctas(int* ctas_per_sm, int* sms) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, rr_copy_kernel, kCopyThreads, 0);
 }
 
-int launch_copy(const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream, unsigned int* sched) {
+int launch_copy(const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream, unsigned int* sched,
+                uint32_t epoch) {
   if (n_items <= 0) return cudaSuccess;
   if (ctas > n_items) ctas = n_items;
-  rr_copy_kernel<<<ctas, kCopyThreads, 0, static_cast<cudaStream_t>(stream)>>>(items, n_items, fence_sys,
-                                                                                sched);
+  rr_copy_kernel<<<ctas, kCopyThreads, 0, static_cast<cudaStream_t>(stream)>>>(items, n_items, fence_sys, sched,
+                                                                                epoch);
   return cudaGetLastError();
 }
 

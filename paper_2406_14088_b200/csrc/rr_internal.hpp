@@ -36,7 +36,12 @@ struct alignas(16) CopyItem {
   float inv_row;       // 1.0f / row_units
   uint16_t ndst;
   uint16_t vec;
-  uint32_t pad[2];
+  // Pipelined relay (exec_plan.cpp): wait until *wait_flag >= epoch before
+  // reading the source (it is being written by the previous GPU of the
+  // chain), and after the copy store epoch into *signal_flag on the next
+  // GPU (release, system scope). 0 = none.
+  uint64_t wait_flag;
+  uint64_t signal_flag;
 };
 static_assert(sizeof(CopyItem) % 16 == 0, "CopyItem must be a multiple of 16 bytes");
 
@@ -72,7 +77,10 @@ __host__ __device__ inline uint16_t weight_value(uint64_t seed, uint64_t tensor,
 
 // Host-callable launchers (kernels.cu). All return a cudaError_t as int.
 // sched: 2 device uints, zero before the first launch (kernels reset them).
-int launch_copy(const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream, unsigned int* sched);
+// sched: 4 device uints (next item, retired CTAs, relay timeouts, unused);
+// epoch: value relay flags are compared against / set to.
+int launch_copy(const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream, unsigned int* sched,
+                uint32_t epoch = 0);
 int copy_max_ctas(int* ctas_per_sm, int* sms);
 // TMA bulk variant (1..kBulkVariants = stage ring shapes / L2 hints); items must all be vec items.
 // With max_ctas != NULL only reports the resident-CTA capacity.

@@ -136,7 +136,8 @@ class Executor:
 
     def __init__(self, plan: ReallocPlan, cuda_device: int, src_ptrs: Dict[int, int], dst_ptrs: Dict[int, int],
                  local: Iterable[int], mode: int = PUSH, chunk_bytes: int = 0,
-                 host_of: Optional[Sequence[int]] = None, mc_ptrs: Optional[Dict[int, int]] = None):
+                 host_of: Optional[Sequence[int]] = None, mc_ptrs: Optional[Dict[int, int]] = None,
+                 relay_flags: Optional[Dict[int, int]] = None):
         n = plan.cluster.device_count()
         self.plan = plan
         sp, dp = (ctypes.c_void_p * n)(), (ctypes.c_void_p * n)()
@@ -152,7 +153,12 @@ class Executor:
             mcs = (ctypes.c_void_p * n)()
             for d, p in mc_ptrs.items():
                 mcs[d] = p
-        opt = RrExecOptions(mode, chunk_bytes, hosts, mcs)
+        rfl = None
+        if relay_flags:
+            rfl = (ctypes.c_void_p * n)()
+            for d, p in relay_flags.items():
+                rfl[d] = p
+        opt = RrExecOptions(mode, chunk_bytes, hosts, mcs, rfl)
         h = ctypes.c_void_p()
         check(lib.rr_exec_create_ex(plan.handle, cuda_device, n, sp, dp, len(loc), arr, ctypes.byref(opt),
                                     ctypes.byref(h)))
@@ -174,6 +180,11 @@ class Executor:
 
     def launch_fanout(self, stream=None, ctas: int = 0) -> None:
         check(lib.rr_exec_launch_fanout(self._h, _stream_ptr(stream), ctas))
+
+    def relay_timeouts(self) -> int:
+        out = ctypes.c_int64()
+        check(lib.rr_exec_relay_timeouts(self._h, ctypes.byref(out)))
+        return out.value
 
     def enable_onload(self, src_bytes: Dict[int, int], chunk_bytes: int = 256 << 20) -> None:
         """Prepare onload pipelining: the local source shards {device: bytes}
@@ -288,11 +299,22 @@ def hosted_devices(n_plan_devices: int, rank: int, world: int) -> List[int]:
     return list(range(rank * k, (rank + 1) * k))
 
 
-def link_bottleneck(plan: ReallocPlan, host_of: Sequence[int], multicast: bool) -> int:
+def relay_slots(plan: ReallocPlan, host_of: Sequence[int], chunk_bytes: int = 0) -> int:
+    """Length of the relay flag array for this host map (same on every rank)."""
+    n = plan.cluster.device_count()
+    hosts = (ctypes.c_int32 * n)(*host_of)
+    out = ctypes.c_int64()
+    check(lib.rr_plan_relay_slots(plan.handle, hosts, chunk_bytes, ctypes.byref(out)))
+    return out.value
+
+
+def link_bottleneck(plan: ReallocPlan, host_of: Sequence[int], multicast: bool = False, relay: bool = False) -> int:
     """Estimated bottleneck link bytes of a GPU (max over hosts of max(egress,
-    ingress)) for hierarchical push delivery, with or without NVLS multicast
+    ingress)) for hierarchical push delivery, optionally with NVLS multicast
     of payloads that reach every host (the switch also loops the source's own
-    copy back, so multicast adds ingress at the source)."""
+    copy back, so multicast adds ingress at the source) or with the pipelined
+    relay for payloads reaching >= 2 other hosts (every chain host receives
+    one copy, all but the last send one)."""
     hosts = set(host_of)
     egress = {h: 0 for h in hosts}
     ingress = {h: 0 for h in hosts}
@@ -301,7 +323,14 @@ def link_bottleneck(plan: ReallocPlan, host_of: Sequence[int], multicast: bool) 
         hs = host_of[s]
         dst_hosts = {host_of[d] for d in dsts}
         remote = dst_hosts - {hs}
-        if multicast and dst_hosts == hosts and remote:
+        if relay and len(remote) >= 2:
+            chain = sorted(remote, key=lambda h: (h - hs) % (max(hosts) + 1))
+            egress[hs] += b
+            for k, h in enumerate(chain):
+                ingress[h] += b
+                if k + 1 < len(chain):
+                    egress[h] += b
+        elif multicast and dst_hosts == hosts and remote:
             egress[hs] += b
             for h in dst_hosts:
                 ingress[h] += b
@@ -415,7 +444,7 @@ class RankRealloc:
     def __init__(self, plans: Sequence[ReallocPlan], shards: Dict[str, Tuple[int, int]],
                  bind: Sequence[Tuple[str, str]], rank: int, world: int, cuda_device: int, group=None,
                  mode: int = PUSH, kernel: int = DEFAULT_KERNEL, hierarchical: bool = True,
-                 multicast: Sequence[str] = ()):
+                 multicast: Sequence[str] = (), relay=False):
         """``multicast`` names shard sets whose per-GPU leader shards (the
         lowest-id plan device of the set on each GPU) are members of one NVLS
         multicast object: a payload bound for every GPU is then stored once
@@ -439,6 +468,24 @@ class RankRealloc:
         self.multicast = list(multicast)
         if multicast and (world < 2 or mode != PUSH or not hierarchical):
             raise ValueError("multicast needs world > 1, push mode and hierarchical delivery")
+        # Pipelined relay per phase (payloads reaching >= 2 other GPUs travel
+        # source -> GPU -> GPU ... chunk by chunk): True = every phase, "auto" =
+        # where it lowers the estimated link bottleneck by >10%.
+        host_of_all = [self.owner[d] for d in range(n)]
+        self.relay_phases: List[int] = []
+        if relay and world > 1 and mode == PUSH and hierarchical:
+            for pi, (_sname, dname) in enumerate(bind):
+                if dname in self.multicast:
+                    continue
+                p = self.plans[pi]
+                if relay != "auto" or (link_bottleneck(p, host_of_all, relay=True) <
+                                       0.9 * link_bottleneck(p, host_of_all)):
+                    self.relay_phases.append(pi)
+        self.relay_bufs: Dict[int, DeviceBuffer] = {}
+        for pi in self.relay_phases:
+            slots = relay_slots(self.plans[pi], host_of_all)
+            self.relay_bufs[pi] = DeviceBuffer(cuda_device, 4 * max(slots, 64))
+            self.relay_bufs[pi].zero()
         self.buffers: Dict[str, Dict[int, object]] = {}
         self.mc_tables: Dict[str, Dict[int, int]] = {}
         mc_leaders: Dict[str, int] = {}
@@ -478,6 +525,8 @@ class RankRealloc:
             mine = {name: {d: b.ipc_handle() for d, b in bufs.items() if mc_leaders.get(name) != d}
                     for name, bufs in self.buffers.items()}
             mine["__flags__"] = {rank: self.flags.ipc_handle()}
+            for pi, b in self.relay_bufs.items():
+                mine[f"__relay{pi}__"] = {rank: b.ipc_handle()}
         gathered: List[dict] = [None] * world  # type: ignore
         if world > 1:
             import torch.distributed as dist
@@ -489,6 +538,7 @@ class RankRealloc:
         self._opened: List[int] = []
         flag_ptrs = [0] * world
         flag_ptrs[rank] = self.flags.ptr
+        relay_remote: Dict[Tuple[int, int], int] = {}
         for r, table in enumerate(gathered):
             if r == rank:
                 continue
@@ -498,16 +548,23 @@ class RankRealloc:
                     self._opened.append(p)
                     if name == "__flags__":
                         flag_ptrs[r] = p
+                    elif name.startswith("__relay"):
+                        relay_remote[(int(name[7:-2]), r)] = p
                     else:
                         self.ptrs[name][d] = p
         self.barrier = Barrier(cuda_device, rank, world, flag_ptrs)
         self.bind = list(bind)
         host_of = [self.owner[d] for d in range(n)]
+        # relay flag array of every plan device's host, as mapped in this process
+        relay_tables: Dict[int, Dict[int, int]] = {}
+        for pi, b in self.relay_bufs.items():
+            relay_tables[pi] = {d: (b.ptr if self.owner[d] == rank else relay_remote[(pi, self.owner[d])])
+                                for d in range(n)}
         self.executors: List[Executor] = []
         for pi, (sname, dname) in enumerate(bind):
             self.executors.append(Executor(self.plans[pi], cuda_device, self.ptrs[sname], self.ptrs[dname],
                                            self.local, mode, host_of=host_of if hierarchical else None,
-                                           mc_ptrs=self.mc_tables.get(dname)))
+                                           mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_tables.get(pi)))
             self.executors[-1].set_kernel(kernel)
         # Every rank must run the same barrier sequence: a phase has a fan-out
         # step if any rank has fan-out work in it.
@@ -563,4 +620,10 @@ class RankRealloc:
         for bufs in self.buffers.values():
             for b in bufs.values():
                 b.free()
+        for b in self.relay_bufs.values():
+            b.free()
         self.flags.free()
+
+    def relay_timeouts(self) -> int:
+        """Relay waits that gave up (bounded spins); nonzero = results invalid."""
+        return sum(e.relay_timeouts() for e in self.executors)

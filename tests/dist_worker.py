@@ -92,6 +92,36 @@ def main() -> int:
             rr.close()
     elif rank == 0:
         print("dist_worker: NVLS multicast not supported, skipped", flush=True)
+    # Pipelined relay: chunks travel source -> GPU -> GPU with per-chunk flags.
+    relay_cases = [
+        (Placement(DeviceMesh(0, 1, 0, 1), ParallelStrategy()), placement(8, 1, 8, 1)),  # replicate from dev 0
+        (placement(8, 1, 1, 8), placement(8, 1, 8, 1)),                                  # tp8 -> dp8
+        (placement(2, 1, 1, 2, offset=2), placement(8, 1, 4, 2)),                        # 2 sources -> dp4 tp2
+    ]
+    for src, dst in relay_cases:
+        plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
+        rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
+                           relay=True)
+        for d, b in rr.buffers["a"].items():
+            R.fill_shard(plan, R.SRC, d, b.ptr, 29)
+        torch.cuda.synchronize()
+        dist.barrier()
+        for rep in range(3):  # epochs advance per launch
+            for b in rr.buffers["b"].values():
+                b.zero()
+            torch.cuda.synchronize()
+            dist.barrier()
+            rr.run_phase(0)
+            torch.cuda.synchronize()
+            for d, b in rr.buffers["b"].items():
+                got = b.to_host()
+                want = O.fill(TINY_GQA, dst, c, d, 29)
+                if not np.array_equal(got, want):
+                    failures.append(f"relay {src.strategy}->{dst.strategy} rep {rep}: device {d} differs in "
+                                    f"{int(np.count_nonzero(got != want))} elements")
+        if rr.relay_timeouts():
+            failures.append(f"relay {src.strategy}->{dst.strategy}: {rr.relay_timeouts()} timeouts")
+        rr.close()
     if os.environ.get("RR_FULL_7B") == "1":
         w = WORKLOADS["llama7b_tp8_dp8_roundtrip"]
         plans = [plan_param_realloc(w.model, s, d, c, BALANCED) for (s, d) in w.phases]
