@@ -33,9 +33,12 @@ class B200Profile:
 
 
 def estimate_seconds(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
-                     profile: B200Profile = B200Profile(), multicast: bool = False) -> Dict[str, float]:
+                     profile: B200Profile = B200Profile(), multicast: bool = False,
+                     relay: bool = False) -> Dict[str, float]:
     """Estimated execution time of `plan` with plan device d hosted on GPU
-    host_of[d] (default: one GPU per plan device)."""
+    host_of[d] (default: one GPU per plan device). `relay`: payloads reaching
+    >= 2 other GPUs use the pipelined relay (one copy in and out per GPU,
+    fan-out fused into phase 0)."""
     n = plan.cluster.device_count()
     host = list(host_of) if host_of is not None else list(range(n))
     hosts = sorted(set(host))
@@ -53,6 +56,14 @@ def estimate_seconds(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
         local = groups.get(hs, [])
         hbm[hs] += b * (1 + len(local))      # one read, one write per local destination
         remote = [h for h in groups if h != hs]
+        if relay and len(remote) >= 2:
+            chain = sorted(remote, key=lambda h: (h - hs) % (max(hosts) + 1))
+            egress[hs] += b
+            for k, h in enumerate(chain):
+                ingress[h] += b
+                egress[h] += b if k + 1 < len(chain) else 0
+                hbm[h] += b * (1 + len(groups[h]))  # leader written, read once, other replicas written
+            continue
         use_mc = multicast and set(groups) == set(hosts) and len(remote) > 0
         if use_mc:
             egress[hs] += b
