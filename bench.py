@@ -240,8 +240,8 @@ def run_b200(args) -> None:
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    clocks = R_clock = ClockSampler(local_rank)
-    R_clock.start()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
     evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in plans]
            for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -390,8 +390,11 @@ def run_b200(args) -> None:
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * sum(1 + (1 + 2 * rr.has_fanout[i] if world > 1 else 0)
-                                             for i in range(len(plans))),
+            # this rank's kernels per step: copy kernels of every phase, plus the
+            # barrier(s) and the fan-out kernels when N > 1
+            "gpu_launches": args.steps * sum(
+                e.kernel_count()[0] + ((1 + rr.has_fanout[i] * (1 + e.kernel_count()[1])) if world > 1 else 0)
+                for i, e in enumerate(rr.executors)),
             "clocks": clock_info,
             "verified": verified,
         }

@@ -231,6 +231,8 @@ rr_status rr_exec_stats(const rr_exec* ex, int phase, int64_t* items, int64_t* b
 rr_status rr_exec_enable_onload(rr_exec* ex, int n_src, const int32_t* src_devices, const int64_t* src_bytes,
                                 int64_t chunk_bytes);
 rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_stream, void* stream, int ctas);
+/* Kernels one rr_exec_launch / rr_exec_launch_fanout issues (0..2 each). */
+rr_status rr_exec_kernel_count(const rr_exec* ex, int* phase0, int* phase1);
 /* Bytes entering / leaving this executor's host over links per launch. */
 rr_status rr_exec_wire(const rr_exec* ex, int64_t* wire_in, int64_t* wire_out);
 void rr_exec_destroy(rr_exec* ex);

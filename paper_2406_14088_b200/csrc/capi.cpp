@@ -745,6 +745,19 @@ rr_status rr_exec_launch(rr_exec* ex, void* stream, int ctas) {
   });
 }
 
+rr_status rr_exec_kernel_count(const rr_exec* ex, int* phase0, int* phase1) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    auto count = [&](const rr_exec::Phase& ph) {
+      if (ph.n == 0) return 0;
+      if (ex->kernel == 0) return 1;
+      return (ph.n > ph.n_vec ? 1 : 0) + (ph.n_vec > 0 ? 1 : 0);
+    };
+    *phase0 = count(ex->phase[0]);
+    *phase1 = count(ex->phase[1]);
+  });
+}
+
 rr_status rr_exec_relay_timeouts(rr_exec* ex, int64_t* timeouts) {
   return guarded([&] {
     need(ex != nullptr, "null executor");

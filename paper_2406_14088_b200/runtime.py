@@ -186,6 +186,12 @@ class Executor:
         check(lib.rr_exec_relay_timeouts(self._h, ctypes.byref(out)))
         return out.value
 
+    def kernel_count(self) -> Tuple[int, int]:
+        """Kernels one launch() / launch_fanout() issues."""
+        a, b = ctypes.c_int(), ctypes.c_int()
+        check(lib.rr_exec_kernel_count(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
     def enable_onload(self, src_bytes: Dict[int, int], chunk_bytes: int = 256 << 20) -> None:
         """Prepare onload pipelining: the local source shards {device: bytes}
         are copied host->device in chunk_bytes pieces (in device order)."""
