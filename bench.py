@@ -209,9 +209,10 @@ def run_b200(args) -> None:
     # bottleneck (single source feeding many GPUs); mc: NVLS multicast instead.
     multicast = [bind[0][1]] if args.mode == "mc" else []
     relay = {"auto": "auto", "relay": True}.get(args.mode, False)
+    overlap = args.overlap == "on"
     kernel = R.DEFAULT_KERNEL if args.kernel < 0 else args.kernel
     rr = R.RankRealloc(plans, shards, bind, rank, world, local_rank, mode=mode, kernel=kernel,
-                       multicast=multicast, relay=relay)
+                       multicast=multicast, relay=relay, overlap=overlap)
     stream = torch.cuda.current_stream()
     seed = 1
     for d, b in rr.buffers["train"].items():
@@ -380,7 +381,7 @@ def run_b200(args) -> None:
             "config": {"workload": w.name, "description": w.description, "plan_devices": w.devices,
                        "plan_devices_per_gpu": w.devices // world, "phases": len(plans),
                        "policy": args.policy, "mode": args.mode, "multicast_sets": rr.multicast,
-                       "relay_phases": rr.relay_phases,
+                       "relay_phases": rr.relay_phases, "overlap_phases": rr.overlap_phases,
                        "copy_kernel": kname,
                        "l2": "inputs larger than L2 (multi-GB shards); no flush needed",
                        "weights": "hash-initialised bf16 (seed 1), verified after timing"},
@@ -428,6 +429,8 @@ def main() -> None:
                     help="push = SM peer stores; relay = push + pipelined relay for payloads reaching >= 2 "
                          "other GPUs; mc = push + NVLS multicast for the first phase's destination (N > 1); "
                          "auto = push, relay where it lowers the link bottleneck")
+    ap.add_argument("--overlap", choices=["on", "off"], default="off",
+                    help="run in-host fan-outs per chunk inside the first phase (N > 1) instead of after a barrier")
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--layers", type=int, default=0, help="truncate the model (profiling only)")
     ap.add_argument("--kernel", type=int, default=-1, help="copy engine: 0 LDG/STG, 1..5 TMA bulk (-1 default)")

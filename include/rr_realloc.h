@@ -254,10 +254,13 @@ typedef struct {
    * source -> host 1 -> host 2 ... chunk by chunk, each host forwarding and
    * fanning out locally as chunks land. NULL = no relay. */
   void* const* relay_flags;
+  int32_t relay_chain;    /* with relay_flags: chain relay for >= 2 remote hosts */
+  int32_t overlap_fanout; /* with relay_flags: per-chunk in-host fan-out inside phase 0 */
 } rr_exec_options;
-/* Length of the relay flag array for this host map and chunk size
- * (identical on every rank). */
-rr_status rr_plan_relay_slots(const rr_plan* plan, const int32_t* host_of, int64_t chunk_bytes, int64_t* slots);
+/* Length of the relay flag array for this host map, chunk size and scheme
+ * switches (identical on every rank). */
+rr_status rr_plan_relay_slots(const rr_plan* plan, const int32_t* host_of, int64_t chunk_bytes, int relay_chain,
+                              int overlap_fanout, int64_t* slots);
 /* Relay waits that timed out (bounded spins) since the executor was created. */
 rr_status rr_exec_relay_timeouts(rr_exec* ex, int64_t* timeouts);
 rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices, void* const* src_bufs,

@@ -52,14 +52,15 @@ class RrOp(Structure):
 
 class RrExecOptions(Structure):
     _fields_ = [("mode", c_int32), ("chunk_bytes", c_int64), ("host_of", POINTER(c_int32)),
-                ("mc_bufs", POINTER(c_void_p)), ("relay_flags", POINTER(c_void_p))]
+                ("mc_bufs", POINTER(c_void_p)), ("relay_flags", POINTER(c_void_p)), ("relay_chain", c_int32),
+                ("overlap_fanout", c_int32)]
 
 
 _P = c_void_p
 _SIGNATURES = {
     "rr_exec_create_ex": (c_int, [_P, c_int, c_int, POINTER(_P), POINTER(_P), c_int, POINTER(c_int32),
                                   POINTER(RrExecOptions), POINTER(_P)]),
-    "rr_plan_relay_slots": (c_int, [_P, POINTER(c_int32), c_int64, POINTER(c_int64)]),
+    "rr_plan_relay_slots": (c_int, [_P, POINTER(c_int32), c_int64, c_int, c_int, POINTER(c_int64)]),
     "rr_exec_relay_timeouts": (c_int, [_P, POINTER(c_int64)]),
     "rr_exec_kernel_count": (c_int, [_P, POINTER(c_int), POINTER(c_int)]),
     "rr_mcast_supported": (c_int, [c_int, POINTER(c_int)]),

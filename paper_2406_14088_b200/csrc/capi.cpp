@@ -680,6 +680,9 @@ rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, vo
   opt.chunk_bytes = chunk_bytes;
   opt.host_of = host_of;
   opt.mc_bufs = nullptr;
+  opt.relay_flags = nullptr;
+  opt.relay_chain = 0;
+  opt.overlap_fanout = 0;
   return rr_exec_create_ex(plan, cuda_device, n_devices, src_bufs, dst_bufs, n_local, local, &opt, out);
 }
 
@@ -707,6 +710,8 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       hm.relay_flags.resize(hm.host.size());
       for (size_t d = 0; d < hm.relay_flags.size(); ++d)
         hm.relay_flags[d] = reinterpret_cast<uint64_t>(options->relay_flags[d]);
+      hm.relay_chain = options->relay_chain != 0;
+      hm.relay_star = options->overlap_fanout != 0;
     }
     const auto jobs = rr::build_jobs(plan->lowered, hm, mode);
     const auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes);
@@ -768,12 +773,15 @@ rr_status rr_exec_relay_timeouts(rr_exec* ex, int64_t* timeouts) {
   });
 }
 
-rr_status rr_plan_relay_slots(const rr_plan* plan, const int32_t* host_of, int64_t chunk_bytes, int64_t* slots) {
+rr_status rr_plan_relay_slots(const rr_plan* plan, const int32_t* host_of, int64_t chunk_bytes, int relay_chain,
+                              int overlap_fanout, int64_t* slots) {
   return guarded([&] {
     need(plan != nullptr && host_of != nullptr, "null plan/host table");
     rr::HostMap hm;
     for (int d = 0; d < plan->cluster.device_count(); ++d) hm.host.push_back(host_of[d]);
     hm.relay_chunk = chunk_bytes > 0 ? chunk_bytes : (256 << 10);
+    hm.relay_chain = relay_chain != 0;
+    hm.relay_star = overlap_fanout != 0;
     *slots = rr::relay_slots(plan->lowered, hm);
   });
 }

@@ -77,20 +77,42 @@ std::vector<int> relay_chain(const std::map<int, std::vector<DeviceId>>& groups,
 // Relay pays off when a payload reaches >= 2 other hosts (it caps every
 // host's egress at one copy). Needs 16-byte geometry on both sides (the
 // source and the forwarders cut identical pieces) and small fan-outs.
-bool relay_eligible(const LoweredOp& op, const std::map<int, std::vector<DeviceId>>& groups, const HostMap& hm) {
+bool flaggable(const LoweredOp& op, const std::map<int, std::vector<DeviceId>>& groups, const HostMap& hm) {
   if (!hm.hierarchical) return false;
-  const int hs = hm.host[static_cast<size_t>(op.src)];
   uint64_t mc = 0;
   if (multicast_target(groups, hm, &mc)) return false;
-  int remote = 0;
-  for (const auto& kv : groups) {
-    if (kv.first != hs) ++remote;
+  for (const auto& kv : groups)
     if (static_cast<int>(kv.second.size()) + 1 > kMaxFan) return false;
-  }
-  if (remote < 2) return false;
   for (const auto& r : op.rects)
     if (((r.src_off | r.dst_off | r.row_bytes | r.src_pitch | r.dst_pitch) & 15) != 0) return false;
   return true;
+}
+
+bool relay_eligible(const LoweredOp& op, const std::map<int, std::vector<DeviceId>>& groups, const HostMap& hm) {
+  if (!hm.relay_chain || !flaggable(op, groups, hm)) return false;
+  const int hs = hm.host[static_cast<size_t>(op.src)];
+  int remote = 0;
+  for (const auto& kv : groups)
+    if (kv.first != hs) ++remote;
+  return remote >= 2;
+}
+
+// Remote hosts whose in-host fan-out overlaps phase 0 (star scheme): they
+// hold >= 2 destinations of a payload that does not take the chain relay.
+std::vector<int> star_hosts(const LoweredOp& op, const std::map<int, std::vector<DeviceId>>& groups,
+                            const HostMap& hm) {
+  std::vector<int> hosts;
+  if (!hm.relay_star || relay_eligible(op, groups, hm) || !flaggable(op, groups, hm)) return hosts;
+  const int hs = hm.host[static_cast<size_t>(op.src)];
+  for (const auto& kv : groups)
+    if (kv.first != hs && kv.second.size() >= 2) hosts.push_back(kv.first);
+  return hosts;
+}
+
+int64_t op_pieces(const LoweredOp& op, int64_t chunk) {
+  int64_t n = 0;
+  for (const auto& r : op.rects) n += pieces_of(r, chunk);
+  return n;
 }
 
 }  // namespace
@@ -98,8 +120,11 @@ bool relay_eligible(const LoweredOp& op, const std::map<int, std::vector<DeviceI
 int64_t relay_slots(const std::vector<LoweredOp>& ops, const HostMap& hm) {
   int64_t n = 0;
   for (const auto& op : ops) {
-    if (!relay_eligible(op, by_host(op, hm), hm)) continue;
-    for (const auto& r : op.rects) n += pieces_of(r, hm.relay_chunk);
+    const auto groups = by_host(op, hm);
+    if (relay_eligible(op, groups, hm))
+      n += op_pieces(op, hm.relay_chunk);
+    else
+      n += op_pieces(op, hm.relay_chunk) * static_cast<int64_t>(star_hosts(op, groups, hm).size());
   }
   return n;
 }
@@ -156,6 +181,49 @@ std::vector<Job> build_jobs(const std::vector<LoweredOp>& ops, const HostMap& hm
         j.relay_wait = true;
         j.relay_base = base;
         if (!j.dsts.empty()) jobs.push_back(std::move(j));
+      }
+      continue;
+    }
+    const std::vector<int> stars = star_hosts(op, groups, hm);
+    if (mode == 0 && !hm.relay_flags.empty() && !stars.empty()) {
+      // Star: the source pushes each chunk to every remote leader and flags
+      // the hosts that fan out; those fan each chunk out as soon as it lands,
+      // inside phase 0.
+      const int64_t pieces = op_pieces(op, hm.relay_chunk);
+      std::map<int, int64_t> base;
+      for (int h : stars) {
+        base[h] = relay_next_slot;
+        relay_next_slot += pieces;
+      }
+      if (hs == hm.me) {
+        Job plain;  // local destinations and single-destination remote hosts
+        plain.src = op.src;
+        plain.op = &op;
+        for (const auto& [h, list] : groups) {
+          if (h == hm.me)
+            plain.dsts.insert(plain.dsts.end(), list.begin(), list.end());
+          else if (!base.count(h))
+            plain.dsts.push_back(list.front());
+        }
+        if (!plain.dsts.empty()) jobs.push_back(std::move(plain));
+        for (int h : stars) {
+          Job j;
+          j.src = op.src;
+          j.op = &op;
+          j.dsts = {groups.at(h).front()};
+          j.relay_signal = true;
+          j.relay_base = base[h];
+          jobs.push_back(std::move(j));
+        }
+      } else if (base.count(hm.me)) {
+        Job j;
+        j.src = mine->second.front();
+        j.src_is_dst_buffer = true;
+        j.op = &op;
+        j.dsts.assign(mine->second.begin() + 1, mine->second.end());
+        j.relay_wait = true;
+        j.relay_base = base[hm.me];
+        jobs.push_back(std::move(j));
       }
       continue;
     }
@@ -368,16 +436,29 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
   // spread their stores over many destinations (NVLink ingress balance).
   // TMA-eligible items (16-byte, no multicast) first; the rest take the
   // LDG/STG kernel.
+  //
+  // With flag-synchronised (relay / star) items the whole phase runs in the
+  // one LDG/STG kernel, so local copies, pushes and per-chunk fan-outs
+  // overlap. Deadlock freedom: within every round the items that never wait
+  // come first, so when a CTA claims a waiting item of round k every push of
+  // rounds <= k on this GPU is already claimed; the push it waits for sits in
+  // round k of another GPU, whose waits in turn only depend on our claimed
+  // pushes. Pushes never wait, so every wait is eventually released.
   std::vector<const Tagged*> vec_items, other;
   size_t total = 0;
-  for (const auto& st : streams) total += st.size();
+  bool flagged = false;
+  for (const auto& st : streams) {
+    total += st.size();
+    for (const auto& t : st) flagged = flagged || t.it.wait_flag || t.it.signal_flag;
+  }
   for (size_t k = 0, seen = 0; seen < total; ++k)
-    for (const auto& st : streams)
-      if (k < st.size()) {
-        const bool tma = st[k].it.vec == kItemVec && !st[k].it.wait_flag && !st[k].it.signal_flag;
-        (tma ? vec_items : other).push_back(&st[k]);
-        ++seen;
-      }
+    for (int waiting = 0; waiting < 2; ++waiting)
+      for (const auto& st : streams)
+        if (k < st.size() && (st[k].it.wait_flag != 0) == (waiting == 1)) {
+          const bool tma = !flagged && st[k].it.vec == kItemVec;
+          (tma ? vec_items : other).push_back(&st[k]);
+          ++seen;
+        }
   acc.n_vec = static_cast<int>(vec_items.size());
   vec_items.insert(vec_items.end(), other.begin(), other.end());
   if (vec_items.size() >= (size_t{1} << 31)) throw rlplan::ValidationError("too many copy items");

@@ -43,10 +43,15 @@ struct HostMap {
   int me = 0;                // executing host
   bool hierarchical = true;  // false: flat delivery, every destination served directly
   std::vector<uint64_t> mc;  // per plan device: multicast address of its group (0 = none)
-  // Pipelined relay for payloads reaching >= 2 other hosts: per plan device,
-  // the (locally mapped) relay flag array of its host; empty = no relay.
+  // Per plan device, the (locally mapped) relay flag array of its host;
+  // empty = no flag-synchronised schemes.
   std::vector<uint64_t> relay_flags;
   int64_t relay_chunk = 256 << 10;
+  // chain: payloads reaching >= 2 other hosts travel source -> host -> host.
+  // star: a payload's in-host fan-out starts per chunk as soon as the chunk
+  // lands, inside phase 0 (no separate fan-out phase).
+  bool relay_chain = true;
+  bool relay_star = false;
 };
 
 // Relay slots a plan needs (flag array length, identical on every rank).

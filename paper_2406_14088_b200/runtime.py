@@ -137,7 +137,8 @@ class Executor:
     def __init__(self, plan: ReallocPlan, cuda_device: int, src_ptrs: Dict[int, int], dst_ptrs: Dict[int, int],
                  local: Iterable[int], mode: int = PUSH, chunk_bytes: int = 0,
                  host_of: Optional[Sequence[int]] = None, mc_ptrs: Optional[Dict[int, int]] = None,
-                 relay_flags: Optional[Dict[int, int]] = None):
+                 relay_flags: Optional[Dict[int, int]] = None, relay_chain: bool = True,
+                 overlap_fanout: bool = False):
         n = plan.cluster.device_count()
         self.plan = plan
         sp, dp = (ctypes.c_void_p * n)(), (ctypes.c_void_p * n)()
@@ -158,7 +159,7 @@ class Executor:
             rfl = (ctypes.c_void_p * n)()
             for d, p in relay_flags.items():
                 rfl[d] = p
-        opt = RrExecOptions(mode, chunk_bytes, hosts, mcs, rfl)
+        opt = RrExecOptions(mode, chunk_bytes, hosts, mcs, rfl, int(relay_chain), int(overlap_fanout))
         h = ctypes.c_void_p()
         check(lib.rr_exec_create_ex(plan.handle, cuda_device, n, sp, dp, len(loc), arr, ctypes.byref(opt),
                                     ctypes.byref(h)))
@@ -305,12 +306,14 @@ def hosted_devices(n_plan_devices: int, rank: int, world: int) -> List[int]:
     return list(range(rank * k, (rank + 1) * k))
 
 
-def relay_slots(plan: ReallocPlan, host_of: Sequence[int], chunk_bytes: int = 0) -> int:
-    """Length of the relay flag array for this host map (same on every rank)."""
+def relay_slots(plan: ReallocPlan, host_of: Sequence[int], chunk_bytes: int = 0, chain: bool = True,
+                overlap: bool = False) -> int:
+    """Length of the relay flag array for this host map and scheme switches
+    (same on every rank)."""
     n = plan.cluster.device_count()
     hosts = (ctypes.c_int32 * n)(*host_of)
     out = ctypes.c_int64()
-    check(lib.rr_plan_relay_slots(plan.handle, hosts, chunk_bytes, ctypes.byref(out)))
+    check(lib.rr_plan_relay_slots(plan.handle, hosts, chunk_bytes, int(chain), int(overlap), ctypes.byref(out)))
     return out.value
 
 
@@ -450,7 +453,7 @@ class RankRealloc:
     def __init__(self, plans: Sequence[ReallocPlan], shards: Dict[str, Tuple[int, int]],
                  bind: Sequence[Tuple[str, str]], rank: int, world: int, cuda_device: int, group=None,
                  mode: int = PUSH, kernel: int = DEFAULT_KERNEL, hierarchical: bool = True,
-                 multicast: Sequence[str] = (), relay=False):
+                 multicast: Sequence[str] = (), relay=False, overlap: bool = False):
         """``multicast`` names shard sets whose per-GPU leader shards (the
         lowest-id plan device of the set on each GPU) are members of one NVLS
         multicast object: a payload bound for every GPU is then stored once
@@ -478,18 +481,26 @@ class RankRealloc:
         # source -> GPU -> GPU ... chunk by chunk): True = every phase, "auto" =
         # where it lowers the estimated link bottleneck by >10%.
         host_of_all = [self.owner[d] for d in range(n)]
+        # ``overlap``: in-host fan-outs start per chunk inside phase 0 (star
+        # scheme, same flag machinery) instead of after a barrier.
         self.relay_phases: List[int] = []
-        if relay and world > 1 and mode == PUSH and hierarchical:
-            for pi, (_sname, dname) in enumerate(bind):
-                if dname in self.multicast:
-                    continue
-                p = self.plans[pi]
-                if relay != "auto" or (link_bottleneck(p, host_of_all, relay=True) <
-                                       0.9 * link_bottleneck(p, host_of_all)):
-                    self.relay_phases.append(pi)
+        self.overlap_phases: List[int] = []
+        flag_ok = world > 1 and mode == PUSH and hierarchical
+        for pi, (_sname, dname) in enumerate(bind):
+            if not flag_ok or dname in self.multicast:
+                continue
+            p = self.plans[pi]
+            if relay and (relay != "auto" or (link_bottleneck(p, host_of_all, relay=True) <
+                                              0.9 * link_bottleneck(p, host_of_all))):
+                self.relay_phases.append(pi)
+            if overlap:
+                self.overlap_phases.append(pi)
         self.relay_bufs: Dict[int, DeviceBuffer] = {}
-        for pi in self.relay_phases:
-            slots = relay_slots(self.plans[pi], host_of_all)
+        for pi in sorted(set(self.relay_phases) | set(self.overlap_phases)):
+            slots = relay_slots(self.plans[pi], host_of_all, chain=pi in self.relay_phases,
+                                overlap=pi in self.overlap_phases)
+            if slots == 0:
+                continue
             self.relay_bufs[pi] = DeviceBuffer(cuda_device, 4 * max(slots, 64))
             self.relay_bufs[pi].zero()
         self.buffers: Dict[str, Dict[int, object]] = {}
@@ -570,7 +581,9 @@ class RankRealloc:
         for pi, (sname, dname) in enumerate(bind):
             self.executors.append(Executor(self.plans[pi], cuda_device, self.ptrs[sname], self.ptrs[dname],
                                            self.local, mode, host_of=host_of if hierarchical else None,
-                                           mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_tables.get(pi)))
+                                           mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_tables.get(pi),
+                                           relay_chain=pi in self.relay_phases,
+                                           overlap_fanout=pi in self.overlap_phases))
             self.executors[-1].set_kernel(kernel)
         # Every rank must run the same barrier sequence: a phase has a fan-out
         # step if any rank has fan-out work in it.

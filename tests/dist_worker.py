@@ -92,6 +92,32 @@ def main() -> int:
             rr.close()
     elif rank == 0:
         print("dist_worker: NVLS multicast not supported, skipped", flush=True)
+    # Overlapped fan-out (star flags) and relay + overlap, over all parity cases.
+    for relay_opt in (False, True):
+        for sp, dp in CASES:
+            src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
+            dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
+            plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
+            rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
+                               relay=relay_opt, overlap=True)
+            for d, b in rr.buffers["a"].items():
+                R.fill_shard(plan, R.SRC, d, b.ptr, 37)
+            for rep in range(2):
+                for b in rr.buffers["b"].values():
+                    b.zero()
+                torch.cuda.synchronize()
+                dist.barrier()
+                rr.run_phase(0)
+                torch.cuda.synchronize()
+                for d, b in rr.buffers["b"].items():
+                    got = b.to_host()
+                    want = O.fill(TINY_GQA, dst, c, d, 37)
+                    if not np.array_equal(got, want):
+                        failures.append(f"overlap relay={relay_opt} {sp}->{dp} rep {rep}: device {d} differs in "
+                                        f"{int(np.count_nonzero(got != want))} elements")
+            if rr.relay_timeouts():
+                failures.append(f"overlap relay={relay_opt} {sp}->{dp}: {rr.relay_timeouts()} timeouts")
+            rr.close()
     # Pipelined relay: chunks travel source -> GPU -> GPU with per-chunk flags.
     relay_cases = [
         (Placement(DeviceMesh(0, 1, 0, 1), ParallelStrategy()), placement(8, 1, 8, 1)),  # replicate from dev 0
