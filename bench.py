@@ -429,7 +429,7 @@ def main() -> None:
                     help="push = SM peer stores; relay = push + pipelined relay for payloads reaching >= 2 "
                          "other GPUs; mc = push + NVLS multicast for the first phase's destination (N > 1); "
                          "auto = push, relay where it lowers the link bottleneck")
-    ap.add_argument("--overlap", choices=["on", "off"], default="off",
+    ap.add_argument("--overlap", choices=["on", "off"], default="on",
                     help="run in-host fan-outs per chunk inside the first phase (N > 1) instead of after a barrier")
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--layers", type=int, default=0, help="truncate the model (profiling only)")
