@@ -848,7 +848,12 @@ rr_status rr_exec_enable_onload(rr_exec* ex, int n_src, const int32_t* src_devic
     for (size_t i = 0; i < n; ++i) {
       int seg = 0;
       const auto it = first_chunk.find(a.src_dev[i]);
-      if (it != first_chunk.end() && !a.src_is_dst[i]) {
+      if (a.items[i].wait_flag) {
+        // Relay / overlapped fan-out items wait on other GPUs' pushes, which
+        // may depend on this GPU's own pushes: launch them after every chunk
+        // (and so every push of this GPU) so no launch waits on a later one.
+        seg = static_cast<int>(C);
+      } else if (it != first_chunk.end() && !a.src_is_dst[i]) {
         const DeviceId d = a.src_dev[i];
         int64_t total = 0;
         for (int k = 0; k < n_src; ++k)
