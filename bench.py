@@ -334,18 +334,26 @@ def run_b200(args) -> None:
         for _ in range(e2e_steps):
             e2e_step()
         e_ms = (time.perf_counter() - e0) * 1e3 / e2e_steps
-        ev = torch.tensor([e_ms, h2d, d2h], dtype=torch.float64, device="cuda")
+        # the onloaded (pipelined) path must produce the same shards
+        e2e_bad = 0
+        for i, (sname, dname) in enumerate(bind):
+            for d, b in rr.buffers[dname].items():
+                e2e_bad += R.verify_shard(plans[i], R.DST, d, b.ptr, seed)[0]
+        ev = torch.tensor([e_ms, h2d, d2h, e2e_bad], dtype=torch.float64, device="cuda")
         if dist:
             mx = ev.clone()
             dist.all_reduce(mx, op=dist.ReduceOp.MAX)
             sm = ev.clone()
             dist.all_reduce(sm)
-            e_ms, h2d, d2h = float(mx[0]), float(sm[1]), float(sm[2])
+            e_ms, h2d, d2h, e2e_bad = float(mx[0]), float(sm[1]), float(sm[2]), float(sm[3])
         else:
-            e_ms, h2d, d2h = float(ev[0]), float(ev[1]), float(ev[2])
+            e_ms, h2d, d2h, e2e_bad = float(ev[0]), float(ev[1]), float(ev[2]), float(ev[3])
+        verified = verified and e2e_bad == 0
         e2e = {"value": round(total_written / (e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_ms, 3),
-               "timing": "host wall clock around stream-synchronised steps, max over ranks"}
+               "timing": "host wall clock around stream-synchronised steps, max over ranks",
+               "path": "public API: RankRealloc.run_phase_onload (H2D chunks pipelined with the copy kernels)",
+               "verified": e2e_bad == 0}
         for hb in list(host.values()) + list(res_host.values()):
             hb.free()
 
