@@ -242,17 +242,16 @@ std::vector<Job> build_jobs(const std::vector<LoweredOp>& ops, const HostMap& hm
       jobs.push_back(std::move(j));
     } else if (mode == 0) {  // push: the source host drives phase A
       if (hs == hm.me) {
-        for (const auto& [h, list] : groups) {
-          Job j;
-          j.phase = 0;
-          j.src = op.src;
-          j.op = &op;
-          if (h == hm.me)
-            j.dsts = list;
-          else
-            j.dsts = {list.front()};
-          jobs.push_back(std::move(j));
-        }
+        // One job: the source is read once for every local destination and
+        // every remote host's leader (build_items splits > kMaxFan targets).
+        Job j;
+        j.phase = 0;
+        j.src = op.src;
+        j.op = &op;
+        if (mine != groups.end()) j.dsts = mine->second;
+        for (const auto& [h, list] : groups)
+          if (h != hm.me) j.dsts.push_back(list.front());
+        jobs.push_back(std::move(j));
       }
     } else if (mine != groups.end()) {  // pull: each destination host fetches for itself
       Job j;

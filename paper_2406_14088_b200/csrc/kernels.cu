@@ -509,6 +509,12 @@ int launch_bulk(int variant, const CopyItem* items, int n_items, int ctas, int f
     case 8: return launch_bulk_t<4, 32768, 3>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
     case 9: return launch_bulk_t<3, 32768, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
     case 10: return launch_bulk_t<3, 65536, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 11: return launch_bulk_t<2, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 12: return launch_bulk_t<3, 8192>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 13: return launch_bulk_t<6, 8192>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 14: return launch_bulk_t<4, 16384, 2>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 15: return launch_bulk_t<4, 16384, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 16: return launch_bulk_t<8, 8192>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -86,7 +86,7 @@ int copy_max_ctas(int* ctas_per_sm, int* sms);
 // With max_ctas != NULL only reports the resident-CTA capacity.
 int launch_bulk(int variant, const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream,
                 int* max_ctas, unsigned int* sched);
-constexpr int kBulkVariants = 10;
+constexpr int kBulkVariants = 16;
 int launch_fill(const FillItem* items, int n_items, uint64_t seed, void* stream);
 int launch_verify(const FillItem* items, int n_items, uint64_t seed, unsigned long long* counters,
                   uint64_t buf_base, void* stream);
