@@ -377,9 +377,14 @@ def run_b200(args) -> None:
         else:
             # bottleneck GPU's link bytes over the slowest rank's kernel time
             achieved = dom_wire / (dom_ms * 1e-3) / 1e9
+            # ncu: NVLink protocol adds 18.75% to the payload bytes on the wire
+            # (profiles/r01_nvlink_counters_n2.json: 9535619072 / 8029995008)
+            proto = 9535619072 / 8029995008
             roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK, "unit": "GB/s",
-                    "frac": round(achieved / NVLINK_PEAK, 4), "traffic": None, "kernel": kname, "phase": dom,
-                    "peak_source": "nominal NVLink 5 per direction (measured peer copy ~770 GB/s)",
+                    "frac": round(achieved / NVLINK_PEAK, 4), "traffic": int(dom_wire * proto),
+                    "traffic_source": "payload x measured NVLink protocol factor (ncu nvltx__bytes)",
+                    "wire_frac_incl_protocol": round(achieved * proto / NVLINK_PEAK, 4), "kernel": kname,
+                    "phase": dom, "peak_source": "nominal NVLink 5 per direction (measured peer copy ~770 GB/s)",
                     "algorithmic_bytes_per_launch": int(dom_wire)}
         nvl = float(allv[:, 3 + P:3 + 2 * P].sum(axis=1).max() / (ms_max * 1e-3) / 1e9) if world > 1 else 0.0
         line = {
