@@ -1,0 +1,403 @@
+// C ABI, executor half (include/rr_realloc.h "execution"): builds the copy
+// items of a lowered plan for one GPU (exec_plan.cpp), uploads them and
+// launches the sm_100a kernels (kernels.cu) phase by phase, optionally
+// pipelined behind a host->device onload.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "capi_internal.hpp"
+#include "exec_plan.hpp"
+#include "rr_internal.hpp"
+
+using namespace rlplan;
+using rr::capi::check_cuda;
+using rr::capi::guarded;
+using rr::capi::need;
+
+// ---------------------------------------------------------------------------
+// Executor object
+// ---------------------------------------------------------------------------
+
+struct rr_exec {
+  struct Phase {
+    rr::CopyItem* d = nullptr;  // 16-byte (vec) items first, then 2-byte items
+    int n = 0, n_vec = 0;
+    int64_t read = 0, written = 0;
+  };
+  int cuda_device = 0;
+  Phase phase[2];  // [0] direct copies, [1] in-host fan-out from leader replicas
+  int fence_sys = 0;
+  int default_ctas = 0;
+  // 0 = LDG/STG rr_copy_kernel, 1..kBulkVariants = TMA bulk ring. Default:
+  // variant 1 (4 x 16 KiB stages, 3 CTAs/SM), the fastest in the r01 sweep.
+  int kernel = 1;
+  int bulk_ctas = 0;
+  unsigned int* d_sched = nullptr;  // dynamic work counter (see retire_cta)
+  int64_t wire_in = 0, wire_out = 0;  // bytes crossing into / out of this host
+  uint32_t epoch = 0;                 // relay flag epoch, advanced by every phase-0 launch
+
+  // Onload pipelining (rr_exec_enable_onload): phase-0 items regrouped into
+  // segments by the last host->device chunk they read; segment s may start
+  // once chunk s has landed.
+  rr::ItemSet phase0_host;             // items + provenance as built
+  std::vector<void*> src_bases;        // source buffer per plan device
+  struct Segment {
+    int offset = 0, n = 0, n_vec = 0;
+  };
+  std::vector<Segment> segments;       // [0] = no dependency, [1 + c] waits for chunk c
+  rr::CopyItem* d_onload = nullptr;
+  struct Chunk {
+    int32_t device;
+    int64_t offset, bytes;
+  };
+  std::vector<Chunk> chunks;
+  std::vector<cudaEvent_t> events;
+};
+
+namespace {
+
+// Host map for an executor: `local` plan devices form this host; without an
+// explicit table every other device is its own host.
+rr::HostMap host_map(const rr_plan* plan, int n_local, const int32_t* local, const int32_t* host_of) {
+  const int n = plan->cluster.device_count();
+  rr::HostMap hm;
+  hm.host.resize(static_cast<size_t>(n));
+  if (host_of) {
+    for (int d = 0; d < n; ++d) hm.host[static_cast<size_t>(d)] = host_of[d];
+    need(n_local > 0, "host_of needs at least one local device");
+    need(local[0] >= 0 && local[0] < n, "local device out of range");
+    hm.me = host_of[local[0]];
+    for (int i = 0; i < n_local; ++i) {
+      need(local[i] >= 0 && local[i] < n, "local device out of range");
+      need(host_of[local[i]] == hm.me, "local devices must share one host");
+    }
+    return hm;
+  }
+  hm.hierarchical = false;
+  for (int d = 0; d < n; ++d) hm.host[static_cast<size_t>(d)] = n + d;  // distinct remote hosts
+  hm.me = -1;
+  for (int i = 0; i < n_local; ++i) {
+    need(local[i] >= 0 && local[i] < n, "local device out of range");
+    hm.host[static_cast<size_t>(local[i])] = hm.me;
+  }
+  return hm;
+}
+
+void upload(const rr::ItemSet& set, rr_exec::Phase& ph) {
+  ph.n = static_cast<int>(set.items.size());
+  ph.n_vec = set.n_vec;
+  ph.read = set.read;
+  ph.written = set.written;
+  if (set.items.empty()) return;
+  const size_t bytes = set.items.size() * sizeof(rr::CopyItem);
+  check_cuda(cudaMalloc(&ph.d, bytes), "cudaMalloc(items)");
+  check_cuda(cudaMemcpy(ph.d, set.items.data(), bytes, cudaMemcpyHostToDevice), "upload items");
+}
+
+void launch_phase(rr_exec* ex, const rr_exec::Phase& ph, void* stream, int ctas) {
+  check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+  if (ph.n == 0) return;
+  if (ex->kernel == 0) {
+    check_cuda(rr::launch_copy(ph.d, ph.n, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys, stream, ex->d_sched,
+                               ex->epoch),
+               "rr_copy_kernel launch");
+    return;
+  }
+  // Relay, multicast and 2-byte items take the LDG/STG kernel, launched
+  // first so relay chains start immediately; then the TMA bulk kernel.
+  if (ph.n > ph.n_vec)
+    check_cuda(rr::launch_copy(ph.d + ph.n_vec, ph.n - ph.n_vec, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys,
+                               stream, ex->d_sched, ex->epoch),
+               "rr_copy_kernel launch (relay / multicast / 2-byte items)");
+  if (ph.n_vec > 0)
+    check_cuda(rr::launch_bulk(ex->kernel, ph.d, ph.n_vec, ctas > 0 ? ctas : ex->bulk_ctas, ex->fence_sys, stream,
+                               nullptr, ex->d_sched),
+               "rr_bulk_kernel launch");
+}
+
+}  // namespace
+
+rr_status rr_plan_work(const rr_plan* plan, int n_local, const int32_t* local, const int32_t* host_of, int mode,
+                       int64_t* out6) {
+  return guarded([&] {
+    need(plan != nullptr && out6 != nullptr, "null plan/output");
+    need(mode == 0 || mode == 1, "mode must be 0 (push) or 1 (pull)");
+    const rr::HostMap hm = host_map(plan, n_local, local, host_of);
+    const auto jobs = rr::build_jobs(plan->lowered, hm, mode);
+    const auto a = rr::build_items(jobs, 0, hm, nullptr, nullptr, int64_t{1} << 30);
+    const auto b = rr::build_items(jobs, 1, hm, nullptr, nullptr, int64_t{1} << 30);
+    out6[0] = a.read;
+    out6[1] = a.written;
+    out6[2] = b.read;
+    out6[3] = b.written;
+    rr::host_wire_bytes(plan->lowered, hm, &out6[4], &out6[5]);
+  });
+}
+
+rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, void* const* src_bufs,
+                         void* const* dst_bufs, int n_local, const int32_t* local, const int32_t* host_of,
+                         int mode, int64_t chunk_bytes, rr_exec** out) {
+  rr_exec_options opt;
+  opt.mode = mode;
+  opt.chunk_bytes = chunk_bytes;
+  opt.host_of = host_of;
+  opt.mc_bufs = nullptr;
+  opt.relay_flags = nullptr;
+  opt.relay_chain = 0;
+  opt.overlap_fanout = 0;
+  return rr_exec_create_ex(plan, cuda_device, n_devices, src_bufs, dst_bufs, n_local, local, &opt, out);
+}
+
+rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices, void* const* src_bufs,
+                            void* const* dst_bufs, int n_local, const int32_t* local,
+                            const rr_exec_options* options, rr_exec** out) {
+  return guarded([&] {
+    need(plan != nullptr && out != nullptr && options != nullptr, "null plan/options/output");
+    const int mode = options->mode;
+    int64_t chunk_bytes = options->chunk_bytes;
+    need(mode == 0 || mode == 1, "mode must be 0 (push) or 1 (pull)");
+    need(n_devices >= plan->cluster.device_count(), "buffer tables must cover every cluster device");
+    if (chunk_bytes <= 0) chunk_bytes = 256 << 10;
+    need(chunk_bytes >= 16, "chunk_bytes too small");
+    rr::HostMap hm = host_map(plan, n_local, local, options->host_of);
+    if (options->mc_bufs) {
+      need(options->host_of != nullptr, "multicast needs a host_of table");
+      need(mode == 0, "multicast is a push-mode path");
+      hm.mc.resize(hm.host.size());
+      for (size_t d = 0; d < hm.mc.size(); ++d) hm.mc[d] = reinterpret_cast<uint64_t>(options->mc_bufs[d]);
+    }
+    hm.relay_chunk = chunk_bytes;
+    if (options->relay_flags) {
+      need(options->host_of != nullptr && mode == 0, "relay needs a host_of table and push mode");
+      hm.relay_flags.resize(hm.host.size());
+      for (size_t d = 0; d < hm.relay_flags.size(); ++d)
+        hm.relay_flags[d] = reinterpret_cast<uint64_t>(options->relay_flags[d]);
+      hm.relay_chain = options->relay_chain != 0;
+      hm.relay_star = options->overlap_fanout != 0;
+    }
+    const auto jobs = rr::build_jobs(plan->lowered, hm, mode);
+    const auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes);
+    const auto b = rr::build_items(jobs, 1, hm, src_bufs, dst_bufs, chunk_bytes);
+
+    auto ex = std::make_unique<rr_exec>();
+    ex->cuda_device = cuda_device;
+    // Remote accesses (peer stores, or peer loads in pull mode) must be
+    // visible system-wide before the following barrier releases them.
+    int64_t win = 0, wout = 0;
+    rr::host_wire_bytes(plan->lowered, hm, &win, &wout);
+    ex->fence_sys = (a.remote_stores || win || wout) ? 1 : 0;
+    ex->wire_in = win;
+    ex->wire_out = wout;
+    check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
+    int per_sm = 0, sms = 0;
+    check_cuda(rr::copy_max_ctas(&per_sm, &sms), "occupancy query");
+    ex->default_ctas = std::max(1, per_sm) * sms;
+    upload(a, ex->phase[0]);
+    upload(b, ex->phase[1]);
+    ex->phase0_host = a;
+    ex->src_bases.assign(static_cast<size_t>(n_devices), nullptr);
+    for (int d = 0; d < n_devices; ++d) ex->src_bases[static_cast<size_t>(d)] = src_bufs ? src_bufs[d] : nullptr;
+    check_cuda(cudaMalloc(&ex->d_sched, 4 * sizeof(unsigned int)), "cudaMalloc(sched)");
+    check_cuda(cudaMemset(ex->d_sched, 0, 4 * sizeof(unsigned int)), "cudaMemset(sched)");
+    check_cuda(rr::launch_bulk(ex->kernel, nullptr, 0, 0, 0, nullptr, &ex->bulk_ctas, nullptr), "bulk occupancy");
+    *out = ex.release();
+  });
+}
+
+rr_status rr_exec_launch(rr_exec* ex, void* stream, int ctas) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    ++ex->epoch;  // every rank launches phase 0 the same number of times
+    launch_phase(ex, ex->phase[0], stream, ctas);
+  });
+}
+
+rr_status rr_exec_kernel_count(const rr_exec* ex, int* phase0, int* phase1) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    auto count = [&](const rr_exec::Phase& ph) {
+      if (ph.n == 0) return 0;
+      if (ex->kernel == 0) return 1;
+      return (ph.n > ph.n_vec ? 1 : 0) + (ph.n_vec > 0 ? 1 : 0);
+    };
+    *phase0 = count(ex->phase[0]);
+    *phase1 = count(ex->phase[1]);
+  });
+}
+
+rr_status rr_exec_relay_timeouts(rr_exec* ex, int64_t* timeouts) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+    unsigned int h[4];
+    check_cuda(cudaMemcpy(h, ex->d_sched, sizeof(h), cudaMemcpyDeviceToHost), "read relay status");
+    *timeouts = h[2];
+  });
+}
+
+rr_status rr_plan_relay_slots(const rr_plan* plan, const int32_t* host_of, int64_t chunk_bytes, int relay_chain,
+                              int overlap_fanout, int64_t* slots) {
+  return guarded([&] {
+    need(plan != nullptr && host_of != nullptr, "null plan/host table");
+    rr::HostMap hm;
+    for (int d = 0; d < plan->cluster.device_count(); ++d) hm.host.push_back(host_of[d]);
+    hm.relay_chunk = chunk_bytes > 0 ? chunk_bytes : (256 << 10);
+    hm.relay_chain = relay_chain != 0;
+    hm.relay_star = overlap_fanout != 0;
+    *slots = rr::relay_slots(plan->lowered, hm);
+  });
+}
+
+rr_status rr_exec_launch_fanout(rr_exec* ex, void* stream, int ctas) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    launch_phase(ex, ex->phase[1], stream, ctas);
+  });
+}
+
+rr_status rr_exec_set_kernel(rr_exec* ex, int kernel) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    need(kernel >= 0 && kernel <= rr::kBulkVariants, "unknown copy kernel");
+    ex->kernel = kernel;
+    if (kernel > 0) {
+      check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+      check_cuda(rr::launch_bulk(kernel, nullptr, 0, 0, 0, nullptr, &ex->bulk_ctas, nullptr), "bulk occupancy");
+    }
+  });
+}
+
+rr_status rr_exec_stats(const rr_exec* ex, int phase, int64_t* items, int64_t* written, int64_t* read) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    need(phase == 0 || phase == 1, "phase must be 0 or 1");
+    const auto& ph = ex->phase[phase];
+    *items = ph.n;
+    *written = ph.written;
+    *read = ph.read;
+  });
+}
+
+rr_status rr_exec_wire(const rr_exec* ex, int64_t* wire_in, int64_t* wire_out) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    *wire_in = ex->wire_in;
+    *wire_out = ex->wire_out;
+  });
+}
+
+rr_status rr_exec_enable_onload(rr_exec* ex, int n_src, const int32_t* src_devices, const int64_t* src_bytes,
+                                 int64_t chunk_bytes) {
+  return guarded([&] {
+    need(ex != nullptr, "null executor");
+    need(n_src >= 0 && chunk_bytes >= 4096, "bad onload arguments");
+    check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+    for (auto e : ex->events) cudaEventDestroy(e);
+    ex->events.clear();
+    ex->chunks.clear();
+    std::map<DeviceId, int> first_chunk;
+    for (int i = 0; i < n_src; ++i) {
+      need(src_devices[i] >= 0 && src_devices[i] < static_cast<int>(ex->src_bases.size()), "onload device range");
+      need(ex->src_bases[static_cast<size_t>(src_devices[i])] != nullptr, "onload device has no source buffer");
+      first_chunk[src_devices[i]] = static_cast<int>(ex->chunks.size());
+      for (int64_t off = 0; off < src_bytes[i]; off += chunk_bytes)
+        ex->chunks.push_back({src_devices[i], off, std::min(chunk_bytes, src_bytes[i] - off)});
+    }
+    // Segment of each item: 0 = independent of the onload, 1 + c = needs chunk c.
+    const rr::ItemSet& a = ex->phase0_host;
+    const size_t n = a.items.size(), C = ex->chunks.size();
+    std::vector<std::vector<int>> seg_vec(C + 1), seg_other(C + 1);
+    for (size_t i = 0; i < n; ++i) {
+      int seg = 0;
+      const auto it = first_chunk.find(a.src_dev[i]);
+      if (a.items[i].wait_flag) {
+        // Relay / overlapped fan-out items wait on other GPUs' pushes, which
+        // may depend on this GPU's own pushes: launch them after every chunk
+        // (and so every push of this GPU) so no launch waits on a later one.
+        seg = static_cast<int>(C);
+      } else if (it != first_chunk.end() && !a.src_is_dst[i]) {
+        const DeviceId d = a.src_dev[i];
+        int64_t total = 0;
+        for (int k = 0; k < n_src; ++k)
+          if (src_devices[k] == d) total = src_bytes[k];
+        need(a.src_end[i] <= total, "an item reads beyond the onloaded bytes of its source");
+        seg = 1 + it->second + static_cast<int>((a.src_end[i] - 1) / chunk_bytes);
+      }
+      (static_cast<int>(i) < a.n_vec ? seg_vec : seg_other)[static_cast<size_t>(seg)].push_back(static_cast<int>(i));
+    }
+    std::vector<rr::CopyItem> ordered;
+    ordered.reserve(n);
+    ex->segments.assign(C + 1, {});
+    for (size_t s = 0; s <= C; ++s) {
+      auto& sg = ex->segments[s];
+      sg.offset = static_cast<int>(ordered.size());
+      for (int i : seg_vec[s]) ordered.push_back(a.items[static_cast<size_t>(i)]);
+      sg.n_vec = static_cast<int>(seg_vec[s].size());
+      for (int i : seg_other[s]) ordered.push_back(a.items[static_cast<size_t>(i)]);
+      sg.n = static_cast<int>(ordered.size()) - sg.offset;
+    }
+    if (ex->d_onload) cudaFree(ex->d_onload);
+    ex->d_onload = nullptr;
+    if (!ordered.empty()) {
+      check_cuda(cudaMalloc(&ex->d_onload, ordered.size() * sizeof(rr::CopyItem)), "cudaMalloc(onload items)");
+      check_cuda(cudaMemcpy(ex->d_onload, ordered.data(), ordered.size() * sizeof(rr::CopyItem),
+                            cudaMemcpyHostToDevice),
+                 "upload onload items");
+    }
+    ex->events.resize(C);
+    for (auto& e : ex->events) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+  });
+}
+
+rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_stream, void* stream, int ctas) {
+  return guarded([&] {
+    need(ex != nullptr && host_bufs != nullptr, "null executor/host buffers");
+    need(!ex->segments.empty(), "rr_exec_enable_onload has not been called");
+    check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+    ++ex->epoch;  // a phase-0 launch like rr_exec_launch
+    auto cs = static_cast<cudaStream_t>(copy_stream);
+    auto ks = static_cast<cudaStream_t>(stream);
+    // The copy stream must not overwrite sources still read by an earlier
+    // launch on the compute stream.
+    cudaEvent_t ready;
+    check_cuda(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "cudaEventCreate");
+    check_cuda(cudaEventRecord(ready, ks), "cudaEventRecord");
+    check_cuda(cudaStreamWaitEvent(cs, ready, 0), "cudaStreamWaitEvent");
+    cudaEventDestroy(ready);
+    for (size_t c = 0; c < ex->chunks.size(); ++c) {
+      const auto& ch = ex->chunks[c];
+      const void* h = host_bufs[ch.device];
+      need(h != nullptr, "missing host buffer for an onloaded device");
+      char* dst = static_cast<char*>(ex->src_bases[static_cast<size_t>(ch.device)]) + ch.offset;
+      check_cuda(cudaMemcpyAsync(dst, static_cast<const char*>(h) + ch.offset, static_cast<size_t>(ch.bytes),
+                                 cudaMemcpyHostToDevice, cs),
+                 "onload cudaMemcpyAsync");
+      check_cuda(cudaEventRecord(ex->events[c], cs), "cudaEventRecord");
+    }
+    for (size_t s = 0; s < ex->segments.size(); ++s) {
+      if (s > 0) check_cuda(cudaStreamWaitEvent(ks, ex->events[s - 1], 0), "cudaStreamWaitEvent");
+      const auto& sg = ex->segments[s];
+      if (sg.n == 0) continue;
+      rr_exec::Phase ph;
+      ph.d = ex->d_onload + sg.offset;
+      ph.n = sg.n;
+      ph.n_vec = sg.n_vec;
+      launch_phase(ex, ph, stream, ctas);
+    }
+  });
+}
+
+void rr_exec_destroy(rr_exec* ex) {
+  if (!ex) return;
+  cudaSetDevice(ex->cuda_device);
+  for (auto& ph : ex->phase)
+    if (ph.d) cudaFree(ph.d);
+  if (ex->d_sched) cudaFree(ex->d_sched);
+  if (ex->d_onload) cudaFree(ex->d_onload);
+  for (auto e : ex->events) cudaEventDestroy(e);
+  delete ex;
+}
