@@ -210,9 +210,11 @@ def run_b200(args) -> None:
     multicast = [bind[0][1]] if args.mode == "mc" else []
     relay = {"auto": "auto", "relay": True}.get(args.mode, False)
     overlap = args.overlap == "on"
+    # --kernel k: k for every phase (sweeps); default: per phase kind
     kernel = R.DEFAULT_KERNEL if args.kernel < 0 else args.kernel
+    flag_kernel = R.DEFAULT_FLAG_KERNEL if args.kernel < 0 else args.kernel
     rr = R.RankRealloc(plans, shards, bind, rank, world, local_rank, mode=mode, kernel=kernel,
-                       multicast=multicast, relay=relay, overlap=overlap)
+                       multicast=multicast, relay=relay, overlap=overlap, flag_kernel=flag_kernel)
     stream = torch.cuda.current_stream()
     seed = 1
     for d, b in rr.buffers["train"].items():
@@ -384,7 +386,9 @@ def run_b200(args) -> None:
                     "frac": round(achieved / NVLINK_PEAK, 4), "traffic": int(dom_wire * proto),
                     "traffic_source": "payload x measured NVLink protocol factor (ncu nvltx__bytes)",
                     "wire_frac_incl_protocol": round(achieved * proto / NVLINK_PEAK, 4), "kernel": kname,
-                    "phase": dom, "peak_source": "nominal NVLink 5 per direction (measured peer copy ~770 GB/s)",
+                    "phase": dom, "peak_source": "nominal NVLink 5 per direction (measured ceilings: SM peer stores "
+                                                               "~710, one copy-engine copy ~780 GB/s; "
+                                                               "profiles/r01_nvlink_probe_n2.txt)",
                     "algorithmic_bytes_per_launch": int(dom_wire)}
         nvl = float(allv[:, 3 + P:3 + 2 * P].sum(axis=1).max() / (ms_max * 1e-3) / 1e9) if world > 1 else 0.0
         line = {
@@ -395,7 +399,7 @@ def run_b200(args) -> None:
                        "plan_devices_per_gpu": w.devices // world, "phases": len(plans),
                        "policy": args.policy, "mode": args.mode, "multicast_sets": rr.multicast,
                        "relay_phases": rr.relay_phases, "overlap_phases": rr.overlap_phases,
-                       "copy_kernel": kname,
+                       "copy_kernel": kname, "bulk_variants": {"plain": kernel, "flag_synchronised": flag_kernel},
                        "l2": "inputs larger than L2 (multi-GB shards); no flush needed",
                        "weights": "hash-initialised bf16 (seed 1), verified after timing"},
             "phase_ms": [round(float(x), 4) for x in ph_ms_all.max(axis=0)],

@@ -214,10 +214,14 @@ rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices,
 rr_status rr_exec_launch(rr_exec* ex, void* stream, int ctas);
 /* Phase 1 (in-host fan-out from leader replicas); no-op when empty. */
 rr_status rr_exec_launch_fanout(rr_exec* ex, void* stream, int ctas);
-/* Copy engine: 0 = vectorised LDG/STG kernel; 1..10 = TMA bulk-copy ring
+/* Copy kernel: 0 = vectorised LDG/STG kernel; 1..16 = TMA bulk-copy ring
  * variants (cp.async.bulk through shared-memory stages; default 1).
- * 2-byte-aligned items always take the LDG/STG kernel. */
+ * 2-byte-aligned and multicast items always take the LDG/STG kernel. */
 rr_status rr_exec_set_kernel(rr_exec* ex, int kernel);
+/* The same for flag-synchronised phases (relay chains, overlapped fan-out),
+ * which run as one kernel: the bulk variant when every item is TMA-eligible,
+ * else the LDG/STG kernel. Default 5. */
+rr_status rr_exec_set_flag_kernel(rr_exec* ex, int kernel);
 /* Per phase: items, bytes stored (sum over destinations), bytes read. */
 rr_status rr_exec_stats(const rr_exec* ex, int phase, int64_t* items, int64_t* bytes_written,
                         int64_t* bytes_read);

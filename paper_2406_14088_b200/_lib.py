@@ -127,6 +127,7 @@ _SIGNATURES = {
     "rr_exec_launch_onload": (c_int, [_P, POINTER(_P), _P, _P, c_int]),
     "rr_exec_wire": (c_int, [_P, POINTER(c_int64), POINTER(c_int64)]),
     "rr_exec_set_kernel": (c_int, [_P, c_int]),
+    "rr_exec_set_flag_kernel": (c_int, [_P, c_int]),
     "rr_exec_stats": (c_int, [_P, c_int, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
     "rr_exec_destroy": (None, [_P]),
     "rr_fill_shard": (c_int, [_P, c_int, c_int32, _P, c_uint64, _P]),

@@ -27,15 +27,19 @@ struct rr_exec {
     rr::CopyItem* d = nullptr;  // 16-byte (vec) items first, then 2-byte items
     int n = 0, n_vec = 0;
     int64_t read = 0, written = 0;
+    bool flagged = false;  // relay / overlapped fan-out flags: one kernel runs the whole phase
   };
   int cuda_device = 0;
   Phase phase[2];  // [0] direct copies, [1] in-host fan-out from leader replicas
   int fence_sys = 0;
   int default_ctas = 0;
-  // 0 = LDG/STG rr_copy_kernel, 1..kBulkVariants = TMA bulk ring. Default:
-  // variant 1 (4 x 16 KiB stages, 3 CTAs/SM), the fastest in the r01 sweep.
-  int kernel = 1;
-  int bulk_ctas = 0;
+  // 0 = LDG/STG rr_copy_kernel, 1..kBulkVariants = TMA bulk ring. Defaults
+  // from the r01 sweeps: variant 1 (4 x 16 KiB stages, 3 CTAs/SM) for plain
+  // phases, variant 5 (3 x 16 KiB, 4 CTAs/SM) for flag-synchronised ones,
+  // where more resident CTAs keep NVLink busy while some spin on a flag
+  // (profiles/r01_flag_kernel_sweep_n{2,4}.txt).
+  int kernel = 1, flag_kernel = 5;
+  int bulk_ctas = 0, flag_bulk_ctas = 0;
   unsigned int* d_sched = nullptr;  // dynamic work counter (see retire_cta)
   int64_t wire_in = 0, wire_out = 0;  // bytes crossing into / out of this host
   uint32_t epoch = 0;                 // relay flag epoch, advanced by every phase-0 launch
@@ -92,6 +96,8 @@ void upload(const rr::ItemSet& set, rr_exec::Phase& ph) {
   ph.n_vec = set.n_vec;
   ph.read = set.read;
   ph.written = set.written;
+  ph.flagged = std::any_of(set.items.begin(), set.items.end(),
+                           [](const rr::CopyItem& it) { return it.wait_flag || it.signal_flag; });
   if (set.items.empty()) return;
   const size_t bytes = set.items.size() * sizeof(rr::CopyItem);
   check_cuda(cudaMalloc(&ph.d, bytes), "cudaMalloc(items)");
@@ -101,21 +107,24 @@ void upload(const rr::ItemSet& set, rr_exec::Phase& ph) {
 void launch_phase(rr_exec* ex, const rr_exec::Phase& ph, void* stream, int ctas) {
   check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
   if (ph.n == 0) return;
-  if (ex->kernel == 0) {
+  const int kernel = ph.flagged ? ex->flag_kernel : ex->kernel;
+  if (kernel == 0) {
     check_cuda(rr::launch_copy(ph.d, ph.n, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys, stream, ex->d_sched,
                                ex->epoch),
                "rr_copy_kernel launch");
     return;
   }
-  // Relay, multicast and 2-byte items take the LDG/STG kernel, launched
-  // first so relay chains start immediately; then the TMA bulk kernel.
+  // Multicast and 2-byte items take the LDG/STG kernel, then the TMA bulk
+  // kernel. A flag-synchronised phase is entirely in one of the two
+  // (exec_plan.cpp build_items).
   if (ph.n > ph.n_vec)
     check_cuda(rr::launch_copy(ph.d + ph.n_vec, ph.n - ph.n_vec, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys,
                                stream, ex->d_sched, ex->epoch),
                "rr_copy_kernel launch (relay / multicast / 2-byte items)");
   if (ph.n_vec > 0)
-    check_cuda(rr::launch_bulk(ex->kernel, ph.d, ph.n_vec, ctas > 0 ? ctas : ex->bulk_ctas, ex->fence_sys, stream,
-                               nullptr, ex->d_sched),
+    check_cuda(rr::launch_bulk(kernel, ph.d, ph.n_vec,
+                               ctas > 0 ? ctas : (ph.flagged ? ex->flag_bulk_ctas : ex->bulk_ctas), ex->fence_sys,
+                               stream, nullptr, ex->d_sched, ex->epoch),
                "rr_bulk_kernel launch");
 }
 
@@ -204,6 +213,8 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
     check_cuda(cudaMalloc(&ex->d_sched, 4 * sizeof(unsigned int)), "cudaMalloc(sched)");
     check_cuda(cudaMemset(ex->d_sched, 0, 4 * sizeof(unsigned int)), "cudaMemset(sched)");
     check_cuda(rr::launch_bulk(ex->kernel, nullptr, 0, 0, 0, nullptr, &ex->bulk_ctas, nullptr), "bulk occupancy");
+    check_cuda(rr::launch_bulk(ex->flag_kernel, nullptr, 0, 0, 0, nullptr, &ex->flag_bulk_ctas, nullptr),
+               "bulk occupancy");
     *out = ex.release();
   });
 }
@@ -221,7 +232,7 @@ rr_status rr_exec_kernel_count(const rr_exec* ex, int* phase0, int* phase1) {
     need(ex != nullptr, "null executor");
     auto count = [&](const rr_exec::Phase& ph) {
       if (ph.n == 0) return 0;
-      if (ex->kernel == 0) return 1;
+      if ((ph.flagged ? ex->flag_kernel : ex->kernel) == 0) return 1;
       return (ph.n > ph.n_vec ? 1 : 0) + (ph.n_vec > 0 ? 1 : 0);
     };
     *phase0 = count(ex->phase[0]);
@@ -259,16 +270,26 @@ rr_status rr_exec_launch_fanout(rr_exec* ex, void* stream, int ctas) {
   });
 }
 
+namespace {
+
+void select_kernel(rr_exec* ex, int kernel, int* slot, int* slot_ctas) {
+  need(ex != nullptr, "null executor");
+  need(kernel >= 0 && kernel <= rr::kBulkVariants, "unknown copy kernel");
+  *slot = kernel;
+  if (kernel > 0) {
+    check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+    check_cuda(rr::launch_bulk(kernel, nullptr, 0, 0, 0, nullptr, slot_ctas, nullptr), "bulk occupancy");
+  }
+}
+
+}  // namespace
+
 rr_status rr_exec_set_kernel(rr_exec* ex, int kernel) {
-  return guarded([&] {
-    need(ex != nullptr, "null executor");
-    need(kernel >= 0 && kernel <= rr::kBulkVariants, "unknown copy kernel");
-    ex->kernel = kernel;
-    if (kernel > 0) {
-      check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
-      check_cuda(rr::launch_bulk(kernel, nullptr, 0, 0, 0, nullptr, &ex->bulk_ctas, nullptr), "bulk occupancy");
-    }
-  });
+  return guarded([&] { select_kernel(ex, kernel, &ex->kernel, &ex->bulk_ctas); });
+}
+
+rr_status rr_exec_set_flag_kernel(rr_exec* ex, int kernel) {
+  return guarded([&] { select_kernel(ex, kernel, &ex->flag_kernel, &ex->flag_bulk_ctas); });
 }
 
 rr_status rr_exec_stats(const rr_exec* ex, int phase, int64_t* items, int64_t* written, int64_t* read) {
@@ -386,6 +407,7 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
       ph.d = ex->d_onload + sg.offset;
       ph.n = sg.n;
       ph.n_vec = sg.n_vec;
+      ph.flagged = ex->phase[0].flagged;
       launch_phase(ex, ph, stream, ctas);
     }
   });

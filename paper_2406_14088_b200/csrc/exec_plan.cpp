@@ -436,25 +436,31 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
   // TMA-eligible items (16-byte, no multicast) first; the rest take the
   // LDG/STG kernel.
   //
-  // With flag-synchronised (relay / star) items the whole phase runs in the
-  // one LDG/STG kernel, so local copies, pushes and per-chunk fan-outs
-  // overlap. Deadlock freedom: within every round the items that never wait
-  // come first, so when a CTA claims a waiting item of round k every push of
-  // rounds <= k on this GPU is already claimed; the push it waits for sits in
-  // round k of another GPU, whose waits in turn only depend on our claimed
-  // pushes. Pushes never wait, so every wait is eventually released.
+  // With flag-synchronised (relay / star) items the whole phase runs in ONE
+  // kernel, so local copies, pushes and per-chunk fan-outs overlap: the TMA
+  // bulk kernel when every item is TMA-eligible, else the LDG/STG kernel
+  // (two launches on one stream would serialise a wait behind the push it
+  // needs on the other GPU). Deadlock freedom: within every round the items
+  // that never wait come first, so when a CTA claims a waiting item of round
+  // k every push of rounds <= k on this GPU is already claimed; the push it
+  // waits for sits in round k of another GPU, whose waits in turn only depend
+  // on our claimed pushes. A CTA never spins while holding unfinished
+  // pushes, so every wait is eventually released.
   std::vector<const Tagged*> vec_items, other;
   size_t total = 0;
-  bool flagged = false;
+  bool flagged = false, all_tma = true;
   for (const auto& st : streams) {
     total += st.size();
-    for (const auto& t : st) flagged = flagged || t.it.wait_flag || t.it.signal_flag;
+    for (const auto& t : st) {
+      flagged = flagged || t.it.wait_flag || t.it.signal_flag;
+      all_tma = all_tma && t.it.vec == kItemVec;
+    }
   }
   for (size_t k = 0, seen = 0; seen < total; ++k)
     for (int waiting = 0; waiting < 2; ++waiting)
       for (const auto& st : streams)
         if (k < st.size() && (st[k].it.wait_flag != 0) == (waiting == 1)) {
-          const bool tma = !flagged && st[k].it.vec == kItemVec;
+          const bool tma = flagged ? all_tma : st[k].it.vec == kItemVec;
           (tma ? vec_items : other).push_back(&st[k]);
           ++seen;
         }

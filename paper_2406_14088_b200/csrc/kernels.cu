@@ -272,28 +272,59 @@ __device__ __forceinline__ void bulk_wait_read() {
 
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// Full completion (writes performed, not only shared memory read) of all but
+// the N most recent bulk groups.
+template <int N>
+__device__ __forceinline__ void bulk_wait_group() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Relay signal after the chunk's bulk stores completed: order them (async
+// proxy) before the generic-proxy flag store, at system scope.
+__device__ __forceinline__ void release_signal(uint64_t flag, uint32_t epoch) {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+}
+
 // One piece = up to `rows` rows of `row_bytes` (all 16-byte multiples).
 struct Piece {
   uint64_t src;
   uint32_t rows, row_bytes, src_pitch, dst_pitch;  // bytes
   uint64_t dst_off;                                 // byte offset added to every dst base
   int item;
+  bool last;  // the item's final piece (its relay signal follows it)
 };
 
-// Walks this CTA's items (blockIdx.x, +gridDim.x, ...) in pieces of at most
-// `cap` bytes.
+// Walks the items this CTA claims from the dynamic counter, in pieces of at
+// most `cap` bytes.
 struct PieceCursor {
   int item;
   uint32_t row, col;  // next row; next column byte offset inside the row
+  bool waited;        // the current item's relay wait is satisfied
 };
 
-__device__ __forceinline__ bool next_piece(const CopyItem* __restrict__ items, int n_items, PieceCursor& c,
-                                           uint32_t cap, Piece& p, unsigned int* sched) {
+enum PieceStatus { kNoWork = 0, kPiece = 1, kBlocked = 2 };
+
+// kBlocked: the next item waits on a relay flag and the caller still holds
+// issued pieces. It must finish them (their signals may be what another GPU
+// waits for) and call again with can_block before this CTA may spin.
+__device__ __forceinline__ PieceStatus next_piece(const CopyItem* __restrict__ items, int n_items, PieceCursor& c,
+                                                  uint32_t cap, Piece& p, unsigned int* sched, bool can_block,
+                                                  uint32_t epoch) {
   while (c.item < n_items) {
     const CopyItem& it = items[c.item];
     const uint32_t row_bytes = it.row_units * 16u;
     const uint32_t sp = it.src_pitch * 16u, dp = it.dst_pitch * 16u;
     if (c.row < it.nrows) {
+      if (it.wait_flag && !c.waited) {
+        if (!can_block) return kBlocked;
+        if (!wait_flag_geq(reinterpret_cast<const uint32_t*>(it.wait_flag), epoch)) atomicAdd(sched + 2, 1u);
+        // the chunk was written by another GPU's generic-proxy stores; order
+        // the TMA (async-proxy) reads of it after the acquire
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        c.waited = true;
+      }
       p.item = c.item;
       if (row_bytes <= cap) {
         const uint32_t rows = min(it.nrows - c.row, max(1u, cap / row_bytes));
@@ -316,18 +347,27 @@ __device__ __forceinline__ bool next_piece(const CopyItem* __restrict__ items, i
       }
       p.src_pitch = sp;
       p.dst_pitch = dp;
-      return true;
+      p.last = c.row >= it.nrows;
+      return kPiece;
     }
     c.item = grab_item(sched);
     c.row = c.col = 0;
+    c.waited = false;
   }
-  return false;
+  return kNoWork;
 }
 
 // HINT bit 0: source reads evict-first in L2; bit 1: destination writes evict-first.
+//
+// Relay / overlapped fan-out items (wait_flag, signal_flag) run here too, so
+// a flag-synchronised phase keeps the TMA ring's HBM efficiency. A CTA never
+// spins on a wait while it holds issued pieces: it first drains its ring
+// (stores, completion, signals), so every claimed push is finished by a CTA
+// that cannot block on it, and the round ordering argument of build_items
+// (exec_plan.cpp) carries over from the LDG/STG kernel.
 template <int S, int STAGE, int HINT>
 __global__ void __launch_bounds__(32) rr_bulk_kernel(const CopyItem* __restrict__ items, int n_items,
-                                                     int fence_sys, unsigned int* sched) {
+                                                     int fence_sys, unsigned int* sched, uint32_t epoch) {
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ __align__(8) uint64_t full[S];
   __shared__ Piece meta[S];
@@ -337,7 +377,7 @@ __global__ void __launch_bounds__(32) rr_bulk_kernel(const CopyItem* __restrict_
   for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 
-  PieceCursor ld{grab_item(sched), 0, 0};
+  PieceCursor ld{grab_item(sched), 0, 0, false};
   Piece p;
   auto issue_load = [&](int s) {
     meta[s] = p;
@@ -353,12 +393,24 @@ __global__ void __launch_bounds__(32) rr_bulk_kernel(const CopyItem* __restrict_
     }
   };
 
-  int issued = 0;
-  while (issued < S && next_piece(items, n_items, ld, STAGE, p, sched)) {
-    issue_load(issued);
-    ++issued;
-  }
-  for (int done = 0; done < issued; ++done) {
+  // Stage k % S holds piece k. Piece k may be loaded once the store group of
+  // piece k - S has finished reading shared memory; keeping one committed
+  // group in flight (wait_group.read 1) leaves S - 1 loads outstanding.
+  int issued = 0, done = 0;
+  uint64_t pending = 0;  // signal flag of a finished chunk not yet released
+  for (;;) {
+    PieceStatus st = kPiece;
+    while (issued < S || issued - done < S - 1) {
+      st = next_piece(items, n_items, ld, STAGE, p, sched, issued == done, epoch);
+      if (st != kPiece) break;
+      if (issued >= S) bulk_wait_read<1>();
+      issue_load(issued % S);
+      ++issued;
+    }
+    if (done == issued) {
+      if (st == kNoWork) break;
+      continue;  // blocked with an empty ring: the next call may spin
+    }
     const int s = done % S;
     mbar_wait(&full[s], (done / S) & 1);
     const Piece q = meta[s];
@@ -375,14 +427,21 @@ __global__ void __launch_bounds__(32) rr_bulk_kernel(const CopyItem* __restrict_
       }
     }
     bulk_commit();
-    if (done >= 1) {
-      // Everything but the group just committed has finished reading its
-      // stage: refill the stage drained in the previous iteration.
-      bulk_wait_read<1>();
-      if (next_piece(items, n_items, ld, STAGE, p, sched)) {
-        issue_load((done - 1) % S);
-        ++issued;
-      }
+    ++done;
+    // A finished chunk is released to the GPU that waits for it one piece
+    // later: by now the store group before this one has usually landed, so
+    // waiting for its completion costs little, whereas waiting for the group
+    // just committed would stall the ring for a full NVLink round trip.
+    if (pending) {
+      bulk_wait_group<1>();
+      release_signal(pending, epoch);
+      pending = 0;
+    }
+    if (q.last && it.signal_flag) pending = it.signal_flag;
+    if (pending && done == issued) {  // about to spin or exit: nothing may stay unreleased
+      bulk_wait_all();
+      release_signal(pending, epoch);
+      pending = 0;
     }
   }
   bulk_wait_all();
@@ -474,7 +533,7 @@ namespace {
 
 template <int S, int STAGE, int HINT = 0>
 int launch_bulk_t(const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream, int* max_ctas,
-                  unsigned int* sched) {
+                  unsigned int* sched, uint32_t epoch) {
   constexpr int kSmem = S * STAGE;
   cudaError_t e = cudaFuncSetAttribute(rr_bulk_kernel<S, STAGE, HINT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
   if (e != cudaSuccess) return e;
@@ -490,31 +549,31 @@ int launch_bulk_t(const CopyItem* items, int n_items, int ctas, int fence_sys, v
   if (n_items <= 0) return cudaSuccess;
   if (ctas > n_items) ctas = n_items;
   rr_bulk_kernel<S, STAGE, HINT><<<ctas, 32, kSmem, static_cast<cudaStream_t>(stream)>>>(items, n_items, fence_sys,
-                                                                                        sched);
+                                                                                        sched, epoch);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 int launch_bulk(int variant, const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream,
-                int* max_ctas, unsigned int* sched) {
+                int* max_ctas, unsigned int* sched, uint32_t epoch) {
   switch (variant) {
-    case 1: return launch_bulk_t<4, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 2: return launch_bulk_t<8, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 3: return launch_bulk_t<4, 32768>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 4: return launch_bulk_t<6, 32768>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 5: return launch_bulk_t<3, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 6: return launch_bulk_t<4, 32768, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 7: return launch_bulk_t<4, 32768, 2>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 8: return launch_bulk_t<4, 32768, 3>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 9: return launch_bulk_t<3, 32768, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 10: return launch_bulk_t<3, 65536, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 11: return launch_bulk_t<2, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 12: return launch_bulk_t<3, 8192>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 13: return launch_bulk_t<6, 8192>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 14: return launch_bulk_t<4, 16384, 2>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 15: return launch_bulk_t<4, 16384, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
-    case 16: return launch_bulk_t<8, 8192>(items, n_items, ctas, fence_sys, stream, max_ctas, sched);
+    case 1: return launch_bulk_t<4, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 2: return launch_bulk_t<8, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 3: return launch_bulk_t<4, 32768>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 4: return launch_bulk_t<6, 32768>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 5: return launch_bulk_t<3, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 6: return launch_bulk_t<4, 32768, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 7: return launch_bulk_t<4, 32768, 2>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 8: return launch_bulk_t<4, 32768, 3>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 9: return launch_bulk_t<3, 32768, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 10: return launch_bulk_t<3, 65536, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 11: return launch_bulk_t<2, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 12: return launch_bulk_t<3, 8192>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 13: return launch_bulk_t<6, 8192>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 14: return launch_bulk_t<4, 16384, 2>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 15: return launch_bulk_t<4, 16384, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
+    case 16: return launch_bulk_t<8, 8192>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
     default: return cudaErrorInvalidValue;
   }
 }

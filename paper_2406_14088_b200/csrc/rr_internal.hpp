@@ -76,16 +76,16 @@ __host__ __device__ inline uint16_t weight_value(uint64_t seed, uint64_t tensor,
 }
 
 // Host-callable launchers (kernels.cu). All return a cudaError_t as int.
-// sched: 2 device uints, zero before the first launch (kernels reset them).
 // sched: 4 device uints (next item, retired CTAs, relay timeouts, unused);
 // epoch: value relay flags are compared against / set to.
 int launch_copy(const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream, unsigned int* sched,
                 uint32_t epoch = 0);
 int copy_max_ctas(int* ctas_per_sm, int* sms);
-// TMA bulk variant (1..kBulkVariants = stage ring shapes / L2 hints); items must all be vec items.
-// With max_ctas != NULL only reports the resident-CTA capacity.
+// TMA bulk variant (1..kBulkVariants = stage ring shapes / L2 hints); items must all be vec items
+// without multicast (relay wait / signal flags are supported). With max_ctas != NULL only reports
+// the resident-CTA capacity.
 int launch_bulk(int variant, const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream,
-                int* max_ctas, unsigned int* sched);
+                int* max_ctas, unsigned int* sched, uint32_t epoch = 0);
 constexpr int kBulkVariants = 16;
 int launch_fill(const FillItem* items, int n_items, uint64_t seed, void* stream);
 int launch_verify(const FillItem* items, int n_items, uint64_t seed, unsigned long long* counters,

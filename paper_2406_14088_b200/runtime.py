@@ -28,9 +28,12 @@ from .rlplan import ReallocPlan
 
 PUSH, PULL = 0, 1
 SRC, DST = 0, 1
-# Copy engine used unless a caller picks one (rr_exec_set_kernel): the TMA
+# Copy kernel used unless a caller picks one (rr_exec_set_kernel): the TMA
 # bulk ring, 4 x 16 KiB stages, 3 CTAs per SM (profiles/r01_sweep_kernels.txt).
 DEFAULT_KERNEL = 1
+# ... and for flag-synchronised phases (rr_exec_set_flag_kernel): 3 x 16 KiB
+# stages, 4 CTAs per SM (profiles/r01_flag_kernel_sweep_n{2,4}.txt).
+DEFAULT_FLAG_KERNEL = 5
 
 
 def _stream_ptr(stream) -> Optional[int]:
@@ -211,8 +214,12 @@ class Executor:
         check(lib.rr_exec_launch_onload(self._h, hp, _stream_ptr(copy_stream), _stream_ptr(stream), ctas))
 
     def set_kernel(self, kernel: int) -> None:
-        """0 = LDG/STG kernel, 1..10 = TMA bulk-copy ring variants."""
+        """0 = LDG/STG kernel, 1..16 = TMA bulk-copy ring variants."""
         check(lib.rr_exec_set_kernel(self._h, kernel))
+
+    def set_flag_kernel(self, kernel: int) -> None:
+        """The kernel of flag-synchronised phases (relay / overlapped fan-out)."""
+        check(lib.rr_exec_set_flag_kernel(self._h, kernel))
 
     def close(self) -> None:
         if self._h and self._h.value:
@@ -453,7 +460,8 @@ class RankRealloc:
     def __init__(self, plans: Sequence[ReallocPlan], shards: Dict[str, Tuple[int, int]],
                  bind: Sequence[Tuple[str, str]], rank: int, world: int, cuda_device: int, group=None,
                  mode: int = PUSH, kernel: int = DEFAULT_KERNEL, hierarchical: bool = True,
-                 multicast: Sequence[str] = (), relay=False, overlap: bool = False):
+                 multicast: Sequence[str] = (), relay=False, overlap: bool = False,
+                 flag_kernel: int = DEFAULT_FLAG_KERNEL):
         """``multicast`` names shard sets whose per-GPU leader shards (the
         lowest-id plan device of the set on each GPU) are members of one NVLS
         multicast object: a payload bound for every GPU is then stored once
@@ -585,6 +593,7 @@ class RankRealloc:
                                            relay_chain=pi in self.relay_phases,
                                            overlap_fanout=pi in self.overlap_phases))
             self.executors[-1].set_kernel(kernel)
+            self.executors[-1].set_flag_kernel(flag_kernel)
         # Every rank must run the same barrier sequence: a phase has a fan-out
         # step if any rank has fan-out work in it.
         counts = [e.fanout_items for e in self.executors]
@@ -595,9 +604,11 @@ class RankRealloc:
             counts = [sum(c[i] for c in allc) for i in range(len(counts))]
         self.has_fanout = [c > 0 for c in counts]
 
-    def set_kernel(self, kernel: int) -> None:
+    def set_kernel(self, kernel: int, flag_kernel: Optional[int] = None) -> None:
         for e in self.executors:
             e.set_kernel(kernel)
+            if flag_kernel is not None:
+                e.set_flag_kernel(flag_kernel)
 
     def run_phase(self, i: int, stream=None, ctas: int = 0) -> None:
         """Phase i: direct copies, barrier, then (if any rank has some) the

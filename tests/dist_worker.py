@@ -92,14 +92,15 @@ def main() -> int:
             rr.close()
     elif rank == 0:
         print("dist_worker: NVLS multicast not supported, skipped", flush=True)
-    # Overlapped fan-out (star flags) and relay + overlap, over all parity cases.
-    for relay_opt in (False, True):
+    # Overlapped fan-out (star flags) and relay + overlap, over all parity
+    # cases, on the TMA bulk kernel (1) and the LDG/STG kernel (0).
+    for relay_opt, kernel in ((False, 1), (True, 1), (False, 0), (True, 0)):
         for sp, dp in CASES:
             src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
             dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
             plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
             rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
-                               relay=relay_opt, overlap=True)
+                               relay=relay_opt, overlap=True, kernel=kernel, flag_kernel=kernel)
             for d, b in rr.buffers["a"].items():
                 R.fill_shard(plan, R.SRC, d, b.ptr, 37)
             for rep in range(2):
@@ -113,10 +114,10 @@ def main() -> int:
                     got = b.to_host()
                     want = O.fill(TINY_GQA, dst, c, d, 37)
                     if not np.array_equal(got, want):
-                        failures.append(f"overlap relay={relay_opt} {sp}->{dp} rep {rep}: device {d} differs in "
+                        failures.append(f"overlap relay={relay_opt} kernel {kernel} {sp}->{dp} rep {rep}: device {d} differs in "
                                         f"{int(np.count_nonzero(got != want))} elements")
             if rr.relay_timeouts():
-                failures.append(f"overlap relay={relay_opt} {sp}->{dp}: {rr.relay_timeouts()} timeouts")
+                failures.append(f"overlap relay={relay_opt} kernel {kernel} {sp}->{dp}: {rr.relay_timeouts()} timeouts")
             rr.close()
     # Pipelined relay: chunks travel source -> GPU -> GPU with per-chunk flags.
     relay_cases = [
@@ -124,10 +125,10 @@ def main() -> int:
         (placement(8, 1, 1, 8), placement(8, 1, 8, 1)),                                  # tp8 -> dp8
         (placement(2, 1, 1, 2, offset=2), placement(8, 1, 4, 2)),                        # 2 sources -> dp4 tp2
     ]
-    for src, dst in relay_cases:
+    for (src, dst), kernel in [(case, k) for case in relay_cases for k in (1, 0)]:
         plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
         rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
-                           relay=True)
+                           relay=True, kernel=kernel, flag_kernel=kernel)
         for d, b in rr.buffers["a"].items():
             R.fill_shard(plan, R.SRC, d, b.ptr, 29)
         torch.cuda.synchronize()
@@ -143,10 +144,10 @@ def main() -> int:
                 got = b.to_host()
                 want = O.fill(TINY_GQA, dst, c, d, 29)
                 if not np.array_equal(got, want):
-                    failures.append(f"relay {src.strategy}->{dst.strategy} rep {rep}: device {d} differs in "
+                    failures.append(f"relay kernel {kernel} {src.strategy}->{dst.strategy} rep {rep}: device {d} differs in "
                                     f"{int(np.count_nonzero(got != want))} elements")
         if rr.relay_timeouts():
-            failures.append(f"relay {src.strategy}->{dst.strategy}: {rr.relay_timeouts()} timeouts")
+            failures.append(f"relay kernel {kernel} {src.strategy}->{dst.strategy}: {rr.relay_timeouts()} timeouts")
         rr.close()
     if os.environ.get("RR_FULL_7B") == "1":
         w = WORKLOADS["llama7b_tp8_dp8_roundtrip"]
