@@ -214,7 +214,8 @@ def run_b200(args) -> None:
     kernel = R.DEFAULT_KERNEL if args.kernel < 0 else args.kernel
     flag_kernel = R.DEFAULT_FLAG_KERNEL if args.kernel < 0 else args.kernel
     rr = R.RankRealloc(plans, shards, bind, rank, world, local_rank, mode=mode, kernel=kernel,
-                       multicast=multicast, relay=relay, overlap=overlap, flag_kernel=flag_kernel)
+                       multicast=multicast, relay=relay, overlap=overlap, flag_kernel=flag_kernel,
+                       chunk_bytes=args.chunk_kib << 10)
     stream = torch.cuda.current_stream()
     seed = 1
     for d, b in rr.buffers["train"].items():
@@ -400,6 +401,7 @@ def run_b200(args) -> None:
                        "policy": args.policy, "mode": args.mode, "multicast_sets": rr.multicast,
                        "relay_phases": rr.relay_phases, "overlap_phases": rr.overlap_phases,
                        "copy_kernel": kname, "bulk_variants": {"plain": kernel, "flag_synchronised": flag_kernel},
+                       "chunk_kib": args.chunk_kib or 256, "ctas": args.ctas or "resident capacity",
                        "l2": "inputs larger than L2 (multi-GB shards); no flush needed",
                        "weights": "hash-initialised bf16 (seed 1), verified after timing"},
             "phase_ms": [round(float(x), 4) for x in ph_ms_all.max(axis=0)],
@@ -449,6 +451,7 @@ def main() -> None:
     ap.add_argument("--overlap", choices=["on", "off"], default="on",
                     help="run in-host fan-outs per chunk inside the first phase (N > 1) instead of after a barrier")
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--chunk-kib", type=int, default=0, help="work-item size in KiB (0 = library default)")
     ap.add_argument("--layers", type=int, default=0, help="truncate the model (profiling only)")
     ap.add_argument("--kernel", type=int, default=-1, help="copy engine: 0 LDG/STG, 1..5 TMA bulk (-1 default)")
     ap.add_argument("--cpu-layers", type=int, default=2)

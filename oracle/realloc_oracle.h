@@ -23,7 +23,10 @@
  * reference's own C++ compiled from /root/reference (oracle/_ref); the plan is
  * checked against every SPEC example (tests/golden/spec_examples.json) and the
  * SPEC replay criterion. Byte-level layout decisions have no
- * reference fixture (the reference never materialises weights).
+ * reference fixture (the reference never materialises weights);
+ * they are pinned against third-party code instead: vLLM's tensor-parallel
+ * weight loaders (tests/golden/vllm_tp_shards.json) and HF transformers'
+ * LLaMA parameter inventory (tests/golden/hf_llama_inventory.json).
  */
 #ifndef REALLOC_ORACLE_H_
 #define REALLOC_ORACLE_H_

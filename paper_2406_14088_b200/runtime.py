@@ -461,12 +461,13 @@ class RankRealloc:
                  bind: Sequence[Tuple[str, str]], rank: int, world: int, cuda_device: int, group=None,
                  mode: int = PUSH, kernel: int = DEFAULT_KERNEL, hierarchical: bool = True,
                  multicast: Sequence[str] = (), relay=False, overlap: bool = False,
-                 flag_kernel: int = DEFAULT_FLAG_KERNEL):
+                 flag_kernel: int = DEFAULT_FLAG_KERNEL, chunk_bytes: int = 0):
         """``multicast`` names shard sets whose per-GPU leader shards (the
         lowest-id plan device of the set on each GPU) are members of one NVLS
         multicast object: a payload bound for every GPU is then stored once
         (K3) instead of once per GPU (needs world > 1, push mode,
-        hierarchical delivery)."""
+        hierarchical delivery). ``chunk_bytes``: work-item size (0 = the
+        library default), also the relay/overlap flag granularity."""
         self.plans, self.rank, self.world, self.cuda_device = list(plans), rank, world, cuda_device
         n = plans[0].cluster.device_count()
         self.local = hosted_devices(n, rank, world)
@@ -505,7 +506,7 @@ class RankRealloc:
                 self.overlap_phases.append(pi)
         self.relay_bufs: Dict[int, DeviceBuffer] = {}
         for pi in sorted(set(self.relay_phases) | set(self.overlap_phases)):
-            slots = relay_slots(self.plans[pi], host_of_all, chain=pi in self.relay_phases,
+            slots = relay_slots(self.plans[pi], host_of_all, chunk_bytes, chain=pi in self.relay_phases,
                                 overlap=pi in self.overlap_phases)
             if slots == 0:
                 continue
@@ -588,7 +589,7 @@ class RankRealloc:
         self.executors: List[Executor] = []
         for pi, (sname, dname) in enumerate(bind):
             self.executors.append(Executor(self.plans[pi], cuda_device, self.ptrs[sname], self.ptrs[dname],
-                                           self.local, mode, host_of=host_of if hierarchical else None,
+                                           self.local, mode, chunk_bytes, host_of=host_of if hierarchical else None,
                                            mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_tables.get(pi),
                                            relay_chain=pi in self.relay_phases,
                                            overlap_fanout=pi in self.overlap_phases))
