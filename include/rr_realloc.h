@@ -235,6 +235,15 @@ rr_status rr_exec_stats(const rr_exec* ex, int phase, int64_t* items, int64_t* b
 rr_status rr_exec_enable_onload(rr_exec* ex, int n_src, const int32_t* src_devices, const int64_t* src_bytes,
                                 int64_t chunk_bytes);
 rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_stream, void* stream, int ctas);
+/* Offload of parameters being parked ("host-device (e.g.,
+ * offload)"; SPEC.md:423 offload nodes): the local source shards
+ * src_devices[i] (their first src_bytes[i] bytes) are copied device->host
+ * into host_bufs[device] (pinned) on copy_stream, starting once the work
+ * already on `stream` is done. A reallocation launched on `stream` after
+ * this call overlaps the copies: both only read the sources. The caller
+ * must order any later write to those source buffers after copy_stream. */
+rr_status rr_exec_launch_offload(rr_exec* ex, int n_src, const int32_t* src_devices, const int64_t* src_bytes,
+                                 void* const* host_bufs, void* copy_stream, void* stream);
 /* Kernels one rr_exec_launch / rr_exec_launch_fanout issues (0..2 each). */
 rr_status rr_exec_kernel_count(const rr_exec* ex, int* phase0, int* phase1);
 /* Bytes entering / leaving this executor's host over links per launch. */

@@ -12,6 +12,10 @@ actually takes on B200, from the same lowered work the kernels run:
   store path (or the multicast rate for multicast payloads);
 * phases serialise, GPUs run in parallel: time = max over GPUs of
   max(HBM time, link time) per phase, plus a fixed launch/barrier cost.
+* offload / onload of parked parameters (SPEC.md:423 prices them at
+  ``bytes / host_to_device_bw``) at the measured host-link rate per GPU; a
+  pipelined onload overlaps phase 0, so that phase takes the longer of the
+  two.
 
 Constants are the r01 measurements (profiles/).
 """
@@ -30,15 +34,24 @@ class B200Profile:
     nvlink_mc_gbs: float = 565.0        # per receiving GPU, NVLS multimem.st (4 GPUs)
     launch_us: float = 8.0              # kernel launch + dynamic-scheduler tail
     barrier_us: float = 12.0            # cross-GPU flag barrier
+    host_link_gbs: float = 55.6         # pinned host <-> HBM per GPU, either direction (r01 ce_probe h2d/*)
+
+
+def host_transfer_seconds(nbytes_per_gpu: int, profile: B200Profile = B200Profile()) -> float:
+    """Duration of an offload or onload node that moves
+    ``nbytes_per_gpu`` between pinned host memory and each GPU's HBM (every
+    GPU has its own host link)."""
+    return nbytes_per_gpu / (profile.host_link_gbs * 1e9)
 
 
 def estimate_seconds(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
                      profile: B200Profile = B200Profile(), multicast: bool = False,
-                     relay: bool = False) -> Dict[str, float]:
+                     relay: bool = False, onload: bool = False) -> Dict[str, float]:
     """Estimated execution time of `plan` with plan device d hosted on GPU
     host_of[d] (default: one GPU per plan device). `relay`: payloads reaching
     >= 2 other GPUs use the pipelined relay (one copy in and out per GPU,
-    fan-out fused into phase 0)."""
+    fan-out fused into phase 0). `onload`: the source shards arrive from
+    pinned host memory pipelined with phase 0 (rr_exec_launch_onload)."""
     n = plan.cluster.device_count()
     host = list(host_of) if host_of is not None else list(range(n))
     hosts = sorted(set(host))
@@ -80,13 +93,20 @@ def estimate_seconds(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
     t_phase0 = max(max(hbm[h] / (profile.hbm_copy_gbs * 1e9),
                        max(egress[h], ingress[h]) / (profile.nvlink_push_gbs * 1e9) +
                        mc_in[h] / (profile.nvlink_mc_gbs * 1e9)) for h in hosts)
+    onload_s = 0.0
+    if onload:
+        src_bytes = {h: 0 for h in hosts}
+        for d in plan.devices(0):
+            src_bytes[host[d]] += plan.shard_bytes(0, d)
+        onload_s = max(host_transfer_seconds(b, profile) for b in src_bytes.values())
+        t_phase0 = max(t_phase0, onload_s)
     t_phase1 = max(fan[h] / (profile.hbm_copy_gbs * 1e9) for h in hosts)
     multi = len(hosts) > 1
     fixed = profile.launch_us * 1e-6 * (2 if t_phase1 > 0 else 1)
     if multi:
         fixed += profile.barrier_us * 1e-6 * (2 if t_phase1 > 0 else 1)
     total = t_phase0 + t_phase1 + fixed
-    return {"seconds": total, "phase0_s": t_phase0, "fanout_s": t_phase1,
+    return {"seconds": total, "phase0_s": t_phase0, "fanout_s": t_phase1, "onload_s": onload_s,
             "spec_est_time_s": plan.est_time,
             "max_link_bytes": max(max(egress[h], ingress[h]) + mc_in[h] for h in hosts),
             "max_hbm_bytes": max(hbm[h] for h in hosts)}

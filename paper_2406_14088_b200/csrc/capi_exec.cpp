@@ -413,6 +413,37 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
   });
 }
 
+rr_status rr_exec_launch_offload(rr_exec* ex, int n_src, const int32_t* src_devices, const int64_t* src_bytes,
+                                 void* const* host_bufs, void* copy_stream, void* stream) {
+  return guarded([&] {
+    need(ex != nullptr && host_bufs != nullptr, "null executor/host buffers");
+    need(n_src >= 0 && (n_src == 0 || (src_devices != nullptr && src_bytes != nullptr)), "bad offload arguments");
+    check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+    for (int i = 0; i < n_src; ++i) {
+      need(src_devices[i] >= 0 && src_devices[i] < static_cast<int>(ex->src_bases.size()), "offload device range");
+      need(ex->src_bases[static_cast<size_t>(src_devices[i])] != nullptr, "offload device has no source buffer");
+      need(host_bufs[src_devices[i]] != nullptr, "missing host buffer for an offloaded device");
+      need(src_bytes[i] >= 0, "negative offload size");
+    }
+    // Sources are complete once the work already on `stream` is; from then
+    // on the copy engine and a reallocation launched next on `stream` only
+    // read them, so the two overlap.
+    auto cs = static_cast<cudaStream_t>(copy_stream);
+    cudaEvent_t ready;
+    check_cuda(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "cudaEventCreate");
+    check_cuda(cudaEventRecord(ready, static_cast<cudaStream_t>(stream)), "cudaEventRecord");
+    check_cuda(cudaStreamWaitEvent(cs, ready, 0), "cudaStreamWaitEvent");
+    cudaEventDestroy(ready);
+    for (int i = 0; i < n_src; ++i) {
+      if (src_bytes[i] == 0) continue;
+      const DeviceId d = src_devices[i];
+      check_cuda(cudaMemcpyAsync(host_bufs[d], ex->src_bases[static_cast<size_t>(d)], static_cast<size_t>(src_bytes[i]),
+                                 cudaMemcpyDeviceToHost, cs),
+                 "offload cudaMemcpyAsync");
+    }
+  });
+}
+
 void rr_exec_destroy(rr_exec* ex) {
   if (!ex) return;
   cudaSetDevice(ex->cuda_device);

@@ -213,6 +213,22 @@ class Executor:
             hp[d] = p
         check(lib.rr_exec_launch_onload(self._h, hp, _stream_ptr(copy_stream), _stream_ptr(stream), ctas))
 
+    def launch_offload(self, src_bytes: Dict[int, int], host_ptrs: Dict[int, int], copy_stream,
+                       stream=None) -> None:
+        """Park the local source shards {device: bytes} in pinned host memory
+        (device -> host on ``copy_stream``, after the work already on
+        ``stream``). A launch() that follows on ``stream`` overlaps it; write
+        the sources only after ``copy_stream`` has drained."""
+        n = self.plan.cluster.device_count()
+        devs = sorted(src_bytes)
+        arr = (ctypes.c_int32 * max(1, len(devs)))(*devs)
+        sizes = (ctypes.c_int64 * max(1, len(devs)))(*[src_bytes[d] for d in devs])
+        hp = (ctypes.c_void_p * n)()
+        for d, p in host_ptrs.items():
+            hp[d] = p
+        check(lib.rr_exec_launch_offload(self._h, len(devs), arr, sizes, hp, _stream_ptr(copy_stream),
+                                         _stream_ptr(stream)))
+
     def set_kernel(self, kernel: int) -> None:
         """0 = LDG/STG kernel, 1..16 = TMA bulk-copy ring variants."""
         check(lib.rr_exec_set_kernel(self._h, kernel))
@@ -637,6 +653,17 @@ class RankRealloc:
             self._onload_key = {**getattr(self, "_onload_key", {}), i: key}
         e.launch_onload(host_ptrs, copy_stream, stream, ctas)
         self._finish_phase(i, stream, ctas)
+
+    def run_phase_offload(self, i: int, host_ptrs: Dict[int, int], copy_stream, stream=None,
+                          ctas: int = 0) -> None:
+        """Phase i while its local source shards are parked in pinned host
+        memory (host_ptrs: device -> pointer) on ``copy_stream``
+        ("host-device (e.g., offload)"): the device->host copies
+        and the reallocation kernels read the same shards concurrently."""
+        sname = self.bind[i][0]
+        self.executors[i].launch_offload({d: b.nbytes for d, b in self.buffers[sname].items()}, host_ptrs,
+                                         copy_stream, stream)
+        self.run_phase(i, stream, ctas)
 
     def close(self) -> None:
         stream_sync()

@@ -51,3 +51,45 @@ def test_onload_pipeline_bitexact(need_gpu, sp, dp, kernel):
         vc.free()
         for h in hosts.values():
             h.free()
+
+
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_offload_overlaps_reallocation_then_onload_round_trip(need_gpu, kernel):
+    """Park the source shards in pinned host memory while the reallocation
+    reads them ("host-device (e.g., offload)"), wipe them,
+    then onload them back pipelined with the same reallocation: every host
+    copy and every destination shard is bit-exact."""
+    import torch
+    c = b200_cluster(8)
+    src = placement(8, 1, 1, 8)
+    dst = placement(8, 1, 8, 1)
+    plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
+    vc = R.VirtualCluster(plan, 0)
+    hosts = {}
+    try:
+        vc.fill_sources(seed=17)
+        for d, b in vc.src.items():
+            hosts[d] = R.HostBuffer(b.nbytes)
+            hosts[d].array()[:] = 0
+        ex = vc.executor(R.PUSH, 8192, kernel)
+        copy = torch.cuda.Stream()
+        cur = torch.cuda.current_stream()
+        ex.launch_offload({d: b.nbytes for d, b in vc.src.items()}, {d: h.ptr for d, h in hosts.items()}, copy, cur)
+        ex.launch(cur)
+        torch.cuda.synchronize()
+        for d, h in hosts.items():
+            assert np.array_equal(h.array(), O.fill(TINY_GQA, src, c, d, 17)), d
+        for d, b in vc.dst.items():
+            assert np.array_equal(b.to_host(), O.fill(TINY_GQA, dst, c, d, 17)), d
+        for b in list(vc.src.values()) + list(vc.dst.values()):
+            b.zero()
+        ex.enable_onload({d: b.nbytes for d, b in vc.src.items()}, chunk_bytes=32 << 10)
+        ex.launch_onload({d: h.ptr for d, h in hosts.items()}, copy, cur)
+        torch.cuda.synchronize()
+        for d, b in vc.dst.items():
+            assert np.array_equal(b.to_host(), O.fill(TINY_GQA, dst, c, d, 17)), d
+        ex.close()
+    finally:
+        vc.free()
+        for h in hosts.values():
+            h.free()
