@@ -46,10 +46,6 @@ def measured_peaks() -> dict:
         return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
-# NCCL's version banner would otherwise precede the JSON line on rank 0's stdout
-os.environ.setdefault("NCCL_DEBUG", "WARN")
-
-
 def env_rank():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))

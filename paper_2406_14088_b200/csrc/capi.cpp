@@ -87,6 +87,15 @@ struct rr_barrier {
   uint32_t epoch = 0;
   uint32_t** d_flags = nullptr;
   int* d_timed_out = nullptr;
+
+  rr_barrier() = default;
+  rr_barrier(const rr_barrier&) = delete;
+  rr_barrier& operator=(const rr_barrier&) = delete;
+  ~rr_barrier() {  // also on a failed rr_barrier_create
+    cudaSetDevice(cuda_device);
+    if (d_flags) cudaFree(d_flags);
+    if (d_timed_out) cudaFree(d_timed_out);
+  }
 };
 
 namespace rr {
@@ -600,10 +609,4 @@ rr_status rr_barrier_status(rr_barrier* b, int* timed_out) {
   });
 }
 
-void rr_barrier_destroy(rr_barrier* b) {
-  if (!b) return;
-  cudaSetDevice(b->cuda_device);
-  cudaFree(b->d_flags);
-  cudaFree(b->d_timed_out);
-  delete b;
-}
+void rr_barrier_destroy(rr_barrier* b) { delete b; }

@@ -60,6 +60,19 @@ struct rr_exec {
   };
   std::vector<Chunk> chunks;
   std::vector<cudaEvent_t> events;
+
+  rr_exec() = default;
+  rr_exec(const rr_exec&) = delete;
+  rr_exec& operator=(const rr_exec&) = delete;
+  // Frees whatever was allocated, also when rr_exec_create_ex fails half way.
+  ~rr_exec() {
+    cudaSetDevice(cuda_device);
+    for (auto& ph : phase)
+      if (ph.d) cudaFree(ph.d);
+    if (d_sched) cudaFree(d_sched);
+    if (d_onload) cudaFree(d_onload);
+    for (auto e : events) cudaEventDestroy(e);
+  }
 };
 
 namespace {
@@ -444,13 +457,4 @@ rr_status rr_exec_launch_offload(rr_exec* ex, int n_src, const int32_t* src_devi
   });
 }
 
-void rr_exec_destroy(rr_exec* ex) {
-  if (!ex) return;
-  cudaSetDevice(ex->cuda_device);
-  for (auto& ph : ex->phase)
-    if (ph.d) cudaFree(ph.d);
-  if (ex->d_sched) cudaFree(ex->d_sched);
-  if (ex->d_onload) cudaFree(ex->d_onload);
-  for (auto e : ex->events) cudaEventDestroy(e);
-  delete ex;
-}
+void rr_exec_destroy(rr_exec* ex) { delete ex; }

@@ -113,6 +113,11 @@ struct rr_mcast {
   CUdeviceptr uc_va = 0, mc_va = 0;
   bool bound = false;
   int fd = -1;
+
+  rr_mcast() = default;
+  rr_mcast(const rr_mcast&) = delete;
+  rr_mcast& operator=(const rr_mcast&) = delete;
+  ~rr_mcast();  // releases whatever exists, also after a failed create/import/bind
 };
 
 rr_status rr_mcast_supported(int cuda_device, int* supported) {
@@ -234,24 +239,24 @@ rr_status rr_mcast_size(const rr_mcast* m, size_t* size) {
   });
 }
 
-void rr_mcast_destroy(rr_mcast* m) {
-  if (!m) return;
+rr_mcast::~rr_mcast() {
   const Driver& d = driver();
-  if (d.ok) {
-    cudaSetDevice(m->cuda_device);
+  if (d.ok && (mc || mem || uc_va || mc_va)) {
+    cudaSetDevice(cuda_device);
     cudaDeviceSynchronize();
-    if (m->mc_va) {
-      d.memUnmap(m->mc_va, m->size);
-      d.addrFree(m->mc_va, m->size);
+    if (mc_va) {
+      d.memUnmap(mc_va, size);
+      d.addrFree(mc_va, size);
     }
-    if (m->uc_va) {
-      d.memUnmap(m->uc_va, m->size);
-      d.addrFree(m->uc_va, m->size);
+    if (uc_va) {
+      d.memUnmap(uc_va, size);
+      d.addrFree(uc_va, size);
     }
-    if (m->bound) d.mcUnbind(m->mc, m->cuda_device, 0, m->size);
-    if (m->mem) d.memRelease(m->mem);
-    if (m->mc) d.memRelease(m->mc);
+    if (bound) d.mcUnbind(mc, cuda_device, 0, size);
+    if (mem) d.memRelease(mem);
+    if (mc) d.memRelease(mc);
   }
-  if (m->fd >= 0) close(m->fd);
-  delete m;
+  if (fd >= 0) close(fd);
 }
+
+void rr_mcast_destroy(rr_mcast* m) { delete m; }
