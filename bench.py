@@ -104,6 +104,8 @@ def cpu_sample_run(workload, layers: int, steps: int, warmup: int, threads: int,
     import numpy as np
     from oracle import oracle as O
     from paper_2406_14088_b200.workloads import truncated
+    if workload.data_bytes:  # already small: the whole batch
+        return cpu_sample_data(workload, steps, warmup, threads, budget_s)
     w = truncated(workload, layers)
     c = w.cluster()
     n = c.device_count()
@@ -147,6 +149,35 @@ def cpu_sample_run(workload, layers: int, steps: int, warmup: int, threads: int,
     return delivered / dt / 1e9, dt, delivered, ok, w
 
 
+def cpu_sample_data(w, steps: int, warmup: int, threads: int, budget_s: float = None):
+    """cpu_sample_run for a data workload: the oracle's plan_data_transfer
+    restatement executed on host buffers."""
+    import numpy as np
+    from oracle import oracle as O
+    c = w.cluster()
+    n = c.device_count()
+    (prod, cons), = w.phases
+    total = w.data_bytes * prod.strategy.dp
+    ops, loc = O.plan_data(prod, cons, c, w.data_bytes, 1)[:2]
+    src = [O.data_fill(prod, c, d, True, total, 1) if O.data_shard_bytes(prod, c, d, True, total) else None
+           for d in range(n)]
+    dst = [np.zeros(O.data_shard_bytes(cons, c, d, False, total) // 2, np.uint16) for d in range(n)]
+    delivered = sum(b * len(dsts) for (_s, dsts, _p, b) in ops + loc)
+    for _ in range(warmup):
+        O.data_execute(prod, cons, c, total, ops + loc, src, dst)
+    t0 = time.perf_counter()
+    done = 0
+    while True:
+        O.data_execute(prod, cons, c, total, ops + loc, src, dst)
+        done += 1
+        el = time.perf_counter() - t0
+        if done >= steps and (budget_s is None or el >= budget_s or done >= 1000):
+            break
+    dt = (time.perf_counter() - t0) / done
+    ok = all(np.array_equal(dst[d], O.data_fill(cons, c, d, False, total, 1)) for d in range(n) if dst[d].size)
+    return delivered / dt / 1e9, dt, delivered, ok, w
+
+
 def run_reference(args) -> None:
     rank, world, _ = env_rank()
     if rank != 0:
@@ -155,6 +186,7 @@ def run_reference(args) -> None:
     w = WORKLOADS[args.workload]
     threads = os.cpu_count() or 1
     gbs, dt, delivered, ok, ws = cpu_sample_run(w, args.cpu_layers, args.steps, max(args.warmup, 1), threads)
+    threads = 1 if w.data_bytes else threads  # the oracle's data transfer is a single-threaded memcpy loop
     sample = (f"{ws.description}; all phases; oracle CPU reallocation (oracle/liboracle.so) with {threads} "
               f"threads; {delivered / 1e9:.2f} GB delivered per step; correct={ok}")
     line = {
@@ -193,7 +225,9 @@ def run_b200(args) -> None:
         w = truncated(w, args.layers)
     c = w.cluster()
     policy = BALANCED if args.policy == "balanced" else SPEC
-    plans = [plan_param_realloc(w.model, s, d, c, policy) for (s, d) in w.phases]
+    t_plan = time.perf_counter()
+    plans = w.plans(policy)
+    plan_ms = (time.perf_counter() - t_plan) * 1e3
     # Shard sets: phase i reads set i and writes set i+1 (round trips reuse set 0).
     names = ["train"] + [f"out{i}" for i in range(len(plans))]
     shards = {"train": (0, R.SRC)}
@@ -213,9 +247,13 @@ def run_b200(args) -> None:
     # --kernel k: k for every phase (sweeps); default: per phase kind
     kernel = R.DEFAULT_KERNEL if args.kernel < 0 else args.kernel
     flag_kernel = R.DEFAULT_FLAG_KERNEL if args.kernel < 0 else args.kernel
+    t_bind = time.perf_counter()
     rr = R.RankRealloc(plans, shards, bind, rank, world, local_rank, mode=mode, kernel=kernel,
                        multicast=multicast, relay=relay, overlap=overlap, flag_kernel=flag_kernel,
                        chunk_bytes=args.chunk_kib << 10)
+    # executor creation only: the shard allocations inside RankRealloc are
+    # timed too, so this is an upper bound of binding + descriptor upload
+    bind_ms = (time.perf_counter() - t_bind) * 1e3
     stream = torch.cuda.current_stream()
     seed = 1
     for d, b in rr.buffers["train"].items():
@@ -367,6 +405,7 @@ def run_b200(args) -> None:
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         gbs, dt, delivered, ok, ws = cpu_sample_run(w, args.cpu_layers, 1, 1, threads, budget_s=args.cpu_budget)
+        threads = 1 if w.data_bytes else threads
         cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
                "sample": f"{ws.description}; all phases; oracle CPU reallocation, {delivered / 1e9:.2f} GB "
                          f"delivered per step, correct={ok}"}
@@ -437,6 +476,9 @@ def run_b200(args) -> None:
                 e.kernel_count()[0] + ((1 + rr.has_fanout[i] * (1 + e.kernel_count()[1])) if world > 1 else 0)
                 for i, e in enumerate(rr.executors)),
             "clocks": clock_info,
+            # host side, once per plan (not in the timed region): planning +
+            # lowering, and rank 0's buffer allocation + executor binding/upload
+            "host_ms": {"plan_and_lower": round(plan_ms, 3), "allocate_and_bind": round(bind_ms, 1)},
             "verified": verified,
         }
         print(json.dumps(line), flush=True)

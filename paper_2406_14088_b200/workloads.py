@@ -12,7 +12,7 @@ from typing import Dict, List, Tuple
 
 from .rlplan import (BALANCED, GATE_UP_CONCAT, GATE_UP_SEPARATE, MODELS, QKV_CONCAT, QKV_GROUPED,
                      QKV_SEPARATE, ClusterSpec, DeviceMesh, ModelSpec, ParallelStrategy, Placement,
-                     b200_cluster)
+                     ReallocPlan, b200_cluster, plan_data_transfer, plan_param_realloc)
 
 
 def layout(devices: int, pp: int, dp: int, tp: int, qkv: int = QKV_SEPARATE,
@@ -27,9 +27,18 @@ class Workload:
     model: ModelSpec
     devices: int                      # plan devices (hosted on 1..devices GPUs)
     phases: Tuple[Tuple[Placement, Placement], ...]
+    # > 0: inter-call data transfer (plan_data_transfer) of
+    # this many bytes per producer DP shard instead of a parameter plan
+    data_bytes: int = 0
 
     def cluster(self) -> ClusterSpec:
         return b200_cluster(self.devices)
+
+    def plans(self, policy: int = BALANCED) -> List[ReallocPlan]:
+        c = self.cluster()
+        if self.data_bytes:
+            return [plan_data_transfer(s, d, self.data_bytes, c, policy) for s, d in self.phases]
+        return [plan_param_realloc(self.model, s, d, c, policy) for s, d in self.phases]
 
 
 def _pp(p: Placement) -> str:
@@ -75,8 +84,22 @@ _register(Workload("llama7b_replicate_to_dp8", "LLaMA-7B bf16 (pp1,dp1,tp1) on d
                    ((Placement(DeviceMesh(0, 1, 0, 1), ParallelStrategy()), layout(8, 1, 8, 1)),)))
 
 
+# Inter-call data transfer (DP-partitioned outputs of one
+# function call redistributed to the next call's layout). 32 MiB per
+# generation DP shard is a 256 MiB batch of per-token RLHF data.
+_register(Workload("data_gen_dp8_to_train_tp8",
+                   "RLHF batch, 32 MiB per DP shard: actor generation (pp1,dp8,tp1) -> training (pp1,dp1,tp8)",
+                   MODELS["llama7b"], 8, ((layout(8, 1, 8, 1), layout(8, 1, 1, 8)),), data_bytes=32 << 20))
+_register(Workload("data_gen_dp8_to_pp2dp2tp2",
+                   "RLHF batch, 32 MiB per DP shard: generation (pp1,dp8,tp1) -> critic (pp2,dp2,tp2)",
+                   MODELS["llama7b"], 8, ((layout(8, 1, 8, 1), layout(8, 2, 2, 2)),), data_bytes=32 << 20))
+
+
 def truncated(w: Workload, layers: int) -> Workload:
-    """Same shapes and layouts with fewer decoder layers (bounded samples)."""
+    """Same shapes and layouts with fewer decoder layers (bounded samples);
+    a data workload has no layers and is returned unchanged."""
+    if w.data_bytes:
+        return w
     m = dataclasses.replace(w.model, num_layers=layers)
     return Workload(f"{w.name}[{layers}L]", w.description + f", truncated to {layers} layers", m, w.devices,
                     w.phases)

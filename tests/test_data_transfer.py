@@ -125,3 +125,22 @@ def test_data_transfer_on_gpu(need_gpu):
             ex.close()
         finally:
             vc.free()
+
+
+def test_data_workloads_plan_and_cpu_sample():
+    """The bench's data workloads build product plans that match the oracle,
+    and the CPU arm's sample reproduces the consumer data."""
+    import dataclasses
+    import importlib.util
+    import os
+    from paper_2406_14088_b200.workloads import WORKLOADS
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for name in ("data_gen_dp8_to_train_tp8", "data_gen_dp8_to_pp2dp2tp2"):
+        w = dataclasses.replace(WORKLOADS[name], data_bytes=1 << 20)
+        (prod, cons), = w.phases
+        p, ops, loc = both(prod, cons, w.cluster(), w.data_bytes, BALANCED)
+        assert [op_tuple(x) for x in w.plans(BALANCED)[0].ops] == ops
+        gbs, dt, delivered, ok, _ = bench.cpu_sample_data(w, 1, 0, 1)
+        assert ok and delivered == sum(b * len(d) for (_s, d, _p, b) in ops + loc) > 0
