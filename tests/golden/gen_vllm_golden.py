@@ -2,7 +2,9 @@
 """Regenerate the third-party fixtures in tests/golden/:
 
 * vllm_tp_shards.json — an independent pin of the byte layout of
-  tensor-parallel shards (DESIGN.md §3 G3/G4/G10), from vLLM;
+  tensor-parallel shards (DESIGN.md §3 G3/G4/G10), from vLLM; the Megatron
+  grouped QKV layout is checked through vLLM's Falcon loader, which
+  de-interleaves exactly that layout (falcon.py load_weights);
 * hf_llama_inventory.json — the parameter inventory (names, [out, in]
   shapes, totals) of HF transformers' LlamaForCausalLM /
   LlamaForSequenceClassification (num_labels=1, the critic's scalar head) at
@@ -62,6 +64,42 @@ def sha(t) -> str:
     return hashlib.sha256(t.contiguous().view(torch.int16).numpy().tobytes()).hexdigest()
 
 
+def falcon_deinterleave(fused, heads: int, kv: int):
+    """[Q; K; V] from a Falcon / Megatron grouped fused QKV weight, computed
+    by vLLM's own FalconModel.load_weights (vllm/model_executor/models/
+    falcon.py) on a stub module that captures what it would load."""
+    import torch.nn as nn
+    from vllm.model_executor.models import falcon as F
+    got = {}
+
+    class Leaf(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.weight = nn.Parameter(fused.new_zeros(fused.shape), requires_grad=False)
+            self.weight.output_dim = 0
+            self.weight.weight_loader = lambda p, w: got.__setitem__("w", w.clone())
+
+    class Att(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.query_key_value = Leaf()
+
+    class Layer(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.self_attention = Att()
+
+    class Stub(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.h = nn.ModuleList([Layer()])
+            self.config = types.SimpleNamespace(num_attention_heads=heads, num_kv_heads=kv,
+                                                new_decoder_architecture=True, multi_query=False)
+
+    F.FalconModel.load_weights(Stub(), [("h.0.self_attention.query_key_value.weight", fused)])
+    return got["w"]
+
+
 def main() -> None:
     import torch
     import vllm
@@ -108,6 +146,21 @@ def main() -> None:
                                                              "sha256": sha(full[b].reshape(h))}
                     qkv = L.QKVParallelLinear(h, hd, heads, kv, bias=False, params_dtype=torch.bfloat16)
                     put(f"layers.{l}.qkv_proj", qkv, [b + 1, b + 2, b + 3], [(b + 1, "q"), (b + 2, "k"), (b + 3, "v")])
+                    if kv % tp == 0:
+                        # Megatron grouped layout of the same rank: per local KV
+                        # group [its q heads; k; v]. The grouped tensor is the
+                        # unique row permutation that vLLM's Falcon loader maps
+                        # back onto vLLM's [Q_r; K_r; V_r]; checked here.
+                        lq, lkv = heads // tp, kv // tp
+                        cat = qkv.weight.data
+                        q_r, k_r, v_r = cat[:lq * hd], cat[lq * hd:(lq + lkv) * hd], cat[(lq + lkv) * hd:]
+                        grouped = torch.cat([q_r.reshape(lkv, lq // lkv, hd, h), k_r.reshape(lkv, 1, hd, h),
+                                             v_r.reshape(lkv, 1, hd, h)], dim=1).reshape(-1, h)
+                        assert torch.equal(falcon_deinterleave(grouped, lq, lkv).view(torch.int16),
+                                           cat.view(torch.int16))
+                        params[f"layers.{l}.qkv_proj_grouped"] = {
+                            "tensors": [b + 1, b + 2, b + 3], "shape": list(grouped.shape), "sha256": sha(grouped),
+                            "layout": "Megatron grouped (qkv_layout 2); verified with vLLM FalconModel.load_weights"}
                     o = L.RowParallelLinear(heads * hd, h, bias=False, params_dtype=torch.bfloat16)
                     put(f"layers.{l}.o_proj", o, [b + 4], [(b + 4, None)])
                     params[f"layers.{l}.post_attention_layernorm"] = {"tensors": [b + 5], "shape": [h],
