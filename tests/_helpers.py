@@ -61,3 +61,23 @@ def emulate_lowered(plan, src_bufs: Dict[int, np.ndarray], dst_bufs: Dict[int, n
             for (so, do, rb, sp, dp, rows) in rects:
                 for r in range(rows):
                     db[do + r * dp: do + r * dp + rb] = sb[so + r * sp: so + r * sp + rb]
+
+
+def random_placement(rng, model, gpus_per_node: int = 8) -> Placement:
+    """A random valid placement on an aligned sub-mesh of one node: random
+    size, offset, (pp, dp, tp) and fused layouts (plan-parity and GPU fuzz)."""
+    from paper_2406_14088_b200 import rlplan as P
+    size = rng.choice([1, 2, 4, 8])
+    offset = rng.randrange(0, gpus_per_node // size) * size
+    while True:
+        tp = rng.choice([t for t in (1, 2, 4, 8) if size % t == 0])
+        pp = rng.choice([q for q in range(1, size // tp + 1) if (size // tp) % q == 0 and q <= model.num_layers])
+        dp = size // (tp * pp)
+        qkv = rng.choice([0, 1, 2])
+        gu = rng.choice([0, 1])
+        p = P.Placement(P.DeviceMesh(0, 1, offset, size), P.ParallelStrategy(dp=dp, tp=tp, pp=pp), qkv, gu)
+        try:
+            P.validate_placement(model, p, P.b200_cluster(gpus_per_node))
+            return p
+        except P.ValidationError:
+            continue

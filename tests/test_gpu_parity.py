@@ -148,3 +148,26 @@ def test_7b_train_gen_roundtrip_full_size(need_gpu):
         assert np.array_equal(rr.buffers["train"][3].to_host(), want3)
     finally:
         rr.close()
+
+
+def test_random_placement_pairs_bitexact_on_gpu(need_gpu):
+    """Fuzz: 80 random (src, dst) placement pairs (sub-meshes, pp/dp/tp,
+    Separate/Concat/Grouped layouts, both policies, push and pull, both copy
+    kernels, random work-item sizes) through the sm_100a kernels, each
+    bit-exact against the oracle's expected destination shards."""
+    import random
+
+    from _helpers import random_placement
+    rng = random.Random(14088)
+    c = b200_cluster(8)
+    models = [TINY_GQA, dataclasses.replace(TINY_GQA, num_layers=5, has_output_head=False),
+              dataclasses.replace(MODELS["tiny"], num_layers=3)]
+    for i in range(80):
+        m = rng.choice(models)
+        src, dst = random_placement(rng, m), random_placement(rng, m)
+        policy = rng.choice([SPEC, BALANCED])
+        mode = rng.choice([R.PUSH, R.PULL])
+        kernel = rng.choice([0, 1, 5])
+        chunk = rng.choice([0, 4096, 65536])
+        _plan, got = run_virtual(m, src, dst, c, policy, mode, chunk=chunk, seed=100 + i, kernel=kernel)
+        assert_same(got, expected(m, src, dst, c, seed=100 + i))

@@ -10,7 +10,7 @@ import time
 
 import pytest
 
-from _helpers import BASELINE_CONFIGS, config_placements, op_tuple, placement
+from _helpers import BASELINE_CONFIGS, config_placements, op_tuple, placement, random_placement
 from oracle import oracle as O
 from paper_2406_14088_b200 import rlplan as P
 from paper_2406_14088_b200.rlplan import BALANCED, SPEC
@@ -128,23 +128,6 @@ def test_balanced_policy_spreads_egress():
     assert bal.est_time < spec.est_time / 3
 
 
-def _random_placement(rng, model, gpus_per_node=8):
-    size = rng.choice([1, 2, 4, 8])
-    offset = rng.randrange(0, gpus_per_node // size) * size
-    while True:
-        tp = rng.choice([t for t in (1, 2, 4, 8) if size % t == 0])
-        pp = rng.choice([q for q in range(1, size // tp + 1) if (size // tp) % q == 0 and q <= model.num_layers])
-        dp = size // (tp * pp)
-        qkv = rng.choice([0, 1, 2])
-        gu = rng.choice([0, 1])
-        p = P.Placement(P.DeviceMesh(0, 1, offset, size), P.ParallelStrategy(dp=dp, tp=tp, pp=pp), qkv, gu)
-        try:
-            P.validate_placement(model, p, P.b200_cluster(gpus_per_node))
-            return p
-        except P.ValidationError:
-            continue
-
-
 def test_random_placement_pairs_replay_exact():
     """SPEC.md:679 acceptance criterion 6: >= 500 random (src, dst) pairs on
     <= 8 devices replay exactly; identical placements yield 0 bytes; < 30 s."""
@@ -156,8 +139,8 @@ def test_random_placement_pairs_replay_exact():
     n = 0
     while n < 520:
         m = rng.choice(models)
-        src = _random_placement(rng, m)
-        dst = _random_placement(rng, m)
+        src = random_placement(rng, m)
+        dst = random_placement(rng, m)
         policy = rng.choice([SPEC, BALANCED])
         p, ops, loc = both(m, src, dst, c, policy)
         assert O.replay(m, src, dst, c, ops, loc) is None, (src, dst, policy)
