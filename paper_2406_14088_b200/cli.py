@@ -1,8 +1,16 @@
 """Command line: the reference CLI's ``realloc-plan`` subcommand (SPEC.md:642,
-SPEC.md:604) plus ``data-plan``, over the B200 planner.
+SPEC.md:604) plus ``data-plan`` and the simulator's
+``augment`` step, over the B200 planner.
 
     python -m paper_2406_14088_b200 realloc-plan CONFIG.json [-o PLAN.json]
     python -m paper_2406_14088_b200 data-plan CONFIG.json [-o PLAN.json]
+    python -m paper_2406_14088_b200 augment PLAN.json [-o NODES.json]
+
+``augment`` takes {"schema": 1, "cluster": ..., "models": {handle: preset or
+object}, "calls": [{"name", "model", "placement": {...}, "offload"}],
+"edges": [{"producer", "consumer", "bytes_per_dp_shard"}], "cyclic": true}
+and prints the inserted param_realloc / data_transfer / offload / onload
+nodes with the SPEC and measured-B200 durations.
 
 CONFIG (single JSON file, schema version 1, no environment variables —
 SPEC.md:657):
@@ -137,11 +145,54 @@ def build(config: Dict[str, Any], data: bool = False) -> Dict[str, Any]:
     return out
 
 
+def build_augment(config: Dict[str, Any]) -> Dict[str, Any]:
+    """``augment``: the nodes an execution plan inserts,
+    each with the SPEC estimate and the measured B200 time."""
+    from .augment import Call, DataEdge, augment, total_seconds
+    if not isinstance(config, dict):
+        raise ConfigError("$: expected an object")
+    if _get(config, "schema", "$", int) != 1:
+        raise ConfigError("$.schema: only schema 1 is supported")
+    cluster = parse_cluster(_get(config, "cluster", "$"))
+    models_cfg = _get(config, "models", "$", dict)
+    models = {k: parse_model(v, f"$.models.{k}") for k, v in models_cfg.items()}
+    calls = []
+    for i, c in enumerate(_get(config, "calls", "$", list)):
+        path = f"$.calls[{i}]"
+        if not isinstance(c, dict):
+            raise ConfigError(f"{path}: expected an object")
+        model = _get(c, "model", path, str)
+        if model not in models:
+            raise ConfigError(f"{path}.model: {model!r} is not in $.models")
+        calls.append(Call(_get(c, "name", path, str), model,
+                          parse_placement(_get(c, "placement", path), cluster, f"{path}.placement"),
+                          bool(_get(c, "offload", path, bool, False))))
+    edges = []
+    for i, e in enumerate(_get(config, "edges", "$", list, [])):
+        path = f"$.edges[{i}]"
+        if not isinstance(e, dict):
+            raise ConfigError(f"{path}: expected an object")
+        edges.append(DataEdge(_get(e, "producer", path, str), _get(e, "consumer", path, str),
+                              _get(e, "bytes_per_dp_shard", path, int)))
+    pol = _get(config, "policy", "$", str, "balanced")
+    if pol not in ("spec", "balanced"):
+        raise ConfigError("$.policy: 'spec' or 'balanced'")
+    try:
+        nodes = augment(calls, edges, models, cluster, cyclic=bool(_get(config, "cyclic", "$", bool, True)),
+                        policy=SPEC if pol == "spec" else BALANCED)
+    except (ValidationError, ValueError) as e:
+        raise ConfigError(f"$: {e}") from None
+    return {"nodes": [{"kind": n.kind, "after": n.between[0], "before": n.between[1], "model": n.model,
+                       "bytes": n.bytes, "spec_seconds": n.spec_seconds, "b200_seconds": n.b200_seconds}
+                      for n in nodes],
+            "totals": total_seconds(nodes)}
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="python -m paper_2406_14088_b200", description=__doc__,
                                  formatter_class=argparse.RawDescriptionHelpFormatter)
     sub = ap.add_subparsers(dest="cmd", required=True)
-    for name in ("realloc-plan", "data-plan"):
+    for name in ("realloc-plan", "data-plan", "augment"):
         p = sub.add_parser(name)
         p.add_argument("config")
         p.add_argument("-o", "--output")
@@ -149,7 +200,7 @@ def main(argv=None) -> int:
     try:
         with open(args.config) as f:
             config = json.load(f)
-        out = build(config, data=args.cmd == "data-plan")
+        out = build_augment(config) if args.cmd == "augment" else build(config, data=args.cmd == "data-plan")
     except (OSError, json.JSONDecodeError) as e:
         print(f"error: {args.config}: {e}", file=sys.stderr)
         return 2

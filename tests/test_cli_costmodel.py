@@ -99,3 +99,26 @@ def test_cost_model_onload_matches_e2e(gpus, measured_ms):
     back = costmodel.estimate_seconds(plan_param_realloc(w.model, *w.phases[1], w.cluster(), BALANCED), host_of)
     assert fwd["onload_s"] > fwd["seconds"] - fwd["onload_s"]  # host-link bound
     assert (fwd["seconds"] + back["seconds"]) * 1e3 == pytest.approx(measured_ms, rel=0.08)
+
+
+def test_augment_cli_on_the_ppo_example(tmp_path):
+    """`augment` over examples/ppo_7b_augment.json: one
+    node per layout change, data edge and offload flag, each priced by the
+    SPEC and by the measured B200 model."""
+    import os
+    ex = os.path.join(os.path.dirname(__file__), "..", "examples", "ppo_7b_augment.json")
+    out = tmp_path / "nodes.json"
+    assert cli.main(["augment", ex, "-o", str(out)]) == 0
+    d = json.load(open(out))
+    kinds = [n["kind"] for n in d["nodes"]]
+    assert kinds.count("param_realloc") == 4 and kinds.count("data_transfer") == 6
+    assert kinds.count("offload") == kinds.count("onload") == 2
+    gen_to_train = next(n for n in d["nodes"] if n["kind"] == "param_realloc" and n["after"] == "ActorGen")
+    # dp8 -> tp8 keeps every byte on its device: SPEC prices it at 0 s, the
+    # B200 model at the local relayout's HBM time
+    assert gen_to_train["bytes"] == 0 and gen_to_train["spec_seconds"] == 0 and gen_to_train["b200_seconds"] > 0
+    bad = json.load(open(ex))
+    bad["calls"][0]["model"] = "nobody"
+    p = tmp_path / "bad.json"
+    p.write_text(json.dumps(bad))
+    assert cli.main(["augment", str(p)]) == 1
