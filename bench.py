@@ -178,12 +178,20 @@ def cpu_sample_data(w, steps: int, warmup: int, threads: int, budget_s: float = 
     return delivered / dt / 1e9, dt, delivered, ok, w
 
 
+def load_workload(args):
+    from paper_2406_14088_b200.workloads import WORKLOADS, from_config
+    if args.config:
+        with open(args.config) as f:
+            return from_config(json.load(f), name=os.path.splitext(os.path.basename(args.config))[0])
+    return WORKLOADS[args.workload]
+
+
 def run_reference(args) -> None:
     rank, world, _ = env_rank()
     if rank != 0:
         return
     from paper_2406_14088_b200.workloads import WORKLOADS
-    w = WORKLOADS[args.workload]
+    w = load_workload(args)
     threads = os.cpu_count() or 1
     gbs, dt, delivered, ok, ws = cpu_sample_run(w, args.cpu_layers, args.steps, max(args.warmup, 1), threads)
     threads = 1 if w.data_bytes else threads  # the oracle's data transfer is a single-threaded memcpy loop
@@ -219,7 +227,7 @@ def run_b200(args) -> None:
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    w = WORKLOADS[args.workload]
+    w = load_workload(args)
     if args.layers:
         from paper_2406_14088_b200.workloads import truncated
         w = truncated(w, args.layers)
@@ -506,6 +514,9 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", default="llama7b_tp8_dp8_roundtrip")
+    ap.add_argument("--config", default=None,
+                    help="realloc-plan/data-plan config JSON (cli.py format, plus \"back\": true) instead of "
+                         "a named workload")
     ap.add_argument("--policy", choices=["balanced", "spec"], default="balanced")
     ap.add_argument("--mode", choices=["auto", "push", "pull", "mc", "relay"], default="auto",
                     help="push = SM peer stores; relay = push + pipelined relay for payloads reaching >= 2 "

@@ -8,7 +8,7 @@ from __future__ import annotations
 
 import dataclasses
 from dataclasses import dataclass
-from typing import Dict, List, Tuple
+from typing import Dict, List, Optional, Tuple
 
 from .rlplan import (BALANCED, GATE_UP_CONCAT, GATE_UP_SEPARATE, MODELS, QKV_CONCAT, QKV_GROUPED,
                      QKV_SEPARATE, ClusterSpec, DeviceMesh, ModelSpec, ParallelStrategy, Placement,
@@ -30,9 +30,10 @@ class Workload:
     # > 0: inter-call data transfer (plan_data_transfer) of
     # this many bytes per producer DP shard instead of a parameter plan
     data_bytes: int = 0
+    cluster_spec: Optional[ClusterSpec] = None  # default: one B200 node with `devices` GPUs
 
     def cluster(self) -> ClusterSpec:
-        return b200_cluster(self.devices)
+        return self.cluster_spec or b200_cluster(self.devices)
 
     def plans(self, policy: int = BALANCED) -> List[ReallocPlan]:
         c = self.cluster()
@@ -103,3 +104,24 @@ def truncated(w: Workload, layers: int) -> Workload:
     m = dataclasses.replace(w.model, num_layers=layers)
     return Workload(f"{w.name}[{layers}L]", w.description + f", truncated to {layers} layers", m, w.devices,
                     w.phases)
+
+
+def from_config(config: dict, name: str = "config") -> Workload:
+    """A workload from a ``realloc-plan`` / ``data-plan`` config (cli.py
+    format) so any placement pair can be benchmarked: ``"back": true`` adds
+    the return phase, ``data_bytes_per_dp_shard`` makes it a data transfer.
+    The plan devices are the cluster's devices."""
+    from .cli import ConfigError, _get, parse_cluster, parse_model, parse_placement
+    if _get(config, "schema", "$", int) != 1:
+        raise ConfigError("$.schema: only schema 1 is supported")
+    cluster = parse_cluster(_get(config, "cluster", "$"))
+    if cluster.n_nodes != 1:
+        raise ConfigError("$.cluster.n_nodes: execution is single-node (CUDA IPC between the node's GPUs)")
+    src = parse_placement(_get(config, "src", "$"), cluster, "$.src")
+    dst = parse_placement(_get(config, "dst", "$"), cluster, "$.dst")
+    back = bool(_get(config, "back", "$", bool, False))
+    data = int(_get(config, "data_bytes_per_dp_shard", "$", int, 0))
+    model = MODELS["tiny"] if data else parse_model(_get(config, "model", "$"))
+    phases = ((src, dst), (dst, src)) if back else ((src, dst),)
+    desc = f"{model.name if not data else 'data'} {_pp(src)} -> {_pp(dst)}" + (" and back" if back else "")
+    return Workload(name, desc, model, cluster.device_count(), phases, data_bytes=data, cluster_spec=cluster)

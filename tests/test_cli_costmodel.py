@@ -122,3 +122,17 @@ def test_augment_cli_on_the_ppo_example(tmp_path):
     p = tmp_path / "bad.json"
     p.write_text(json.dumps(bad))
     assert cli.main(["augment", str(p)]) == 1
+
+
+def test_bench_config_workload_matches_the_preset():
+    """bench.py --config: a realloc-plan config with "back": true is the
+    same two-phase workload as the named 7B round trip."""
+    import os
+    from paper_2406_14088_b200.workloads import from_config
+    ex = os.path.join(os.path.dirname(__file__), "..", "examples", "llama7b_train_gen_roundtrip.json")
+    w = from_config(json.load(open(ex)))
+    ref = WORKLOADS["llama7b_tp8_dp8_roundtrip"]
+    assert len(w.phases) == 2 and w.devices == ref.devices and w.model == ref.model
+    for a, b in zip(w.plans(BALANCED), ref.plans(BALANCED)):
+        assert a.total_bytes == b.total_bytes and a.num_rects() == b.num_rects()
+        assert [op.src for op in a.ops] == [op.src for op in b.ops]
