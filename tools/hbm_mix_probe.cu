@@ -394,6 +394,61 @@ __global__ void __launch_bounds__(32) w_tma_run(char* dst, size_t bytes, size_t 
   }
 }
 
+
+// Phase-separated broadcast: every CTA loads its slice of a round into
+// shared memory, a grid-wide barrier, then stores it to the 8 destinations
+// and waits for the stores to complete, another barrier. DRAM then sees
+// long pure-read and pure-write periods instead of a fine-grained mix.
+__device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& gen) {
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int target = (gen + 1) * gridDim.x;
+    atomicAdd(bar, 1u);
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {  // bounded: a wrong occupancy must not hang the GPU
+      unsigned int v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (v >= target) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 2000000000ull) break;
+    }
+  }
+  ++gen;
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(32) bc_phased(const char* src, Dsts dsts, size_t bytes, unsigned int* bar,
+                                                uint32_t per_cta, int barriers) {
+  extern __shared__ __align__(128) uint8_t buf[];
+  __shared__ __align__(8) uint64_t full;
+  unsigned int gen = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&full);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  const size_t round_bytes = size_t(per_cta) * gridDim.x;
+  uint32_t phase = 0;
+  for (size_t base = 0; base < bytes; base += round_bytes) {
+    const size_t off = base + size_t(blockIdx.x) * per_cta;
+    const uint32_t n = off < bytes ? (uint32_t)min(size_t(per_cta), bytes - off) : 0;
+    if (threadIdx.x == 0 && n) {
+      mbar_expect(&full, n);
+      for (uint32_t k = 0; k < n; k += 32768) bload(buf + k, src + off + k, min(32768u, n - k), &full);
+      mbar_wait(&full, phase);
+    }
+    phase ^= n ? 1 : 0;
+    if (barriers) grid_sync(bar, gen);
+    if (threadIdx.x == 0 && n) {
+      for (int j = 0; j < 8; ++j) bstore(dsts.d[j] + off, buf, n);
+      commit();
+      wait_all();
+    }
+    if (barriers) grid_sync(bar, gen);
+  }
+}
+
 static cudaEvent_t t0, t1;
 
 template <class F>
@@ -533,6 +588,22 @@ int main() {
     }
     std::snprintf(nm, sizeof nm, "w/v8run%zuk", run >> 10);
     rep(nm, sms * 4, double(32 * G), best_ms([&] { w_v8_run<<<sms * 4, 512>>>(a + 32 * G, 32 * G, run, ctr); }));
+  }
+  unsigned int* bar = nullptr;
+  CK(cudaMalloc(&bar, 4));
+  for (uint32_t per : {65536u, 98304u, 196608u}) {
+    CK(cudaFuncSetAttribute(bc_phased, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bc_phased, 32, per));
+    for (int barriers : {1, 0}) {
+      const int ctas = sms * occ;  // all resident: the grid barrier needs it
+      char nm[40];
+      std::snprintf(nm, sizeof nm, "bc/phased%uk%s", per >> 10, barriers ? "" : "-nobar");
+      rep(nm, ctas, 9.0 * sbo, best_ms([&] {
+            CK(cudaMemsetAsync(bar, 0, 4));
+            bc_phased<<<ctas, 32, per>>>(s, d, sbo, bar, per, barriers);
+          }));
+    }
   }
   // check the last broadcast: every destination equals the source pattern (0x03)
   unsigned char h[2] = {0, 0};
