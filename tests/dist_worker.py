@@ -149,6 +149,44 @@ def main() -> int:
         if rr.relay_timeouts():
             failures.append(f"relay kernel {kernel} {src.strategy}->{dst.strategy}: {rr.relay_timeouts()} timeouts")
         rr.close()
+    # Fuzz: random placement pairs with random delivery options (same seed on
+    # every rank, so all ranks build the same plans and executors).
+    import random
+
+    from _helpers import random_placement
+    rng = random.Random(int(os.environ.get("RR_FUZZ_SEED", "2406")))
+    for i in range(int(os.environ.get("RR_FUZZ_CASES", "24"))):
+        src, dst = random_placement(rng, TINY_GQA), random_placement(rng, TINY_GQA)
+        mode = rng.choice([R.PUSH, R.PULL])
+        hier = rng.random() < 0.7
+        relay = rng.choice([False, True, "auto"])
+        overlap = rng.random() < 0.5
+        kernel = rng.choice([0, 1, 5])
+        chunk = rng.choice([0, 8192, 65536])
+        plan = plan_param_realloc(TINY_GQA, src, dst, c, rng.choice([0, 1]))
+        rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
+                           mode=mode, kernel=kernel, flag_kernel=kernel, hierarchical=hier, relay=relay,
+                           overlap=overlap, chunk_bytes=chunk)
+        for d, b in rr.buffers["a"].items():
+            R.fill_shard(plan, R.SRC, d, b.ptr, 50 + i)
+        for rep in range(2):
+            for b in rr.buffers["b"].values():
+                b.zero()
+            torch.cuda.synchronize()
+            dist.barrier()
+            rr.run_phase(0)
+            torch.cuda.synchronize()
+            for d, b in rr.buffers["b"].items():
+                got = b.to_host()
+                want = O.fill(TINY_GQA, dst, c, d, 50 + i)
+                if not np.array_equal(got, want):
+                    failures.append(f"fuzz {i} {src}->{dst} mode {mode} hier {hier} relay {relay} overlap {overlap} "
+                                    f"kernel {kernel} chunk {chunk} rep {rep}: device {d} differs in "
+                                    f"{int(np.count_nonzero(got != want))} elements")
+        if rr.relay_timeouts() or rr.barrier.timed_out():
+            failures.append(f"fuzz {i}: flag or barrier timeouts")
+        dist.barrier()
+        rr.close()
     if os.environ.get("RR_FULL_7B") == "1":
         w = WORKLOADS["llama7b_tp8_dp8_roundtrip"]
         plans = [plan_param_realloc(w.model, s, d, c, BALANCED) for (s, d) in w.phases]
