@@ -151,7 +151,7 @@ def cpu_sample_run(workload, layers: int, steps: int, warmup: int, threads: int,
 
 def cpu_sample_data(w, steps: int, warmup: int, threads: int, budget_s: float = None):
     """cpu_sample_run for a data workload: the oracle's plan_data_transfer
-    restatement executed on host buffers."""
+    restatement executed on host buffers with `threads` threads."""
     import numpy as np
     from oracle import oracle as O
     c = w.cluster()
@@ -164,11 +164,11 @@ def cpu_sample_data(w, steps: int, warmup: int, threads: int, budget_s: float = 
     dst = [np.zeros(O.data_shard_bytes(cons, c, d, False, total) // 2, np.uint16) for d in range(n)]
     delivered = sum(b * len(dsts) for (_s, dsts, _p, b) in ops + loc)
     for _ in range(warmup):
-        O.data_execute(prod, cons, c, total, ops + loc, src, dst)
+        O.data_execute(prod, cons, c, total, ops + loc, src, dst, threads)
     t0 = time.perf_counter()
     done = 0
     while True:
-        O.data_execute(prod, cons, c, total, ops + loc, src, dst)
+        O.data_execute(prod, cons, c, total, ops + loc, src, dst, threads)
         done += 1
         el = time.perf_counter() - t0
         if done >= steps and (budget_s is None or el >= budget_s or done >= 1000):
@@ -194,7 +194,6 @@ def run_reference(args) -> None:
     w = load_workload(args)
     threads = os.cpu_count() or 1
     gbs, dt, delivered, ok, ws = cpu_sample_run(w, args.cpu_layers, args.steps, max(args.warmup, 1), threads)
-    threads = 1 if w.data_bytes else threads  # the oracle's data transfer is a single-threaded memcpy loop
     sample = (f"{ws.description}; all phases; oracle CPU reallocation (oracle/liboracle.so) with {threads} "
               f"threads; {delivered / 1e9:.2f} GB delivered per step; correct={ok}")
     line = {
@@ -413,7 +412,6 @@ def run_b200(args) -> None:
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         gbs, dt, delivered, ok, ws = cpu_sample_run(w, args.cpu_layers, 1, 1, threads, budget_s=args.cpu_budget)
-        threads = 1 if w.data_bytes else threads
         cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
                "sample": f"{ws.description}; all phases; oracle CPU reallocation, {delivered / 1e9:.2f} GB "
                          f"delivered per step, correct={ok}"}

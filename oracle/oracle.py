@@ -341,6 +341,8 @@ _lib.orc_data_shard_bytes.argtypes = [POINTER(OrcPlacement), POINTER(OrcCluster)
 _lib.orc_data_fill.argtypes = [POINTER(OrcPlacement), POINTER(OrcCluster), c_int, c_int, c_int64, c_uint64, c_void_p]
 _lib.orc_data_execute.argtypes = [POINTER(OrcPlacement), POINTER(OrcPlacement), POINTER(OrcCluster), c_int64,
                                   POINTER(OrcOp), c_int, POINTER(c_void_p), POINTER(c_void_p)]
+_lib.orc_data_execute_mt.argtypes = [POINTER(OrcPlacement), POINTER(OrcPlacement), POINTER(OrcCluster), c_int64,
+                                     POINTER(OrcOp), c_int, POINTER(c_void_p), POINTER(c_void_p), c_int]
 
 
 def plan_data(producer, consumer, cluster, data_bytes_per_dp_shard: int, policy: int = 0):
@@ -371,15 +373,16 @@ def data_fill(placement, cluster, dev: int, producer: bool, total_bytes: int, se
     return buf
 
 
-def data_execute(producer, consumer, cluster, total_bytes: int, ops, src_bufs, dst_bufs) -> None:
+def data_execute(producer, consumer, cluster, total_bytes: int, ops, src_bufs, dst_bufs, threads: int = 1) -> None:
     n = cluster.n_nodes * cluster.gpus_per_node
     sp, dp = (c_void_p * n)(), (c_void_p * n)()
     for i in range(n):
         sp[i] = src_bufs[i].ctypes.data if src_bufs[i] is not None else None
         dp[i] = dst_bufs[i].ctypes.data if dst_bufs[i] is not None else None
     arr = _ops_array(ops)
-    assert _lib.orc_data_execute(ctypes.byref(_placement(producer)), ctypes.byref(_placement(consumer)),
-                                 ctypes.byref(_cluster(cluster)), total_bytes, arr, len(ops), sp, dp) == 0
+    assert _lib.orc_data_execute_mt(ctypes.byref(_placement(producer)), ctypes.byref(_placement(consumer)),
+                                    ctypes.byref(_cluster(cluster)), total_bytes, arr, len(ops), sp, dp,
+                                    threads) == 0
 
 
 def replay_data(producer, consumer, cluster, data_bytes_per_dp_shard: int, ops, local_ops):

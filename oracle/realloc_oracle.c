@@ -626,19 +626,68 @@ int orc_data_fill(const orc_placement* p, const orc_cluster* c, int dev, int pro
   return 0;
 }
 
-int orc_data_execute(const orc_placement* prod, const orc_placement* cons, const orc_cluster* c, int64_t total,
-                     const orc_op* ops, int n_ops, void* const* src_bufs, void* const* dst_bufs) {
-  const int64_t elems = total / 2;
+typedef struct {
+  uint16_t* dst;
+  const uint16_t* src;
+  size_t bytes;
+} data_piece;
+
+typedef struct {
+  data_piece* pieces;
+  int64_t n, next;
+} data_ctx;
+
+static void* data_worker(void* arg) {
+  data_ctx* x = (data_ctx*)arg;
+  for (;;) {
+    const int64_t i = __atomic_fetch_add(&x->next, 1, __ATOMIC_RELAXED);
+    if (i >= x->n) break;
+    memcpy(x->pieces[i].dst, x->pieces[i].src, x->pieces[i].bytes);
+  }
+  return NULL;
+}
+
+int orc_data_execute_mt(const orc_placement* prod, const orc_placement* cons, const orc_cluster* c, int64_t total,
+                        const orc_op* ops, int n_ops, void* const* src_bufs, void* const* dst_bufs, int threads) {
+  const int64_t elems = total / 2, piece = 1 << 19; /* 1 MiB of bf16 words per task */
+  data_ctx x = {NULL, 0, 0};
+  int64_t cap = 256;
+  x.pieces = malloc(sizeof(data_piece) * (size_t)cap);
   for (int o = 0; o < n_ops; ++o) {
     const orc_op* op = &ops[o];
     const int64_t s0 = op->slice * elems / op->slices, s1 = (op->slice + 1) * elems / op->slices;
     int64_t sf, df;
-    if (data_range(prod, c, op->src, 1, total, &sf) < 0) return -1;
+    if (data_range(prod, c, op->src, 1, total, &sf) < 0) {
+      free(x.pieces);
+      return -1;
+    }
     for (int k = 0; k < op->n_dst; ++k) {
-      if (data_range(cons, c, op->dst[k], 0, total, &df) < 0) return -1;
-      memcpy((uint16_t*)dst_bufs[op->dst[k]] + (s0 - df), (const uint16_t*)src_bufs[op->src] + (s0 - sf),
-             (size_t)(s1 - s0) * 2);
+      if (data_range(cons, c, op->dst[k], 0, total, &df) < 0) {
+        free(x.pieces);
+        return -1;
+      }
+      for (int64_t e = s0; e < s1; e += piece) {
+        if (x.n == cap) {
+          cap *= 2;
+          x.pieces = realloc(x.pieces, sizeof(data_piece) * (size_t)cap);
+        }
+        const int64_t n = e + piece < s1 ? piece : s1 - e;
+        data_piece p = {(uint16_t*)dst_bufs[op->dst[k]] + (e - df), (const uint16_t*)src_bufs[op->src] + (e - sf),
+                        (size_t)n * 2};
+        x.pieces[x.n++] = p;
+      }
     }
   }
+  if (threads < 1) threads = 1;
+  pthread_t* th = malloc(sizeof(pthread_t) * (size_t)threads);
+  for (int i = 0; i < threads; ++i) pthread_create(&th[i], NULL, data_worker, &x);
+  for (int i = 0; i < threads; ++i) pthread_join(th[i], NULL);
+  free(th);
+  free(x.pieces);
   return 0;
+}
+
+int orc_data_execute(const orc_placement* prod, const orc_placement* cons, const orc_cluster* c, int64_t total,
+                     const orc_op* ops, int n_ops, void* const* src_bufs, void* const* dst_bufs) {
+  return orc_data_execute_mt(prod, cons, c, total, ops, n_ops, src_bufs, dst_bufs, 1);
 }

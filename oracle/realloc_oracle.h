@@ -99,6 +99,10 @@ int orc_data_fill(const orc_placement* p, const orc_cluster* c, int dev, int pro
 int orc_data_execute(const orc_placement* producer, const orc_placement* consumer, const orc_cluster* c,
                      int64_t total_bytes, const orc_op* ops, int n_ops, void* const* src_bufs,
                      void* const* dst_bufs);
+/* The same with `threads` worker threads (1 MiB memcpy tasks). */
+int orc_data_execute_mt(const orc_placement* producer, const orc_placement* consumer, const orc_cluster* c,
+                        int64_t total_bytes, const orc_op* ops, int n_ops, void* const* src_bufs,
+                        void* const* dst_bufs, int threads);
 
 #ifdef __cplusplus
 }
