@@ -125,7 +125,7 @@ def cpu_sample_run(workload, layers: int, steps: int, warmup: int, threads: int,
         shards(first_src)[d][:] = O.fill(w.model, first_src, c, d, 1)
     delivered = 0
     for (src, dst, ops) in phases:
-        for (s, dsts, (lo, hi, k, G, rep), b) in ops:
+        for (s, dsts, _payload, b) in ops:
             delivered += b * len(dsts)
 
     def step():

@@ -38,13 +38,26 @@ struct ParallelStrategy {
 enum class QkvLayout : int { Separate = 0, Concat = 1, Grouped = 2 };
 //   Separate: gate, up as two tensors.  Concat: rows [G_r; U_r].
 enum class GateUpLayout : int { Separate = 0, Concat = 1 };
+// K/V weights when tp exceeds the KV heads (DESIGN.md §3 G6).
+//   Split:          k/v rows split evenly over tp like every row-split tensor
+//                   (the reference's arithmetic).
+//   ReplicateHeads: Megatron / vLLM: tp rank r holds whole KV head
+//                   floor(r * kv_heads / tp); needs tp % kv_heads == 0.
+//   Both are the same layout when tp <= kv_heads.
+enum class KvLayout : int { Split = 0, ReplicateHeads = 1 };
 
 struct Placement {
   DeviceMesh mesh;
   ParallelStrategy strategy;
   QkvLayout qkv = QkvLayout::Separate;
   GateUpLayout gate_up = GateUpLayout::Separate;
+  KvLayout kv = KvLayout::Split;
 };
+
+// Number of distinct K/V slices a placement's TP ranks hold: kv_heads under
+// ReplicateHeads with tp > kv_heads, else tp. Rank r holds slice
+// floor(r * kv_degree / tp).
+int kv_degree(const ModelSpec& model, const Placement& p);
 
 // ValidationError unless the strategy fits the mesh and model: dp,tp,pp >= 1,
 // dp*tp*pp == mesh size, pp <= num_layers, tp a power of two dividing the
@@ -70,12 +83,21 @@ DeviceId device_at(const Placement& p, const ClusterSpec& cluster, int pp_rank, 
 // lcm(tp_src, tp_dst) of every TP-split tensor in the range;
 // tp_degree == 1 with `replicated` set carries the replicated tensors
 // (norms, scalar value head) of the range (G5).
+//
+// `part` separates K/V when a placement replicates KV heads (G6): a plan in
+// which either side has kv_degree != tp carries split payloads without k/v
+// (part 1) and K/V payloads (part 2: slice tp_rank of tp_degree =
+// lcm(kv_degree_src, kv_degree_dst) of every k and v in the range). All
+// other plans use part 0 (every TP-split tensor).
+enum PayloadPart : int { kPartAll = 0, kPartNoKv = 1, kPartKv = 2 };
+
 struct ShardDescriptor {
   Count layer_start = 0;
   Count layer_end = 0;
   int tp_rank = 0;
   int tp_degree = 1;
   bool replicated = false;
+  int part = kPartAll;
   bool operator==(const ShardDescriptor&) const = default;
 };
 

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define RR_ABI_VERSION 1
+#define RR_ABI_VERSION 2 /* 2: rr_placement.kv_layout, rr_shard.part */
 
 typedef enum {
   RR_OK = 0,
@@ -77,12 +77,15 @@ typedef struct {
 } rr_mesh;
 
 /* qkv_layout: 0 separate, 1 concat [Q;K;V], 2 Megatron grouped.
- * gate_up_layout: 0 separate, 1 concat [G;U]. (DESIGN.md §3 G4) */
+ * gate_up_layout: 0 separate, 1 concat [G;U]. (DESIGN.md §3 G4)
+ * kv_layout: 0 k/v rows split over tp, 1 whole KV heads replicated when
+ * tp > kv heads (Megatron / vLLM). (DESIGN.md §3 G6) */
 typedef struct {
   rr_mesh mesh;
   int32_t dp, tp, pp, n_microbatches;
   int32_t qkv_layout;
   int32_t gate_up_layout;
+  int32_t kv_layout;
 } rr_placement;
 
 typedef struct { /* SPEC.md:547-549; layers -1 and L are embed / final+head */
@@ -91,6 +94,7 @@ typedef struct { /* SPEC.md:547-549; layers -1 and L are embed / final+head */
   int32_t tp_rank;
   int32_t tp_degree;
   int32_t replicated;
+  int32_t part; /* 0 every TP-split tensor, 1 all but k/v, 2 k/v only (G6) */
 } rr_shard;
 
 typedef struct { /* SPEC.md:550-552 */

@@ -42,13 +42,13 @@ class OrcCluster(Structure):
 class OrcPlacement(Structure):
     _fields_ = [("node_offset", c_int32), ("node_count", c_int32), ("gpu_offset", c_int32),
                 ("gpu_count", c_int32), ("dp", c_int32), ("tp", c_int32), ("pp", c_int32),
-                ("qkv_layout", c_int32), ("gate_up_layout", c_int32)]
+                ("qkv_layout", c_int32), ("gate_up_layout", c_int32), ("kv_layout", c_int32)]
 
 
 class OrcOp(Structure):
     _fields_ = [("src", c_int32), ("n_dst", c_int32), ("dst", c_int32 * MAX_DST), ("layer_start", c_int64),
                 ("layer_end", c_int64), ("slice", c_int32), ("slices", c_int32), ("replicated", c_int32),
-                ("bytes", c_int64)]
+                ("bytes", c_int64), ("part", c_int32)]
 
 
 def _build_if_missing() -> None:
@@ -85,11 +85,12 @@ def _cluster(c) -> OrcCluster:
 def _placement(p) -> OrcPlacement:
     m, s = p.mesh, p.strategy
     return OrcPlacement(m.node_offset, m.node_count, m.gpu_offset, m.gpu_count, s.dp, s.tp, s.pp,
-                        getattr(p, "qkv_layout", 0), getattr(p, "gate_up_layout", 0))
+                        getattr(p, "qkv_layout", 0), getattr(p, "gate_up_layout", 0), getattr(p, "kv_layout", 0))
 
 
-# An op as a plain tuple: (src, dst tuple, (layer_start, layer_end, slice, slices, replicated), bytes)
-OpTuple = Tuple[int, Tuple[int, ...], Tuple[int, int, int, int, bool], int]
+# An op as a plain tuple: (src, dst tuple, (layer_start, layer_end, slice, slices, replicated, part), bytes);
+# part: 0 every TP-split tensor, 1 all but k/v, 2 k/v only (DESIGN.md §3 G6)
+OpTuple = Tuple[int, Tuple[int, ...], Tuple[int, int, int, int, bool, int], int]
 
 
 def param_count(model, include_output_embedding: bool) -> int:
@@ -105,8 +106,8 @@ def stage_layer_map(num_layers: int, pp: int) -> Optional[List[Tuple[int, int]]]
 
 
 def _op_tuple(o: OrcOp) -> OpTuple:
-    return (o.src, tuple(o.dst[: o.n_dst]), (o.layer_start, o.layer_end, o.slice, o.slices, bool(o.replicated)),
-            o.bytes)
+    return (o.src, tuple(o.dst[: o.n_dst]),
+            (o.layer_start, o.layer_end, o.slice, o.slices, bool(o.replicated), o.part), o.bytes)
 
 
 def plan(model, src, dst, cluster, policy: int = 0):
@@ -147,12 +148,13 @@ def fill(model, placement, cluster, dev: int, seed: int) -> np.ndarray:
 
 def _ops_array(ops: Sequence[OpTuple]):
     arr = (OrcOp * max(1, len(ops)))()
-    for i, (s, d, (lo, hi, k, G, rep), b) in enumerate(ops):
+    for i, (s, d, (lo, hi, k, G, rep, part), b) in enumerate(ops):
         arr[i].src, arr[i].n_dst = s, len(d)
         for j, x in enumerate(d):
             arr[i].dst[j] = x
         arr[i].layer_start, arr[i].layer_end = lo, hi
         arr[i].slice, arr[i].slices, arr[i].replicated, arr[i].bytes = k, G, int(rep), b
+        arr[i].part = part
     return arr
 
 
@@ -175,12 +177,21 @@ def _mesh_devices(placement, cluster) -> List[int]:
             for n in range(m.node_count) for g in range(m.gpu_count)]
 
 
-def _units(model, placement, cluster, G: int):
+def _kv_slices(model, placement) -> int:
+    """DESIGN.md §3 G6: distinct K/V slices over the TP ranks."""
+    tp = placement.strategy.tp
+    return model.num_kv_heads if getattr(placement, "kv_layout", 0) == 1 and tp > model.num_kv_heads else tp
+
+
+def _units(model, placement, cluster, G: int, Gkv: int = 0):
     """Per device: set of shard units it holds — (ext_layer, k) for each of the
     G finest slices of the split tensors and (ext_layer, 'rep') for the
-    replicated ones (SPEC.md:596 finest common slicing)."""
+    replicated ones (SPEC.md:596 finest common slicing). With Gkv (K/V
+    carried separately, G6), k and v are units (layer, 'kv', k) of the Gkv
+    finest K/V slices and the (ext_layer, k) units exclude them."""
     L = model.num_layers
     s = placement.strategy
+    kv = _kv_slices(model, placement)
     stages = stage_layer_map(L, s.pp)
     devs = _mesh_devices(placement, cluster)
     out = {}
@@ -197,6 +208,9 @@ def _units(model, placement, cluster, G: int):
                 units.update((e, k) for k in range(tp_r * per, (tp_r + 1) * per))
             if has_rep:
                 units.add((e, "rep"))
+            if Gkv and 0 <= e < L:
+                mine, per_kv = tp_r * kv // s.tp, Gkv // kv
+                units.update((e, "kv", k) for k in range(mine * per_kv, (mine + 1) * per_kv))
         out[d] = units
     return out
 
@@ -209,15 +223,20 @@ def replay(model, src, dst, cluster, ops: Sequence[OpTuple], local_ops: Sequence
     requirement — no missing, no extra, no duplicate units. Returns None on
     success, else a description of the first discrepancy."""
     G = src.strategy.tp * dst.strategy.tp // np.gcd(src.strategy.tp, dst.strategy.tp)
-    held = _units(model, src, cluster, G)
-    need = _units(model, dst, cluster, G)
+    e1, e2 = _kv_slices(model, src), _kv_slices(model, dst)
+    Gkv = e1 * e2 // np.gcd(e1, e2) if (e1, e2) != (src.strategy.tp, dst.strategy.tp) else 0
+    held = _units(model, src, cluster, G, Gkv)
+    need = _units(model, dst, cluster, G, Gkv)
     got = {d: [] for d in need}
-    for (s, dsts, (lo, hi, k, slices, rep), _b) in list(ops) + list(local_ops):
+    for (s, dsts, (lo, hi, k, slices, rep, part), _b) in list(ops) + list(local_ops):
         units = []
         for e in range(lo, hi):
             if rep:
                 if e != -1:  # the embedding has no replicated tensor
                     units.append((e, "rep"))
+            elif part == 2:
+                if 0 <= e < model.num_layers:
+                    units.append((e, "kv", k))
             else:
                 if e == model.num_layers and not model.has_output_head:
                     continue
@@ -396,7 +415,7 @@ def replay_data(producer, consumer, cluster, data_bytes_per_dp_shard: int, ops, 
         return {d: (i // (s.tp * s.dp), (i // s.tp) % s.dp) for i, d in enumerate(devs)}
     pr, cr = ranks(producer), ranks(consumer)
     got = {d: [] for d in cr}
-    for (s, dsts, (lo, hi, k, slices, rep), _b) in list(ops) + list(local_ops):
+    for (s, dsts, (lo, hi, k, slices, rep, _part), _b) in list(ops) + list(local_ops):
         if slices != G or rep or s not in pr:
             return f"bad payload from {s}"
         pp_r, dp_r = pr[s]

@@ -124,7 +124,21 @@ static int placement_ok(const orc_model* m, const orc_placement* p, const orc_cl
   if (p->qkv_layout < 0 || p->qkv_layout > 2 || p->gate_up_layout < 0 || p->gate_up_layout > 1) return 0;
   if (p->pp > m->layers || (p->tp & (p->tp - 1)) || m->heads % p->tp) return 0;
   if (p->qkv_layout == 2 && m->kv_heads % p->tp) return 0;
+  if (p->kv_layout < 0 || p->kv_layout > 1) return 0;
+  if (p->kv_layout == 1 && p->tp > m->kv_heads && p->tp % m->kv_heads) return 0;
   return 1;
+}
+
+/* Distinct K/V slices over the TP ranks (DESIGN.md §3 G6): whole KV heads
+ * when they are replicated and tp exceeds them, else one slice per rank. */
+static int kv_slices(const orc_model* m, const orc_placement* p) {
+  return p->kv_layout == 1 && p->tp > m->kv_heads ? (int)m->kv_heads : p->tp;
+}
+
+static int is_kv(const orc_model* m, int64_t id) {
+  if (id < 1 || id > 9 * m->layers) return 0;
+  const int kind = (int)((id - 1) % 9);
+  return kind == K_K || kind == K_V;
 }
 
 /* reference cluster.cpp:95-101 */
@@ -135,12 +149,21 @@ static double bandwidth(const orc_cluster* c, int a, int b) {
 
 /* ---- plan: SPEC.md:569-577 ------------------------------------------------ */
 
-static int64_t range_bytes(const orc_model* m, int64_t lo, int64_t hi, int replicated, int64_t slices) {
+/* Whether tensor id travels in a payload of this kind (part: 0 every split
+ * tensor, 1 all but k/v, 2 k/v only). */
+static int in_part(const orc_model* m, int64_t id, int replicated, int part) {
+  const tensor_shape s = shape_of(m, id);
+  if ((s.split == REPLICATED) != replicated) return 0;
+  if (replicated || part == 0) return 1;
+  return (part == 2) == is_kv(m, id);
+}
+
+static int64_t range_bytes(const orc_model* m, int64_t lo, int64_t hi, int replicated, int64_t slices, int part) {
   int64_t n = 0;
   for (int64_t id = 0; id < n_tensors(m); ++id) {
     const tensor_shape s = shape_of(m, id);
     if (s.layer < lo || s.layer >= hi) continue;
-    if ((s.split == REPLICATED) != replicated) continue;
+    if (!in_part(m, id, replicated, part)) continue;
     n += s.rows * s.cols / (replicated ? 1 : slices);
   }
   return n * m->param_bytes;
@@ -156,12 +179,12 @@ typedef struct {
   int cap, n;
 } op_list;
 
-static int add_need(op_list* L, int src, int dst, int64_t lo, int64_t hi, int k, int G, int rep,
+static int add_need(op_list* L, int src, int dst, int64_t lo, int64_t hi, int k, int G, int rep, int part,
                     int64_t bytes) {
   for (int i = 0; i < L->n; ++i) {
     orc_op* op = &L->list[i];
     if (op->src == src && op->layer_start == lo && op->layer_end == hi && op->slice == k &&
-        op->slices == G && op->replicated == rep) {
+        op->slices == G && op->replicated == rep && op->part == part) {
       if (op->n_dst >= ORC_MAX_DST) return -1;
       op->dst[op->n_dst++] = dst;
       return 0;
@@ -172,7 +195,7 @@ static int add_need(op_list* L, int src, int dst, int64_t lo, int64_t hi, int k,
   memset(op, 0, sizeof(*op));
   op->src = src; op->n_dst = 1; op->dst[0] = dst;
   op->layer_start = lo; op->layer_end = hi;
-  op->slice = k; op->slices = G; op->replicated = rep; op->bytes = bytes;
+  op->slice = k; op->slices = G; op->replicated = rep; op->part = part; op->bytes = bytes;
   return 0;
 }
 
@@ -203,8 +226,17 @@ int orc_plan(const orc_model* m, const orc_placement* src, const orc_placement* 
              int cap_local, int* n_local, int64_t* total_bytes, double* est_time) {
   if (!placement_ok(m, src, c) || !placement_ok(m, dst, c)) return -1;
   const int G = (int)(src->tp / gcd64(src->tp, dst->tp) * dst->tp);
+  /* K/V travel separately when either side replicates KV heads (G6). */
+  const int e1 = kv_slices(m, src), e2 = kv_slices(m, dst);
+  const int kv_sep = e1 != src->tp || e2 != dst->tp;
+  const int Gkv = (int)(e1 / gcd64(e1, e2) * e2);
+  const int split_part = kv_sep ? 1 : 0;
   for (int64_t id = 0; id < n_tensors(m); ++id) {
     const tensor_shape s = shape_of(m, id);
+    if (kv_sep && is_kv(m, id)) {
+      if (s.rows % Gkv) return -1;
+      continue;
+    }
     if (s.split == SPLIT_ROWS && s.rows % G) return -1;
     if (s.split == SPLIT_COLS && s.cols % G) return -1;
   }
@@ -221,7 +253,8 @@ int orc_plan(const orc_model* m, const orc_placement* src, const orc_placement* 
       stage_range(m, dst->pp, j, &jlo, &jhi);
       const int64_t lo = ilo > jlo ? ilo : jlo, hi = ihi < jhi ? ihi : jhi;
       if (lo >= hi) continue;
-      const int64_t split_b = range_bytes(m, lo, hi, 0, G), rep_b = range_bytes(m, lo, hi, 1, 1);
+      const int64_t split_b = range_bytes(m, lo, hi, 0, G, split_part), rep_b = range_bytes(m, lo, hi, 1, 1, 0);
+      const int64_t kv_b = kv_sep ? range_bytes(m, lo, hi, 0, Gkv, 2) : 0;
       for (int dp = 0; dp < dst->dp && !rc; ++dp) {
         for (int tr = 0; tr < dst->tp && !rc; ++tr) {
           const int d = device_at(dst, c, j, dp, tr);
@@ -232,7 +265,21 @@ int orc_plan(const orc_model* m, const orc_placement* src, const orc_placement* 
               for (int sdp = 0; sdp < src->dp; ++sdp) holders[nh++] = device_at(src, c, i, sdp, k / per_src);
               qsort(holders, (size_t)nh, sizeof(int), cmp_int);
               const int s = pick_source(c, holders, nh, d, policy, egress, split_b);
-              rc = add_need(s == d ? &Lc : &R, s, d, lo, hi, k, G, 0, split_b);
+              rc = add_need(s == d ? &Lc : &R, s, d, lo, hi, k, G, 0, split_part, split_b);
+            }
+          }
+          if (kv_b > 0) {
+            /* the K/V slice this rank holds, at the finest common slicing;
+             * holders are every source rank whose own K/V slice covers it */
+            const int mine = tr * e2 / dst->tp, per_dst = Gkv / e2, per_src = Gkv / e1;
+            for (int k = mine * per_dst; k < (mine + 1) * per_dst && !rc; ++k) {
+              int nh = 0;
+              for (int sdp = 0; sdp < src->dp; ++sdp)
+                for (int st = 0; st < src->tp; ++st)
+                  if (st * e1 / src->tp == k / per_src) holders[nh++] = device_at(src, c, i, sdp, st);
+              qsort(holders, (size_t)nh, sizeof(int), cmp_int);
+              const int s = pick_source(c, holders, nh, d, policy, egress, kv_b);
+              rc = add_need(s == d ? &Lc : &R, s, d, lo, hi, k, Gkv, 0, 2, kv_b);
             }
           }
           if (rep_b > 0 && !rc) {
@@ -241,7 +288,7 @@ int orc_plan(const orc_model* m, const orc_placement* src, const orc_placement* 
               for (int st = 0; st < src->tp; ++st) holders[nh++] = device_at(src, c, i, sdp, st);
             qsort(holders, (size_t)nh, sizeof(int), cmp_int);
             const int s = pick_source(c, holders, nh, d, policy, egress, rep_b);
-            rc = add_need(s == d ? &Lc : &R, s, d, lo, hi, 0, 1, 1, rep_b);
+            rc = add_need(s == d ? &Lc : &R, s, d, lo, hi, 0, 1, 1, 0, rep_b);
           }
         }
       }
@@ -288,6 +335,7 @@ typedef struct {
   tensor_loc* loc; /* n_tensors entries */
   int64_t bytes;
   int tp_rank, tp;
+  int kv_slice, kv_slices; /* K/V rows held: slice kv_slice of kv_slices (G6) */
 } dev_layout;
 
 static int64_t align256(int64_t v) { return (v + 255) / 256 * 256; }
@@ -296,7 +344,12 @@ static void place_split(const orc_model* m, dev_layout* L, int64_t id, int64_t* 
   const tensor_shape s = shape_of(m, id);
   tensor_loc* t = &L->loc[id];
   t->base = *at;
-  if (s.split == SPLIT_ROWS) {
+  if (s.split == SPLIT_ROWS && is_kv(m, id)) {
+    t->mode = MODE_ROWS;
+    t->lo = L->kv_slice * s.rows / L->kv_slices;
+    t->hi = (L->kv_slice + 1) * s.rows / L->kv_slices;
+    *at += (t->hi - t->lo) * s.cols * m->param_bytes;
+  } else if (s.split == SPLIT_ROWS) {
     t->mode = MODE_ROWS;
     t->lo = L->tp_rank * s.rows / L->tp;
     t->hi = (L->tp_rank + 1) * s.rows / L->tp;
@@ -323,6 +376,8 @@ static int build_layout(const orc_model* m, const orc_placement* p, const orc_cl
   if (rank_of(p, c, dev, &pr, &dr, &tr)) return 0;
   L->tp_rank = tr;
   L->tp = p->tp;
+  L->kv_slices = kv_slices(m, p);
+  L->kv_slice = tr * L->kv_slices / p->tp;
   int64_t lo, hi, at = 0;
   stage_range(m, p->pp, pr, &lo, &hi);
   for (int64_t e = lo; e < hi; ++e) {
@@ -511,7 +566,7 @@ int orc_execute(const orc_model* m, const orc_placement* src, const orc_placemen
       for (int64_t id = 0; id < n_tensors(m); ++id) {
         const tensor_shape s = shape_of(m, id);
         if (s.layer < op->layer_start || s.layer >= op->layer_end) continue;
-        if ((s.split == REPLICATED) != op->replicated) continue;
+        if (!in_part(m, id, op->replicated, op->part)) continue;
         int64_t r0 = 0, r1 = s.rows, c0 = 0, c1 = s.cols;
         if (s.split == SPLIT_ROWS) {
           r0 = op->slice * s.rows / op->slices;
@@ -574,7 +629,7 @@ int orc_plan_data(const orc_placement* prod, const orc_placement* cons, const or
         for (int t = 0; t < prod->tp; ++t) holders[nh++] = device_at(prod, c, s, k / (G / prod->dp), t);
       qsort(holders, (size_t)nh, sizeof(int), cmp_int);
       const int s = pick_source(c, holders, nh, d, policy, egress, slice);
-      rc = add_need(s == d ? &Lc : &R, s, d, 0, 0, k, G, 0, slice);
+      rc = add_need(s == d ? &Lc : &R, s, d, 0, 0, k, G, 0, 0, slice);
     }
   }
   if (rc) { free(egress); return -1; }

@@ -55,6 +55,7 @@ typedef struct {
   int32_t dp, tp, pp;
   int32_t qkv_layout;     /* 0 separate, 1 concat, 2 grouped */
   int32_t gate_up_layout; /* 0 separate, 1 concat */
+  int32_t kv_layout;      /* 0 k/v rows split over tp, 1 whole KV heads replicated when tp > kv */
 } orc_placement;
 
 typedef struct {
@@ -64,6 +65,7 @@ typedef struct {
   int64_t layer_start, layer_end;
   int32_t slice, slices, replicated;
   int64_t bytes;
+  int32_t part; /* 0 every split tensor, 1 all but k/v, 2 k/v only */
 } orc_op;
 
 int64_t orc_param_count(const orc_model* m, int include_output_embedding);

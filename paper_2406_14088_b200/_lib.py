@@ -37,12 +37,13 @@ class RrMesh(Structure):
 
 class RrPlacement(Structure):
     _fields_ = [("mesh", RrMesh), ("dp", c_int32), ("tp", c_int32), ("pp", c_int32),
-                ("n_microbatches", c_int32), ("qkv_layout", c_int32), ("gate_up_layout", c_int32)]
+                ("n_microbatches", c_int32), ("qkv_layout", c_int32), ("gate_up_layout", c_int32),
+                ("kv_layout", c_int32)]
 
 
 class RrShard(Structure):
     _fields_ = [("layer_start", c_int64), ("layer_end", c_int64), ("tp_rank", c_int32),
-                ("tp_degree", c_int32), ("replicated", c_int32)]
+                ("tp_degree", c_int32), ("replicated", c_int32), ("part", c_int32)]
 
 
 class RrOp(Structure):

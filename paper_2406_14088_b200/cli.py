@@ -20,7 +20,7 @@ SPEC.md:657):
                  "intra_node_bw": 9e11, "inter_node_bw": 5e10, "host_to_device_bw": 5.5e10},
      "model": "llama7b"  |  {"name": ..., "hidden_size": ..., ...},
      "src": {"mesh": "trainer01", "dp": 1, "tp": 8, "pp": 1, "qkv_layout": "separate",
-             "gate_up_layout": "separate"},
+             "gate_up_layout": "separate", "kv_layout": "split" | "replicate"},
      "dst": {"mesh": "trainer01", "dp": 8, "tp": 1, "pp": 1},
      "policy": "spec" | "balanced",
      "gpus_per_host": 1,                      (plan devices per GPU, cost model)
@@ -44,6 +44,7 @@ from .rlplan import (BALANCED, MODELS, SPEC, ClusterSpec, ModelSpec, ParallelStr
 
 QKV = {"separate": 0, "concat": 1, "grouped": 2}
 GATE_UP = {"separate": 0, "concat": 1}
+KV = {"split": 0, "replicate": 1}
 
 
 class ConfigError(ValueError):
@@ -108,9 +109,12 @@ def parse_placement(d, cluster: ClusterSpec, path: str) -> Placement:
         raise ConfigError(f"{path}.qkv_layout: one of {sorted(QKV)}")
     if gu not in GATE_UP:
         raise ConfigError(f"{path}.gate_up_layout: one of {sorted(GATE_UP)}")
+    kv = _get(d, "kv_layout", path, str, "split")
+    if kv not in KV:
+        raise ConfigError(f"{path}.kv_layout: one of {sorted(KV)}")
     s = ParallelStrategy(dp=_get(d, "dp", path, int), tp=_get(d, "tp", path, int), pp=_get(d, "pp", path, int),
                          n_microbatches=_get(d, "n_microbatches", path, int, 1))
-    return Placement(mesh, s, QKV[qkv], GATE_UP[gu])
+    return Placement(mesh, s, QKV[qkv], GATE_UP[gu], KV[kv])
 
 
 def build(config: Dict[str, Any], data: bool = False) -> Dict[str, Any]:

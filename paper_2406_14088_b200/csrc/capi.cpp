@@ -70,13 +70,15 @@ Placement to_placement(const rr_placement* p) {
   out.strategy = ParallelStrategy{p->dp, p->tp, p->pp, p->n_microbatches};
   need(p->qkv_layout >= 0 && p->qkv_layout <= 2, "qkv_layout must be 0, 1 or 2");
   need(p->gate_up_layout >= 0 && p->gate_up_layout <= 1, "gate_up_layout must be 0 or 1");
+  need(p->kv_layout >= 0 && p->kv_layout <= 1, "kv_layout must be 0 or 1");
   out.qkv = static_cast<QkvLayout>(p->qkv_layout);
   out.gate_up = static_cast<GateUpLayout>(p->gate_up_layout);
+  out.kv = static_cast<KvLayout>(p->kv_layout);
   return out;
 }
 
 rr_shard to_shard(const ShardDescriptor& d) {
-  return rr_shard{d.layer_start, d.layer_end, d.tp_rank, d.tp_degree, d.replicated ? 1 : 0};
+  return rr_shard{d.layer_start, d.layer_end, d.tp_rank, d.tp_degree, d.replicated ? 1 : 0, d.part};
 }
 
 }  // namespace

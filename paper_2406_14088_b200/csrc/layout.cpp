@@ -64,7 +64,9 @@ void validate_placement(const ModelSpec& m, const Placement& p, const ClusterSpe
   need(s.pp <= m.num_layers, "pp must not exceed num_layers");
   need(is_power_of_two(s.tp), "tp must be a power of two");
   need(m.num_attention_heads % s.tp == 0, "tp must divide num_attention_heads");
+  const bool kv_heads = p.kv == KvLayout::ReplicateHeads && s.tp > m.num_kv_heads;
   for (const auto& t : tensor_inventory(m)) {
+    if (kv_heads && (t.kind == kK || t.kind == kV)) continue;  // whole heads, checked below
     if (t.split == SplitKind::Rows) need(t.rows % s.tp == 0, "tp must divide every row-split dimension");
     if (t.split == SplitKind::Cols) need(t.cols % s.tp == 0, "tp must divide every column-split dimension");
   }
@@ -73,6 +75,16 @@ void validate_placement(const ModelSpec& m, const Placement& p, const ClusterSpe
   need(g >= 0 && g <= 1, "unknown gate_up layout");
   if (p.qkv == QkvLayout::Grouped)
     need(m.num_kv_heads % s.tp == 0, "grouped QKV layout needs tp to divide num_kv_heads");
+  const int kv = static_cast<int>(p.kv);
+  need(kv >= 0 && kv <= 1, "unknown kv layout");
+  if (p.kv == KvLayout::ReplicateHeads && s.tp > m.num_kv_heads)
+    need(s.tp % m.num_kv_heads == 0, "replicated KV heads need tp to be a multiple of num_kv_heads");
+}
+
+int kv_degree(const ModelSpec& m, const Placement& p) {
+  const int tp = p.strategy.tp;
+  if (p.kv == KvLayout::ReplicateHeads && tp > m.num_kv_heads) return static_cast<int>(m.num_kv_heads);
+  return tp;
 }
 
 RankCoord rank_of(const Placement& p, const ClusterSpec& cluster, DeviceId d) {
@@ -105,6 +117,7 @@ ShardLayout shard_layout(const ModelSpec& m, const Placement& p, const ClusterSp
   const auto stages = stage_layer_map(m.num_layers, p.strategy.pp);
   const Count L = m.num_layers;
   const int t = p.strategy.tp, r = rc.tp_rank;
+  const int e = kv_degree(m, p), kv_slice = r * e / t;  // K/V slice this rank holds (G6)
   const Bytes pb = m.param_bytes;
   Bytes cursor = 0;
 
@@ -116,6 +129,10 @@ ShardLayout shard_layout(const ModelSpec& m, const Placement& p, const ClusterSp
   // This rank's part of a tensor per its split kind.
   auto put_part = [&](int id) {
     const LogicalTensor& T = inv[static_cast<size_t>(id)];
+    if (T.kind == kK || T.kind == kV) {
+      put(id, kv_slice * T.rows / e, (kv_slice + 1) * T.rows / e, 0, T.cols);
+      return;
+    }
     switch (T.split) {
       case SplitKind::Rows: put(id, r * T.rows / t, (r + 1) * T.rows / t, 0, T.cols); break;
       case SplitKind::Cols: put(id, 0, T.rows, r * T.cols / t, (r + 1) * T.cols / t); break;

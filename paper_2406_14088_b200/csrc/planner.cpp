@@ -45,29 +45,38 @@ std::pair<Count, Count> ext_range(const std::vector<std::pair<Count, Count>>& st
   return {lo, hi};
 }
 
+bool is_kv(const LogicalTensor& t) { return t.kind == kK || t.kind == kV; }
+
+// Whether tensor t belongs to a payload of the given kind (G5, G6).
+bool in_payload(const LogicalTensor& t, bool replicated, int part) {
+  const bool rep = t.split == SplitKind::Replicated;
+  if (rep != replicated) return false;
+  if (rep) return true;
+  return part == kPartAll || (part == kPartKv) == is_kv(t);
+}
+
 Bytes range_bytes(const std::vector<LogicalTensor>& inv, const ModelSpec& m, Count lo, Count hi,
-                  bool replicated, Count degree) {
+                  bool replicated, Count degree, int part = kPartAll) {
   Bytes n = 0;
   for (const auto& t : inv) {
     if (t.ext_layer < lo || t.ext_layer >= hi) continue;
-    const bool rep = t.split == SplitKind::Replicated;
-    if (rep != replicated) continue;
-    n += t.rows * t.cols / (rep ? 1 : degree);
+    if (!in_payload(t, replicated, part)) continue;
+    n += t.rows * t.cols / (replicated ? 1 : degree);
   }
   return n * m.param_bytes;
 }
 
-using OpKey = std::tuple<DeviceId, Count, Count, int, int, bool>;
+using OpKey = std::tuple<DeviceId, Count, Count, int, int, bool, int>;
 
 OpKey key_of(DeviceId src, const ShardDescriptor& p) {
-  return {src, p.layer_start, p.layer_end, p.tp_rank, p.tp_degree, p.replicated};
+  return {src, p.layer_start, p.layer_end, p.tp_rank, p.tp_degree, p.replicated, p.part};
 }
 
 }  // namespace
 
 Bytes payload_bytes(const ModelSpec& model, const ShardDescriptor& p) {
   const auto inv = tensor_inventory(model);
-  return range_bytes(inv, model, p.layer_start, p.layer_end, p.replicated, p.tp_degree);
+  return range_bytes(inv, model, p.layer_start, p.layer_end, p.replicated, p.tp_degree, p.part);
 }
 
 ReallocPlan plan_param_realloc(const ModelSpec& m, const Placement& src, const Placement& dst,
@@ -79,7 +88,17 @@ ReallocPlan plan_param_realloc(const ModelSpec& m, const Placement& src, const P
   const Count L = m.num_layers;
   const int tp1 = src.strategy.tp, tp2 = dst.strategy.tp;
   const int G = static_cast<int>(lcm_count(tp1, tp2));
+  // K/V as their own payloads when either side replicates KV heads (G6).
+  const int e1 = kv_degree(m, src), e2 = kv_degree(m, dst);
+  const bool kv_class = e1 != tp1 || e2 != tp2;
+  const int Gkv = static_cast<int>(lcm_count(e1, e2));
+  const int split_part = kv_class ? kPartNoKv : kPartAll;
   for (const auto& t : inv) {
+    if (kv_class && is_kv(t)) {
+      if (t.rows % Gkv)
+        throw ValidationError("plan_param_realloc: lcm(kv slices) must divide the k/v rows");
+      continue;
+    }
     if (t.split == SplitKind::Rows && t.rows % G)
       throw ValidationError("plan_param_realloc: lcm(tp) must divide every row-split dimension");
     if (t.split == SplitKind::Cols && t.cols % G)
@@ -131,7 +150,8 @@ ReallocPlan plan_param_realloc(const ModelSpec& m, const Placement& src, const P
       const auto dj = ext_range(d_stages, j, L);
       const Count lo = std::max(si.first, dj.first), hi = std::min(si.second, dj.second);
       if (lo >= hi) continue;
-      const Bytes split_bytes = range_bytes(inv, m, lo, hi, false, G);
+      const Bytes split_bytes = range_bytes(inv, m, lo, hi, false, G, split_part);
+      const Bytes kv_bytes = kv_class ? range_bytes(inv, m, lo, hi, false, Gkv, kPartKv) : 0;
       const Bytes rep_bytes = range_bytes(inv, m, lo, hi, true, 1);
       std::vector<DeviceId> all_src;
       for (int dp = 0; dp < src.strategy.dp; ++dp)
@@ -146,8 +166,23 @@ ReallocPlan plan_param_realloc(const ModelSpec& m, const Placement& src, const P
               for (int sdp = 0; sdp < src.strategy.dp; ++sdp)
                 holders.push_back(device_at(src, cluster, i, sdp, k / (G / tp1)));
               std::sort(holders.begin(), holders.end());
-              const ShardDescriptor payload{lo, hi, k, G, false};
+              const ShardDescriptor payload{lo, hi, k, G, false, split_part};
               emit(choose(holders, d, split_bytes), d, payload, split_bytes);
+            }
+          }
+          if (kv_bytes > 0) {
+            // K/V slices of this rank's head range; every source TP rank
+            // whose kv slice covers k holds it (replicas included).
+            const int s2 = tr * e2 / tp2;
+            for (int k = s2 * (Gkv / e2); k < (s2 + 1) * (Gkv / e2); ++k) {
+              const int q = k / (Gkv / e1);
+              std::vector<DeviceId> holders;
+              for (int sdp = 0; sdp < src.strategy.dp; ++sdp)
+                for (int st = q * (tp1 / e1); st < (q + 1) * (tp1 / e1); ++st)
+                  holders.push_back(device_at(src, cluster, i, sdp, st));
+              std::sort(holders.begin(), holders.end());
+              const ShardDescriptor payload{lo, hi, k, Gkv, false, kPartKv};
+              emit(choose(holders, d, kv_bytes), d, payload, kv_bytes);
             }
           }
           if (rep_bytes > 0) {
@@ -178,7 +213,8 @@ std::string plan_to_json(const ReallocPlan& plan, const ModelSpec& model, const 
       << ",\"tp\":" << p.strategy.tp << ",\"pp\":" << p.strategy.pp
       << ",\"n_microbatches\":" << p.strategy.n_microbatches
       << ",\"qkv_layout\":" << static_cast<int>(p.qkv)
-      << ",\"gate_up_layout\":" << static_cast<int>(p.gate_up) << "}";
+      << ",\"gate_up_layout\":" << static_cast<int>(p.gate_up) << ",\"kv_layout\":" << static_cast<int>(p.kv)
+      << "}";
   };
   auto ops = [&](const std::vector<BroadcastOp>& list) {
     o << "[";
@@ -190,6 +226,7 @@ std::string plan_to_json(const ReallocPlan& plan, const ModelSpec& model, const 
         << "],\"slice_index\":" << op.payload.tp_rank
         << ",\"slice_count\":" << op.payload.tp_degree
         << ",\"replicated\":" << (op.payload.replicated ? "true" : "false")
+        << (op.payload.part ? (op.payload.part == kPartKv ? ",\"part\":\"kv\"" : ",\"part\":\"no_kv\"") : "")
         << ",\"bytes\":" << op.bytes << "}";
     }
     o << "]";
@@ -261,20 +298,37 @@ std::vector<LoweredOp> lower_plan(const ModelSpec& m, const Placement& src, cons
     for (DeviceId d : lo.dst) {
       const RankCoord rc = rank_of(dst, cluster, d);
       // Shards of one stage share their byte layout across TP ranks, so a
-      // replicated payload may fan out to every TP rank; a split slice
-      // belongs to exactly one destination TP rank.
-      if (rc.pp_rank != r0.pp_rank || (!lo.payload.replicated && rc.tp_rank != r0.tp_rank))
+      // replicated payload may fan out to every TP rank, and so may a K/V
+      // slice held by several ranks (replicated heads, G6); any other split
+      // slice belongs to exactly one destination TP rank.
+      const bool shared = lo.payload.replicated || lo.payload.part == kPartKv;
+      if (rc.pp_rank != r0.pp_rank || (!shared && rc.tp_rank != r0.tp_rank))
         throw ValidationError("lower_plan: destinations of one op differ in geometry");
     }
     if (!s_lay.count(lo.src)) s_lay[lo.src] = shard_layout(m, src, cluster, lo.src);
     if (!d_lay.count(lo.dst.front())) d_lay[lo.dst.front()] = shard_layout(m, dst, cluster, lo.dst.front());
+    if (lo.payload.part == kPartKv) {
+      // the rectangles below are computed for dst.front() and stored at the
+      // same offsets on every destination: their K/V blocks must coincide
+      for (DeviceId d : lo.dst) {
+        if (!d_lay.count(d)) d_lay[d] = shard_layout(m, dst, cluster, d);
+        const auto& a = d_lay[lo.dst.front()].blocks;
+        const auto& b = d_lay[d].blocks;
+        bool same = a.size() == b.size();
+        for (size_t i = 0; same && i < a.size(); ++i) {
+          const int kind = inv[static_cast<size_t>(a[i].tensor)].kind;
+          if (kind != kK && kind != kV) continue;
+          same = a[i].tensor == b[i].tensor && a[i].r0 == b[i].r0 && a[i].r1 == b[i].r1 && a[i].offset == b[i].offset;
+        }
+        if (!same) throw ValidationError("lower_plan: K/V destinations of one op hold different blocks");
+      }
+    }
     const auto sidx = by_tensor(s_lay[lo.src]);
     const auto didx = by_tensor(d_lay[lo.dst.front()]);
     const ShardDescriptor& p = lo.payload;
     for (const auto& T : inv) {
       if (T.ext_layer < p.layer_start || T.ext_layer >= p.layer_end) continue;
-      const bool rep = T.split == SplitKind::Replicated;
-      if (rep != p.replicated) continue;
+      if (!in_payload(T, p.replicated, p.part)) continue;
       Rect want{0, T.rows, 0, T.cols};
       if (T.split == SplitKind::Rows) {
         want.r0 = p.tp_rank * T.rows / p.tp_degree;

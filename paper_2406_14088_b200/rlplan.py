@@ -23,11 +23,16 @@ __all__ = [
     "validate_mesh", "enumerate_meshes", "overlap", "link_bandwidth", "local_bandwidth",
     "mesh_to_string", "mesh_from_string", "stage_layer_map", "validate_placement",
     "plan_param_realloc", "plan_data_transfer", "is_power_of_two", "ceil_div", "MODELS", "b200_cluster",
-    "QKV_SEPARATE", "QKV_CONCAT", "QKV_GROUPED", "GATE_UP_SEPARATE", "GATE_UP_CONCAT",
+    "QKV_SEPARATE", "QKV_CONCAT", "QKV_GROUPED", "GATE_UP_SEPARATE", "GATE_UP_CONCAT", "KV_SPLIT",
+    "KV_REPLICATE_HEADS", "PART_ALL", "PART_NO_KV", "PART_KV",
     "SPEC", "BALANCED",
 ]
 
 QKV_SEPARATE, QKV_CONCAT, QKV_GROUPED = 0, 1, 2
+# K/V when tp > kv heads (DESIGN.md §3 G6): rows split evenly, or whole heads replicated (Megatron/vLLM)
+KV_SPLIT, KV_REPLICATE_HEADS = 0, 1
+# ShardDescriptor.part: every TP-split tensor, all but k/v, k/v only (G6)
+PART_ALL, PART_NO_KV, PART_KV = 0, 1, 2
 GATE_UP_SEPARATE, GATE_UP_CONCAT = 0, 1
 SPEC, BALANCED = 0, 1
 
@@ -136,11 +141,12 @@ class Placement:
     strategy: ParallelStrategy
     qkv_layout: int = QKV_SEPARATE
     gate_up_layout: int = GATE_UP_SEPARATE
+    kv_layout: int = KV_SPLIT
 
     def _c(self) -> RrPlacement:
         s = self.strategy
         return RrPlacement(self.mesh._c(), s.dp, s.tp, s.pp, s.n_microbatches, self.qkv_layout,
-                           self.gate_up_layout)
+                           self.gate_up_layout, self.kv_layout)
 
 
 @dataclass(frozen=True)
@@ -151,6 +157,7 @@ class ShardDescriptor:
     tp_rank: int
     tp_degree: int
     replicated: bool = False
+    part: int = PART_ALL
 
 
 @dataclass(frozen=True)
@@ -296,7 +303,7 @@ class ReallocPlan:
             p = op.payload
             out.append(BroadcastOp(op.src, tuple(op.dst[k] for k in range(op.n_dst)),
                                    ShardDescriptor(p.layer_start, p.layer_end, p.tp_rank, p.tp_degree,
-                                                   bool(p.replicated)), op.bytes))
+                                                   bool(p.replicated), p.part), op.bytes))
         return out
 
     @property

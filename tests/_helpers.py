@@ -21,7 +21,8 @@ def placement(gpus: int, pp: int, dp: int, tp: int, offset: int = 0, qkv: int = 
 
 def op_tuple(op) -> tuple:
     p = op.payload
-    return (op.src, tuple(op.dst), (p.layer_start, p.layer_end, p.tp_rank, p.tp_degree, p.replicated), op.bytes)
+    return (op.src, tuple(op.dst), (p.layer_start, p.layer_end, p.tp_rank, p.tp_degree, p.replicated, p.part),
+            op.bytes)
 
 
 def scaled(name: str, layers: Optional[int] = None, vocab: Optional[int] = None):
@@ -65,7 +66,8 @@ def emulate_lowered(plan, src_bufs: Dict[int, np.ndarray], dst_bufs: Dict[int, n
 
 def random_placement(rng, model, gpus_per_node: int = 8) -> Placement:
     """A random valid placement on an aligned sub-mesh of one node: random
-    size, offset, (pp, dp, tp) and fused layouts (plan-parity and GPU fuzz)."""
+    size, offset, (pp, dp, tp), fused layouts and K/V layout (plan-parity and
+    GPU fuzz)."""
     from paper_2406_14088_b200 import rlplan as P
     size = rng.choice([1, 2, 4, 8])
     offset = rng.randrange(0, gpus_per_node // size) * size
@@ -75,7 +77,8 @@ def random_placement(rng, model, gpus_per_node: int = 8) -> Placement:
         dp = size // (tp * pp)
         qkv = rng.choice([0, 1, 2])
         gu = rng.choice([0, 1])
-        p = P.Placement(P.DeviceMesh(0, 1, offset, size), P.ParallelStrategy(dp=dp, tp=tp, pp=pp), qkv, gu)
+        kv = rng.choice([0, 1])
+        p = P.Placement(P.DeviceMesh(0, 1, offset, size), P.ParallelStrategy(dp=dp, tp=tp, pp=pp), qkv, gu, kv)
         try:
             P.validate_placement(model, p, P.b200_cluster(gpus_per_node))
             return p

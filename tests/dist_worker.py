@@ -155,15 +155,18 @@ def main() -> int:
 
     from _helpers import random_placement
     rng = random.Random(int(os.environ.get("RR_FUZZ_SEED", "2406")))
+    fuzz_models = [TINY_GQA, dataclasses.replace(TINY_GQA, name="tiny_mqa", num_attention_heads=8, num_kv_heads=1,
+                                                 num_layers=3)]
     for i in range(int(os.environ.get("RR_FUZZ_CASES", "24"))):
-        src, dst = random_placement(rng, TINY_GQA), random_placement(rng, TINY_GQA)
+        fm = fuzz_models[i % 2]
+        src, dst = random_placement(rng, fm), random_placement(rng, fm)
         mode = rng.choice([R.PUSH, R.PULL])
         hier = rng.random() < 0.7
         relay = rng.choice([False, True, "auto"])
         overlap = rng.random() < 0.5
         kernel = rng.choice([0, 1, 5])
         chunk = rng.choice([0, 8192, 65536])
-        plan = plan_param_realloc(TINY_GQA, src, dst, c, rng.choice([0, 1]))
+        plan = plan_param_realloc(fm, src, dst, c, rng.choice([0, 1]))
         rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
                            mode=mode, kernel=kernel, flag_kernel=kernel, hierarchical=hier, relay=relay,
                            overlap=overlap, chunk_bytes=chunk)
@@ -178,7 +181,7 @@ def main() -> int:
             torch.cuda.synchronize()
             for d, b in rr.buffers["b"].items():
                 got = b.to_host()
-                want = O.fill(TINY_GQA, dst, c, d, 50 + i)
+                want = O.fill(fm, dst, c, d, 50 + i)
                 if not np.array_equal(got, want):
                     failures.append(f"fuzz {i} {src}->{dst} mode {mode} hier {hier} relay {relay} overlap {overlap} "
                                     f"kernel {kernel} chunk {chunk} rep {rep}: device {d} differs in "

@@ -46,7 +46,7 @@ from oracle import oracle as O  # noqa: E402
 SEED = 11
 # (name, hidden, ffn, layers, heads, kv_heads, vocab, tp degrees)
 MODELS = [
-    ("tiny", 256, 688, 4, 4, 2, 1024, (1, 2)),
+    ("tiny", 256, 688, 4, 4, 2, 1024, (1, 2, 4)),  # tp4 > 2 KV heads: vLLM replicates them
     ("tiny_gqa4", 512, 1376, 2, 8, 4, 2048, (2, 4)),
 ]
 
@@ -108,7 +108,7 @@ def main() -> None:
     from vllm.model_executor.layers import vocab_parallel_embedding as V
 
     out = {"generator": f"tests/golden/gen_vllm_golden.py with vllm {vllm.__version__}", "seed": SEED,
-           "layout": "(pp1, dp1, tp) placement, qkv Concat [Q_r;K_r;V_r], gate_up Concat [G_r;U_r]",
+           "layout": "(pp1, dp1, tp) placement, qkv Concat [Q_r;K_r;V_r], gate_up Concat [G_r;U_r], KV heads replicated when tp > kv",
            "models": {}, "cases": []}
     for name, h, ffn, nl, heads, kv, vocab, tps in MODELS:
         hd = h // heads

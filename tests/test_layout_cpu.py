@@ -150,7 +150,10 @@ def test_random_pairs_lowering_reproduces_oracle():
     rng = random.Random(5150)
     c = P.b200_cluster(8)
     models = [TINY_GQA, dataclasses.replace(TINY_GQA, num_layers=5, has_output_head=False),
-              dataclasses.replace(P.MODELS["tiny"], num_layers=3)]
+              dataclasses.replace(P.MODELS["tiny"], num_layers=3),
+              # 1 and 2 KV heads: replicated-head layouts (G6) at tp > kv
+              dataclasses.replace(TINY_GQA, name="tiny_mqa", num_attention_heads=8, num_kv_heads=1, num_layers=3),
+              dataclasses.replace(TINY_GQA, name="tiny_kv2", num_attention_heads=8, num_kv_heads=2, num_layers=2)]
     for i in range(100):
         m = rng.choice(models)
         src, dst = random_placement(rng, m), random_placement(rng, m)

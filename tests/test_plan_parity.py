@@ -181,3 +181,52 @@ def test_plan_json_export():
         assert (e["src"], tuple(e["dst"]), tuple(e["layer_range"]), e["slice_index"], e["slice_count"],
                 e["bytes"]) == (op.src, op.dst, (op.payload.layer_start, op.payload.layer_end),
                                 op.payload.tp_rank, op.payload.tp_degree, op.bytes)
+
+
+KV_MODELS = [dataclasses.replace(P.MODELS["tiny"], name="tiny_mqa", hidden_size=512, num_attention_heads=8,
+                                 num_kv_heads=1, intermediate_size=1024, num_layers=3),
+             dataclasses.replace(P.MODELS["tiny"], name="tiny_kv2", hidden_size=512, num_attention_heads=8,
+                                 num_kv_heads=2, intermediate_size=1024, num_layers=2)]
+
+
+def test_replicated_kv_heads_plans_match_oracle_and_replay():
+    """DESIGN.md §3 G6 ReplicateHeads: with tp > kv heads every rank holds a
+    whole KV head, so K/V travel as their own payloads (part 2) at lcm of
+    the two sides' K/V slicings while everything else keeps the SPEC lcm(tp)
+    slicing (part 1). 300 random pairs on MQA / 2-KV-head models: the product
+    equals the oracle restatement, replay is exact, and some K/V payloads
+    fan out to several replicas of a head."""
+    rng = random.Random(679)
+    c = P.b200_cluster(8)
+    kv_ops = multi = 0
+    for _ in range(300):
+        m = rng.choice(KV_MODELS)
+        src, dst = random_placement(rng, m), random_placement(rng, m)
+        policy = rng.choice([SPEC, BALANCED])
+        p, ops, loc = both(m, src, dst, c, policy)
+        assert O.replay(m, src, dst, c, ops, loc) is None, (src, dst, policy)
+        check_invariants(m, src, dst, c, p)
+        kv = [op for op in p.ops + p.local_ops if op.payload.part == P.PART_KV]
+        kv_ops += len(kv)
+        multi += sum(len(op.dst) > 1 for op in kv)
+    assert kv_ops > 100 and multi > 10
+
+
+def test_kv_layout_validation_and_bytes():
+    m = KV_MODELS[1]  # 2 KV heads
+    c = P.b200_cluster(8)
+    rep = dataclasses.replace(placement(8, 1, 1, 8), kv_layout=P.KV_REPLICATE_HEADS)
+    split = placement(8, 1, 1, 8)
+    one = placement(1, 1, 1, 1)
+    # every tp8 rank of the replicated layout holds a whole head: 4x the K/V bytes of the split layout
+    kv_rows = m.num_kv_heads * m.head_dim()
+    p_rep = P.plan_param_realloc(m, one, rep, c)
+    p_split = P.plan_param_realloc(m, one, split, c)
+    extra = sum(op.bytes * len(op.dst) for op in p_rep.ops) - sum(op.bytes * len(op.dst) for op in p_split.ops)
+    assert extra == m.num_layers * 2 * (kv_rows // 2 - kv_rows // 8) * m.hidden_size * 2 * 7
+    # split <-> replicated on the same mesh only moves K/V rows
+    p = P.plan_param_realloc(m, split, rep, c)
+    assert {op.payload.part for op in p.ops} == {P.PART_KV}
+    bad = dataclasses.replace(placement(8, 1, 1, 8), kv_layout=P.KV_REPLICATE_HEADS)
+    with pytest.raises(P.ValidationError, match="multiple of num_kv_heads"):
+        P.validate_placement(dataclasses.replace(m, num_kv_heads=3, num_attention_heads=24, hidden_size=768), bad, c)
