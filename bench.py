@@ -418,7 +418,10 @@ def run_b200(args) -> None:
 
     if rank == 0:
         peaks = measured_peaks()
-        kname = "rr_copy_kernel" if kernel == 0 else "rr_bulk_kernel"
+        # library default (kernel None): the bulk ring, LDG/STG for plain phases under 64 MiB
+        small = kernel is None and dom not in rr.overlap_phases + rr.relay_phases and \
+            rr.executors[dom].bytes_written < (64 << 20)
+        kname = "rr_copy_kernel" if kernel == 0 or small else "rr_bulk_kernel"
         if world == 1:
             achieved = dom_hbm / (dom_ms * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -466,7 +469,8 @@ def run_b200(args) -> None:
                        "plan_devices_per_gpu": w.devices // world, "phases": len(plans),
                        "policy": args.policy, "mode": args.mode, "multicast_sets": rr.multicast,
                        "relay_phases": rr.relay_phases, "overlap_phases": rr.overlap_phases,
-                       "copy_kernel": kname, "bulk_variants": {"plain": kernel, "flag_synchronised": flag_kernel},
+                       "copy_kernel": kname, "bulk_variants": {"plain": 1 if kernel is None else kernel,
+                                                                      "flag_synchronised": flag_kernel},
                        "chunk_kib": args.chunk_kib or 256, "ctas": args.ctas or "resident capacity",
                        "l2": "inputs larger than L2 (multi-GB shards); no flush needed",
                        "weights": "hash-initialised bf16 (seed 1), verified after timing"},

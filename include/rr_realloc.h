@@ -220,8 +220,12 @@ rr_status rr_exec_launch(rr_exec* ex, void* stream, int ctas);
 rr_status rr_exec_launch_fanout(rr_exec* ex, void* stream, int ctas);
 /* Copy kernel: 0 = vectorised LDG/STG kernel; 1..16 = TMA bulk-copy ring
  * variants (cp.async.bulk through shared-memory stages; default 1).
- * 2-byte-aligned and multicast items always take the LDG/STG kernel. */
+ * 2-byte-aligned and multicast items always take the LDG/STG kernel.
+ * Without this call, a plain phase storing fewer than the small-phase bytes
+ * (default 64 MiB, rr_exec_set_small_phase_bytes; 0 = never) takes the
+ * LDG/STG kernel: few items, latency-bound. */
 rr_status rr_exec_set_kernel(rr_exec* ex, int kernel);
+rr_status rr_exec_set_small_phase_bytes(rr_exec* ex, int64_t bytes);
 /* The same for flag-synchronised phases (relay chains, overlapped fan-out),
  * which run as one kernel: the bulk variant when every item is TMA-eligible,
  * else the LDG/STG kernel. Default 5. */

@@ -126,6 +126,7 @@ _SIGNATURES = {
     "rr_exec_launch_fanout": (c_int, [_P, _P, c_int]),
     "rr_exec_enable_onload": (c_int, [_P, c_int, POINTER(c_int32), POINTER(c_int64), c_int64]),
     "rr_exec_launch_onload": (c_int, [_P, POINTER(_P), _P, _P, c_int]),
+    "rr_exec_set_small_phase_bytes": (c_int, [_P, c_int64]),
     "rr_exec_launch_offload": (c_int, [_P, c_int, POINTER(c_int32), POINTER(c_int64), POINTER(_P), _P, _P]),
     "rr_exec_wire": (c_int, [_P, POINTER(c_int64), POINTER(c_int64)]),
     "rr_exec_set_kernel": (c_int, [_P, c_int]),

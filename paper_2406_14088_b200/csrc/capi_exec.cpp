@@ -39,6 +39,13 @@ struct rr_exec {
   // where more resident CTAs keep NVLink busy while some spin on a flag
   // (profiles/r01_flag_kernel_sweep_n{2,4}.txt).
   int kernel = 1, flag_kernel = 5;
+  // Plain phases that store fewer bytes than this take the LDG/STG kernel
+  // unless a kernel was chosen explicitly: a small phase has few items, and
+  // the bulk ring issues each item's (often narrow-row) stores from one
+  // thread, whereas the LDG/STG kernel spreads an item over 256 threads
+  // (tiny BASELINE config: 16 vs 39 us, profiles/r01_launch_latency_n1.json).
+  bool kernel_explicit = false;
+  int64_t small_phase_bytes = int64_t{64} << 20;
   int bulk_ctas = 0, flag_bulk_ctas = 0;
   unsigned int* d_sched = nullptr;  // dynamic work counter (see retire_cta)
   int64_t wire_in = 0, wire_out = 0;  // bytes crossing into / out of this host
@@ -117,10 +124,16 @@ void upload(const rr::ItemSet& set, rr_exec::Phase& ph) {
   check_cuda(cudaMemcpy(ph.d, set.items.data(), bytes, cudaMemcpyHostToDevice), "upload items");
 }
 
+int phase_kernel(const rr_exec* ex, const rr_exec::Phase& ph) {
+  if (ph.flagged) return ex->flag_kernel;
+  if (!ex->kernel_explicit && ph.written < ex->small_phase_bytes) return 0;
+  return ex->kernel;
+}
+
 void launch_phase(rr_exec* ex, const rr_exec::Phase& ph, void* stream, int ctas) {
   check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
   if (ph.n == 0) return;
-  const int kernel = ph.flagged ? ex->flag_kernel : ex->kernel;
+  const int kernel = phase_kernel(ex, ph);
   if (kernel == 0) {
     check_cuda(rr::launch_copy(ph.d, ph.n, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys, stream, ex->d_sched,
                                ex->epoch),
@@ -245,7 +258,7 @@ rr_status rr_exec_kernel_count(const rr_exec* ex, int* phase0, int* phase1) {
     need(ex != nullptr, "null executor");
     auto count = [&](const rr_exec::Phase& ph) {
       if (ph.n == 0) return 0;
-      if ((ph.flagged ? ex->flag_kernel : ex->kernel) == 0) return 1;
+      if (phase_kernel(ex, ph) == 0) return 1;
       return (ph.n > ph.n_vec ? 1 : 0) + (ph.n_vec > 0 ? 1 : 0);
     };
     *phase0 = count(ex->phase[0]);
@@ -298,7 +311,17 @@ void select_kernel(rr_exec* ex, int kernel, int* slot, int* slot_ctas) {
 }  // namespace
 
 rr_status rr_exec_set_kernel(rr_exec* ex, int kernel) {
-  return guarded([&] { select_kernel(ex, kernel, &ex->kernel, &ex->bulk_ctas); });
+  return guarded([&] {
+    select_kernel(ex, kernel, &ex->kernel, &ex->bulk_ctas);
+    ex->kernel_explicit = true;
+  });
+}
+
+rr_status rr_exec_set_small_phase_bytes(rr_exec* ex, int64_t bytes) {
+  return guarded([&] {
+    need(ex != nullptr && bytes >= 0, "null executor or negative size");
+    ex->small_phase_bytes = bytes;
+  });
 }
 
 rr_status rr_exec_set_flag_kernel(rr_exec* ex, int kernel) {

@@ -30,7 +30,7 @@ PUSH, PULL = 0, 1
 SRC, DST = 0, 1
 # Copy kernel used unless a caller picks one (rr_exec_set_kernel): the TMA
 # bulk ring, 4 x 16 KiB stages, 3 CTAs per SM (profiles/r01_sweep_kernels.txt).
-DEFAULT_KERNEL = 1
+DEFAULT_KERNEL = None  # library default: TMA bulk ring, LDG/STG for small phases
 # ... and for flag-synchronised phases (rr_exec_set_flag_kernel): 3 x 16 KiB
 # stages, 4 CTAs per SM (profiles/r01_flag_kernel_sweep_n{2,4}.txt).
 DEFAULT_FLAG_KERNEL = 5
@@ -269,11 +269,12 @@ class VirtualCluster:
         for d, b in self.src.items():
             fill_shard(self.plan, SRC, d, b.ptr, seed)
 
-    def executor(self, mode: int = PUSH, chunk_bytes: int = 0, kernel: int = DEFAULT_KERNEL) -> Executor:
+    def executor(self, mode: int = PUSH, chunk_bytes: int = 0, kernel: Optional[int] = DEFAULT_KERNEL) -> Executor:
         devs = sorted(set(self.src) | set(self.dst))
         ex = Executor(self.plan, self.cuda_device, {d: b.ptr for d, b in self.src.items()},
                       {d: b.ptr for d, b in self.dst.items()}, devs, mode, chunk_bytes)
-        ex.set_kernel(kernel)
+        if kernel is not None:
+            ex.set_kernel(kernel)
         return ex
 
     def verify_destinations(self, seed: int) -> Dict[int, Tuple[int, int]]:
@@ -475,7 +476,7 @@ class RankRealloc:
 
     def __init__(self, plans: Sequence[ReallocPlan], shards: Dict[str, Tuple[int, int]],
                  bind: Sequence[Tuple[str, str]], rank: int, world: int, cuda_device: int, group=None,
-                 mode: int = PUSH, kernel: int = DEFAULT_KERNEL, hierarchical: bool = True,
+                 mode: int = PUSH, kernel: Optional[int] = DEFAULT_KERNEL, hierarchical: bool = True,
                  multicast: Sequence[str] = (), relay=False, overlap: bool = False,
                  flag_kernel: int = DEFAULT_FLAG_KERNEL, chunk_bytes: int = 0):
         """``multicast`` names shard sets whose per-GPU leader shards (the
@@ -609,7 +610,8 @@ class RankRealloc:
                                            mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_tables.get(pi),
                                            relay_chain=pi in self.relay_phases,
                                            overlap_fanout=pi in self.overlap_phases))
-            self.executors[-1].set_kernel(kernel)
+            if kernel is not None:
+                self.executors[-1].set_kernel(kernel)
             self.executors[-1].set_flag_kernel(flag_kernel)
         # Every rank must run the same barrier sequence: a phase has a fan-out
         # step if any rank has fan-out work in it.
