@@ -37,9 +37,19 @@ CASES = [
 
 
 def main() -> int:
-    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    rank, world, lrank = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    # More ranks than GPUs (e.g. world 8 on a 4-GPU box, the 8-GPU code path):
+    # two processes share a GPU, their kernels time-slice, IPC and flags work
+    # as across GPUs. NCCL refuses two ranks per GPU, so gloo carries the
+    # host-side collectives; multicast needs distinct GPUs and is skipped.
+    gpus = torch.cuda.device_count()
+    local = lrank % gpus
+    oversub = world > gpus
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if oversub:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = b200_cluster(8)
     failures = []
     combos = [(m, k, h) for m in (R.PUSH, R.PULL) for k in (0, 1) for h in (True, False)]
@@ -67,7 +77,7 @@ def main() -> int:
             dist.barrier()
             rr.close()
     # NVLS multicast (K3): one-to-many payloads stored once through multimem.st.
-    if R.multicast_supported(local):
+    if R.multicast_supported(local) and not oversub:
         mc_cases = [
             (Placement(DeviceMesh(0, 1, 0, 1), ParallelStrategy()), placement(8, 1, 8, 1)),  # replicate from dev 0
             (placement(8, 1, 1, 8), placement(8, 1, 8, 1)),                                  # tp8 -> dp8
@@ -91,7 +101,7 @@ def main() -> int:
                                     f"{int(np.count_nonzero(got != want))} elements (items {uses_mc})")
             rr.close()
     elif rank == 0:
-        print("dist_worker: NVLS multicast not supported, skipped", flush=True)
+        print("dist_worker: NVLS multicast not supported or GPUs shared, skipped", flush=True)
     # Overlapped fan-out (star flags) and relay + overlap, over all parity
     # cases, on the TMA bulk kernel (1) and the LDG/STG kernel (0).
     for relay_opt, kernel in ((False, 1), (True, 1), (False, 0), (True, 0)):
@@ -190,7 +200,7 @@ def main() -> int:
             failures.append(f"fuzz {i}: flag or barrier timeouts")
         dist.barrier()
         rr.close()
-    if os.environ.get("RR_FULL_7B") == "1":
+    if os.environ.get("RR_FULL_7B") == "1" and not oversub:
         w = WORKLOADS["llama7b_tp8_dp8_roundtrip"]
         plans = [plan_param_realloc(w.model, s, d, c, BALANCED) for (s, d) in w.phases]
         rr = R.RankRealloc(plans, {"train": (0, R.SRC), "gen": (0, R.DST)}, [("train", "gen"), ("gen", "train")],
@@ -210,7 +220,7 @@ def main() -> int:
                     failures.append(f"7B {name} shard {d}: {bad} mismatches (first {first})")
         dist.barrier()
         rr.close()
-    flag = torch.tensor([len(failures)], device="cuda")
+    flag = torch.tensor([len(failures)], device="cpu" if oversub else "cuda")
     dist.all_reduce(flag)
     for f in failures:
         print(f"rank {rank}: {f}", flush=True)

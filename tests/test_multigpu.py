@@ -35,3 +35,15 @@ def test_cross_gpu_bitexact(n_gpus, world):
     r = _torchrun(world, {"RR_FULL_7B": "1"})
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     assert f"dist_worker world={world}: OK" in r.stdout
+
+
+def test_world8_with_two_processes_per_gpu(n_gpus):
+    """The 8-rank code path (one plan device per rank, 8-way barriers, IPC
+    and relay/overlap flags among 8 processes) on a 4-GPU box: two ranks per
+    GPU, whose kernels time-slice. The pool has no 8-GPU boxes; this is the
+    closest hardware check of N=8 (correctness only, not speed)."""
+    if n_gpus != 4:
+        pytest.skip("runs on exactly 4 GPUs")
+    r = _torchrun(8, {"RR_FUZZ_CASES": "12"}, timeout=1500)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    assert "dist_worker world=8: OK" in r.stdout
