@@ -221,11 +221,22 @@ def run_b200(args) -> None:
     rank, world, local_rank = env_rank()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
+    # More ranks than GPUs is a correctness check of the N-rank code path
+    # only (two processes share a GPU and time-slice; NCCL refuses that, so
+    # gloo with host tensors carries the bench's own collectives). The line
+    # then says "oversubscribed" and is not a measurement.
+    gpus = torch.cuda.device_count()
+    oversub = world > gpus
+    local_rank = local_rank % gpus
+    coll = "cpu" if oversub else "cuda"
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     w = load_workload(args)
     if args.layers:
         from paper_2406_14088_b200.workloads import truncated
@@ -321,7 +332,7 @@ def run_b200(args) -> None:
     # replicas are local) plus every store that lands here (local stores and
     # incoming peer stores); peer stores leave through the links instead.
     ph_hbm = [e.bytes_read + e.bytes_written - e.wire_out + e.wire_in for e in rr.executors]
-    vals = torch.tensor([ms, written, read] + phase_ms + ph_wire + ph_hbm, dtype=torch.float64, device="cuda")
+    vals = torch.tensor([ms, written, read] + phase_ms + ph_wire + ph_hbm, dtype=torch.float64, device=coll)
     if dist:
         allv = [torch.zeros_like(vals) for _ in range(world)]
         dist.all_gather(allv, vals)
@@ -345,7 +356,7 @@ def run_b200(args) -> None:
         for d, b in rr.buffers[dname].items():
             m, _ = R.verify_shard(plans[i], R.DST, d, b.ptr, seed)
             bad += m
-    bad_t = torch.tensor([bad], dtype=torch.int64, device="cuda")
+    bad_t = torch.tensor([bad], dtype=torch.int64, device=coll)
     if dist:
         dist.all_reduce(bad_t)
     verified = int(bad_t.item()) == 0 and not timed_out
@@ -390,7 +401,7 @@ def run_b200(args) -> None:
         for i, (sname, dname) in enumerate(bind):
             for d, b in rr.buffers[dname].items():
                 e2e_bad += R.verify_shard(plans[i], R.DST, d, b.ptr, seed)[0]
-        ev = torch.tensor([e_ms, h2d, d2h, e2e_bad], dtype=torch.float64, device="cuda")
+        ev = torch.tensor([e_ms, h2d, d2h, e2e_bad], dtype=torch.float64, device=coll)
         if dist:
             mx = ev.clone()
             dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -491,6 +502,8 @@ def run_b200(args) -> None:
             "host_ms": {"plan_and_lower": round(plan_ms, 3), "allocate_and_bind": round(bind_ms, 1)},
             "verified": verified,
         }
+        if oversub:
+            line["oversubscribed"] = f"{world} ranks on {gpus} GPUs: correctness run, not a measurement"
         print(json.dumps(line), flush=True)
     rr.close()
     if dist:
