@@ -28,9 +28,11 @@ from .rlplan import ReallocPlan
 
 PUSH, PULL = 0, 1
 SRC, DST = 0, 1
-# Copy kernel used unless a caller picks one (rr_exec_set_kernel): the TMA
-# bulk ring, 4 x 16 KiB stages, 3 CTAs per SM (profiles/r01_sweep_kernels.txt).
-DEFAULT_KERNEL = None  # library default: TMA bulk ring, LDG/STG for small phases
+# Copy kernel unless a caller picks one (rr_exec_set_kernel): None keeps the
+# library default, the TMA bulk ring (4 x 16 KiB stages, 3 CTAs per SM;
+# profiles/r01_sweep_kernels.txt) with the LDG/STG kernel for plain phases
+# storing < 64 MiB (profiles/r01_launch_latency_n1.json).
+DEFAULT_KERNEL = None
 # ... and for flag-synchronised phases (rr_exec_set_flag_kernel): 3 x 16 KiB
 # stages, 4 CTAs per SM (profiles/r01_flag_kernel_sweep_n{2,4}.txt).
 DEFAULT_FLAG_KERNEL = 5
