@@ -136,3 +136,26 @@ def test_bench_config_workload_matches_the_preset():
     for a, b in zip(w.plans(BALANCED), ref.plans(BALANCED)):
         assert a.total_bytes == b.total_bytes and a.num_rects() == b.num_rects()
         assert [op.src for op in a.ops] == [op.src for op in b.ops]
+
+
+def test_realloc_plan_cli_replicated_kv_heads(tmp_path):
+    """kv_layout "replicate" in a realloc-plan config (DESIGN.md §3 G6): an
+    MQA model moved from one device to tp8 with replicated heads carries K/V
+    as their own payloads, and the plan JSON says so."""
+    cfg = json.load(open(os.path.join(os.path.dirname(__file__), "..", "examples", "llama7b_train_to_gen.json")))
+    cfg["model"] = {"name": "mqa", "hidden_size": 512, "intermediate_size": 1024, "num_layers": 2,
+                    "num_attention_heads": 8, "num_kv_heads": 1, "vocab_size": 1024, "max_position_embeddings": 256}
+    cfg["src"] = {"mesh": "trainer01:gpu[0-0]", "dp": 1, "tp": 1, "pp": 1}
+    cfg["dst"] = {"mesh": "trainer01", "dp": 1, "tp": 8, "pp": 1, "kv_layout": "replicate"}
+    p = tmp_path / "mqa.json"
+    p.write_text(json.dumps(cfg))
+    out = cli.build(json.load(open(p)))
+    assert out["dst"]["kv_layout"] == 1
+    parts = {op.get("part") for op in out["ops"]}
+    assert "kv" in parts and "no_kv" in parts
+    kv_ops = [op for op in out["ops"] if op.get("part") == "kv"]
+    assert len(kv_ops) == 1 and sorted(kv_ops[0]["dst"]) == list(range(1, 8))  # the one head, to every replica
+    cfg["dst"]["kv_layout"] = "sideways"
+    p.write_text(json.dumps(cfg))
+    with pytest.raises(cli.ConfigError, match="kv_layout"):
+        cli.build(json.load(open(p)))
