@@ -254,6 +254,9 @@ rr_status rr_exec_launch_offload(rr_exec* ex, int n_src, const int32_t* src_devi
                                  void* const* host_bufs, void* copy_stream, void* stream);
 /* Kernels one rr_exec_launch / rr_exec_launch_fanout issues (0..2 each). */
 rr_status rr_exec_kernel_count(const rr_exec* ex, int* phase0, int* phase1);
+/* Which kernels a phase launches: *ldst = 1 if the LDG/STG kernel runs,
+ * *bulk = the TMA bulk variant that runs (0 = none). */
+rr_status rr_exec_phase_kernels(const rr_exec* ex, int phase, int* ldst, int* bulk);
 /* Bytes entering / leaving this executor's host over links per launch. */
 rr_status rr_exec_wire(const rr_exec* ex, int64_t* wire_in, int64_t* wire_out);
 void rr_exec_destroy(rr_exec* ex);

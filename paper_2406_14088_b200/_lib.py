@@ -64,6 +64,7 @@ _SIGNATURES = {
     "rr_plan_relay_slots": (c_int, [_P, POINTER(c_int32), c_int64, c_int, c_int, POINTER(c_int64)]),
     "rr_exec_relay_timeouts": (c_int, [_P, POINTER(c_int64)]),
     "rr_exec_kernel_count": (c_int, [_P, POINTER(c_int), POINTER(c_int)]),
+    "rr_exec_phase_kernels": (c_int, [_P, c_int, POINTER(c_int), POINTER(c_int)]),
     "rr_mcast_supported": (c_int, [c_int, POINTER(c_int)]),
     "rr_mcast_create": (c_int, [c_int, c_size_t, c_int, POINTER(c_int), POINTER(c_size_t), POINTER(_P)]),
     "rr_mcast_import": (c_int, [c_int, c_int, c_size_t, c_int, POINTER(_P)]),

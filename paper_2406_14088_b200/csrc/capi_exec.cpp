@@ -18,6 +18,12 @@ using rr::capi::check_cuda;
 using rr::capi::guarded;
 using rr::capi::need;
 
+namespace {
+constexpr int64_t kDefaultChunk = int64_t{256} << 10;      // work-item size of large phases
+constexpr int64_t kSmallPhaseBytes = int64_t{64} << 20;    // below: LDG/STG kernel (phase_kernel)
+constexpr int64_t kMinSmallChunk = 4096;                   // 256 threads x one 16-byte load
+}  // namespace
+
 // ---------------------------------------------------------------------------
 // Executor object
 // ---------------------------------------------------------------------------
@@ -45,7 +51,7 @@ struct rr_exec {
   // thread, whereas the LDG/STG kernel spreads an item over 256 threads
   // (tiny BASELINE config: 16 vs 39 us, profiles/r01_launch_latency_n1.json).
   bool kernel_explicit = false;
-  int64_t small_phase_bytes = int64_t{64} << 20;
+  int64_t small_phase_bytes = kSmallPhaseBytes;
   int bulk_ctas = 0, flag_bulk_ctas = 0;
   unsigned int* d_sched = nullptr;  // dynamic work counter (see retire_cta)
   int64_t wire_in = 0, wire_out = 0;  // bytes crossing into / out of this host
@@ -154,6 +160,24 @@ void launch_phase(rr_exec* ex, const rr_exec::Phase& ph, void* stream, int ctas)
                "rr_bulk_kernel launch");
 }
 
+// A small plain phase runs on the LDG/STG kernel (phase_kernel) and is
+// latency-bound: it lasts as long as its largest item, and with 256 KiB items
+// most resident CTAs idle (tiny BASELINE config: 78 items for 1184 CTAs).
+// Re-cut it so that every resident CTA gets about one item, each a few
+// 16-byte loads per thread. Only when the caller left chunk_bytes at the
+// default; flag-synchronised phases keep the slot granularity every rank
+// agrees on.
+rr::ItemSet refine_small(rr::ItemSet set, const std::vector<rr::Job>& jobs, int phase, const rr::HostMap& hm,
+                         void* const* src_bufs, void* const* dst_bufs, int resident_ctas) {
+  if (set.items.empty() || set.written >= kSmallPhaseBytes) return set;
+  if (std::any_of(set.items.begin(), set.items.end(),
+                  [](const rr::CopyItem& it) { return it.wait_flag || it.signal_flag; }))
+    return set;
+  const int64_t chunk = std::max<int64_t>(kMinSmallChunk, (set.read / std::max(1, resident_ctas)) & ~int64_t{15});
+  if (chunk >= kDefaultChunk) return set;
+  return rr::build_items(jobs, phase, hm, src_bufs, dst_bufs, chunk);
+}
+
 }  // namespace
 
 rr_status rr_plan_work(const rr_plan* plan, int n_local, const int32_t* local, const int32_t* host_of, int mode,
@@ -196,7 +220,7 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
     int64_t chunk_bytes = options->chunk_bytes;
     need(mode == 0 || mode == 1, "mode must be 0 (push) or 1 (pull)");
     need(n_devices >= plan->cluster.device_count(), "buffer tables must cover every cluster device");
-    if (chunk_bytes <= 0) chunk_bytes = 256 << 10;
+    if (chunk_bytes <= 0) chunk_bytes = kDefaultChunk;
     need(chunk_bytes >= 16, "chunk_bytes too small");
     rr::HostMap hm = host_map(plan, n_local, local, options->host_of);
     if (options->mc_bufs) {
@@ -214,9 +238,16 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       hm.relay_chain = options->relay_chain != 0;
       hm.relay_star = options->overlap_fanout != 0;
     }
+    check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
+    int per_sm = 0, sms = 0;
+    check_cuda(rr::copy_max_ctas(&per_sm, &sms), "occupancy query");
     const auto jobs = rr::build_jobs(plan->lowered, hm, mode);
-    const auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes);
-    const auto b = rr::build_items(jobs, 1, hm, src_bufs, dst_bufs, chunk_bytes);
+    auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes);
+    auto b = rr::build_items(jobs, 1, hm, src_bufs, dst_bufs, chunk_bytes);
+    if (options->chunk_bytes <= 0) {
+      a = refine_small(std::move(a), jobs, 0, hm, src_bufs, dst_bufs, std::max(1, per_sm) * sms);
+      b = refine_small(std::move(b), jobs, 1, hm, src_bufs, dst_bufs, std::max(1, per_sm) * sms);
+    }
 
     auto ex = std::make_unique<rr_exec>();
     ex->cuda_device = cuda_device;
@@ -227,9 +258,6 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
     ex->fence_sys = (a.remote_stores || win || wout) ? 1 : 0;
     ex->wire_in = win;
     ex->wire_out = wout;
-    check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
-    int per_sm = 0, sms = 0;
-    check_cuda(rr::copy_max_ctas(&per_sm, &sms), "occupancy query");
     ex->default_ctas = std::max(1, per_sm) * sms;
     upload(a, ex->phase[0]);
     upload(b, ex->phase[1]);
@@ -266,6 +294,24 @@ rr_status rr_exec_kernel_count(const rr_exec* ex, int* phase0, int* phase1) {
   });
 }
 
+rr_status rr_exec_phase_kernels(const rr_exec* ex, int phase, int* ldst, int* bulk) {
+  return guarded([&] {
+    need(ex != nullptr && ldst != nullptr && bulk != nullptr, "null executor/output");
+    need(phase == 0 || phase == 1, "phase must be 0 or 1");
+    const auto& ph = ex->phase[phase];
+    *ldst = 0;
+    *bulk = 0;
+    if (ph.n == 0) return;
+    const int kernel = phase_kernel(ex, ph);
+    if (kernel == 0) {
+      *ldst = 1;
+      return;
+    }
+    *ldst = ph.n > ph.n_vec ? 1 : 0;
+    *bulk = ph.n_vec > 0 ? kernel : 0;
+  });
+}
+
 rr_status rr_exec_relay_timeouts(rr_exec* ex, int64_t* timeouts) {
   return guarded([&] {
     need(ex != nullptr, "null executor");
@@ -282,7 +328,7 @@ rr_status rr_plan_relay_slots(const rr_plan* plan, const int32_t* host_of, int64
     need(plan != nullptr && host_of != nullptr, "null plan/host table");
     rr::HostMap hm;
     for (int d = 0; d < plan->cluster.device_count(); ++d) hm.host.push_back(host_of[d]);
-    hm.relay_chunk = chunk_bytes > 0 ? chunk_bytes : (256 << 10);
+    hm.relay_chunk = chunk_bytes > 0 ? chunk_bytes : kDefaultChunk;
     hm.relay_chain = relay_chain != 0;
     hm.relay_star = overlap_fanout != 0;
     *slots = rr::relay_slots(plan->lowered, hm);

@@ -198,6 +198,12 @@ class Executor:
         check(lib.rr_exec_kernel_count(self._h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
 
+    def phase_kernels(self, phase: int = 0) -> Tuple[bool, int]:
+        """(LDG/STG kernel runs, TMA bulk variant that runs or 0) for a phase."""
+        a, b = ctypes.c_int(), ctypes.c_int()
+        check(lib.rr_exec_phase_kernels(self._h, phase, ctypes.byref(a), ctypes.byref(b)))
+        return bool(a.value), b.value
+
     def enable_onload(self, src_bytes: Dict[int, int], chunk_bytes: int = 256 << 20) -> None:
         """Prepare onload pipelining: the local source shards {device: bytes}
         are copied host->device in chunk_bytes pieces (in device order)."""

@@ -78,6 +78,38 @@ def test_tiny_baseline_config_bitexact(need_gpu):
             assert_same(got, oracle_cpu_realloc(w.model, src, dst, c, policy))
 
 
+@pytest.mark.parametrize("model,sp,dp", [
+    ("tiny", (1, 1, 2), (1, 2, 1)),        # BASELINE configs[0]: 3.4 MB, latency-bound
+    ("tiny", (1, 1, 2), (2, 1, 1)),        # tp -> pp
+    ("tiny", (1, 1, 4), (1, 4, 1)),        # 4-way all-gather, strided row-parallel rows
+    ("tiny_gqa", (2, 1, 2), (1, 1, 4)),    # pp + tp remap, k/v split
+])
+def test_small_phase_recut_bitexact(need_gpu, model, sp, dp):
+    """With the default chunk, a phase below the small-phase size is re-cut to
+    about one item per resident CTA (capi_exec.cpp refine_small); every byte
+    still lands exactly once and in place."""
+    m = MODELS["tiny"] if model == "tiny" else TINY_GQA
+    n = sp[0] * sp[1] * sp[2]
+    c = b200_cluster(max(n, 2))
+    src, dst = placement(n, *sp), placement(n, *dp)
+    plan = plan_param_realloc(m, src, dst, c, BALANCED)
+    vc = R.VirtualCluster(plan, 0)
+    try:
+        vc.fill_sources(3)
+        coarse = vc.executor(R.PUSH, 256 << 10, None)  # explicit chunk: no re-cut
+        fine = vc.executor(R.PUSH, 0, None)
+        assert fine.items > coarse.items, (fine.items, coarse.items)
+        assert fine.bytes_written == coarse.bytes_written and fine.bytes_read == coarse.bytes_read
+        fine.launch()
+        R.stream_sync()
+        got = {d: b.to_host() for d, b in vc.dst.items()}
+        coarse.close()
+        fine.close()
+    finally:
+        vc.free()
+    assert_same(got, expected(m, src, dst, c, seed=3))
+
+
 @pytest.mark.parametrize("sp,dp", [
     ((4, 1, 2, 2, 1), (1, 1, 8, 1, 1)),   # 34B-style: pp4 tp2 Megatron-grouped -> tp8 concat
     ((2, 1, 4, 2, 1), (1, 2, 4, 0, 0)),   # pipeline remap + fused -> separate

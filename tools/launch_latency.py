@@ -29,8 +29,10 @@ def main() -> None:
         vc = R.VirtualCluster(plan, 0)
         vc.fill_sources(1)
         stream = torch.cuda.current_stream()
-        for kernel in (0, 1, None):
-            ex = vc.executor(R.PUSH, 0, kernel)
+        # chunk 0 = library default (small phases re-cut to ~one item per
+        # resident CTA); 256 KiB = the fixed large-phase item size, for A/B
+        for chunk, kernel in ((0, 0), (0, 1), (0, None), (256 << 10, None)):
+            ex = vc.executor(R.PUSH, chunk, kernel)
             for _ in range(20):
                 ex.launch(stream)
             torch.cuda.synchronize()
@@ -60,7 +62,7 @@ def main() -> None:
                 ex.launch(stream)
             e.record(stream)
             torch.cuda.synchronize()
-            out[f"{name}/kernel{'-default' if kernel is None else kernel}"] = {"host_submit_us": round(host_us, 2),
+            out[f"{name}/kernel{'-default' if kernel is None else kernel}{'/chunk256k' if chunk else ''}"] = {"host_submit_us": round(host_us, 2),
                                             "single_event_us": round(sorted(singles)[len(singles) // 2], 2),
                                             "queued_gpu_us_per_launch": round(s.elapsed_time(e) * 1e3 / n, 2),
                                             "items": ex.items}
