@@ -8,6 +8,11 @@
 //   pf/A        base + cp.async.bulk.prefetch.L2 of the source A bytes ahead of
 //               the run being loaded (reads become early, non-blocking L2 fills)
 //   stEF        base with L2::evict_first on the stores
+//   dmaj/W      destination-major: the source is cut into W-byte slabs; work
+//               item i = (slab, destination, run), claimed in order, so one
+//               slab is stored to destination 0, then 1, ... and the DRAM
+//               sees about one write stream at a time; the slab is read from
+//               DRAM once and then hits L2
 // GB/s = algorithmic (read + 8 x write) bytes / time; best of 5.
 // Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tools/bcast_l2_probe tools/bcast_l2_probe.cu
 #include <cuda_runtime.h>
@@ -113,6 +118,47 @@ __global__ void __launch_bounds__(32) bc_run(const char* src, Dsts dsts, size_t 
   }
 }
 
+template <int S, int K>
+__global__ void __launch_bounds__(32) bc_dmaj(const char* src, Dsts dsts, size_t bytes, size_t slab,
+                                              unsigned int* ctr) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[S];
+  if (threadIdx.x) return;
+  for (int s = 0; s < S; ++s) mbar_init(&full[s]);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const size_t per_slab = slab / K;                       // runs per slab and destination
+  const size_t nitems = bytes / slab * 8 * per_slab;      // bytes is a multiple of slab
+  size_t issued = 0, done = 0;
+  size_t pos[S];
+  int dj[S];
+  size_t i = atomicAdd(ctr, 1u);
+  for (;;) {
+    while ((issued < S || issued - done < S - 1) && i < nitems) {
+      if (issued >= S) wait_read1();
+      const int s = issued % S;
+      const size_t sl = i / (8 * per_slab), rem = i % (8 * per_slab);
+      dj[s] = static_cast<int>(rem / per_slab);
+      pos[s] = sl * slab + (rem % per_slab) * K;
+      mbar_expect(&full[s], K);
+      bload(ring + s * K, src + pos[s], K, &full[s]);
+      ++issued;
+      i = atomicAdd(ctr, 1u);
+    }
+    if (done == issued) break;
+    const int s = done % S;
+    mbar_wait(&full[s], (done / S) & 1);
+    bstore(dsts.d[dj[s]] + pos[s], ring + s * K, K, 0);
+    commit();
+    ++done;
+  }
+  wait_all();
+  __threadfence();
+  if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+    atomicExch(ctr, 0u);
+    atomicExch(ctr + 1, 0u);
+  }
+}
+
 cudaEvent_t t0, t1;
 
 template <class F>
@@ -175,6 +221,20 @@ int main() {
     }
   }
   go("base", sms, 0, 0, 0);
+  auto dmaj = [&](auto kern, int smem, const char* tag, std::initializer_list<int> mults) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    for (int m : mults)
+      for (size_t w : {size_t(1) << 20, size_t(2) << 20, size_t(4) << 20}) {
+        const float ms = best_ms([&] { kern<<<sms * m, 32, smem>>>(s, d, sbo, w, ctr); });
+        std::printf("dmaj%s/%zuM ctas=%-4d %8.3f ms %8.1f GB/s (writes alone %7.1f GB/s)\n", tag, w >> 20, sms * m, ms,
+                    9.0 * sbo / (ms * 1e6), 8.0 * sbo / (ms * 1e6));
+        std::fflush(stdout);
+      }
+  };
+  dmaj(bc_dmaj<4, 16384>, 4 * 16384, "4x16k", {3});
+  dmaj(bc_dmaj<4, 8192>, 4 * 8192, "4x8k", {4, 6});
+  dmaj(bc_dmaj<2, 16384>, 2 * 16384, "2x16k", {4, 6});
+  dmaj(bc_dmaj<3, 8192>, 3 * 8192, "3x8k", {6, 8});
   unsigned char h[2] = {0, 0};
   CK(cudaMemcpy(&h[0], d.d[7] + sbo - 1, 1, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(&h[1], d.d[0], 1, cudaMemcpyDeviceToHost));
