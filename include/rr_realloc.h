@@ -209,7 +209,9 @@ rr_status rr_enable_peer(int cuda_device, int peer_device);
  *          destination copy (local relayout + NVLink peer stores, K1/K2).
  * mode 1 = PULL: a local destination loads from the (possibly remote)
  *          source and stores locally.
- * chunk_bytes: work-item granularity (0 = default 256 KiB). */
+ * chunk_bytes: work-item granularity. 0 = library default: 256 KiB, except
+ * that a plain phase too small for that is cut into ~16 items per resident
+ * bulk CTA (>= 32 KiB), or ~1 item per CTA below 64 MiB stored (>= 4 KiB). */
 rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices,
                          void* const* src_bufs, void* const* dst_bufs, int n_local,
                          const int32_t* local, const int32_t* host_of, int mode, int64_t chunk_bytes,

@@ -160,20 +160,30 @@ void launch_phase(rr_exec* ex, const rr_exec::Phase& ph, void* stream, int ctas)
                "rr_bulk_kernel launch");
 }
 
-// A small plain phase runs on the LDG/STG kernel (phase_kernel) and is
-// latency-bound: it lasts as long as its largest item, and with 256 KiB items
-// most resident CTAs idle (tiny BASELINE config: 78 items for 1184 CTAs).
-// Re-cut it so that every resident CTA gets about one item, each a few
-// 16-byte loads per thread. Only when the caller left chunk_bytes at the
-// default; flag-synchronised phases keep the slot granularity every rank
-// agrees on.
-rr::ItemSet refine_small(rr::ItemSet set, const std::vector<rr::Job>& jobs, int phase, const rr::HostMap& hm,
-                         void* const* src_bufs, void* const* dst_bufs, int resident_ctas) {
-  if (set.items.empty() || set.written >= kSmallPhaseBytes) return set;
+// Work-item size of a plain phase when the caller left chunk_bytes at the
+// default. Dynamic claiming balances the CTAs to within about one item, so
+// the tail of a phase is one item's worth of work:
+// - a small phase (LDG/STG kernel, phase_kernel) is latency-bound and lasts
+//   as long as its largest item; with 256 KiB items the tiny BASELINE plan
+//   had 78 items for 1184 resident CTAs. It is re-cut to about one item per
+//   resident CTA (>= 4 KiB: 256 threads x one 16-byte load);
+// - a larger phase gets at least kItemsPerBulkCta items per resident bulk CTA
+//   (>= 32 KiB per item): a 256 MiB data-transfer phase had 1024 items for
+//   444 CTAs, so its last wave ran a third full.
+// Flag-synchronised phases keep the slot granularity every rank agrees on.
+constexpr int64_t kItemsPerBulkCta = 16;
+constexpr int64_t kMinBulkChunk = int64_t{32} << 10;
+
+rr::ItemSet refine_chunk(rr::ItemSet set, const std::vector<rr::Job>& jobs, int phase, const rr::HostMap& hm,
+                         void* const* src_bufs, void* const* dst_bufs, int ldst_ctas, int bulk_ctas) {
+  if (set.items.empty()) return set;
   if (std::any_of(set.items.begin(), set.items.end(),
                   [](const rr::CopyItem& it) { return it.wait_flag || it.signal_flag; }))
     return set;
-  const int64_t chunk = std::max<int64_t>(kMinSmallChunk, (set.read / std::max(1, resident_ctas)) & ~int64_t{15});
+  const int64_t chunk =
+      set.written < kSmallPhaseBytes
+          ? std::max<int64_t>(kMinSmallChunk, (set.read / std::max(1, ldst_ctas)) & ~int64_t{15})
+          : std::max<int64_t>(kMinBulkChunk, (set.read / (kItemsPerBulkCta * std::max(1, bulk_ctas))) & ~int64_t{15});
   if (chunk >= kDefaultChunk) return set;
   return rr::build_items(jobs, phase, hm, src_bufs, dst_bufs, chunk);
 }
@@ -245,8 +255,11 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
     auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes);
     auto b = rr::build_items(jobs, 1, hm, src_bufs, dst_bufs, chunk_bytes);
     if (options->chunk_bytes <= 0) {
-      a = refine_small(std::move(a), jobs, 0, hm, src_bufs, dst_bufs, std::max(1, per_sm) * sms);
-      b = refine_small(std::move(b), jobs, 1, hm, src_bufs, dst_bufs, std::max(1, per_sm) * sms);
+      int bulk_ctas = 0;
+      check_cuda(rr::launch_bulk(1, nullptr, 0, 0, 0, nullptr, &bulk_ctas, nullptr), "bulk occupancy");
+      const int ldst_ctas = std::max(1, per_sm) * sms;
+      a = refine_chunk(std::move(a), jobs, 0, hm, src_bufs, dst_bufs, ldst_ctas, bulk_ctas);
+      b = refine_chunk(std::move(b), jobs, 1, hm, src_bufs, dst_bufs, ldst_ctas, bulk_ctas);
     }
 
     auto ex = std::make_unique<rr_exec>();
