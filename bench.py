@@ -481,7 +481,7 @@ def run_b200(args) -> None:
                        "relay_phases": rr.relay_phases, "overlap_phases": rr.overlap_phases,
                        "copy_kernel": kname, "bulk_variants": {"plain": 1 if kernel is None else kernel,
                                                                       "flag_synchronised": flag_kernel},
-                       "chunk_kib": args.chunk_kib or "256 (phases < 64 MiB: ~one item per resident CTA)", "ctas": args.ctas or "resident capacity",
+                       "chunk_kib": args.chunk_kib or "library default (256; smaller for phases too small for it)", "ctas": args.ctas or "resident capacity",
                        "l2": "inputs larger than L2 (multi-GB shards); no flush needed",
                        "weights": "hash-initialised bf16 (seed 1), verified after timing"},
             "phase_ms": [round(float(x), 4) for x in ph_ms_all.max(axis=0)],
