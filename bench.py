@@ -315,6 +315,10 @@ def run_b200(args) -> None:
     torch.cuda.synchronize()
     clock_info = clocks.stop()
     ms = t0.elapsed_time(t1) / args.steps
+    # per-step spread on this rank: step k runs from its first event to step k+1's
+    starts = [evs[k][0][0] for k in range(args.steps)]
+    step_ms = sorted([starts[k].elapsed_time(starts[k + 1]) for k in range(args.steps - 1)] +
+                     [starts[-1].elapsed_time(t1)])
     phase_ms = [sum(evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(args.steps)) / args.steps
                 for i in range(len(plans))]
     timed_out = (rr.barrier.timed_out() or rr.relay_timeouts() > 0) if world > 1 else False
@@ -485,6 +489,8 @@ def run_b200(args) -> None:
                        "l2": "inputs larger than L2 (multi-GB shards); no flush needed",
                        "weights": "hash-initialised bf16 (seed 1), verified after timing"},
             "phase_ms": [round(float(x), 4) for x in ph_ms_all.max(axis=0)],
+            "step_ms": {"median": round(step_ms[len(step_ms) // 2], 4), "best": round(step_ms[0], 4),
+                        "worst": round(step_ms[-1], 4), "of": "rank 0's timed steps (CUDA events)"},
             "nvlink_gbs_per_gpu": round(nvl, 2),
             "bytes_per_step": int(total_written),
             "roofline": roof,
