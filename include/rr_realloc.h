@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define RR_ABI_VERSION 2 /* 2: rr_placement.kv_layout, rr_shard.part */
+#define RR_ABI_VERSION 3 /* 2: rr_placement.kv_layout, rr_shard.part; 3: rr_exec_options.ce_min_run_bytes */
 
 typedef enum {
   RR_OK = 0,
@@ -282,11 +282,25 @@ typedef struct {
   void* const* relay_flags;
   int32_t relay_chain;    /* with relay_flags: chain relay for >= 2 remote hosts */
   int32_t overlap_fanout; /* with relay_flags: per-chunk in-host fan-out inside phase 0 */
+  /* Copy-engine runs (push mode): where a local source shard and a remote
+   * destination shard hold the same blocks at the same relative offsets over
+   * >= this many bytes, and the plan moves (>= 98% of) that range between
+   * them, phase 0 moves it with one copy-engine copy (cudaMemcpyAsync on a
+   * side stream, forked from and joined back into the launch stream) instead
+   * of SM peer stores. 0 = default (256 MiB), < 0 = never. */
+  int64_t ce_min_run_bytes;
 } rr_exec_options;
 /* Length of the relay flag array for this host map, chunk size and scheme
  * switches (identical on every rank). */
 rr_status rr_plan_relay_slots(const rr_plan* plan, const int32_t* host_of, int64_t chunk_bytes, int relay_chain,
                               int overlap_fanout, int64_t* slots);
+/* Copy-engine runs a push executor driving `local` (with `host_of`) would
+ * issue, host only: 5 int64 per run {src device, dst device, src byte
+ * offset, dst byte offset, bytes}; pass out5 = NULL to query *n. */
+rr_status rr_plan_ce_runs(const rr_plan* plan, int n_local, const int32_t* local, const int32_t* host_of,
+                          int64_t min_run_bytes, int64_t* out5, int cap, int* n);
+/* Copy-engine runs phase 0 issues (see rr_exec_options.ce_min_run_bytes). */
+rr_status rr_exec_ce_runs(const rr_exec* ex, int* n_runs, int64_t* bytes);
 /* Relay waits that timed out (bounded spins) since the executor was created. */
 rr_status rr_exec_relay_timeouts(rr_exec* ex, int64_t* timeouts);
 rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices, void* const* src_bufs,

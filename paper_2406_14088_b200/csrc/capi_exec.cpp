@@ -22,6 +22,10 @@ namespace {
 constexpr int64_t kDefaultChunk = int64_t{256} << 10;      // work-item size of large phases
 constexpr int64_t kSmallPhaseBytes = int64_t{64} << 20;    // below: LDG/STG kernel (phase_kernel)
 constexpr int64_t kMinSmallChunk = 4096;                   // 256 threads x one 16-byte load
+// Copy-engine runs: a whole copy of >= 256 MiB over NVLink reaches 764-780
+// GB/s against ~700-716 for SM stores, pairwise at 2 and 4 GPUs; at 64 MiB
+// the engine's per-copy cost already eats the gain (profiles/r01_ce_probe_*).
+constexpr int64_t kDefaultCeRunBytes = int64_t{256} << 20;
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -74,6 +78,18 @@ struct rr_exec {
   std::vector<Chunk> chunks;
   std::vector<cudaEvent_t> events;
 
+  // Copy-engine runs of phase 0 (rr::CeRun): issued on ce_stream, forked
+  // from and joined back into the launching stream around the kernels.
+  struct CeCopy {
+    void* dst;
+    const void* src;
+    size_t bytes;
+  };
+  std::vector<CeCopy> ce;
+  int64_t ce_bytes = 0;
+  cudaStream_t ce_stream = nullptr;
+  cudaEvent_t ce_fork = nullptr, ce_join = nullptr;
+
   rr_exec() = default;
   rr_exec(const rr_exec&) = delete;
   rr_exec& operator=(const rr_exec&) = delete;
@@ -85,6 +101,9 @@ struct rr_exec {
     if (d_sched) cudaFree(d_sched);
     if (d_onload) cudaFree(d_onload);
     for (auto e : events) cudaEventDestroy(e);
+    if (ce_fork) cudaEventDestroy(ce_fork);
+    if (ce_join) cudaEventDestroy(ce_join);
+    if (ce_stream) cudaStreamDestroy(ce_stream);
   }
 };
 
@@ -175,7 +194,8 @@ constexpr int64_t kItemsPerBulkCta = 16;
 constexpr int64_t kMinBulkChunk = int64_t{32} << 10;
 
 rr::ItemSet refine_chunk(rr::ItemSet set, const std::vector<rr::Job>& jobs, int phase, const rr::HostMap& hm,
-                         void* const* src_bufs, void* const* dst_bufs, int ldst_ctas, int bulk_ctas) {
+                         void* const* src_bufs, void* const* dst_bufs, int ldst_ctas, int bulk_ctas,
+                         const std::vector<rr::CeRun>* ce) {
   if (set.items.empty()) return set;
   if (std::any_of(set.items.begin(), set.items.end(),
                   [](const rr::CopyItem& it) { return it.wait_flag || it.signal_flag; }))
@@ -185,7 +205,52 @@ rr::ItemSet refine_chunk(rr::ItemSet set, const std::vector<rr::Job>& jobs, int 
           ? std::max<int64_t>(kMinSmallChunk, (set.read / std::max(1, ldst_ctas)) & ~int64_t{15})
           : std::max<int64_t>(kMinBulkChunk, (set.read / (kItemsPerBulkCta * std::max(1, bulk_ctas))) & ~int64_t{15});
   if (chunk >= kDefaultChunk) return set;
-  return rr::build_items(jobs, phase, hm, src_bufs, dst_bufs, chunk);
+  return rr::build_items(jobs, phase, hm, src_bufs, dst_bufs, chunk, ce);
+}
+
+// Copy-engine runs for a push executor: for every (local source, remote
+// destination) pair of a plain phase-0 job, the maximal ranges where the two
+// shard layouts coincide (rr::matching_runs), kept when >= min_bytes and when
+// at least 98% of the range is bytes this pair is planned to move (so the
+// engine does not carry data the destination gets elsewhere, e.g. locally).
+std::vector<rr::CeRun> ce_runs(rr_plan* plan, const std::vector<rr::Job>& jobs, const rr::HostMap& hm,
+                               int64_t min_bytes) {
+  std::map<std::pair<DeviceId, DeviceId>, std::vector<const rlplan::CopyRect*>> pairs;
+  for (const auto& j : jobs) {
+    if (j.phase != 0 || j.src_is_dst_buffer || j.multicast || j.relay_wait || j.relay_signal) continue;
+    for (DeviceId d : j.dsts)
+      if (hm.host[static_cast<size_t>(d)] != hm.me)
+        for (const auto& r : j.op->rects) pairs[{j.src, d}].push_back(&r);
+  }
+  std::vector<rr::CeRun> out;
+  for (const auto& [sd, rects] : pairs) {
+    for (const auto& u : rr::matching_runs(plan->layout(0, sd.first), plan->layout(1, sd.second), sd.first,
+                                           sd.second, min_bytes)) {
+      int64_t planned = 0;
+      for (const rlplan::CopyRect* r : rects)
+        if (r->dst_off >= u.dst_off && rr::rect_dst_end(*r) <= u.dst_off + u.bytes) planned += rr::rect_bytes(*r);
+      if (planned * 50 >= u.bytes * 49) out.push_back(u);
+    }
+  }
+  return out;
+}
+
+// Copy-engine runs: start them on ce_stream once the work already queued on
+// `after` (or, with an event, that event) is done; join them back into
+// `into` so that whatever follows there (barrier, next phase) sees them.
+void ce_issue(rr_exec* ex, cudaStream_t after, cudaEvent_t after_event = nullptr) {
+  if (after_event == nullptr) {
+    check_cuda(cudaEventRecord(ex->ce_fork, after), "cudaEventRecord(ce fork)");
+    after_event = ex->ce_fork;
+  }
+  check_cuda(cudaStreamWaitEvent(ex->ce_stream, after_event, 0), "cudaStreamWaitEvent(ce fork)");
+  for (const auto& c : ex->ce)
+    check_cuda(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "copy-engine run");
+}
+
+void ce_join(rr_exec* ex, cudaStream_t into) {
+  check_cuda(cudaEventRecord(ex->ce_join, ex->ce_stream), "cudaEventRecord(ce join)");
+  check_cuda(cudaStreamWaitEvent(into, ex->ce_join, 0), "cudaStreamWaitEvent(ce join)");
 }
 
 }  // namespace
@@ -207,6 +272,29 @@ rr_status rr_plan_work(const rr_plan* plan, int n_local, const int32_t* local, c
   });
 }
 
+rr_status rr_plan_ce_runs(const rr_plan* plan, int n_local, const int32_t* local, const int32_t* host_of,
+                          int64_t min_run_bytes, int64_t* out5, int cap, int* n) {
+  return guarded([&] {
+    need(plan != nullptr && n != nullptr, "null plan/output");
+    need(min_run_bytes > 0, "min_run_bytes must be positive");
+    const rr::HostMap hm = host_map(plan, n_local, local, host_of);
+    const auto jobs = rr::build_jobs(plan->lowered, hm, 0);
+    const auto runs = ce_runs(const_cast<rr_plan*>(plan), jobs, hm, min_run_bytes);
+    *n = static_cast<int>(runs.size());
+    if (out5 == nullptr) return;
+    need(cap >= *n, "output table too small");
+    for (size_t i = 0; i < runs.size(); ++i) {
+      const auto& u = runs[i];
+      int64_t* o = out5 + 5 * i;
+      o[0] = u.src;
+      o[1] = u.dst;
+      o[2] = u.src_off;
+      o[3] = u.dst_off;
+      o[4] = u.bytes;
+    }
+  });
+}
+
 rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, void* const* src_bufs,
                          void* const* dst_bufs, int n_local, const int32_t* local, const int32_t* host_of,
                          int mode, int64_t chunk_bytes, rr_exec** out) {
@@ -218,6 +306,7 @@ rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, vo
   opt.relay_flags = nullptr;
   opt.relay_chain = 0;
   opt.overlap_fanout = 0;
+  opt.ce_min_run_bytes = 0;
   return rr_exec_create_ex(plan, cuda_device, n_devices, src_bufs, dst_bufs, n_local, local, &opt, out);
 }
 
@@ -252,14 +341,18 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
     int per_sm = 0, sms = 0;
     check_cuda(rr::copy_max_ctas(&per_sm, &sms), "occupancy query");
     const auto jobs = rr::build_jobs(plan->lowered, hm, mode);
-    auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes);
+    const int64_t ce_min = options->ce_min_run_bytes == 0 ? kDefaultCeRunBytes : options->ce_min_run_bytes;
+    const std::vector<rr::CeRun> runs =
+        (mode == 0 && ce_min > 0 && src_bufs && dst_bufs) ? ce_runs(const_cast<rr_plan*>(plan), jobs, hm, ce_min)
+                                                          : std::vector<rr::CeRun>{};
+    auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes, &runs);
     auto b = rr::build_items(jobs, 1, hm, src_bufs, dst_bufs, chunk_bytes);
     if (options->chunk_bytes <= 0) {
       int bulk_ctas = 0;
       check_cuda(rr::launch_bulk(1, nullptr, 0, 0, 0, nullptr, &bulk_ctas, nullptr), "bulk occupancy");
       const int ldst_ctas = std::max(1, per_sm) * sms;
-      a = refine_chunk(std::move(a), jobs, 0, hm, src_bufs, dst_bufs, ldst_ctas, bulk_ctas);
-      b = refine_chunk(std::move(b), jobs, 1, hm, src_bufs, dst_bufs, ldst_ctas, bulk_ctas);
+      a = refine_chunk(std::move(a), jobs, 0, hm, src_bufs, dst_bufs, ldst_ctas, bulk_ctas, &runs);
+      b = refine_chunk(std::move(b), jobs, 1, hm, src_bufs, dst_bufs, ldst_ctas, bulk_ctas, nullptr);
     }
 
     auto ex = std::make_unique<rr_exec>();
@@ -274,6 +367,16 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
     ex->default_ctas = std::max(1, per_sm) * sms;
     upload(a, ex->phase[0]);
     upload(b, ex->phase[1]);
+    for (const auto& u : runs) {
+      ex->ce.push_back({static_cast<char*>(dst_bufs[u.dst]) + u.dst_off, static_cast<const char*>(src_bufs[u.src]) + u.src_off,
+                        static_cast<size_t>(u.bytes)});
+      ex->ce_bytes += u.bytes;
+    }
+    if (!ex->ce.empty()) {
+      check_cuda(cudaStreamCreateWithFlags(&ex->ce_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      check_cuda(cudaEventCreateWithFlags(&ex->ce_fork, cudaEventDisableTiming), "cudaEventCreate");
+      check_cuda(cudaEventCreateWithFlags(&ex->ce_join, cudaEventDisableTiming), "cudaEventCreate");
+    }
     ex->phase0_host = a;
     ex->src_bases.assign(static_cast<size_t>(n_devices), nullptr);
     for (int d = 0; d < n_devices; ++d) ex->src_bases[static_cast<size_t>(d)] = src_bufs ? src_bufs[d] : nullptr;
@@ -290,7 +393,11 @@ rr_status rr_exec_launch(rr_exec* ex, void* stream, int ctas) {
   return guarded([&] {
     need(ex != nullptr, "null executor");
     ++ex->epoch;  // every rank launches phase 0 the same number of times
+    auto st = static_cast<cudaStream_t>(stream);
+    check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
+    if (!ex->ce.empty()) ce_issue(ex, st);
     launch_phase(ex, ex->phase[0], stream, ctas);
+    if (!ex->ce.empty()) ce_join(ex, st);
   });
 }
 
@@ -322,6 +429,14 @@ rr_status rr_exec_phase_kernels(const rr_exec* ex, int phase, int* ldst, int* bu
     }
     *ldst = ph.n > ph.n_vec ? 1 : 0;
     *bulk = ph.n_vec > 0 ? kernel : 0;
+  });
+}
+
+rr_status rr_exec_ce_runs(const rr_exec* ex, int* n_runs, int64_t* bytes) {
+  return guarded([&] {
+    need(ex != nullptr && n_runs != nullptr && bytes != nullptr, "null executor/output");
+    *n_runs = static_cast<int>(ex->ce.size());
+    *bytes = ex->ce_bytes;
   });
 }
 
@@ -393,8 +508,8 @@ rr_status rr_exec_stats(const rr_exec* ex, int phase, int64_t* items, int64_t* w
     need(phase == 0 || phase == 1, "phase must be 0 or 1");
     const auto& ph = ex->phase[phase];
     *items = ph.n;
-    *written = ph.written;
-    *read = ph.read;
+    *written = ph.written + (phase == 0 ? ex->ce_bytes : 0);
+    *read = ph.read + (phase == 0 ? ex->ce_bytes : 0);
   });
 }
 
@@ -504,6 +619,10 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
       ph.n_vec = sg.n_vec;
       ph.flagged = ex->phase[0].flagged;
       launch_phase(ex, ph, stream, ctas);
+    }
+    if (!ex->ce.empty()) {  // the runs read whole source ranges: after the last chunk
+      ce_issue(ex, ks, ex->events.empty() ? nullptr : ex->events.back());
+      ce_join(ex, ks);
     }
   });
 }

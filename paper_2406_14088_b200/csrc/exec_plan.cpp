@@ -9,6 +9,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 
 namespace rr {
 
@@ -308,7 +309,39 @@ void host_wire_bytes(const std::vector<LoweredOp>& ops, const HostMap& hm, int64
   *out = o;
 }
 
+std::vector<CeRun> matching_runs(const rlplan::ShardLayout& s, const rlplan::ShardLayout& d, DeviceId sd,
+                                 DeviceId dd, int64_t min_bytes) {
+  using Key = std::tuple<int, rlplan::Count, rlplan::Count, rlplan::Count, rlplan::Count>;
+  const auto key = [](const rlplan::TensorBlock& b) { return Key{b.tensor, b.r0, b.r1, b.c0, b.c1}; };
+  const auto bytes = [](const rlplan::TensorBlock& b) { return (b.r1 - b.r0) * (b.c1 - b.c0) * 2; };  // bf16 (G10)
+  std::map<Key, size_t> where;
+  for (size_t k = 0; k < d.blocks.size(); ++k) where.emplace(key(d.blocks[k]), k);
+  std::vector<CeRun> out;
+  for (size_t i = 0; i < s.blocks.size();) {
+    const auto it = where.find(key(s.blocks[i]));
+    if (it == where.end()) {
+      ++i;
+      continue;
+    }
+    size_t j = it->second;
+    const int64_t s0 = s.blocks[i].offset, d0 = d.blocks[j].offset;
+    int64_t end = s0 + bytes(s.blocks[i]);
+    for (++i, ++j; i < s.blocks.size() && j < d.blocks.size() && key(s.blocks[i]) == key(d.blocks[j]) &&
+                   s.blocks[i].offset - s0 == d.blocks[j].offset - d0;
+         ++i, ++j)
+      end = s.blocks[i].offset + bytes(s.blocks[i]);
+    if (end - s0 >= min_bytes) out.push_back({sd, dd, s0, d0, end - s0});
+  }
+  return out;
+}
+
 namespace {
+
+bool ce_covered(const std::vector<CeRun>& runs, DeviceId src, DeviceId dst, const CopyRect& r) {
+  for (const auto& u : runs)
+    if (u.src == src && u.dst == dst && r.dst_off >= u.dst_off && rect_dst_end(r) <= u.dst_off + u.bytes) return true;
+  return false;
+}
 
 // An item plus where it reads from (for onload pipelining).
 struct Tagged {
@@ -382,7 +415,7 @@ uint64_t base_of(void* const* bufs, DeviceId d, const char* what) {
 }  // namespace
 
 ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, void* const* src_bufs,
-                    void* const* dst_bufs, int64_t chunk_bytes) {
+                    void* const* dst_bufs, int64_t chunk_bytes, const std::vector<CeRun>* ce) {
   ItemSet acc;
   std::vector<std::vector<Tagged>> streams;
   const bool accounting = src_bufs == nullptr;
@@ -392,8 +425,10 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
                                            : base_of(src_bufs, j.src, "source");
     for (size_t g = 0; g < j.dsts.size(); g += kMaxFan) {
       std::vector<uint64_t> dsts;
+      std::vector<DeviceId> devs;  // parallel to dsts
       const bool mc0 = j.multicast && g == 0;
       for (size_t k = g; k < std::min(j.dsts.size(), g + kMaxFan); ++k) {
+        devs.push_back(j.dsts[k]);
         if (mc0 && k == 0) {
           dsts.push_back(accounting ? 0 : j.mc_base);
           acc.remote_stores = true;
@@ -406,14 +441,26 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
       int64_t relay_slot = j.relay_base;
       if ((j.relay_wait || j.relay_signal) && j.dsts.size() > static_cast<size_t>(kMaxFan))
         throw rlplan::ValidationError("relay job with more than kMaxFan destinations");
+      // Copy-engine runs: plain jobs that read a real source shard
+      const bool ce_job = ce && !ce->empty() && phase == 0 && !mc0 && !j.src_is_dst_buffer && !j.relay_wait &&
+                          !j.relay_signal;
+      std::vector<uint64_t> kept;
       for (CopyRect r : j.op->rects) {
         if (j.src_is_dst_buffer) {  // fan-out reads the leader's copy: destination geometry
           r.src_off = r.dst_off;
           r.src_pitch = r.dst_pitch;
         }
+        const std::vector<uint64_t>* to = &dsts;
+        if (ce_job) {
+          kept.clear();
+          for (size_t k = 0; k < dsts.size(); ++k)
+            if (!ce_covered(*ce, j.src, devs[k], r)) kept.push_back(dsts[k]);
+          if (kept.empty()) continue;
+          if (kept.size() != dsts.size()) to = &kept;
+        }
         // Same-address copies (identical placement and buffers) are no-ops.
-        if (!accounting && !mc0 && !j.relay_wait && !j.relay_signal && dsts.size() == 1 &&
-            s + static_cast<uint64_t>(r.src_off) == dsts[0] + static_cast<uint64_t>(r.dst_off))
+        if (!accounting && !mc0 && !j.relay_wait && !j.relay_signal && to->size() == 1 &&
+            s + static_cast<uint64_t>(r.src_off) == (*to)[0] + static_cast<uint64_t>(r.dst_off))
           continue;
         if (j.relay_wait || j.relay_signal) {
           // relay pieces are cut at the slot granularity every rank agrees on
@@ -427,7 +474,7 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
           add_rect(streams.back(), acc, s, dsts, r, hm.relay_chunk, mc0, j.src, j.src_is_dst_buffer, tags);
           continue;
         }
-        add_rect(streams.back(), acc, s, dsts, r, chunk_bytes, mc0, j.src, j.src_is_dst_buffer);
+        add_rect(streams.back(), acc, s, *to, r, chunk_bytes, mc0, j.src, j.src_is_dst_buffer);
       }
     }
   }

@@ -66,8 +66,31 @@ void host_wire_bytes(const std::vector<rlplan::LoweredOp>& ops, const HostMap& h
 
 int64_t rect_bytes(const rlplan::CopyRect& r);
 
+// A contiguous byte range moved whole by a copy engine from a source shard
+// (src device, source placement) into a destination shard (dst device,
+// destination placement): both layouts hold the same blocks there at the
+// same relative offsets, so byte x of the source range is byte x of the
+// destination range. It replaces the SM items of every rect whose
+// destination extent it contains, for that destination.
+struct CeRun {
+  rlplan::DeviceId src = -1, dst = -1;
+  int64_t src_off = 0, dst_off = 0, bytes = 0;
+};
+
+// Maximal runs (>= min_bytes) between source layout `s` and destination
+// layout `d` whose blocks match one to one (same tensor rectangle, same
+// offset relative to the run start).
+std::vector<CeRun> matching_runs(const rlplan::ShardLayout& s, const rlplan::ShardLayout& d, rlplan::DeviceId sd,
+                                 rlplan::DeviceId dd, int64_t min_bytes);
+
+// Byte extent [first, last) a rect writes in its destination shard.
+inline int64_t rect_dst_end(const rlplan::CopyRect& r) {
+  return r.dst_off + (r.rows - 1) * r.dst_pitch + r.row_bytes;
+}
+
 // Items of one phase, chunked and interleaved across jobs; 16-byte items
-// first, then 2-byte items.
+// first, then 2-byte items. `ce` (may be null): runs whose (rect,
+// destination) pairs are left out of the items.
 struct ItemSet {
   std::vector<CopyItem> items;
   int n_vec = 0;
@@ -83,6 +106,6 @@ struct ItemSet {
 // Resolve jobs of `phase` into items. src_bufs/dst_bufs are indexed by plan
 // device; nullptr tables mean "accounting only" (addresses left at offsets).
 ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, void* const* src_bufs,
-                    void* const* dst_bufs, int64_t chunk_bytes);
+                    void* const* dst_bufs, int64_t chunk_bytes, const std::vector<CeRun>* ce = nullptr);
 
 }  // namespace rr

@@ -371,6 +371,19 @@ class ReallocPlan:
         keys = ("read", "written", "fanout_read", "fanout_written", "wire_in", "wire_out")
         return dict(zip(keys, out))
 
+    def ce_runs(self, local: Sequence[int], host_of: Optional[Sequence[int]] = None,
+                min_run_bytes: int = 256 << 20) -> List[Tuple[int, int, int, int, int]]:
+        """Copy-engine runs a push executor driving `local` would issue (host
+        only): (src device, dst device, src offset, dst offset, bytes)."""
+        arr = (ctypes.c_int32 * max(1, len(local)))(*local)
+        n = self.cluster.device_count()
+        hosts = (ctypes.c_int32 * n)(*host_of) if host_of is not None else None
+        cnt = ctypes.c_int()
+        check(lib.rr_plan_ce_runs(self._h, len(local), arr, hosts, min_run_bytes, None, 0, ctypes.byref(cnt)))
+        out = (ctypes.c_int64 * (5 * max(1, cnt.value)))()
+        check(lib.rr_plan_ce_runs(self._h, len(local), arr, hosts, min_run_bytes, out, cnt.value, ctypes.byref(cnt)))
+        return [tuple(out[5 * i:5 * i + 5]) for i in range(cnt.value)]
+
     def devices(self, side: int) -> List[int]:
         p = self.src if side == 0 else self.dst
         return p.mesh.devices(self.cluster)

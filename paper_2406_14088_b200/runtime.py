@@ -143,7 +143,7 @@ class Executor:
                  local: Iterable[int], mode: int = PUSH, chunk_bytes: int = 0,
                  host_of: Optional[Sequence[int]] = None, mc_ptrs: Optional[Dict[int, int]] = None,
                  relay_flags: Optional[Dict[int, int]] = None, relay_chain: bool = True,
-                 overlap_fanout: bool = False):
+                 overlap_fanout: bool = False, ce_min_run_bytes: int = 0):
         n = plan.cluster.device_count()
         self.plan = plan
         sp, dp = (ctypes.c_void_p * n)(), (ctypes.c_void_p * n)()
@@ -164,7 +164,8 @@ class Executor:
             rfl = (ctypes.c_void_p * n)()
             for d, p in relay_flags.items():
                 rfl[d] = p
-        opt = RrExecOptions(mode, chunk_bytes, hosts, mcs, rfl, int(relay_chain), int(overlap_fanout))
+        opt = RrExecOptions(mode, chunk_bytes, hosts, mcs, rfl, int(relay_chain), int(overlap_fanout),
+                            ce_min_run_bytes)
         h = ctypes.c_void_p()
         check(lib.rr_exec_create_ex(plan.handle, cuda_device, n, sp, dp, len(loc), arr, ctypes.byref(opt),
                                     ctypes.byref(h)))
@@ -197,6 +198,12 @@ class Executor:
         a, b = ctypes.c_int(), ctypes.c_int()
         check(lib.rr_exec_kernel_count(self._h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
+
+    def ce_runs(self) -> Tuple[int, int]:
+        """(copy-engine runs, their bytes) that launch() issues beside the kernels."""
+        n, b = ctypes.c_int(), ctypes.c_int64()
+        check(lib.rr_exec_ce_runs(self._h, ctypes.byref(n), ctypes.byref(b)))
+        return n.value, b.value
 
     def phase_kernels(self, phase: int = 0) -> Tuple[bool, int]:
         """(LDG/STG kernel runs, TMA bulk variant that runs or 0) for a phase."""
@@ -486,7 +493,7 @@ class RankRealloc:
                  bind: Sequence[Tuple[str, str]], rank: int, world: int, cuda_device: int, group=None,
                  mode: int = PUSH, kernel: Optional[int] = DEFAULT_KERNEL, hierarchical: bool = True,
                  multicast: Sequence[str] = (), relay=False, overlap: bool = False,
-                 flag_kernel: int = DEFAULT_FLAG_KERNEL, chunk_bytes: int = 0):
+                 flag_kernel: int = DEFAULT_FLAG_KERNEL, chunk_bytes: int = 0, ce_min_run_bytes: int = 0):
         """``multicast`` names shard sets whose per-GPU leader shards (the
         lowest-id plan device of the set on each GPU) are members of one NVLS
         multicast object: a payload bound for every GPU is then stored once
@@ -617,7 +624,8 @@ class RankRealloc:
                                            self.local, mode, chunk_bytes, host_of=host_of if hierarchical else None,
                                            mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_tables.get(pi),
                                            relay_chain=pi in self.relay_phases,
-                                           overlap_fanout=pi in self.overlap_phases))
+                                           overlap_fanout=pi in self.overlap_phases,
+                                           ce_min_run_bytes=ce_min_run_bytes))
             if kernel is not None:
                 self.executors[-1].set_kernel(kernel)
             self.executors[-1].set_flag_kernel(flag_kernel)

@@ -167,6 +167,7 @@ def main() -> int:
     rng = random.Random(int(os.environ.get("RR_FUZZ_SEED", "2406")))
     fuzz_models = [TINY_GQA, dataclasses.replace(TINY_GQA, name="tiny_mqa", num_attention_heads=8, num_kv_heads=1,
                                                  num_layers=3)]
+    ce_cases = 0  # fuzz cases in which this rank issued copy-engine runs
     for i in range(int(os.environ.get("RR_FUZZ_CASES", "24"))):
         fm = fuzz_models[i % 2]
         src, dst = random_placement(rng, fm), random_placement(rng, fm)
@@ -176,10 +177,12 @@ def main() -> int:
         overlap = rng.random() < 0.5
         kernel = rng.choice([0, 1, 5])
         chunk = rng.choice([0, 8192, 65536])
+        ce = rng.choice([-1, 0, 4096])  # copy-engine runs: off, default (256 MiB: none here), >= 4 KiB
         plan = plan_param_realloc(fm, src, dst, c, rng.choice([0, 1]))
         rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
                            mode=mode, kernel=kernel, flag_kernel=kernel, hierarchical=hier, relay=relay,
-                           overlap=overlap, chunk_bytes=chunk)
+                           overlap=overlap, chunk_bytes=chunk, ce_min_run_bytes=ce)
+        ce_cases += int(any(e.ce_runs()[0] for e in rr.executors))
         for d, b in rr.buffers["a"].items():
             R.fill_shard(plan, R.SRC, d, b.ptr, 50 + i)
         for rep in range(2):
@@ -194,7 +197,7 @@ def main() -> int:
                 want = O.fill(fm, dst, c, d, 50 + i)
                 if not np.array_equal(got, want):
                     failures.append(f"fuzz {i} {src}->{dst} mode {mode} hier {hier} relay {relay} overlap {overlap} "
-                                    f"kernel {kernel} chunk {chunk} rep {rep}: device {d} differs in "
+                                    f"kernel {kernel} chunk {chunk} ce {ce} rep {rep}: device {d} differs in "
                                     f"{int(np.count_nonzero(got != want))} elements")
         if rr.relay_timeouts() or rr.barrier.timed_out():
             failures.append(f"fuzz {i}: flag or barrier timeouts")
@@ -225,6 +228,7 @@ def main() -> int:
     for f in failures:
         print(f"rank {rank}: {f}", flush=True)
     if rank == 0:
+        print(f"dist_worker: fuzz cases with copy-engine runs on rank 0: {ce_cases}", flush=True)
         print(f"dist_worker world={world}: {'OK' if flag.item() == 0 else 'FAILED'}", flush=True)
     dist.destroy_process_group()
     return 0 if flag.item() == 0 else 1

@@ -1,0 +1,59 @@
+"""Copy-engine runs (rr_plan_ce_runs, capi_exec.cpp ce_runs): ranges moved
+whole by a copy engine must be byte-identical between the source shard and
+the destination shard they are copied into, and must carry (almost) only
+bytes the plan moves between that pair. Checked on CPU against the oracle's
+shard contents (oracle/realloc_oracle.c orc_fill)."""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+from _helpers import placement
+from oracle import oracle as O
+from paper_2406_14088_b200.rlplan import BALANCED, MODELS, b200_cluster, plan_param_realloc
+
+TINY_GQA = dataclasses.replace(MODELS["tiny"], name="tiny_gqa", hidden_size=512, num_attention_heads=16,
+                               num_kv_heads=8, intermediate_size=1024)
+
+
+def _hosts(n_dev: int, world: int):
+    return [d * world // n_dev for d in range(n_dev)]
+
+
+@pytest.mark.parametrize("sp,dp,world", [
+    ((2, 1, 4, 0, 0), (1, 2, 4, 0, 0), 2),   # 13B-style pipeline-stage remap
+    ((2, 1, 4, 0, 0), (1, 2, 4, 0, 0), 4),
+    ((2, 1, 4, 0, 0), (1, 2, 4, 0, 0), 8),
+    ((2, 2, 2, 1, 1), (1, 4, 2, 1, 1), 4),   # fused QKV / gate-up on both sides, dp replicas
+    ((1, 1, 8, 0, 0), (1, 8, 1, 0, 0), 2),   # tp -> dp: no run may appear
+    ((2, 1, 4, 0, 0), (1, 1, 8, 0, 0), 2),   # tp split changes: no run
+])
+def test_runs_are_byte_identical(sp, dp, world):
+    c = b200_cluster(8)
+    src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
+    dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
+    plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
+    host_of = _hosts(8, world)
+    seed = 5
+    fills_s, fills_d = {}, {}
+    total = 0
+    for r in range(world):
+        local = [d for d in range(8) if host_of[d] == r]
+        for (s, d, so, do, nb) in plan.ce_runs(local, host_of, min_run_bytes=4096):
+            assert host_of[s] == r and host_of[d] != r, "runs go from a local source to a remote destination"
+            if s not in fills_s:
+                fills_s[s] = O.fill(TINY_GQA, src, c, s, seed).view(np.uint8)
+            if d not in fills_d:
+                fills_d[d] = O.fill(TINY_GQA, dst, c, d, seed).view(np.uint8)
+            a, b = fills_s[s], fills_d[d]
+            assert so + nb <= a.size and do + nb <= b.size
+            assert np.array_equal(a[so:so + nb], b[do:do + nb]), (s, d, so, do, nb)
+            total += nb
+    if sp[2] != dp[2]:
+        assert total == 0, "a TP change leaves no identically laid-out range"
+    else:
+        # every cross-host byte of a pure stage remap goes through runs
+        wire = sum(plan.work([d for d in range(8) if host_of[d] == r], 0, host_of)["wire_in"] for r in range(world))
+        assert total >= 0.98 * wire, (total, wire)

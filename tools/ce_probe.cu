@@ -9,6 +9,9 @@
 //   mix/<pct>        pct% of each peer's bytes by CE (one stream per peer),
 //                    the rest by the SM kernel at the same time
 //   h2d/<M>[x<s>]    pinned host -> device, M MiB pieces over s streams
+//   pair/sm, pair/ce GPUs paired (d <-> d^1), each pushes 2 GiB to its partner
+//                    only (a pipeline-stage remap's pattern): SM stores vs one
+//                    whole copy-engine copy
 // Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tools/ce_probe tools/ce_probe.cu
 #include <cuda_runtime.h>
 
@@ -52,6 +55,11 @@ __global__ void k_a2a(const char* __restrict__ base, Targets t, int self, int g,
   uint4* to = (uint4*)(t.to[p] + size_t(self) * s + skip);
   const size_t n = (s - skip) / 16;
   for (size_t i = (blockIdx.x % per) * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)per * blockDim.x)
+    to[i] = __ldg(from + i);
+}
+
+__global__ void k_copy(const uint4* __restrict__ from, uint4* __restrict__ to, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     to[i] = __ldg(from + i);
 }
 
@@ -150,6 +158,21 @@ int main(int argc, char** argv) {
   for (int p = 0; p < G; ++p) t.to[p] = dst[p];
   const int ctas = (sms * 2 / (G - 1)) * (G - 1);
 
+  {
+    // pairwise: d -> d^1 only, 2 GiB (the whole src/dst buffers are >= 2 GiB when G <= 2; else use G*S)
+    const size_t pb = std::min(size_t(2) << 30, G * S);
+    report("pair/sm", double(pb), timed([&](int d) {
+      k_copy<<<sms * 2, 512, 0, st[d][kMax]>>>((const uint4*)src[d], (uint4*)dst[d ^ 1], pb / 16);
+    }));
+    report("pair/ce", double(pb), timed([&](int d) {
+      CK(cudaMemcpyAsync(dst[d ^ 1], src[d], pb, cudaMemcpyDefault, st[d][kMax]));
+    }));
+    report("pair/ce64", double(pb), timed([&](int d) {
+      for (size_t off = 0; off < pb; off += size_t(64) << 20)
+        CK(cudaMemcpyAsync(dst[d ^ 1] + off, src[d] + off, std::min(size_t(64) << 20, pb - off), cudaMemcpyDefault,
+                           st[d][kMax]));
+    }));
+  }
   report("a2a/sm", egress, timed([&](int d) { k_a2a<<<ctas, 512, 0, st[d][kMax]>>>(src[d], t, d, G, S, 0); }));
   report("a2a/ce-whole", egress, timed([&](int d) { enqueue_ce(d, S, true, 0); }));
   for (int m : {1, 4, 16}) {
