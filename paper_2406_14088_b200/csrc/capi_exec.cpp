@@ -84,6 +84,8 @@ struct rr_exec {
     void* dst;
     const void* src;
     size_t bytes;
+    DeviceId src_dev;  // source plan device and byte offset in its shard (onload pipelining)
+    int64_t src_off;
   };
   std::vector<CeCopy> ce;
   int64_t ce_bytes = 0;
@@ -369,7 +371,7 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
     upload(b, ex->phase[1]);
     for (const auto& u : runs) {
       ex->ce.push_back({static_cast<char*>(dst_bufs[u.dst]) + u.dst_off, static_cast<const char*>(src_bufs[u.src]) + u.src_off,
-                        static_cast<size_t>(u.bytes)});
+                        static_cast<size_t>(u.bytes), u.src, u.src_off});
       ex->ce_bytes += u.bytes;
     }
     if (!ex->ce.empty()) {
@@ -538,6 +540,13 @@ rr_status rr_exec_enable_onload(rr_exec* ex, int n_src, const int32_t* src_devic
       for (int64_t off = 0; off < src_bytes[i]; off += chunk_bytes)
         ex->chunks.push_back({src_devices[i], off, std::min(chunk_bytes, src_bytes[i] - off)});
     }
+    // A copy-engine run over an onloaded source must lie inside the onloaded
+    // bytes, like every item (checked below).
+    for (const auto& c : ex->ce)
+      for (int k = 0; k < n_src; ++k)
+        if (src_devices[k] == c.src_dev)
+          need(c.src_off + static_cast<int64_t>(c.bytes) <= src_bytes[k],
+               "a copy-engine run reads beyond the onloaded bytes of its source");
     // Segment of each item: 0 = independent of the onload, 1 + c = needs chunk c.
     const rr::ItemSet& a = ex->phase0_host;
     const size_t n = a.items.size(), C = ex->chunks.size();
@@ -609,6 +618,36 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
                  "onload cudaMemcpyAsync");
       check_cuda(cudaEventRecord(ex->events[c], cs), "cudaEventRecord");
     }
+    if (!ex->ce.empty()) {
+      // Copy-engine runs follow the onload: the part of a run that reads
+      // chunk c starts once chunk c has landed; runs over sources that are
+      // not onloaded start right away.
+      check_cuda(cudaEventRecord(ex->ce_fork, ks), "cudaEventRecord(ce fork)");
+      check_cuda(cudaStreamWaitEvent(ex->ce_stream, ex->ce_fork, 0), "cudaStreamWaitEvent(ce fork)");
+      auto onloaded = [&](DeviceId d) {
+        return std::any_of(ex->chunks.begin(), ex->chunks.end(), [&](const rr_exec::Chunk& ch) { return ch.device == d; });
+      };
+      auto piece = [&](const rr_exec::CeCopy& c, int64_t lo, int64_t hi) {  // source bytes [lo, hi) of the shard
+        const int64_t a = std::max(lo, c.src_off), b = std::min(hi, c.src_off + static_cast<int64_t>(c.bytes));
+        if (a >= b) return;
+        check_cuda(cudaMemcpyAsync(static_cast<char*>(c.dst) + (a - c.src_off),
+                                   static_cast<const char*>(c.src) + (a - c.src_off), static_cast<size_t>(b - a),
+                                   cudaMemcpyDeviceToDevice, ex->ce_stream),
+                   "copy-engine run");
+      };
+      for (const auto& c : ex->ce)
+        if (!onloaded(c.src_dev)) piece(c, c.src_off, c.src_off + static_cast<int64_t>(c.bytes));
+      for (size_t k = 0; k < ex->chunks.size(); ++k) {
+        const auto& ch = ex->chunks[k];
+        bool any = false;
+        for (const auto& c : ex->ce) any = any || (c.src_dev == ch.device && c.src_off < ch.offset + ch.bytes &&
+                                                  c.src_off + static_cast<int64_t>(c.bytes) > ch.offset);
+        if (!any) continue;
+        check_cuda(cudaStreamWaitEvent(ex->ce_stream, ex->events[k], 0), "cudaStreamWaitEvent(ce chunk)");
+        for (const auto& c : ex->ce)
+          if (c.src_dev == ch.device) piece(c, ch.offset, ch.offset + ch.bytes);
+      }
+    }
     for (size_t s = 0; s < ex->segments.size(); ++s) {
       if (s > 0) check_cuda(cudaStreamWaitEvent(ks, ex->events[s - 1], 0), "cudaStreamWaitEvent");
       const auto& sg = ex->segments[s];
@@ -620,10 +659,7 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
       ph.flagged = ex->phase[0].flagged;
       launch_phase(ex, ph, stream, ctas);
     }
-    if (!ex->ce.empty()) {  // the runs read whole source ranges: after the last chunk
-      ce_issue(ex, ks, ex->events.empty() ? nullptr : ex->events.back());
-      ce_join(ex, ks);
-    }
+    if (!ex->ce.empty()) ce_join(ex, ks);
   });
 }
 
