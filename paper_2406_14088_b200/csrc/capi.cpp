@@ -293,7 +293,7 @@ rr_status rr_plan_to_json(const rr_plan* plan, char* buf, size_t cap, size_t* ne
 rr_status rr_plan_shard_bytes(const rr_plan* plan, int side, int32_t device, int64_t* bytes) {
   return guarded([&] {
     need(plan != nullptr, "null plan");
-    *bytes = const_cast<rr_plan*>(plan)->layout(side, device).bytes;
+    *bytes = plan->layout(side, device).bytes;
   });
 }
 
@@ -333,7 +333,7 @@ rr_status rr_plan_layout(const rr_plan* plan, int side, int32_t device, int64_t*
                          int64_t cap_blocks, int64_t* n_blocks) {
   return guarded([&] {
     need(plan != nullptr, "null plan");
-    const auto& lay = const_cast<rr_plan*>(plan)->layout(side, device);
+    const auto& lay = plan->layout(side, device);
     *n_blocks = static_cast<int64_t>(lay.blocks.size());
     if (cap_blocks < *n_blocks) raise(RR_ERANGE, "rr_plan_layout: buffer too small");
     for (size_t i = 0; i < lay.blocks.size(); ++i) {
@@ -540,7 +540,7 @@ struct DeviceArray {
 rr_status rr_fill_shard(const rr_plan* plan, int side, int32_t device, void* buf, uint64_t seed, void* stream) {
   return guarded([&] {
     need(plan != nullptr && buf != nullptr, "null plan/buffer");
-    const auto& lay = const_cast<rr_plan*>(plan)->layout(side, device);
+    const auto& lay = plan->layout(side, device);
     const auto items = fill_items(lay, *plan, reinterpret_cast<uint64_t>(buf));
     DeviceArray<rr::FillItem> d(items);
     auto s = static_cast<cudaStream_t>(stream);
@@ -553,7 +553,7 @@ rr_status rr_verify_shard(const rr_plan* plan, int side, int32_t device, const v
                           void* stream, int64_t* mismatches, int64_t* first) {
   return guarded([&] {
     need(plan != nullptr && buf != nullptr, "null plan/buffer");
-    const auto& lay = const_cast<rr_plan*>(plan)->layout(side, device);
+    const auto& lay = plan->layout(side, device);
     const uint64_t base = reinterpret_cast<uint64_t>(buf);
     const auto items = fill_items(lay, *plan, base);
     DeviceArray<rr::FillItem> d(items);

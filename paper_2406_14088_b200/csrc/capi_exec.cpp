@@ -215,7 +215,7 @@ rr::ItemSet refine_chunk(rr::ItemSet set, const std::vector<rr::Job>& jobs, int 
 // shard layouts coincide (rr::matching_runs), kept when >= min_bytes and when
 // at least 98% of the range is bytes this pair is planned to move (so the
 // engine does not carry data the destination gets elsewhere, e.g. locally).
-std::vector<rr::CeRun> ce_runs(rr_plan* plan, const std::vector<rr::Job>& jobs, const rr::HostMap& hm,
+std::vector<rr::CeRun> ce_runs(const rr_plan* plan, const std::vector<rr::Job>& jobs, const rr::HostMap& hm,
                                int64_t min_bytes) {
   std::map<std::pair<DeviceId, DeviceId>, std::vector<const rlplan::CopyRect*>> pairs;
   for (const auto& j : jobs) {
@@ -281,7 +281,7 @@ rr_status rr_plan_ce_runs(const rr_plan* plan, int n_local, const int32_t* local
     need(min_run_bytes > 0, "min_run_bytes must be positive");
     const rr::HostMap hm = host_map(plan, n_local, local, host_of);
     const auto jobs = rr::build_jobs(plan->lowered, hm, 0);
-    const auto runs = ce_runs(const_cast<rr_plan*>(plan), jobs, hm, min_run_bytes);
+    const auto runs = ce_runs(plan, jobs, hm, min_run_bytes);
     *n = static_cast<int>(runs.size());
     if (out5 == nullptr) return;
     need(cap >= *n, "output table too small");
@@ -345,7 +345,7 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
     const auto jobs = rr::build_jobs(plan->lowered, hm, mode);
     const int64_t ce_min = options->ce_min_run_bytes == 0 ? kDefaultCeRunBytes : options->ce_min_run_bytes;
     const std::vector<rr::CeRun> runs =
-        (mode == 0 && ce_min > 0 && src_bufs && dst_bufs) ? ce_runs(const_cast<rr_plan*>(plan), jobs, hm, ce_min)
+        (mode == 0 && ce_min > 0 && src_bufs && dst_bufs) ? ce_runs(plan, jobs, hm, ce_min)
                                                           : std::vector<rr::CeRun>{};
     auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes, &runs);
     auto b = rr::build_items(jobs, 1, hm, src_bufs, dst_bufs, chunk_bytes);

@@ -72,12 +72,12 @@ struct rr_plan {
   rlplan::ReallocPlan plan;
   std::vector<std::vector<int32_t>> remote_dst, local_dst;  // int32 copies for rr_op
   std::vector<rlplan::LoweredOp> lowered;
-  std::map<std::pair<int, rlplan::DeviceId>, rlplan::ShardLayout> layouts;
-  std::mutex mu;  // guards lazily built layouts
+  mutable std::map<std::pair<int, rlplan::DeviceId>, rlplan::ShardLayout> layouts;
+  mutable std::mutex mu;  // guards lazily built layouts
   bool data = false;  // inter-call data transfer plan (plan_data_transfer)
   rlplan::Bytes data_total = 0;  // its total data bytes
 
-  const rlplan::ShardLayout& layout(int side, rlplan::DeviceId d) {
+  const rlplan::ShardLayout& layout(int side, rlplan::DeviceId d) const {
     std::lock_guard<std::mutex> lock(mu);
     auto key = std::make_pair(side, d);
     auto it = layouts.find(key);
