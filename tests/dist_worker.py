@@ -203,6 +203,51 @@ def main() -> int:
             failures.append(f"fuzz {i}: flag or barrier timeouts")
         dist.barrier()
         rr.close()
+    # Copy-engine runs on stage remaps (forced down to 4 KiB ranges so the
+    # tiny model has some), push and hierarchical/flat, with the onload path.
+    ce_total = 0
+    for sp, dp in (((2, 1, 4, 0, 0), (1, 2, 4, 0, 0)), ((2, 2, 2, 1, 1), (1, 4, 2, 1, 1)),
+                   ((1, 2, 4, 2, 1), (2, 1, 4, 2, 1))):
+        for hier in (True, False):
+            src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
+            dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
+            plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
+            rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
+                               hierarchical=hier, ce_min_run_bytes=4096)
+            ce_total += sum(e.ce_runs()[0] for e in rr.executors)
+            for d, b in rr.buffers["a"].items():
+                R.fill_shard(plan, R.SRC, d, b.ptr, 77)
+            for onload in (False, True):
+                for b in rr.buffers["b"].values():
+                    b.zero()
+                torch.cuda.synchronize()
+                dist.barrier()
+                if onload:
+                    host = {d: R.HostBuffer(plan.shard_bytes(R.SRC, d)) for d in rr.buffers["a"]}
+                    for d, hb in host.items():
+                        hb.array()[:] = rr.buffers["a"][d].to_host()
+                    copy_stream = torch.cuda.Stream()
+                    # small chunks so that runs straddle several of them
+                    rr.run_phase_onload(0, {d: hb.ptr for d, hb in host.items()}, copy_stream, chunk_bytes=64 << 10)
+                else:
+                    rr.run_phase(0)
+                torch.cuda.synchronize()
+                for d, b in rr.buffers["b"].items():
+                    bad, first = R.verify_shard(plan, R.DST, d, b.ptr, 77)
+                    if bad:
+                        failures.append(f"ce {sp}->{dp} hier {hier} onload {onload}: device {d} {bad} mismatches")
+                if onload:
+                    for hb in host.values():
+                        hb.free()
+            if rr.barrier.timed_out():
+                failures.append(f"ce {sp}->{dp}: barrier timed out")
+            dist.barrier()
+            rr.close()
+    if world > 1 and not oversub:
+        t = torch.tensor([ce_total], device="cuda")
+        dist.all_reduce(t)
+        if t.item() == 0:
+            failures.append("copy-engine cases issued no runs")
     if os.environ.get("RR_FULL_7B") == "1" and not oversub:
         w = WORKLOADS["llama7b_tp8_dp8_roundtrip"]
         plans = [plan_param_realloc(w.model, s, d, c, BALANCED) for (s, d) in w.phases]
