@@ -478,6 +478,10 @@ def run_b200(args) -> None:
         line = {
             "metric": METRIC, "value": round(value_gbs, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True, "scaling": "strong",
+            "scaling_note": ("total work fixed (the workload's plan devices spread over N GPUs): at N=1 every "
+                             "move is a local HBM relayout, at N>1 each GPU must also receive the slices held "
+                             "on other GPUs over NVLink (900 GB/s per direction vs ~6.5 TB/s HBM), so time "
+                             "need not fall with N; compare each N against its own roofline"),
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": w.name, "description": w.description, "plan_devices": w.devices,
                        "plan_devices_per_gpu": w.devices // world, "phases": len(plans),
