@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""NCCL comparison for the DP fan-out workloads.
+"""NCCL comparison for the DP fan-out and stage-remap workloads.
 
 The upstream runtime moves weights with NCCL broadcasts. The
 NCCL baseline here does the standard thing: move whole source shards with a
@@ -10,6 +10,7 @@ Times are CUDA events around collective + unpack, max over ranks; the result
 is verified on device. Run with torchrun, one process per GPU:
 
   torchrun --nproc-per-node N tools/nccl_compare.py --workload llama7b_tp8_dp8_roundtrip
+  torchrun --nproc-per-node N tools/nccl_compare.py --workload llama13b_pp2tp4_to_dp2tp4 --kind p2p
 """
 from __future__ import annotations
 
@@ -34,6 +35,8 @@ def main() -> int:
     ap.add_argument("--workload", default="llama7b_tp8_dp8_roundtrip")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--kind", choices=["auto", "p2p"], default="auto",
+                    help="auto: broadcast (one source) or all_gather; p2p: send/recv of whole source shards")
     args = ap.parse_args()
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -48,7 +51,34 @@ def main() -> int:
     sizes = {d: plan.shard_bytes(R.SRC, d) for d in src_devs}
     S = max(sizes.values())
     stream = torch.cuda.current_stream()
-    if len(src_devs) == 1:
+    if args.kind == "p2p":
+        # Stage remap (e.g. 13B pp2 -> dp2): every source shard some remote
+        # rank's destinations read is sent whole to that rank with NCCL
+        # send/recv (exactly the needed bytes when TP is unchanged), then
+        # unpacked locally by the pull executor.
+        kind = "p2p"
+        owner_of = {d: r for r in range(world) for d in R.hosted_devices(n, r, world)}
+        need_from: dict = {}  # (src device, receiving rank) pairs
+        for s_dev, dsts, _rects in plan.lowered():
+            for d in dsts:
+                if owner_of[d] != owner_of[s_dev]:
+                    need_from[(s_dev, owner_of[d])] = True
+        mine = {d: torch.zeros(sizes[d], dtype=torch.uint8, device="cuda") for d in src_devs if d in hosted}
+        for d, t in mine.items():
+            R.fill_shard(plan, R.SRC, d, t.data_ptr(), 7)
+        recv = {s_dev: torch.zeros(sizes[s_dev], dtype=torch.uint8, device="cuda")
+                for (s_dev, q) in need_from if q == rank}
+        src_ptrs = {d: t.data_ptr() for d, t in mine.items()}
+        src_ptrs.update({d: t.data_ptr() for d, t in recv.items()})
+        sends = sorted((s_dev, q) for (s_dev, q) in need_from if owner_of[s_dev] == rank)
+        recvs = sorted((s_dev, owner_of[s_dev]) for (s_dev, q) in need_from if q == rank)
+
+        def collective():
+            ops = [dist.P2POp(dist.isend, mine[s_dev], q) for (s_dev, q) in sends]
+            ops += [dist.P2POp(dist.irecv, recv[s_dev], q) for (s_dev, q) in recvs]
+            for w_ in dist.batch_isend_irecv(ops):
+                w_.wait()
+    elif len(src_devs) == 1:
         kind = "broadcast"
         d0 = src_devs[0]
         owner = d0 // (n // world)
