@@ -9,7 +9,9 @@ actually takes on B200, from the same lowered work the kernels run:
   local destination; hierarchical fan-out included) at the measured
   effective copy bandwidth of the TMA bulk kernel;
 * per GPU, link bytes in and out at the measured NVLink rate of the peer
-  store path (or the multicast rate for multicast payloads);
+  store path (or the multicast rate for multicast payloads), except the
+  bytes of copy-engine runs (rr_exec_options.ce_min_run_bytes), which move
+  at the measured copy-engine rate on the same link;
 * phases serialise, GPUs run in parallel: time = max over GPUs of
   max(HBM time, link time) per phase, plus a fixed launch/barrier cost.
 * offload / onload of parked parameters (SPEC.md:423 prices them at
@@ -32,6 +34,7 @@ class B200Profile:
     hbm_copy_gbs: float = 6340.0        # read+write bytes/s of rr_bulk_kernel (7B tp8->dp8 forward, 1 GPU)
     nvlink_push_gbs: float = 708.0      # per GPU per direction, SM peer stores (2/4 GPUs, all-to-all)
     nvlink_mc_gbs: float = 565.0        # per receiving GPU, NVLS multimem.st (4 GPUs)
+    nvlink_ce_gbs: float = 777.0        # per GPU per direction, whole copy-engine copies, pairwise (2/4 GPUs)
     launch_us: float = 8.0              # kernel launch + dynamic-scheduler tail
     barrier_us: float = 12.0            # cross-GPU flag barrier
     host_link_gbs: float = 55.6         # pinned host <-> HBM per GPU, either direction (r01 ce_probe h2d/*)
@@ -46,12 +49,15 @@ def host_transfer_seconds(nbytes_per_gpu: int, profile: B200Profile = B200Profil
 
 def estimate_seconds(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
                      profile: B200Profile = B200Profile(), multicast: bool = False,
-                     relay: bool = False, onload: bool = False) -> Dict[str, float]:
+                     relay: bool = False, onload: bool = False, copy_engine: bool = True) -> Dict[str, float]:
     """Estimated execution time of `plan` with plan device d hosted on GPU
     host_of[d] (default: one GPU per plan device). `relay`: payloads reaching
     >= 2 other GPUs use the pipelined relay (one copy in and out per GPU,
     fan-out fused into phase 0). `onload`: the source shards arrive from
-    pinned host memory pipelined with phase 0 (rr_exec_launch_onload)."""
+    pinned host memory pipelined with phase 0 (rr_exec_launch_onload).
+    `copy_engine`: ranges laid out identically on both sides move as
+    copy-engine runs (the executor default; not combined with relay or
+    multicast here)."""
     n = plan.cluster.device_count()
     host = list(host_of) if host_of is not None else list(range(n))
     hosts = sorted(set(host))
@@ -90,9 +96,26 @@ def estimate_seconds(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
             extra = len(groups[h]) - 1       # hierarchical fan-out inside host h
             hbm[h] += b                      # the leader replica is written once
             fan[h] += b * (1 + extra) if extra else 0  # read the leader, write the others
-    t_phase0 = max(max(hbm[h] / (profile.hbm_copy_gbs * 1e9),
-                       max(egress[h], ingress[h]) / (profile.nvlink_push_gbs * 1e9) +
-                       mc_in[h] / (profile.nvlink_mc_gbs * 1e9)) for h in hosts)
+    # copy-engine runs: their bytes leave the SM push totals and take the
+    # copy-engine rate on the same link
+    ce_out = {h: 0 for h in hosts}
+    ce_in = {h: 0 for h in hosts}
+    if copy_engine and not relay and not multicast and len(hosts) > 1:
+        for h in hosts:
+            local = [d for d in range(n) if host[d] == h]
+            for (s, d, _so, _do, nb) in plan.ce_runs(local, host):
+                ce_out[h] += nb
+                ce_in[host[d]] += nb
+        for h in hosts:
+            egress[h] = max(0, egress[h] - ce_out[h])
+            ingress[h] = max(0, ingress[h] - ce_in[h])
+
+    def link_s(h: int) -> float:
+        out = egress[h] / (profile.nvlink_push_gbs * 1e9) + ce_out[h] / (profile.nvlink_ce_gbs * 1e9)
+        inn = ingress[h] / (profile.nvlink_push_gbs * 1e9) + ce_in[h] / (profile.nvlink_ce_gbs * 1e9)
+        return max(out, inn) + mc_in[h] / (profile.nvlink_mc_gbs * 1e9)
+
+    t_phase0 = max(max(hbm[h] / (profile.hbm_copy_gbs * 1e9), link_s(h)) for h in hosts)
     onload_s = 0.0
     if onload:
         src_bytes = {h: 0 for h in hosts}
@@ -108,5 +131,5 @@ def estimate_seconds(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
     total = t_phase0 + t_phase1 + fixed
     return {"seconds": total, "phase0_s": t_phase0, "fanout_s": t_phase1, "onload_s": onload_s,
             "spec_est_time_s": plan.est_time,
-            "max_link_bytes": max(max(egress[h], ingress[h]) + mc_in[h] for h in hosts),
+            "max_link_bytes": max(max(egress[h] + ce_out[h], ingress[h] + ce_in[h]) + mc_in[h] for h in hosts),
             "max_hbm_bytes": max(hbm[h] for h in hosts)}

@@ -84,6 +84,20 @@ def test_cost_model_matches_round1_measurements(gpus, measured_ms, tol):
     assert est["phase0_s"] * 1e3 == pytest.approx(measured_ms, rel=tol)
 
 
+@pytest.mark.parametrize("gpus,measured_ms,ce", [
+    (2, 18.54, True),    # 13B stage remap with copy-engine runs (profiles/r01_configs_n2.jsonl)
+    (4, 9.32, True),     # (profiles/r01_configs_n4.jsonl)
+    (2, 19.65, False),   # the same with SM peer stores only (profiles/r01_ce_runs_ab_n2_n4.jsonl)
+    (4, 9.84, False),
+])
+def test_cost_model_stage_remap(gpus, measured_ms, ce):
+    w = WORKLOADS["llama13b_pp2tp4_to_dp2tp4"]
+    plan = plan_param_realloc(w.model, *w.phases[0], w.cluster(), BALANCED)
+    host_of = [d // (8 // gpus) for d in range(8)]
+    est = costmodel.estimate_seconds(plan, host_of, copy_engine=ce)
+    assert est["phase0_s"] * 1e3 == pytest.approx(measured_ms, rel=0.05)
+
+
 @pytest.mark.parametrize("gpus,measured_ms", [
     (1, 294.4),   # r01 bench e2e, 1 GPU (profiles/r01_bench_default_n1.json): 16.06 GB onloaded per step
     (2, 152.4),   # round-1 bench e2e at 2 GPUs, 8.03 GB onloaded per GPU
