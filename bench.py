@@ -268,7 +268,9 @@ def run_b200(args) -> None:
     t_bind = time.perf_counter()
     rr = R.RankRealloc(plans, shards, bind, rank, world, local_rank, mode=mode, kernel=kernel,
                        multicast=multicast, relay=relay, overlap=overlap, flag_kernel=flag_kernel,
-                       chunk_bytes=args.chunk_kib << 10, ce_min_run_bytes=-1 if args.ce == "off" else 0)
+                       chunk_bytes=args.chunk_kib << 10, ce_min_run_bytes=-1 if args.ce == "off" else 0,
+                       staged={"on": True, "off": False, "auto": "auto"}[args.staged],
+                       stage_chunk_bytes=args.stage_mib << 20)
     # executor creation only: the shard allocations inside RankRealloc are
     # timed too, so this is an upper bound of binding + descriptor upload
     bind_ms = (time.perf_counter() - t_bind) * 1e3
@@ -488,7 +490,8 @@ def run_b200(args) -> None:
                        "policy": args.policy, "mode": args.mode, "multicast_sets": rr.multicast,
                        "relay_phases": rr.relay_phases, "overlap_phases": rr.overlap_phases,
                        "copy_kernel": kname,
-                       "ce_runs": [list(e.ce_runs()) for e in rr.executors], "bulk_variants": {"plain": 1 if kernel is None else kernel,
+                       "ce_runs": [list(e.ce_runs()) for e in rr.executors],
+                       "staged_phases": rr.staged_phases, "bulk_variants": {"plain": 1 if kernel is None else kernel,
                                                                       "flag_synchronised": flag_kernel},
                        "chunk_kib": args.chunk_kib or "library default (256; smaller for phases too small for it)", "ctas": args.ctas or "resident capacity",
                        "l2": "inputs larger than L2 (multi-GB shards); no flush needed",
@@ -550,6 +553,11 @@ def main() -> None:
     ap.add_argument("--ce", choices=["on", "off"], default="on",
                     help="copy-engine runs for >= 256 MiB ranges laid out identically in a source and a remote "
                          "destination shard (push mode; library default)")
+    ap.add_argument("--staged", choices=["auto", "on", "off"], default="auto",
+                    help="staged gather for phases that read other GPUs' sources: whole source shards pushed by "
+                         "copy engines in rotation rounds, unpacked per 512 MiB piece; auto = from 4 GPUs on, "
+                         "all-gather-shaped phases")
+    ap.add_argument("--stage-mib", type=int, default=512, help="staged-gather piece size (MiB)")
     ap.add_argument("--overlap", choices=["on", "off"], default="on",
                     help="run in-host fan-outs per chunk inside the first phase (N > 1) instead of after a barrier")
     ap.add_argument("--ctas", type=int, default=0)

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define RR_ABI_VERSION 3 /* 2: rr_placement.kv_layout, rr_shard.part; 3: rr_exec_options.ce_min_run_bytes */
+#define RR_ABI_VERSION 4 /* 2: rr_placement.kv_layout, rr_shard.part; 3: rr_exec_options.ce_min_run_bytes; 4: staged gather */
 
 typedef enum {
   RR_OK = 0,
@@ -289,16 +289,36 @@ typedef struct {
    * side stream, forked from and joined back into the launch stream) instead
    * of SM peer stores. 0 = default (256 MiB), < 0 = never. */
   int64_t ce_min_run_bytes;
+  /* Staged gather (ABI v4; pull mode with host_of, host ids 0..n_hosts-1):
+   * every remote source shard this host reads is pushed whole by its host's
+   * copy engine into a staging buffer here, in stage_chunk_bytes pieces,
+   * in rounds that pair each host with one sender at a time
+   * (rr_plan_stage_slots); each piece is flagged in the receiver's stage
+   * flag array and the unpack items here wait per piece. src_bufs[d] of a
+   * remote source d is this host's staging buffer for d.
+   * stage_remote[d * n_hosts + h]: host h's staging buffer for local source
+   * d, mapped here (NULL where h does not read d). stage_flags[h]: host h's
+   * stage flag array (rr_plan_stage_slots uint32, zeroed once), mapped
+   * here. stage_chunk_bytes = 0: off. */
+  int64_t stage_chunk_bytes;
+  int32_t n_hosts;
+  void* const* stage_remote;
+  void* const* stage_flags;
 } rr_exec_options;
 /* Length of the relay flag array for this host map, chunk size and scheme
  * switches (identical on every rank). */
 rr_status rr_plan_relay_slots(const rr_plan* plan, const int32_t* host_of, int64_t chunk_bytes, int relay_chain,
                               int overlap_fanout, int64_t* slots);
+/* Staged gather: length of the stage flag array every host allocates (the
+ * maximum over hosts of its pieces) for this host map and piece size. */
+rr_status rr_plan_stage_slots(const rr_plan* plan, const int32_t* host_of, int64_t chunk_bytes, int64_t* slots);
 /* Copy-engine runs a push executor driving `local` (with `host_of`) would
  * issue, host only: 5 int64 per run {src device, dst device, src byte
  * offset, dst byte offset, bytes}; pass out5 = NULL to query *n. */
 rr_status rr_plan_ce_runs(const rr_plan* plan, int n_local, const int32_t* local, const int32_t* host_of,
                           int64_t min_run_bytes, int64_t* out5, int cap, int* n);
+/* Staged-gather pieces this executor pushes per launch, and their bytes. */
+rr_status rr_exec_stage_pushes(const rr_exec* ex, int* n_pushes, int64_t* bytes);
 /* Copy-engine runs phase 0 issues (see rr_exec_options.ce_min_run_bytes). */
 rr_status rr_exec_ce_runs(const rr_exec* ex, int* n_runs, int64_t* bytes);
 /* Relay waits that timed out (bounded spins) since the executor was created. */

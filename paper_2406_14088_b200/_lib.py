@@ -54,7 +54,8 @@ class RrOp(Structure):
 class RrExecOptions(Structure):
     _fields_ = [("mode", c_int32), ("chunk_bytes", c_int64), ("host_of", POINTER(c_int32)),
                 ("mc_bufs", POINTER(c_void_p)), ("relay_flags", POINTER(c_void_p)), ("relay_chain", c_int32),
-                ("overlap_fanout", c_int32), ("ce_min_run_bytes", c_int64)]
+                ("overlap_fanout", c_int32), ("ce_min_run_bytes", c_int64), ("stage_chunk_bytes", c_int64),
+                ("n_hosts", c_int32), ("stage_remote", POINTER(c_void_p)), ("stage_flags", POINTER(c_void_p))]
 
 
 _P = c_void_p
@@ -66,6 +67,8 @@ _SIGNATURES = {
     "rr_exec_kernel_count": (c_int, [_P, POINTER(c_int), POINTER(c_int)]),
     "rr_exec_phase_kernels": (c_int, [_P, c_int, POINTER(c_int), POINTER(c_int)]),
     "rr_exec_ce_runs": (c_int, [_P, POINTER(c_int), POINTER(c_int64)]),
+    "rr_exec_stage_pushes": (c_int, [_P, POINTER(c_int), POINTER(c_int64)]),
+    "rr_plan_stage_slots": (c_int, [_P, POINTER(c_int32), c_int64, POINTER(c_int64)]),
     "rr_plan_ce_runs": (c_int, [_P, c_int, POINTER(c_int32), POINTER(c_int32), c_int64, POINTER(c_int64), c_int,
                                 POINTER(c_int)]),
     "rr_mcast_supported": (c_int, [c_int, POINTER(c_int)]),

@@ -89,6 +89,29 @@ struct rr_exec {
   };
   std::vector<CeCopy> ce;
   int64_t ce_bytes = 0;
+  // Staged gather, sender side: whole local source shards pushed piece by
+  // piece into the other hosts' staging buffers, each piece followed by a
+  // one-thread kernel that flags it in the receiver's stage flag array.
+  struct StagePush {
+    void* dst;
+    const void* src;
+    size_t bytes;
+    uint32_t* flag;
+    DeviceId src_dev;  // source plan device and byte offset in its shard (onload pipelining)
+    int64_t src_off;
+  };
+  std::vector<StagePush> stage;
+  int64_t stage_bytes = 0;
+  // A staged executor's unpack kernel runs one CTA per SM unless the caller
+  // picks a count: more CTAs only add HBM pressure and spinning against the
+  // copy engines (profiles/r01_staged_sweep_n4.txt: 16.27 ms at 148 CTAs vs
+  // 16.84 at 296 and 16.66 at 74, 7B tp8->dp8 forward, 4 GPUs).
+  int stage_ctas = 0;
+  // With an onload, the staged unpack runs from the start on its own stream
+  // (and work counter) beside the per-chunk local copies.
+  cudaStream_t unpack_stream = nullptr;
+  cudaEvent_t unpack_fork = nullptr, unpack_join = nullptr;
+  unsigned int* d_sched2 = nullptr;
   cudaStream_t ce_stream = nullptr;
   cudaEvent_t ce_fork = nullptr, ce_join = nullptr;
 
@@ -106,6 +129,10 @@ struct rr_exec {
     if (ce_fork) cudaEventDestroy(ce_fork);
     if (ce_join) cudaEventDestroy(ce_join);
     if (ce_stream) cudaStreamDestroy(ce_stream);
+    if (unpack_fork) cudaEventDestroy(unpack_fork);
+    if (unpack_join) cudaEventDestroy(unpack_join);
+    if (unpack_stream) cudaStreamDestroy(unpack_stream);
+    if (d_sched2) cudaFree(d_sched2);
   }
 };
 
@@ -157,12 +184,13 @@ int phase_kernel(const rr_exec* ex, const rr_exec::Phase& ph) {
   return ex->kernel;
 }
 
-void launch_phase(rr_exec* ex, const rr_exec::Phase& ph, void* stream, int ctas) {
+void launch_phase(rr_exec* ex, const rr_exec::Phase& ph, void* stream, int ctas, unsigned int* sched = nullptr) {
+  if (sched == nullptr) sched = ex->d_sched;
   check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
   if (ph.n == 0) return;
   const int kernel = phase_kernel(ex, ph);
   if (kernel == 0) {
-    check_cuda(rr::launch_copy(ph.d, ph.n, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys, stream, ex->d_sched,
+    check_cuda(rr::launch_copy(ph.d, ph.n, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys, stream, sched,
                                ex->epoch),
                "rr_copy_kernel launch");
     return;
@@ -172,12 +200,15 @@ void launch_phase(rr_exec* ex, const rr_exec::Phase& ph, void* stream, int ctas)
   // (exec_plan.cpp build_items).
   if (ph.n > ph.n_vec)
     check_cuda(rr::launch_copy(ph.d + ph.n_vec, ph.n - ph.n_vec, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys,
-                               stream, ex->d_sched, ex->epoch),
+                               stream, sched, ex->epoch),
                "rr_copy_kernel launch (relay / multicast / 2-byte items)");
   if (ph.n_vec > 0)
     check_cuda(rr::launch_bulk(kernel, ph.d, ph.n_vec,
-                               ctas > 0 ? ctas : (ph.flagged ? ex->flag_bulk_ctas : ex->bulk_ctas), ex->fence_sys,
-                               stream, nullptr, ex->d_sched, ex->epoch),
+                               ctas > 0 ? ctas
+                                        : (ex->stage_ctas > 0 ? ex->stage_ctas
+                                                              : (ph.flagged ? ex->flag_bulk_ctas : ex->bulk_ctas)),
+                               ex->fence_sys,
+                               stream, nullptr, sched, ex->epoch),
                "rr_bulk_kernel launch");
 }
 
@@ -248,6 +279,10 @@ void ce_issue(rr_exec* ex, cudaStream_t after, cudaEvent_t after_event = nullptr
   check_cuda(cudaStreamWaitEvent(ex->ce_stream, after_event, 0), "cudaStreamWaitEvent(ce fork)");
   for (const auto& c : ex->ce)
     check_cuda(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "copy-engine run");
+  for (const auto& p : ex->stage) {
+    check_cuda(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "staged push");
+    check_cuda(rr::launch_signal(p.flag, ex->epoch, ex->ce_stream), "staged push signal");
+  }
 }
 
 void ce_join(rr_exec* ex, cudaStream_t into) {
@@ -271,6 +306,27 @@ rr_status rr_plan_work(const rr_plan* plan, int n_local, const int32_t* local, c
     out6[2] = b.read;
     out6[3] = b.written;
     rr::host_wire_bytes(plan->lowered, hm, &out6[4], &out6[5]);
+  });
+}
+
+rr_status rr_plan_stage_slots(const rr_plan* plan, const int32_t* host_of, int64_t chunk_bytes, int64_t* slots) {
+  return guarded([&] {
+    need(plan != nullptr && host_of != nullptr && slots != nullptr, "null plan/host table/output");
+    need(chunk_bytes > 0, "chunk_bytes must be positive");
+    const int n = plan->cluster.device_count();
+    std::vector<int> host(host_of, host_of + n);
+    std::vector<int64_t> src_bytes(static_cast<size_t>(n));
+    for (int d = 0; d < n; ++d) src_bytes[static_cast<size_t>(d)] = plan->layout(0, d).bytes;
+    int64_t best = 0;
+    std::vector<int> hosts(host);
+    std::sort(hosts.begin(), hosts.end());
+    hosts.erase(std::unique(hosts.begin(), hosts.end()), hosts.end());
+    for (int h : hosts) {
+      int64_t k = 0;
+      rr::stage_slots(plan->lowered, host, h, src_bytes, chunk_bytes, &k);
+      best = std::max(best, k);
+    }
+    *slots = best;
   });
 }
 
@@ -309,6 +365,10 @@ rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, vo
   opt.relay_chain = 0;
   opt.overlap_fanout = 0;
   opt.ce_min_run_bytes = 0;
+  opt.stage_chunk_bytes = 0;
+  opt.n_hosts = 0;
+  opt.stage_remote = nullptr;
+  opt.stage_flags = nullptr;
   return rr_exec_create_ex(plan, cuda_device, n_devices, src_bufs, dst_bufs, n_local, local, &opt, out);
 }
 
@@ -338,6 +398,23 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
         hm.relay_flags[d] = reinterpret_cast<uint64_t>(options->relay_flags[d]);
       hm.relay_chain = options->relay_chain != 0;
       hm.relay_star = options->overlap_fanout != 0;
+    }
+    std::vector<int64_t> src_bytes(static_cast<size_t>(plan->cluster.device_count()), 0);
+    const bool staged = options->stage_chunk_bytes > 0;
+    if (staged) {
+      need(mode == 1 && options->host_of != nullptr, "a staged gather runs in pull mode with a host_of table");
+      need(options->stage_flags != nullptr && options->stage_remote != nullptr && options->n_hosts > 0,
+           "staged gather needs stage_flags, stage_remote and n_hosts");
+      need(options->relay_flags == nullptr && options->mc_bufs == nullptr, "staged gather excludes relay/multicast");
+      for (size_t d = 0; d < hm.host.size(); ++d) {
+        need(hm.host[d] >= 0 && hm.host[d] < options->n_hosts, "host ids must lie in 0..n_hosts-1");
+        src_bytes[d] = plan->layout(0, static_cast<DeviceId>(d)).bytes;
+      }
+      int64_t n_slots = 0;
+      hm.stage_chunk = options->stage_chunk_bytes;
+      hm.stage_slot0 = rr::stage_slots(plan->lowered, hm.host, hm.me, src_bytes, hm.stage_chunk, &n_slots);
+      hm.stage_flags = reinterpret_cast<uint64_t>(options->stage_flags[hm.me]);
+      need(n_slots == 0 || hm.stage_flags != 0, "missing this host's stage flag array");
     }
     check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
     int per_sm = 0, sms = 0;
@@ -374,7 +451,41 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
                         static_cast<size_t>(u.bytes), u.src, u.src_off});
       ex->ce_bytes += u.bytes;
     }
-    if (!ex->ce.empty()) {
+    if (staged) {
+      ex->stage_ctas = sms;
+      check_cuda(cudaStreamCreateWithFlags(&ex->unpack_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      check_cuda(cudaEventCreateWithFlags(&ex->unpack_fork, cudaEventDisableTiming), "cudaEventCreate");
+      check_cuda(cudaEventCreateWithFlags(&ex->unpack_join, cudaEventDisableTiming), "cudaEventCreate");
+      check_cuda(cudaMalloc(&ex->d_sched2, 4 * sizeof(unsigned int)), "cudaMalloc(sched)");
+      check_cuda(cudaMemset(ex->d_sched2, 0, 4 * sizeof(unsigned int)), "cudaMemset(sched)");
+      // Sender side: round r = 1..H-1 pushes to the host r places after
+      // this one (the receiver's arrival order, rr::stage_sources).
+      std::vector<int> hosts(hm.host.begin(), hm.host.end());
+      std::sort(hosts.begin(), hosts.end());
+      hosts.erase(std::unique(hosts.begin(), hosts.end()), hosts.end());
+      const int H = static_cast<int>(hosts.size());
+      const int pos = static_cast<int>(std::find(hosts.begin(), hosts.end(), hm.me) - hosts.begin());
+      for (int r = 1; r < H; ++r) {
+        const int h = hosts[static_cast<size_t>((pos + r) % H)];
+        int64_t n_slots = 0;
+        const auto slot0 = rr::stage_slots(plan->lowered, hm.host, h, src_bytes, hm.stage_chunk, &n_slots);
+        for (DeviceId sdev : rr::stage_sources(plan->lowered, hm.host, h)) {
+          if (hm.host[static_cast<size_t>(sdev)] != hm.me) continue;
+          void* remote = options->stage_remote[static_cast<size_t>(sdev) * options->n_hosts + h];
+          auto* flags = static_cast<uint32_t*>(options->stage_flags[h]);
+          need(remote != nullptr && flags != nullptr, "missing a receiver's staging buffer or flag array");
+          need(src_bufs != nullptr && src_bufs[sdev] != nullptr, "missing a staged source buffer");
+          const int64_t total = src_bytes[static_cast<size_t>(sdev)];
+          for (int64_t off = 0, c = 0; off < total; off += hm.stage_chunk, ++c) {
+            const int64_t nb = std::min(hm.stage_chunk, total - off);
+            ex->stage.push_back({static_cast<char*>(remote) + off, static_cast<const char*>(src_bufs[sdev]) + off,
+                                 static_cast<size_t>(nb), flags + slot0[static_cast<size_t>(sdev)] + c, sdev, off});
+            ex->stage_bytes += nb;
+          }
+        }
+      }
+    }
+    if (!ex->ce.empty() || !ex->stage.empty()) {
       check_cuda(cudaStreamCreateWithFlags(&ex->ce_stream, cudaStreamNonBlocking), "cudaStreamCreate");
       check_cuda(cudaEventCreateWithFlags(&ex->ce_fork, cudaEventDisableTiming), "cudaEventCreate");
       check_cuda(cudaEventCreateWithFlags(&ex->ce_join, cudaEventDisableTiming), "cudaEventCreate");
@@ -397,9 +508,10 @@ rr_status rr_exec_launch(rr_exec* ex, void* stream, int ctas) {
     ++ex->epoch;  // every rank launches phase 0 the same number of times
     auto st = static_cast<cudaStream_t>(stream);
     check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
-    if (!ex->ce.empty()) ce_issue(ex, st);
+    const bool side = !ex->ce.empty() || !ex->stage.empty();
+    if (side) ce_issue(ex, st);
     launch_phase(ex, ex->phase[0], stream, ctas);
-    if (!ex->ce.empty()) ce_join(ex, st);
+    if (side) ce_join(ex, st);
   });
 }
 
@@ -442,6 +554,14 @@ rr_status rr_exec_ce_runs(const rr_exec* ex, int* n_runs, int64_t* bytes) {
   });
 }
 
+rr_status rr_exec_stage_pushes(const rr_exec* ex, int* n_pushes, int64_t* bytes) {
+  return guarded([&] {
+    need(ex != nullptr && n_pushes != nullptr && bytes != nullptr, "null executor/output");
+    *n_pushes = static_cast<int>(ex->stage.size());
+    *bytes = ex->stage_bytes;
+  });
+}
+
 rr_status rr_exec_relay_timeouts(rr_exec* ex, int64_t* timeouts) {
   return guarded([&] {
     need(ex != nullptr, "null executor");
@@ -449,6 +569,10 @@ rr_status rr_exec_relay_timeouts(rr_exec* ex, int64_t* timeouts) {
     unsigned int h[4];
     check_cuda(cudaMemcpy(h, ex->d_sched, sizeof(h), cudaMemcpyDeviceToHost), "read relay status");
     *timeouts = h[2];
+    if (ex->d_sched2) {
+      check_cuda(cudaMemcpy(h, ex->d_sched2, sizeof(h), cudaMemcpyDeviceToHost), "read relay status");
+      *timeouts += h[2];
+    }
   });
 }
 
@@ -550,11 +674,17 @@ rr_status rr_exec_enable_onload(rr_exec* ex, int n_src, const int32_t* src_devic
     // Segment of each item: 0 = independent of the onload, 1 + c = needs chunk c.
     const rr::ItemSet& a = ex->phase0_host;
     const size_t n = a.items.size(), C = ex->chunks.size();
-    std::vector<std::vector<int>> seg_vec(C + 1), seg_other(C + 1);
+    std::vector<std::vector<int>> seg_vec(C + 2), seg_other(C + 2);
     for (size_t i = 0; i < n; ++i) {
       int seg = 0;
       const auto it = first_chunk.find(a.src_dev[i]);
-      if (a.items[i].wait_flag) {
+      if (a.items[i].wait_flag && ex->stage_ctas > 0) {
+        // Staged unpack: its pieces come from the other GPUs' copy engines,
+        // which never wait for a kernel here, so it runs from the start on
+        // its own stream (rr_exec_launch_onload), unpacking while the onload
+        // is still running.
+        seg = static_cast<int>(C) + 1;
+      } else if (a.items[i].wait_flag) {
         // Relay / overlapped fan-out items wait on other GPUs' pushes, which
         // may depend on this GPU's own pushes: launch them after every chunk
         // (and so every push of this GPU) so no launch waits on a later one.
@@ -571,8 +701,8 @@ rr_status rr_exec_enable_onload(rr_exec* ex, int n_src, const int32_t* src_devic
     }
     std::vector<rr::CopyItem> ordered;
     ordered.reserve(n);
-    ex->segments.assign(C + 1, {});
-    for (size_t s = 0; s <= C; ++s) {
+    ex->segments.assign(C + 2, {});
+    for (size_t s = 0; s <= C + 1; ++s) {
       auto& sg = ex->segments[s];
       sg.offset = static_cast<int>(ordered.size());
       for (int i : seg_vec[s]) ordered.push_back(a.items[static_cast<size_t>(i)]);
@@ -618,12 +748,45 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
                  "onload cudaMemcpyAsync");
       check_cuda(cudaEventRecord(ex->events[c], cs), "cudaEventRecord");
     }
+    if (!ex->ce.empty() || !ex->stage.empty()) {
+      check_cuda(cudaEventRecord(ex->ce_fork, ks), "cudaEventRecord(ce fork)");
+      check_cuda(cudaStreamWaitEvent(ex->ce_stream, ex->ce_fork, 0), "cudaStreamWaitEvent(ce fork)");
+    }
+    if (!ex->stage.empty()) {
+      // Staged pushes follow the onload of the bytes they send: each waits
+      // for the chunk holding its last byte (chunks land in order per
+      // device). While the host link is the bottleneck the rotation order
+      // would hold every later round back until the whole onload is done, so
+      // pushes go out in the order their bytes land, each piece to every
+      // receiver in turn.
+      std::vector<std::pair<int, size_t>> order;  // (last chunk, push index)
+      for (size_t i = 0; i < ex->stage.size(); ++i) {
+        const auto& p = ex->stage[i];
+        int last = -1;
+        for (size_t k = 0; k < ex->chunks.size(); ++k) {
+          const auto& ch = ex->chunks[k];
+          if (ch.device == p.src_dev && ch.offset < p.src_off + static_cast<int64_t>(p.bytes)) last = static_cast<int>(k);
+        }
+        order.push_back({last, i});
+      }
+      std::stable_sort(order.begin(), order.end(),
+                       [](const auto& a, const auto& b) { return a.first < b.first; });
+      int waited = -1;
+      for (const auto& [last, i] : order) {
+        const auto& p = ex->stage[i];
+        if (last > waited) {
+          check_cuda(cudaStreamWaitEvent(ex->ce_stream, ex->events[static_cast<size_t>(last)], 0),
+                     "cudaStreamWaitEvent(staged push)");
+          waited = last;
+        }
+        check_cuda(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "staged push");
+        check_cuda(rr::launch_signal(p.flag, ex->epoch, ex->ce_stream), "staged push signal");
+      }
+    }
     if (!ex->ce.empty()) {
       // Copy-engine runs follow the onload: the part of a run that reads
       // chunk c starts once chunk c has landed; runs over sources that are
       // not onloaded start right away.
-      check_cuda(cudaEventRecord(ex->ce_fork, ks), "cudaEventRecord(ce fork)");
-      check_cuda(cudaStreamWaitEvent(ex->ce_stream, ex->ce_fork, 0), "cudaStreamWaitEvent(ce fork)");
       auto onloaded = [&](DeviceId d) {
         return std::any_of(ex->chunks.begin(), ex->chunks.end(), [&](const rr_exec::Chunk& ch) { return ch.device == d; });
       };
@@ -648,18 +811,33 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
           if (c.src_dev == ch.device) piece(c, ch.offset, ch.offset + ch.bytes);
       }
     }
-    for (size_t s = 0; s < ex->segments.size(); ++s) {
-      if (s > 0) check_cuda(cudaStreamWaitEvent(ks, ex->events[s - 1], 0), "cudaStreamWaitEvent");
-      const auto& sg = ex->segments[s];
-      if (sg.n == 0) continue;
+    auto segment_phase = [&](const rr_exec::Segment& sg) {
       rr_exec::Phase ph;
       ph.d = ex->d_onload + sg.offset;
       ph.n = sg.n;
       ph.n_vec = sg.n_vec;
       ph.flagged = ex->phase[0].flagged;
+      return ph;
+    };
+    const auto& staged_seg = ex->segments.back();  // C + 1: staged unpack
+    if (staged_seg.n > 0) {
+      check_cuda(cudaEventRecord(ex->unpack_fork, ks), "cudaEventRecord(unpack fork)");
+      check_cuda(cudaStreamWaitEvent(ex->unpack_stream, ex->unpack_fork, 0), "cudaStreamWaitEvent(unpack fork)");
+      launch_phase(ex, segment_phase(staged_seg), ex->unpack_stream, ctas, ex->d_sched2);
+    }
+    for (size_t s = 0; s + 1 < ex->segments.size(); ++s) {
+      if (s > 0) check_cuda(cudaStreamWaitEvent(ks, ex->events[s - 1], 0), "cudaStreamWaitEvent");
+      const auto& sg = ex->segments[s];
+      if (sg.n == 0) continue;
+      rr_exec::Phase ph = segment_phase(sg);
+      if (ex->stage_ctas > 0) ph.flagged = false;  // local copies only: the plain-phase kernel
       launch_phase(ex, ph, stream, ctas);
     }
-    if (!ex->ce.empty()) ce_join(ex, ks);
+    if (staged_seg.n > 0) {
+      check_cuda(cudaEventRecord(ex->unpack_join, ex->unpack_stream), "cudaEventRecord(unpack join)");
+      check_cuda(cudaStreamWaitEvent(ks, ex->unpack_join, 0), "cudaStreamWaitEvent(unpack join)");
+    }
+    if (!ex->ce.empty() || !ex->stage.empty()) ce_join(ex, ks);
   });
 }
 

@@ -130,6 +130,38 @@ int64_t relay_slots(const std::vector<LoweredOp>& ops, const HostMap& hm) {
   return n;
 }
 
+std::vector<DeviceId> stage_sources(const std::vector<LoweredOp>& ops, const std::vector<int>& host, int h) {
+  std::vector<int> hosts(host.begin(), host.end());
+  std::sort(hosts.begin(), hosts.end());
+  hosts.erase(std::unique(hosts.begin(), hosts.end()), hosts.end());
+  const int H = static_cast<int>(hosts.size());
+  const int pos = static_cast<int>(std::find(hosts.begin(), hosts.end(), h) - hosts.begin());
+  std::vector<bool> needed(host.size(), false);
+  for (const auto& op : ops)
+    if (host[static_cast<size_t>(op.src)] != h)
+      for (DeviceId d : op.dst)
+        if (host[static_cast<size_t>(d)] == h) needed[static_cast<size_t>(op.src)] = true;
+  std::vector<DeviceId> out;
+  for (int r = 1; r < H; ++r) {
+    const int g = hosts[static_cast<size_t>((pos - r + H) % H)];
+    for (size_t s = 0; s < host.size(); ++s)
+      if (needed[s] && host[s] == g) out.push_back(static_cast<DeviceId>(s));
+  }
+  return out;
+}
+
+std::vector<int64_t> stage_slots(const std::vector<LoweredOp>& ops, const std::vector<int>& host, int h,
+                                 const std::vector<int64_t>& src_bytes, int64_t chunk, int64_t* n_slots) {
+  std::vector<int64_t> slot0(host.size(), -1);
+  int64_t n = 0;
+  for (DeviceId s : stage_sources(ops, host, h)) {
+    slot0[static_cast<size_t>(s)] = n;
+    n += (src_bytes[static_cast<size_t>(s)] + chunk - 1) / chunk;
+  }
+  *n_slots = n;
+  return slot0;
+}
+
 std::vector<Job> build_jobs(const std::vector<LoweredOp>& ops, const HostMap& hm, int mode) {
   std::vector<Job> jobs;
   if (!hm.hierarchical) {
@@ -259,10 +291,11 @@ std::vector<Job> build_jobs(const std::vector<LoweredOp>& ops, const HostMap& hm
       j.phase = 0;
       j.src = op.src;
       j.op = &op;
-      j.dsts = hs == hm.me ? mine->second : std::vector<DeviceId>{mine->second.front()};
+      const bool all_local = hs == hm.me || hm.stage_chunk > 0;  // staged: the source is local memory
+      j.dsts = all_local ? mine->second : std::vector<DeviceId>{mine->second.front()};
       jobs.push_back(std::move(j));
     }
-    if (hs != hm.me && mine != groups.end() && mine->second.size() > 1) {
+    if (hs != hm.me && mine != groups.end() && mine->second.size() > 1 && !(mode == 1 && hm.stage_chunk > 0)) {
       Job j;
       j.phase = 1;
       j.src = mine->second.front();
@@ -357,6 +390,10 @@ struct Tagged {
 struct RelayTags {
   uint64_t wait_base = 0, signal_base = 0;
   int64_t* slot = nullptr;
+  // staged gather: wait on stage_base + 4 * (stage_slot0 + piece of the
+  // item's last source byte)
+  uint64_t stage_base = 0;
+  int64_t stage_slot0 = 0, stage_chunk = 0;
 };
 
 void add_rect(std::vector<Tagged>& out, ItemSet& acc, uint64_t src, const std::vector<uint64_t>& dsts,
@@ -391,7 +428,10 @@ void add_rect(std::vector<Tagged>& out, ItemSet& acc, uint64_t src, const std::v
       if (relay.wait_base) it.wait_flag = relay.wait_base + off;
       if (relay.signal_base) it.signal_flag = relay.signal_base + off;
     }
-    out.push_back({it, src_dev, src_begin + ((rows - 1) * sp + cols) * unit, src_is_dst});
+    const int64_t src_end = src_begin + ((rows - 1) * sp + cols) * unit;
+    if (relay.stage_base)
+      it.wait_flag = relay.stage_base + 4u * static_cast<uint64_t>(relay.stage_slot0 + (src_end - 1) / relay.stage_chunk);
+    out.push_back({it, src_dev, src_end, src_is_dst});
     const int64_t bytes = rows * cols * unit;
     acc.read += bytes;
     acc.written += bytes * static_cast<int64_t>(dsts.size());
@@ -474,6 +514,15 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
           add_rect(streams.back(), acc, s, dsts, r, hm.relay_chunk, mc0, j.src, j.src_is_dst_buffer, tags);
           continue;
         }
+        if (hm.stage_chunk > 0 && phase == 0 && hm.host[static_cast<size_t>(j.src)] != hm.me) {
+          RelayTags tags;  // reads a staging buffer: wait for the piece
+          tags.stage_base = accounting ? 4 : hm.stage_flags;  // nonzero in accounting mode too
+          tags.stage_slot0 = hm.stage_slot0.at(static_cast<size_t>(j.src));
+          tags.stage_chunk = hm.stage_chunk;
+          if (tags.stage_slot0 < 0) throw rlplan::ValidationError("staged source without slots");
+          add_rect(streams.back(), acc, s, *to, r, chunk_bytes, mc0, j.src, j.src_is_dst_buffer, tags);
+          continue;
+        }
         add_rect(streams.back(), acc, s, *to, r, chunk_bytes, mc0, j.src, j.src_is_dst_buffer);
       }
     }
@@ -511,6 +560,15 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
           (tma ? vec_items : other).push_back(&st[k]);
           ++seen;
         }
+  if (hm.stage_chunk > 0) {
+    // staged gather: items that can run now first, then the staged ones in
+    // the order their pieces arrive (slot order)
+    for (auto* list : {&vec_items, &other}) {
+      std::stable_sort(list->begin(), list->end(), [](const Tagged* a, const Tagged* b) {
+        return a->it.wait_flag < b->it.wait_flag;  // 0 (no wait) first
+      });
+    }
+  }
   acc.n_vec = static_cast<int>(vec_items.size());
   vec_items.insert(vec_items.end(), other.begin(), other.end());
   if (vec_items.size() >= (size_t{1} << 31)) throw rlplan::ValidationError("too many copy items");

@@ -52,7 +52,27 @@ struct HostMap {
   // lands, inside phase 0 (no separate fan-out phase).
   bool relay_chain = true;
   bool relay_star = false;
+  // Staged gather (pull mode): the remote source shards this host reads
+  // arrive whole in local staging buffers (passed as their source buffers),
+  // pushed by their hosts' copy engines in stage_chunk pieces, each piece
+  // flagged in this host's stage flag array (stage_flags, mapped here).
+  // Every local destination is written directly (no fan-out phase), and an
+  // item reading staged bytes waits for the piece holding its last byte.
+  int64_t stage_chunk = 0;               // 0 = off
+  uint64_t stage_flags = 0;
+  std::vector<int64_t> stage_slot0;      // per plan device: its first slot here, -1 = not staged
 };
+
+// Staged gather: the remote sources host `h` reads, in arrival order. Round
+// r = 1..H-1 (H = number of hosts, hosts ranked by id) brings the sources
+// held by the host r places before h, so in every round each host receives
+// from exactly one host and sends to exactly one.
+std::vector<rlplan::DeviceId> stage_sources(const std::vector<rlplan::LoweredOp>& ops, const std::vector<int>& host,
+                                            int h);
+// Slot of every staged source's first piece in host h's flag array (-1 for
+// the others), and the array length.
+std::vector<int64_t> stage_slots(const std::vector<rlplan::LoweredOp>& ops, const std::vector<int>& host, int h,
+                                 const std::vector<int64_t>& src_bytes, int64_t chunk, int64_t* n_slots);
 
 // Relay slots a plan needs (flag array length, identical on every rank).
 int64_t relay_slots(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm);

@@ -509,7 +509,19 @@ __global__ void rr_barrier_kernel(uint32_t* const* __restrict__ flags, int rank,
   __syncthreads();
 }
 
+// Staged gather: release one piece to the host that waits for it, after
+// the copy-engine copy queued before this kernel on the same stream.
+__global__ void rr_signal_kernel(uint32_t* flag, uint32_t epoch) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+}
+
 }  // namespace
+
+int launch_signal(uint32_t* flag, uint32_t epoch, void* stream) {
+  rr_signal_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag, epoch);
+  return cudaGetLastError();
+}
 
 int copy_max_ctas(int* ctas_per_sm, int* sms) {
   int dev = 0;

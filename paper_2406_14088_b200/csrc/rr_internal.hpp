@@ -90,6 +90,7 @@ constexpr int kBulkVariants = 16;
 int launch_fill(const FillItem* items, int n_items, uint64_t seed, void* stream);
 int launch_verify(const FillItem* items, int n_items, uint64_t seed, unsigned long long* counters,
                   uint64_t buf_base, void* stream);
+int launch_signal(uint32_t* flag, uint32_t epoch, void* stream);
 int launch_barrier(uint32_t* const* flags, int rank, int world, uint32_t epoch, int* timed_out,
                    void* stream);
 

@@ -143,7 +143,9 @@ class Executor:
                  local: Iterable[int], mode: int = PUSH, chunk_bytes: int = 0,
                  host_of: Optional[Sequence[int]] = None, mc_ptrs: Optional[Dict[int, int]] = None,
                  relay_flags: Optional[Dict[int, int]] = None, relay_chain: bool = True,
-                 overlap_fanout: bool = False, ce_min_run_bytes: int = 0):
+                 overlap_fanout: bool = False, ce_min_run_bytes: int = 0, stage_chunk_bytes: int = 0,
+                 n_hosts: int = 0, stage_remote: Optional[Dict[Tuple[int, int], int]] = None,
+                 stage_flags: Optional[Dict[int, int]] = None):
         n = plan.cluster.device_count()
         self.plan = plan
         sp, dp = (ctypes.c_void_p * n)(), (ctypes.c_void_p * n)()
@@ -164,8 +166,16 @@ class Executor:
             rfl = (ctypes.c_void_p * n)()
             for d, p in relay_flags.items():
                 rfl[d] = p
+        srem = sfl = None
+        if stage_chunk_bytes:
+            srem = (ctypes.c_void_p * (n * n_hosts))()
+            for (d, h), p in (stage_remote or {}).items():
+                srem[d * n_hosts + h] = p
+            sfl = (ctypes.c_void_p * n_hosts)()
+            for h, p in (stage_flags or {}).items():
+                sfl[h] = p
         opt = RrExecOptions(mode, chunk_bytes, hosts, mcs, rfl, int(relay_chain), int(overlap_fanout),
-                            ce_min_run_bytes)
+                            ce_min_run_bytes, stage_chunk_bytes, n_hosts, srem, sfl)
         h = ctypes.c_void_p()
         check(lib.rr_exec_create_ex(plan.handle, cuda_device, n, sp, dp, len(loc), arr, ctypes.byref(opt),
                                     ctypes.byref(h)))
@@ -203,6 +213,12 @@ class Executor:
         """(copy-engine runs, their bytes) that launch() issues beside the kernels."""
         n, b = ctypes.c_int(), ctypes.c_int64()
         check(lib.rr_exec_ce_runs(self._h, ctypes.byref(n), ctypes.byref(b)))
+        return n.value, b.value
+
+    def stage_pushes(self) -> Tuple[int, int]:
+        """(staged-gather pieces, their bytes) that launch() pushes per call."""
+        n, b = ctypes.c_int(), ctypes.c_int64()
+        check(lib.rr_exec_stage_pushes(self._h, ctypes.byref(n), ctypes.byref(b)))
         return n.value, b.value
 
     def phase_kernels(self, phase: int = 0) -> Tuple[bool, int]:
@@ -343,6 +359,31 @@ def hosted_devices(n_plan_devices: int, rank: int, world: int) -> List[int]:
         raise ValueError(f"{world} ranks cannot evenly host {n_plan_devices} plan devices")
     k = n_plan_devices // world
     return list(range(rank * k, (rank + 1) * k))
+
+
+def _all_gather_shaped(plan: ReallocPlan, host_of: Sequence[int], world: int) -> bool:
+    """Every GPU both sends sources to and receives sources from others, and
+    no range moves as a copy-engine run already (stage remaps)."""
+    needs = [False] * world
+    sends = [False] * world
+    for s, dsts, _r in plan.lowered():
+        for d in dsts:
+            if host_of[d] != host_of[s]:
+                needs[host_of[d]] = True
+                sends[host_of[s]] = True
+    if not (all(needs) and all(sends)):
+        return False
+    n = plan.cluster.device_count()
+    return not any(plan.ce_runs([d for d in range(n) if host_of[d] == r], host_of) for r in range(world))
+
+
+def stage_slots(plan: ReallocPlan, host_of: Sequence[int], chunk_bytes: int) -> int:
+    """Length of the stage flag array every host allocates for a staged gather."""
+    n = plan.cluster.device_count()
+    hosts = (ctypes.c_int32 * n)(*host_of)
+    out = ctypes.c_int64()
+    check(lib.rr_plan_stage_slots(plan.handle, hosts, chunk_bytes, ctypes.byref(out)))
+    return out.value
 
 
 def relay_slots(plan: ReallocPlan, host_of: Sequence[int], chunk_bytes: int = 0, chain: bool = True,
@@ -493,7 +534,8 @@ class RankRealloc:
                  bind: Sequence[Tuple[str, str]], rank: int, world: int, cuda_device: int, group=None,
                  mode: int = PUSH, kernel: Optional[int] = DEFAULT_KERNEL, hierarchical: bool = True,
                  multicast: Sequence[str] = (), relay=False, overlap: bool = False,
-                 flag_kernel: int = DEFAULT_FLAG_KERNEL, chunk_bytes: int = 0, ce_min_run_bytes: int = 0):
+                 flag_kernel: int = DEFAULT_FLAG_KERNEL, chunk_bytes: int = 0, ce_min_run_bytes: int = 0,
+                 staged=False, stage_chunk_bytes: int = 512 << 20):
         """``multicast`` names shard sets whose per-GPU leader shards (the
         lowest-id plan device of the set on each GPU) are members of one NVLS
         multicast object: a payload bound for every GPU is then stored once
@@ -536,6 +578,22 @@ class RankRealloc:
                 self.relay_phases.append(pi)
             if overlap:
                 self.overlap_phases.append(pi)
+        # Staged gather (copy engines in rotation rounds, pull-mode unpack per
+        # piece) for phases whose destinations read sources on other GPUs.
+        # True: every such phase; "auto": from 4 GPUs on, all-gather-shaped
+        # phases (every GPU sends and receives) that copy-engine runs do not
+        # already cover. It replaces the overlapped fan-out of that phase.
+        self.staged_phases: List[int] = []
+        if staged and world > 1 and hierarchical and mode == PUSH:
+            for pi, (_sname, dname) in enumerate(bind):
+                if pi in self.relay_phases or dname in self.multicast:
+                    continue
+                p = self.plans[pi]
+                if staged == "auto" and (world < 4 or not _all_gather_shaped(p, host_of_all, world)):
+                    continue
+                if any(host_of_all[s] != host_of_all[d] for s, dsts, _r in p.lowered() for d in dsts):
+                    self.staged_phases.append(pi)
+            self.overlap_phases = [pi for pi in self.overlap_phases if pi not in self.staged_phases]
         self.relay_bufs: Dict[int, DeviceBuffer] = {}
         for pi in sorted(set(self.relay_phases) | set(self.overlap_phases)):
             slots = relay_slots(self.plans[pi], host_of_all, chunk_bytes, chain=pi in self.relay_phases,
@@ -544,6 +602,17 @@ class RankRealloc:
                 continue
             self.relay_bufs[pi] = DeviceBuffer(cuda_device, 4 * max(slots, 64))
             self.relay_bufs[pi].zero()
+        self.stage_bufs: Dict[int, Dict[int, DeviceBuffer]] = {}
+        self.stage_flag_bufs: Dict[int, DeviceBuffer] = {}
+        self.stage_chunk = stage_chunk_bytes
+        for pi in self.staged_phases:
+            p = self.plans[pi]
+            need = sorted({s for s, dsts, _r in p.lowered() if host_of_all[s] != rank and
+                           any(host_of_all[d] == rank for d in dsts)})
+            self.stage_bufs[pi] = {s: DeviceBuffer(cuda_device, p.shard_bytes(SRC, s)) for s in need}
+            slots = stage_slots(p, host_of_all, stage_chunk_bytes)
+            self.stage_flag_bufs[pi] = DeviceBuffer(cuda_device, 4 * max(slots, 64))
+            self.stage_flag_bufs[pi].zero()
         self.buffers: Dict[str, Dict[int, object]] = {}
         self.mc_tables: Dict[str, Dict[int, int]] = {}
         mc_leaders: Dict[str, int] = {}
@@ -585,6 +654,9 @@ class RankRealloc:
             mine["__flags__"] = {rank: self.flags.ipc_handle()}
             for pi, b in self.relay_bufs.items():
                 mine[f"__relay{pi}__"] = {rank: b.ipc_handle()}
+            for pi, bufs in self.stage_bufs.items():
+                mine[f"__stage{pi}__"] = {s: b.ipc_handle() for s, b in bufs.items()}
+                mine[f"__sflag{pi}__"] = {rank: self.stage_flag_bufs[pi].ipc_handle()}
         gathered: List[dict] = [None] * world  # type: ignore
         if world > 1:
             import torch.distributed as dist
@@ -597,17 +669,25 @@ class RankRealloc:
         flag_ptrs = [0] * world
         flag_ptrs[rank] = self.flags.ptr
         relay_remote: Dict[Tuple[int, int], int] = {}
+        stage_remote: Dict[int, Dict[Tuple[int, int], int]] = {pi: {} for pi in self.staged_phases}
+        stage_flags: Dict[int, Dict[int, int]] = {pi: {rank: b.ptr} for pi, b in self.stage_flag_bufs.items()}
         for r, table in enumerate(gathered):
             if r == rank:
                 continue
             for name, handles in table.items():
                 for d, h in handles.items():
+                    if name.startswith("__stage") and self.owner[d] != rank:
+                        continue  # another GPU's staging for a source not held here
                     p = open_ipc(cuda_device, h)
                     self._opened.append(p)
                     if name == "__flags__":
                         flag_ptrs[r] = p
                     elif name.startswith("__relay"):
                         relay_remote[(int(name[7:-2]), r)] = p
+                    elif name.startswith("__stage"):
+                        stage_remote[int(name[7:-2])][(d, r)] = p
+                    elif name.startswith("__sflag"):
+                        stage_flags[int(name[7:-2])][r] = p
                     else:
                         self.ptrs[name][d] = p
         self.barrier = Barrier(cuda_device, rank, world, flag_ptrs)
@@ -620,12 +700,23 @@ class RankRealloc:
                                 for d in range(n)}
         self.executors: List[Executor] = []
         for pi, (sname, dname) in enumerate(bind):
-            self.executors.append(Executor(self.plans[pi], cuda_device, self.ptrs[sname], self.ptrs[dname],
-                                           self.local, mode, chunk_bytes, host_of=host_of if hierarchical else None,
-                                           mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_tables.get(pi),
-                                           relay_chain=pi in self.relay_phases,
-                                           overlap_fanout=pi in self.overlap_phases,
-                                           ce_min_run_bytes=ce_min_run_bytes))
+            if pi in self.staged_phases:
+                # pull-mode unpack from local staging buffers; this GPU's own
+                # sources are pushed to the others by its copy engine
+                src = {d: ptr for d, ptr in self.ptrs[sname].items() if self.owner[d] == rank}
+                src.update({d: b.ptr for d, b in self.stage_bufs[pi].items()})
+                self.executors.append(Executor(self.plans[pi], cuda_device, src, self.ptrs[dname], self.local, PULL,
+                                               chunk_bytes, host_of=host_of, stage_chunk_bytes=self.stage_chunk,
+                                               n_hosts=world, stage_remote=stage_remote[pi],
+                                               stage_flags=stage_flags[pi]))
+            else:
+                self.executors.append(Executor(self.plans[pi], cuda_device, self.ptrs[sname], self.ptrs[dname],
+                                               self.local, mode, chunk_bytes,
+                                               host_of=host_of if hierarchical else None,
+                                               mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_tables.get(pi),
+                                               relay_chain=pi in self.relay_phases,
+                                               overlap_fanout=pi in self.overlap_phases,
+                                               ce_min_run_bytes=ce_min_run_bytes))
             if kernel is not None:
                 self.executors[-1].set_kernel(kernel)
             self.executors[-1].set_flag_kernel(flag_kernel)
@@ -697,6 +788,11 @@ class RankRealloc:
             for b in bufs.values():
                 b.free()
         for b in self.relay_bufs.values():
+            b.free()
+        for bufs in self.stage_bufs.values():
+            for b in bufs.values():
+                b.free()
+        for b in self.stage_flag_bufs.values():
             b.free()
         self.flags.free()
 

@@ -243,6 +243,45 @@ def main() -> int:
                 failures.append(f"ce {sp}->{dp}: barrier timed out")
             dist.barrier()
             rr.close()
+    # Staged gather (copy-engine rotation + per-piece unpack), small pieces.
+    staged_total = 0
+    for sp, dp in (((1, 1, 8, 0, 0), (1, 8, 1, 0, 0)), ((2, 1, 4, 1, 1), (1, 1, 8, 0, 0)),
+                   ((1, 2, 4, 0, 0), (4, 1, 2, 2, 1)), ((1, 8, 1, 0, 0), (1, 1, 8, 0, 0))):
+        src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
+        dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
+        plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
+        rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
+                           staged=True, stage_chunk_bytes=64 << 10)
+        staged_total += len(rr.staged_phases)
+        for d, b in rr.buffers["a"].items():
+            R.fill_shard(plan, R.SRC, d, b.ptr, 91)
+        for onload in (False, True, False):  # repeated launches exercise the flag epochs
+            for b in rr.buffers["b"].values():
+                b.zero()
+            torch.cuda.synchronize()
+            dist.barrier()
+            if onload:
+                host = {d: R.HostBuffer(plan.shard_bytes(R.SRC, d)) for d in rr.buffers["a"]}
+                for d, hb in host.items():
+                    hb.array()[:] = rr.buffers["a"][d].to_host()
+                rr.run_phase_onload(0, {d: hb.ptr for d, hb in host.items()}, torch.cuda.Stream(),
+                                    chunk_bytes=64 << 10)
+            else:
+                rr.run_phase(0)
+            torch.cuda.synchronize()
+            for d, b in rr.buffers["b"].items():
+                bad, first = R.verify_shard(plan, R.DST, d, b.ptr, 91)
+                if bad:
+                    failures.append(f"staged {sp}->{dp} onload {onload}: device {d} {bad} mismatches")
+            if onload:
+                for hb in host.values():
+                    hb.free()
+        if rr.relay_timeouts() or rr.barrier.timed_out():
+            failures.append(f"staged {sp}->{dp}: flag or barrier timeouts")
+        dist.barrier()
+        rr.close()
+    if world > 1 and staged_total == 0:
+        failures.append("staged cases ran no staged phase")
     if world > 1 and not oversub:
         t = torch.tensor([ce_total], device="cuda")
         dist.all_reduce(t)

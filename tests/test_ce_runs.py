@@ -57,3 +57,19 @@ def test_runs_are_byte_identical(sp, dp, world):
         # every cross-host byte of a pure stage remap goes through runs
         wire = sum(plan.work([d for d in range(8) if host_of[d] == r], 0, host_of)["wire_in"] for r in range(world))
         assert total >= 0.98 * wire, (total, wire)
+
+
+@pytest.mark.parametrize("world,expect", [(2, 4 * 4), (4, 6 * 4), (8, 7 * 4)])
+def test_stage_slots_7b_all_gather(world, expect):
+    """Staged gather (rr_plan_stage_slots): every host receives the tp8
+    source shards it does not hold, each in ceil(2.008 GB / 512 MiB) = 4
+    pieces."""
+    from paper_2406_14088_b200 import runtime as R
+    from paper_2406_14088_b200.workloads import WORKLOADS
+    w = WORKLOADS["llama7b_tp8_dp8_roundtrip"]
+    plan = plan_param_realloc(w.model, *w.phases[0], w.cluster(), BALANCED)
+    host_of = _hosts(8, world)
+    assert R.stage_slots(plan, host_of, 512 << 20) == expect
+    # the gen -> train phase reads only local replicas: nothing to stage
+    back = plan_param_realloc(w.model, *w.phases[1], w.cluster(), BALANCED)
+    assert R.stage_slots(back, host_of, 512 << 20) == 0

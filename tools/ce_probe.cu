@@ -9,6 +9,10 @@
 //   mix/<pct>        pct% of each peer's bytes by CE (one stream per peer),
 //                    the rest by the SM kernel at the same time
 //   h2d/<M>[x<s>]    pinned host -> device, M MiB pieces over s streams
+//   rot/ce           all-to-all as G-1 rounds on ONE stream: round r sends the
+//                    whole slice to peer (d + r) % G, so every round is a
+//                    permutation (each GPU receives from exactly one peer)
+//   rot/cepull       the same rounds with each GPU's engine pulling from (d - r) % G
 //   pair/sm, pair/ce GPUs paired (d <-> d^1), each pushes 2 GiB to its partner
 //                    only (a pipeline-stage remap's pattern): SM stores vs one
 //                    whole copy-engine copy
@@ -173,6 +177,18 @@ int main(int argc, char** argv) {
                            st[d][kMax]));
     }));
   }
+  report("rot/ce", egress, timed([&](int d) {
+    for (int r = 1; r < G; ++r) {
+      const int p = (d + r) % G;
+      CK(cudaMemcpyAsync(dst[p] + size_t(d) * S, src[d] + size_t(p) * S, S, cudaMemcpyDefault, st[d][kMax]));
+    }
+  }));
+  report("rot/cepull", egress, timed([&](int d) {  // the same rounds, each GPU's engine pulling from its peer
+    for (int r = 1; r < G; ++r) {
+      const int p = (d - r + G) % G;
+      CK(cudaMemcpyAsync(dst[d] + size_t(p) * S, src[p] + size_t(d) * S, S, cudaMemcpyDefault, st[d][kMax]));
+    }
+  }));
   report("a2a/sm", egress, timed([&](int d) { k_a2a<<<ctas, 512, 0, st[d][kMax]>>>(src[d], t, d, G, S, 0); }));
   report("a2a/ce-whole", egress, timed([&](int d) { enqueue_ce(d, S, true, 0); }));
   for (int m : {1, 4, 16}) {
