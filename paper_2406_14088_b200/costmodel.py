@@ -35,6 +35,7 @@ class B200Profile:
     nvlink_push_gbs: float = 708.0      # per GPU per direction, SM peer stores (2/4 GPUs, all-to-all)
     nvlink_mc_gbs: float = 565.0        # per receiving GPU, NVLS multimem.st (4 GPUs)
     nvlink_ce_gbs: float = 777.0        # per GPU per direction, whole copy-engine copies, pairwise (2/4 GPUs)
+    nvlink_ce_rot_gbs: float = 771.0    # copy-engine rotation rounds (staged gather), 4 GPUs
     launch_us: float = 8.0              # kernel launch + dynamic-scheduler tail
     barrier_us: float = 12.0            # cross-GPU flag barrier
     host_link_gbs: float = 55.6         # pinned host <-> HBM per GPU, either direction (r01 ce_probe h2d/*)
@@ -49,7 +50,8 @@ def host_transfer_seconds(nbytes_per_gpu: int, profile: B200Profile = B200Profil
 
 def estimate_seconds(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
                      profile: B200Profile = B200Profile(), multicast: bool = False,
-                     relay: bool = False, onload: bool = False, copy_engine: bool = True) -> Dict[str, float]:
+                     relay: bool = False, onload: bool = False, copy_engine: bool = True,
+                     staged: bool = False) -> Dict[str, float]:
     """Estimated execution time of `plan` with plan device d hosted on GPU
     host_of[d] (default: one GPU per plan device). `relay`: payloads reaching
     >= 2 other GPUs use the pipelined relay (one copy in and out per GPU,
@@ -57,7 +59,9 @@ def estimate_seconds(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
     pinned host memory pipelined with phase 0 (rr_exec_launch_onload).
     `copy_engine`: ranges laid out identically on both sides move as
     copy-engine runs (the executor default; not combined with relay or
-    multicast here)."""
+    multicast here). `staged`: the remote bytes move as a staged gather
+    (copy-engine rotation rounds into staging buffers, then an unpack that
+    reads them once more from HBM)."""
     n = plan.cluster.device_count()
     host = list(host_of) if host_of is not None else list(range(n))
     hosts = sorted(set(host))
@@ -110,7 +114,14 @@ def estimate_seconds(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
             egress[h] = max(0, egress[h] - ce_out[h])
             ingress[h] = max(0, ingress[h] - ce_in[h])
 
+    if staged and len(hosts) > 1:
+        for h in hosts:
+            hbm[h] += 2 * ingress[h] + fan[h]  # staging written, read back; the unpack writes every replica
+            fan[h] = 0
+
     def link_s(h: int) -> float:
+        if staged:
+            return max(egress[h], ingress[h]) / (profile.nvlink_ce_rot_gbs * 1e9)
         out = egress[h] / (profile.nvlink_push_gbs * 1e9) + ce_out[h] / (profile.nvlink_ce_gbs * 1e9)
         inn = ingress[h] / (profile.nvlink_push_gbs * 1e9) + ce_in[h] / (profile.nvlink_ce_gbs * 1e9)
         return max(out, inn) + mc_in[h] / (profile.nvlink_mc_gbs * 1e9)

@@ -84,6 +84,16 @@ def test_cost_model_matches_round1_measurements(gpus, measured_ms, tol):
     assert est["phase0_s"] * 1e3 == pytest.approx(measured_ms, rel=tol)
 
 
+def test_cost_model_staged_gather():
+    """7B tp8->dp8 forward at 4 GPUs with the staged gather (bench default
+    from 4 GPUs on): 16.25 ms measured (profiles/r01_staged_ab_n4.txt)."""
+    w = WORKLOADS["llama7b_tp8_dp8_roundtrip"]
+    plan = plan_param_realloc(w.model, *w.phases[0], w.cluster(), BALANCED)
+    host_of = [d // 2 for d in range(8)]
+    est = costmodel.estimate_seconds(plan, host_of, staged=True)
+    assert est["phase0_s"] * 1e3 == pytest.approx(16.25, rel=0.05)
+
+
 @pytest.mark.parametrize("gpus,measured_ms,ce", [
     (2, 18.54, True),    # 13B stage remap with copy-engine runs (profiles/r01_configs_n2.jsonl)
     (4, 9.32, True),     # (profiles/r01_configs_n4.jsonl)
