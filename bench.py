@@ -465,6 +465,13 @@ def run_b200(args) -> None:
                                                                "~710, one copy-engine copy ~780 GB/s; "
                                                                "profiles/r01_nvlink_probe_n2.txt)",
                     "algorithmic_bytes_per_launch": int(dom_wire)}
+            if dom in rr.staged_phases or rr.executors[dom].ce_runs()[0] > 0:
+                # copy engines carry (most of) this phase's link bytes: the SM
+                # stores' protocol factor does not apply to them
+                roof.update({"traffic": None, "wire_frac_incl_protocol": None,
+                             "traffic_source": "copy-engine transfers: no per-kernel ncu counter",
+                             "kernel": ("copy engines (staged gather) + " if dom in rr.staged_phases
+                                        else "copy-engine runs + ") + kname})
             if hbm_roof["frac"] > roof["frac"]:
                 hbm_roof.update({"traffic": None, "kernel": kname, "phase": dom,
                                  "per_gpu": "max over ranks of this GPU's reads + stores landing in its HBM",

@@ -362,16 +362,29 @@ def hosted_devices(n_plan_devices: int, rank: int, world: int) -> List[int]:
 
 
 def _all_gather_shaped(plan: ReallocPlan, host_of: Sequence[int], world: int) -> bool:
-    """Every GPU both sends sources to and receives sources from others, and
+    """Every GPU both sends sources to and receives sources from others,
+    every GPU that reads a remote source shard reads (>= 98% of) all of it
+    (the staged gather moves whole shards), each GPU receives >= 1 GiB, and
     no range moves as a copy-engine run already (stage remaps)."""
     needs = [False] * world
     sends = [False] * world
-    for s, dsts, _r in plan.lowered():
-        for d in dsts:
-            if host_of[d] != host_of[s]:
-                needs[host_of[d]] = True
-                sends[host_of[s]] = True
+    read: Dict[Tuple[int, int], int] = {}
+    for s, dsts, rects in plan.lowered():
+        b = sum(r[2] * r[5] for r in rects)
+        for h in {host_of[d] for d in dsts if host_of[d] != host_of[s]}:
+            needs[h] = True
+            sends[host_of[s]] = True
+            read[(s, h)] = read.get((s, h), 0) + b
     if not (all(needs) and all(sends)):
+        return False
+    if any(b * 50 < plan.shard_bytes(SRC, s) * 49 for (s, _h), b in read.items()):
+        return False
+    # small phases stay on SM stores: copy-engine submissions and piece
+    # signals cost microseconds each
+    received = [0] * world
+    for (s, h), b in read.items():
+        received[h] += b
+    if min(received) < (1 << 30):
         return False
     n = plan.cluster.device_count()
     return not any(plan.ce_runs([d for d in range(n) if host_of[d] == r], host_of) for r in range(world))

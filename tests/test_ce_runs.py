@@ -73,3 +73,19 @@ def test_stage_slots_7b_all_gather(world, expect):
     # the gen -> train phase reads only local replicas: nothing to stage
     back = plan_param_realloc(w.model, *w.phases[1], w.cluster(), BALANCED)
     assert R.stage_slots(back, host_of, 512 << 20) == 0
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_staged_auto_policy(world):
+    """RankRealloc(staged="auto") stages only all-gather-shaped phases whose
+    receivers read whole remote shards (7B tp8 -> dp8), never the partial
+    TP-change reads of 34B/70B (whole shards would cross the links 2-4x),
+    stage remaps (copy-engine runs), single-source broadcasts or small data
+    phases."""
+    from paper_2406_14088_b200 import runtime as R
+    from paper_2406_14088_b200.workloads import WORKLOADS
+    host_of = _hosts(8, world)
+    picked = {name: [R._all_gather_shaped(p, host_of, world) for p in w.plans(BALANCED)]
+              for name, w in WORKLOADS.items() if w.devices == 8}
+    assert picked.pop("llama7b_tp8_dp8_roundtrip") == [True, False]
+    assert not any(any(v) for v in picked.values()), picked
