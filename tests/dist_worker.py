@@ -168,6 +168,7 @@ def main() -> int:
     fuzz_models = [TINY_GQA, dataclasses.replace(TINY_GQA, name="tiny_mqa", num_attention_heads=8, num_kv_heads=1,
                                                  num_layers=3)]
     ce_cases = 0  # fuzz cases in which this rank issued copy-engine runs
+    staged_cases = 0  # fuzz cases with a staged-gather phase
     for i in range(int(os.environ.get("RR_FUZZ_CASES", "24"))):
         fm = fuzz_models[i % 2]
         src, dst = random_placement(rng, fm), random_placement(rng, fm)
@@ -178,11 +179,14 @@ def main() -> int:
         kernel = rng.choice([0, 1, 5])
         chunk = rng.choice([0, 8192, 65536])
         ce = rng.choice([-1, 0, 4096])  # copy-engine runs: off, default (256 MiB: none here), >= 4 KiB
+        staged = rng.random() < 0.25    # staged gather (push mode, hierarchical, no relay), 32 KiB pieces
         plan = plan_param_realloc(fm, src, dst, c, rng.choice([0, 1]))
         rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
                            mode=mode, kernel=kernel, flag_kernel=kernel, hierarchical=hier, relay=relay,
-                           overlap=overlap, chunk_bytes=chunk, ce_min_run_bytes=ce)
+                           overlap=overlap, chunk_bytes=chunk, ce_min_run_bytes=ce, staged=staged,
+                           stage_chunk_bytes=32 << 10)
         ce_cases += int(any(e.ce_runs()[0] for e in rr.executors))
+        staged_cases += int(bool(rr.staged_phases))
         for d, b in rr.buffers["a"].items():
             R.fill_shard(plan, R.SRC, d, b.ptr, 50 + i)
         for rep in range(2):
@@ -197,7 +201,7 @@ def main() -> int:
                 want = O.fill(fm, dst, c, d, 50 + i)
                 if not np.array_equal(got, want):
                     failures.append(f"fuzz {i} {src}->{dst} mode {mode} hier {hier} relay {relay} overlap {overlap} "
-                                    f"kernel {kernel} chunk {chunk} ce {ce} rep {rep}: device {d} differs in "
+                                    f"kernel {kernel} chunk {chunk} ce {ce} staged {rr.staged_phases} rep {rep}: device {d} differs in "
                                     f"{int(np.count_nonzero(got != want))} elements")
         if rr.relay_timeouts() or rr.barrier.timed_out():
             failures.append(f"fuzz {i}: flag or barrier timeouts")
@@ -312,7 +316,8 @@ def main() -> int:
     for f in failures:
         print(f"rank {rank}: {f}", flush=True)
     if rank == 0:
-        print(f"dist_worker: fuzz cases with copy-engine runs on rank 0: {ce_cases}", flush=True)
+        print(f"dist_worker: fuzz cases with copy-engine runs on rank 0: {ce_cases}, staged: {staged_cases}",
+              flush=True)
         print(f"dist_worker world={world}: {'OK' if flag.item() == 0 else 'FAILED'}", flush=True)
     dist.destroy_process_group()
     return 0 if flag.item() == 0 else 1
