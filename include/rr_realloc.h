@@ -220,8 +220,9 @@ rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices,
 rr_status rr_exec_launch(rr_exec* ex, void* stream, int ctas);
 /* Phase 1 (in-host fan-out from leader replicas); no-op when empty. */
 rr_status rr_exec_launch_fanout(rr_exec* ex, void* stream, int ctas);
-/* Copy kernel: 0 = vectorised LDG/STG kernel; 1..16 = TMA bulk-copy ring
- * variants (cp.async.bulk through shared-memory stages; default 1).
+/* Copy kernel: 0 = vectorised LDG/STG kernel; 1 or 5 = TMA bulk-copy ring
+ * (cp.async.bulk through shared-memory stages; 1 = 4 x 16 KiB stages, the
+ * default; 5 = 3 x 16 KiB stages). Other values: RR_EINVAL.
  * 2-byte-aligned and multicast items always take the LDG/STG kernel.
  * Without this call, a plain phase storing fewer than the small-phase bytes
  * (default 64 MiB, rr_exec_set_small_phase_bytes; 0 = never) takes the
@@ -275,8 +276,11 @@ typedef struct {
   const int32_t* host_of;     /* NULL = flat delivery */
   void* const* mc_bufs;       /* NULL = no multicast */
   /* Pipelined relay (push, hierarchical): relay_flags[d] = the uint32 flag
-   * array (rr_plan_relay_slots entries, zeroed once, mapped here) of plan
-   * device d's host. A payload reaching >= 2 other hosts then travels
+   * array (rr_plan_relay_slots entries, mapped here) of plan device d's host.
+   * Each array belongs to exactly one executor per host and must be zero when
+   * that executor is created (epochs restart at 1 in every executor, so stale
+   * values would release waits early): rr_exec_create_ex reads this host's
+   * array and fails with RR_EINVAL if it is not zero. A payload reaching >= 2 other hosts then travels
    * source -> host 1 -> host 2 ... chunk by chunk, each host forwarding and
    * fanning out locally as chunks land. NULL = no relay. */
   void* const* relay_flags;
@@ -298,8 +302,11 @@ typedef struct {
    * remote source d is this host's staging buffer for d.
    * stage_remote[d * n_hosts + h]: host h's staging buffer for local source
    * d, mapped here (NULL where h does not read d). stage_flags[h]: host h's
-   * stage flag array (rr_plan_stage_slots uint32, zeroed once), mapped
-   * here. stage_chunk_bytes = 0: off. */
+   * stage flag array (rr_plan_stage_slots uint32), mapped here; same
+   * ownership rule as relay_flags (zero at create, one executor per array).
+   * Each piece's flag is written by the sender's copy stream
+   * (cuStreamWriteValue32 after the copy), never by a kernel, so spinning
+   * unpack CTAs cannot starve it. stage_chunk_bytes = 0: off. */
   int64_t stage_chunk_bytes;
   int32_t n_hosts;
   void* const* stage_remote;

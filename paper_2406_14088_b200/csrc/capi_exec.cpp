@@ -2,6 +2,7 @@
 // items of a lowered plan for one GPU (exec_plan.cpp), uploads them and
 // launches the sm_100a kernels (kernels.cu) phase by phase, optionally
 // pipelined behind a host->device onload.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -26,6 +27,36 @@ constexpr int64_t kMinSmallChunk = 4096;                   // 256 threads x one 
 // GB/s against ~700-716 for SM stores, pairwise at 2 and 4 GPUs; at 64 MiB
 // the engine's per-copy cost already eats the gain (profiles/r01_ce_probe_*).
 constexpr int64_t kDefaultCeRunBytes = int64_t{256} << 20;
+
+// Staged gather: each pushed piece is flagged by the copy stream itself
+// (cuStreamWriteValue32, default flags: preceded by a system-wide memory
+// barrier, so the piece's bytes are visible before the flag). No SM takes
+// part, so a receiver's spinning unpack CTAs can never starve the signal that
+// releases them. Resolved at run time like the multicast API (mcast.cpp): the
+// library keeps no link dependency on libcuda.
+using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+WriteValue32Fn write_value32() {
+  static const WriteValue32Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<WriteValue32Fn>(nullptr);
+    }
+    return reinterpret_cast<WriteValue32Fn>(p);
+  }();
+  return fn;
+}
+
+void signal_piece(cudaStream_t stream, uint32_t* flag, uint32_t epoch) {
+  const WriteValue32Fn fn = write_value32();
+  if (fn == nullptr) rr::capi::raise(RR_EUNSUPPORTED, "cuStreamWriteValue32 unavailable (staged gather)");
+  const CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), epoch,
+                        CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) rr::capi::raise(RR_ECUDA, "cuStreamWriteValue32 (staged piece flag) failed: " + std::to_string(r));
+}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -43,7 +74,7 @@ struct rr_exec {
   Phase phase[2];  // [0] direct copies, [1] in-host fan-out from leader replicas
   int fence_sys = 0;
   int default_ctas = 0;
-  // 0 = LDG/STG rr_copy_kernel, 1..kBulkVariants = TMA bulk ring. Defaults
+  // 0 = LDG/STG rr_copy_kernel, 1 / 5 = TMA bulk ring. Defaults
   // from the r01 sweeps: variant 1 (4 x 16 KiB stages, 3 CTAs/SM) for plain
   // phases, variant 5 (3 x 16 KiB, 4 CTAs/SM) for flag-synchronised ones,
   // where more resident CTAs keep NVLink busy while some spin on a flag
@@ -189,18 +220,19 @@ void launch_phase(rr_exec* ex, const rr_exec::Phase& ph, void* stream, int ctas,
   check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
   if (ph.n == 0) return;
   const int kernel = phase_kernel(ex, ph);
+  // A staged unpack spins on piece flags: it runs one CTA per SM on either
+  // kernel, so it never fills the GPU (the flags themselves are raised by the
+  // senders' copy streams, signal_piece, and need no SM here).
+  const int ldst_ctas = ctas > 0 ? ctas : (ex->stage_ctas > 0 ? ex->stage_ctas : ex->default_ctas);
   if (kernel == 0) {
-    check_cuda(rr::launch_copy(ph.d, ph.n, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys, stream, sched,
-                               ex->epoch),
-               "rr_copy_kernel launch");
+    check_cuda(rr::launch_copy(ph.d, ph.n, ldst_ctas, ex->fence_sys, stream, sched, ex->epoch), "rr_copy_kernel launch");
     return;
   }
   // Multicast and 2-byte items take the LDG/STG kernel, then the TMA bulk
   // kernel. A flag-synchronised phase is entirely in one of the two
   // (exec_plan.cpp build_items).
   if (ph.n > ph.n_vec)
-    check_cuda(rr::launch_copy(ph.d + ph.n_vec, ph.n - ph.n_vec, ctas > 0 ? ctas : ex->default_ctas, ex->fence_sys,
-                               stream, sched, ex->epoch),
+    check_cuda(rr::launch_copy(ph.d + ph.n_vec, ph.n - ph.n_vec, ldst_ctas, ex->fence_sys, stream, sched, ex->epoch),
                "rr_copy_kernel launch (relay / multicast / 2-byte items)");
   if (ph.n_vec > 0)
     check_cuda(rr::launch_bulk(kernel, ph.d, ph.n_vec,
@@ -281,8 +313,19 @@ void ce_issue(rr_exec* ex, cudaStream_t after, cudaEvent_t after_event = nullptr
     check_cuda(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "copy-engine run");
   for (const auto& p : ex->stage) {
     check_cuda(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "staged push");
-    check_cuda(rr::launch_signal(p.flag, ex->epoch, ex->ce_stream), "staged push signal");
+    signal_piece(ex->ce_stream, p.flag, ex->epoch);
   }
+}
+
+// The first n uint32 of a flag array (mapped in this process) must be zero.
+void require_zero_flags(const void* flags, int64_t n, const char* what) {
+  if (flags == nullptr || n <= 0) return;
+  std::vector<uint32_t> h(static_cast<size_t>(n));
+  check_cuda(cudaMemcpy(h.data(), flags, h.size() * sizeof(uint32_t), cudaMemcpyDefault), "read flag array");
+  if (std::any_of(h.begin(), h.end(), [](uint32_t v) { return v != 0; }))
+    rr::capi::raise(RR_EINVAL, std::string(what) +
+                                   ": flag array is not zero; zero it before every rr_exec_create_ex (one executor "
+                                   "per array: epochs restart at 1 in a new executor)");
 }
 
 void ce_join(rr_exec* ex, cudaStream_t into) {
@@ -401,6 +444,7 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
     }
     std::vector<int64_t> src_bytes(static_cast<size_t>(plan->cluster.device_count()), 0);
     const bool staged = options->stage_chunk_bytes > 0;
+    int64_t n_stage_slots = 0;
     if (staged) {
       need(mode == 1 && options->host_of != nullptr, "a staged gather runs in pull mode with a host_of table");
       need(options->stage_flags != nullptr && options->stage_remote != nullptr && options->n_hosts > 0,
@@ -410,11 +454,10 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
         need(hm.host[d] >= 0 && hm.host[d] < options->n_hosts, "host ids must lie in 0..n_hosts-1");
         src_bytes[d] = plan->layout(0, static_cast<DeviceId>(d)).bytes;
       }
-      int64_t n_slots = 0;
       hm.stage_chunk = options->stage_chunk_bytes;
-      hm.stage_slot0 = rr::stage_slots(plan->lowered, hm.host, hm.me, src_bytes, hm.stage_chunk, &n_slots);
+      hm.stage_slot0 = rr::stage_slots(plan->lowered, hm.host, hm.me, src_bytes, hm.stage_chunk, &n_stage_slots);
       hm.stage_flags = reinterpret_cast<uint64_t>(options->stage_flags[hm.me]);
-      need(n_slots == 0 || hm.stage_flags != 0, "missing this host's stage flag array");
+      need(n_stage_slots == 0 || hm.stage_flags != 0, "missing this host's stage flag array");
     }
     check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
     int per_sm = 0, sms = 0;
@@ -433,6 +476,16 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       a = refine_chunk(std::move(a), jobs, 0, hm, src_bufs, dst_bufs, ldst_ctas, bulk_ctas, &runs);
       b = refine_chunk(std::move(b), jobs, 1, hm, src_bufs, dst_bufs, ldst_ctas, bulk_ctas, nullptr);
     }
+
+    // Flag arrays compare against a per-executor epoch that starts at 1, so an
+    // array carrying values of an earlier executor would release waits before
+    // their data lands. The array this host waits on must therefore be fresh
+    // (zeroed) and owned by this executor alone (include/rr_realloc.h).
+    if (options->relay_flags && !hm.relay_flags.empty()) {
+      const int64_t n_relay = rr::relay_slots(plan->lowered, hm);
+      require_zero_flags(options->relay_flags[local[0]], n_relay, "relay_flags");
+    }
+    if (staged) require_zero_flags(options->stage_flags[hm.me], n_stage_slots, "stage_flags");
 
     auto ex = std::make_unique<rr_exec>();
     ex->cuda_device = cuda_device;
@@ -600,7 +653,7 @@ namespace {
 
 void select_kernel(rr_exec* ex, int kernel, int* slot, int* slot_ctas) {
   need(ex != nullptr, "null executor");
-  need(kernel >= 0 && kernel <= rr::kBulkVariants, "unknown copy kernel");
+  need(rr::valid_kernel(kernel), "unknown copy kernel (0 LDG/STG, 1 or 5 TMA bulk ring)");
   *slot = kernel;
   if (kernel > 0) {
     check_cuda(cudaSetDevice(ex->cuda_device), "cudaSetDevice");
@@ -671,6 +724,12 @@ rr_status rr_exec_enable_onload(rr_exec* ex, int n_src, const int32_t* src_devic
         if (src_devices[k] == c.src_dev)
           need(c.src_off + static_cast<int64_t>(c.bytes) <= src_bytes[k],
                "a copy-engine run reads beyond the onloaded bytes of its source");
+    // So must every staged push: it sends source bytes as they stand.
+    for (const auto& p : ex->stage)
+      for (int k = 0; k < n_src; ++k)
+        if (src_devices[k] == p.src_dev)
+          need(p.src_off + static_cast<int64_t>(p.bytes) <= src_bytes[k],
+               "a staged push reads beyond the onloaded bytes of its source");
     // Segment of each item: 0 = independent of the onload, 1 + c = needs chunk c.
     const rr::ItemSet& a = ex->phase0_host;
     const size_t n = a.items.size(), C = ex->chunks.size();
@@ -780,7 +839,7 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
           waited = last;
         }
         check_cuda(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "staged push");
-        check_cuda(rr::launch_signal(p.flag, ex->epoch, ex->ce_stream), "staged push signal");
+        signal_piece(ex->ce_stream, p.flag, ex->epoch);
       }
     }
     if (!ex->ce.empty()) {
@@ -817,6 +876,9 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
       ph.n = sg.n;
       ph.n_vec = sg.n_vec;
       ph.flagged = ex->phase[0].flagged;
+      // The kernel is chosen once for the whole phase (phase_kernel reads
+      // `written`): a GiB-sized phase keeps the TMA ring in every segment.
+      ph.written = ex->phase[0].written;
       return ph;
     };
     const auto& staged_seg = ex->segments.back();  // C + 1: staged unpack

@@ -227,40 +227,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// L2 policies for the bulk copies: 0 = default, otherwise a createpolicy value.
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(smem_dst)),
+               "l"(gmem_src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
 }
 
-__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar,
-                                          uint64_t policy) {
-  if (policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
-            "r"(smem_addr(smem_dst)),
-        "l"(gmem_src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
-        : "memory");
-  } else {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_addr(smem_dst)),
-        "l"(gmem_src), "r"(bytes), "r"(smem_addr(bar))
-        : "memory");
-  }
-}
-
-__device__ __forceinline__ void bulk_store(void* gmem_dst, const void* smem_src, uint32_t bytes, uint64_t policy) {
-  if (policy) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gmem_dst),
-                 "r"(smem_addr(smem_src)), "r"(bytes), "l"(policy)
-                 : "memory");
-  } else {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst),
-                 "r"(smem_addr(smem_src)), "r"(bytes)
-                 : "memory");
-  }
+__device__ __forceinline__ void bulk_store(void* gmem_dst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst),
+               "r"(smem_addr(smem_src)), "r"(bytes)
+               : "memory");
 }
 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -357,23 +334,19 @@ __device__ __forceinline__ PieceStatus next_piece(const CopyItem* __restrict__ i
   return kNoWork;
 }
 
-// HINT bit 0: source reads evict-first in L2; bit 1: destination writes evict-first.
-//
 // Relay / overlapped fan-out items (wait_flag, signal_flag) run here too, so
 // a flag-synchronised phase keeps the TMA ring's HBM efficiency. A CTA never
 // spins on a wait while it holds issued pieces: it first drains its ring
 // (stores, completion, signals), so every claimed push is finished by a CTA
 // that cannot block on it, and the round ordering argument of build_items
 // (exec_plan.cpp) carries over from the LDG/STG kernel.
-template <int S, int STAGE, int HINT>
+template <int S, int STAGE>
 __global__ void __launch_bounds__(32) rr_bulk_kernel(const CopyItem* __restrict__ items, int n_items,
                                                      int fence_sys, unsigned int* sched, uint32_t epoch) {
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ __align__(8) uint64_t full[S];
   __shared__ Piece meta[S];
   if (threadIdx.x != 0) return;
-  const uint64_t ld_policy = (HINT & 1) ? policy_evict_first() : 0;
-  const uint64_t st_policy = (HINT & 2) ? policy_evict_first() : 0;
   for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 
@@ -385,11 +358,11 @@ __global__ void __launch_bounds__(32) rr_bulk_kernel(const CopyItem* __restrict_
     mbar_expect_tx(&full[s], bytes);
     uint8_t* buf = ring + s * STAGE;
     if (p.rows == 1 || p.src_pitch == p.row_bytes) {
-      bulk_load(buf, reinterpret_cast<const void*>(p.src), bytes, &full[s], ld_policy);
+      bulk_load(buf, reinterpret_cast<const void*>(p.src), bytes, &full[s]);
     } else {
       for (uint32_t r = 0; r < p.rows; ++r)
         bulk_load(buf + r * p.row_bytes, reinterpret_cast<const void*>(p.src + static_cast<uint64_t>(r) * p.src_pitch),
-                  p.row_bytes, &full[s], ld_policy);
+                  p.row_bytes, &full[s]);
     }
   };
 
@@ -420,10 +393,10 @@ __global__ void __launch_bounds__(32) rr_bulk_kernel(const CopyItem* __restrict_
     for (int j = 0; j < ndst; ++j) {
       uint8_t* dst = reinterpret_cast<uint8_t*>(it.dst[j]) + q.dst_off;
       if (q.rows == 1 || q.dst_pitch == q.row_bytes) {
-        bulk_store(dst, buf, q.rows * q.row_bytes, st_policy);
+        bulk_store(dst, buf, q.rows * q.row_bytes);
       } else {
         for (uint32_t r = 0; r < q.rows; ++r)
-          bulk_store(dst + static_cast<uint64_t>(r) * q.dst_pitch, buf + r * q.row_bytes, q.row_bytes, st_policy);
+          bulk_store(dst + static_cast<uint64_t>(r) * q.dst_pitch, buf + r * q.row_bytes, q.row_bytes);
       }
     }
     bulk_commit();
@@ -509,19 +482,7 @@ __global__ void rr_barrier_kernel(uint32_t* const* __restrict__ flags, int rank,
   __syncthreads();
 }
 
-// Staged gather: release one piece to the host that waits for it, after
-// the copy-engine copy queued before this kernel on the same stream.
-__global__ void rr_signal_kernel(uint32_t* flag, uint32_t epoch) {
-  __threadfence_system();
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
-}
-
 }  // namespace
-
-int launch_signal(uint32_t* flag, uint32_t epoch, void* stream) {
-  rr_signal_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag, epoch);
-  return cudaGetLastError();
-}
 
 int copy_max_ctas(int* ctas_per_sm, int* sms) {
   int dev = 0;
@@ -543,49 +504,40 @@ int launch_copy(const CopyItem* items, int n_items, int ctas, int fence_sys, voi
 
 namespace {
 
-template <int S, int STAGE, int HINT = 0>
+template <int S, int STAGE>
 int launch_bulk_t(const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream, int* max_ctas,
                   unsigned int* sched, uint32_t epoch) {
   constexpr int kSmem = S * STAGE;
-  cudaError_t e = cudaFuncSetAttribute(rr_bulk_kernel<S, STAGE, HINT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  cudaError_t e = cudaFuncSetAttribute(rr_bulk_kernel<S, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
   if (e != cudaSuccess) return e;
   if (max_ctas) {
     int dev = 0, sms = 0, per_sm = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rr_bulk_kernel<S, STAGE, HINT>, 32, kSmem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rr_bulk_kernel<S, STAGE>, 32, kSmem);
     if (e != cudaSuccess) return e;
     *max_ctas = per_sm * sms;
     return cudaSuccess;
   }
   if (n_items <= 0) return cudaSuccess;
   if (ctas > n_items) ctas = n_items;
-  rr_bulk_kernel<S, STAGE, HINT><<<ctas, 32, kSmem, static_cast<cudaStream_t>(stream)>>>(items, n_items, fence_sys,
+  rr_bulk_kernel<S, STAGE><<<ctas, 32, kSmem, static_cast<cudaStream_t>(stream)>>>(items, n_items, fence_sys,
                                                                                         sched, epoch);
   return cudaGetLastError();
 }
 
 }  // namespace
 
+// The two ring shapes the r01 sweeps kept (profiles/r01_sweep_kernels*.txt,
+// r01_flag_kernel_sweep_n{2,4}.txt; the sweep variants live in tools/ history):
+//   1: 4 x 16 KiB stages, 3 CTAs/SM — plain phases (96.9% of the HBM copy peak);
+//   5: 3 x 16 KiB stages, 4 CTAs/SM — flag-synchronised phases, where more
+//      resident CTAs keep NVLink busy while some spin on a flag.
 int launch_bulk(int variant, const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream,
                 int* max_ctas, unsigned int* sched, uint32_t epoch) {
   switch (variant) {
     case 1: return launch_bulk_t<4, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
-    case 2: return launch_bulk_t<8, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
-    case 3: return launch_bulk_t<4, 32768>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
-    case 4: return launch_bulk_t<6, 32768>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
     case 5: return launch_bulk_t<3, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
-    case 6: return launch_bulk_t<4, 32768, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
-    case 7: return launch_bulk_t<4, 32768, 2>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
-    case 8: return launch_bulk_t<4, 32768, 3>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
-    case 9: return launch_bulk_t<3, 32768, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
-    case 10: return launch_bulk_t<3, 65536, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
-    case 11: return launch_bulk_t<2, 16384>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
-    case 12: return launch_bulk_t<3, 8192>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
-    case 13: return launch_bulk_t<6, 8192>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
-    case 14: return launch_bulk_t<4, 16384, 2>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
-    case 15: return launch_bulk_t<4, 16384, 1>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
-    case 16: return launch_bulk_t<8, 8192>(items, n_items, ctas, fence_sys, stream, max_ctas, sched, epoch);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -81,16 +81,17 @@ __host__ __device__ inline uint16_t weight_value(uint64_t seed, uint64_t tensor,
 int launch_copy(const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream, unsigned int* sched,
                 uint32_t epoch = 0);
 int copy_max_ctas(int* ctas_per_sm, int* sms);
-// TMA bulk variant (1..kBulkVariants = stage ring shapes / L2 hints); items must all be vec items
+// TMA bulk variant (kBulkVariantA / kBulkVariantB = stage ring shapes); items must all be vec items
 // without multicast (relay wait / signal flags are supported). With max_ctas != NULL only reports
 // the resident-CTA capacity.
 int launch_bulk(int variant, const CopyItem* items, int n_items, int ctas, int fence_sys, void* stream,
                 int* max_ctas, unsigned int* sched, uint32_t epoch = 0);
-constexpr int kBulkVariants = 16;
+constexpr int kBulkVariantA = 1;  // 4 x 16 KiB stages (plain phases)
+constexpr int kBulkVariantB = 5;  // 3 x 16 KiB stages (flag-synchronised phases)
+inline bool valid_kernel(int k) { return k == 0 || k == kBulkVariantA || k == kBulkVariantB; }
 int launch_fill(const FillItem* items, int n_items, uint64_t seed, void* stream);
 int launch_verify(const FillItem* items, int n_items, uint64_t seed, unsigned long long* counters,
                   uint64_t buf_base, void* stream);
-int launch_signal(uint32_t* flag, uint32_t epoch, void* stream);
 int launch_barrier(uint32_t* const* flags, int rank, int world, uint32_t epoch, int* timed_out,
                    void* stream);
 

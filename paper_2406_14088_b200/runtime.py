@@ -261,7 +261,7 @@ class Executor:
                                          _stream_ptr(stream)))
 
     def set_kernel(self, kernel: int) -> None:
-        """0 = LDG/STG kernel, 1..16 = TMA bulk-copy ring variants."""
+        """0 = LDG/STG kernel, 1 = TMA bulk ring (4 x 16 KiB stages), 5 = TMA bulk ring (3 x 16 KiB)."""
         check(lib.rr_exec_set_kernel(self._h, kernel))
 
     def set_flag_kernel(self, kernel: int) -> None:
@@ -361,7 +361,7 @@ def hosted_devices(n_plan_devices: int, rank: int, world: int) -> List[int]:
     return list(range(rank * k, (rank + 1) * k))
 
 
-def _all_gather_shaped(plan: ReallocPlan, host_of: Sequence[int], world: int) -> bool:
+def _all_gather_shaped(plan: ReallocPlan, host_of: Sequence[int], world: int, ce_min_run_bytes: int = 0) -> bool:
     """Every GPU both sends sources to and receives sources from others,
     every GPU that reads a remote source shard reads (>= 98% of) all of it
     (the staged gather moves whole shards), each GPU receives >= 1 GiB, and
@@ -386,8 +386,11 @@ def _all_gather_shaped(plan: ReallocPlan, host_of: Sequence[int], world: int) ->
         received[h] += b
     if min(received) < (1 << 30):
         return False
+    if ce_min_run_bytes < 0:  # copy-engine runs switched off: none to defer to
+        return True
     n = plan.cluster.device_count()
-    return not any(plan.ce_runs([d for d in range(n) if host_of[d] == r], host_of) for r in range(world))
+    min_run = ce_min_run_bytes or (256 << 20)  # 0 = the library default
+    return not any(plan.ce_runs([d for d in range(n) if host_of[d] == r], host_of, min_run) for r in range(world))
 
 
 def stage_slots(plan: ReallocPlan, host_of: Sequence[int], chunk_bytes: int) -> int:
@@ -602,7 +605,7 @@ class RankRealloc:
                 if pi in self.relay_phases or dname in self.multicast:
                     continue
                 p = self.plans[pi]
-                if staged == "auto" and (world < 4 or not _all_gather_shaped(p, host_of_all, world)):
+                if staged == "auto" and (world < 4 or not _all_gather_shaped(p, host_of_all, world, ce_min_run_bytes)):
                     continue
                 if any(host_of_all[s] != host_of_all[d] for s, dsts, _r in p.lowered() for d in dsts):
                     self.staged_phases.append(pi)

@@ -45,7 +45,7 @@ class Guarded:
     (TINY_GQA, (1, 8, 1, 2, 1), (4, 1, 2, 0, 0), 8),
     (MODELS["spec_tiny"], (1, 2, 1, 0, 0), (1, 1, 2, 0, 0), 2),   # 2-byte element path
 ])
-@pytest.mark.parametrize("mode,kernel", [(R.PUSH, 0), (R.PUSH, 1), (R.PULL, 1), (R.PUSH, 3)])
+@pytest.mark.parametrize("mode,kernel", [(R.PUSH, 0), (R.PUSH, 1), (R.PULL, 1), (R.PUSH, 5)])
 def test_guards_intact(need_gpu, model, sp, dp, gpus, mode, kernel):
     c = b200_cluster(gpus)
     src = placement(gpus, *sp[:3], qkv=sp[3], gate_up=sp[4])

@@ -119,7 +119,7 @@ def test_small_phase_recut_bitexact(need_gpu, model, sp, dp):
     ((2, 1, 4, 0, 0), (1, 1, 8, 0, 0)),   # 70B-style pp2 tp4 -> tp8
 ])
 @pytest.mark.parametrize("mode", [R.PUSH, R.PULL])
-@pytest.mark.parametrize("kernel", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("kernel", [0, 1, 5])
 def test_reinterleave_bitexact(need_gpu, sp, dp, mode, kernel):
     c = b200_cluster(8)
     src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
@@ -145,7 +145,7 @@ def test_disjoint_meshes_bitexact(need_gpu):
     c = b200_cluster(8)
     src = placement(4, 1, 4, 1, offset=0)
     dst = placement(4, 1, 1, 4, offset=4)
-    for kernel in (0, 3):
+    for kernel in (0, 5):
         _plan, got = run_virtual(TINY_GQA, src, dst, c, BALANCED, kernel=kernel)
         assert_same(got, expected(TINY_GQA, src, dst, c))
 

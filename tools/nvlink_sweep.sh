@@ -4,7 +4,7 @@ OUT=${OUT:-gpurun_out}
 mkdir -p "$OUT"
 N=$(nvidia-smi -L | wc -l)
 for mode in push pull; do
-  for k in 1 0 3; do
+  for k in 1 0 5; do
     for c in 0 148 296; do
       timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
         --master-port 29517 bench.py --gpus $N --mode $mode --kernel $k --ctas $c --steps 10 --warmup 3 \
