@@ -95,67 +95,139 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# reference / CPU arm
+# workloads as plain data, and the reference / CPU arm
 # ---------------------------------------------------------------------------
 
-def cpu_sample_run(workload, layers: int, steps: int, warmup: int, threads: int, budget_s: float = None):
-    """Time the oracle CPU reallocation (all phases) on `workload` truncated to
-    `layers` decoder layers. Returns (GB/s delivered, seconds/step, bytes/step)."""
+def plain_workload(name: str):
+    """A named workload of paper_2406_14088_b200/workloads.json as duck-typed
+    objects with the reference types' attribute names (ModelSpec, Placement,
+    DeviceMesh, ParallelStrategy, ClusterSpec), which the oracle accepts. The
+    reference arm runs on these and never imports the product package."""
+    from types import SimpleNamespace as NS
+    with open(os.path.join(ROOT, "paper_2406_14088_b200", "workloads.json")) as f:
+        table = json.load(f)
+    e = next((w for w in table["workloads"] if w["name"] == name), None)
+    if e is None:
+        raise SystemExit(f"unknown workload {name!r}")
+    model = NS(name=e["model"], **table["models"][e["model"]])
+
+    def placement(d):
+        no, nc, go, gc = d["mesh"]
+        return NS(mesh=NS(node_offset=no, node_count=nc, gpu_offset=go, gpu_count=gc),
+                  strategy=NS(dp=d["dp"], tp=d["tp"], pp=d["pp"]), qkv_layout=d.get("qkv_layout", 0),
+                  gate_up_layout=d.get("gate_up_layout", 0), kv_layout=d.get("kv_layout", 0))
+    src, dst = placement(e["src"]), placement(e["dst"])
+    return NS(name=name, description=e["description"], model=model, devices=e["devices"],
+              phases=[(src, dst), (dst, src)] if e["back"] else [(src, dst)], data_bytes=e.get("data_bytes", 0),
+              cluster=NS(n_nodes=1, gpus_per_node=e["devices"], intra_node_bw=900e9, inter_node_bw=50e9))
+
+
+def workload_config(w) -> dict:
+    """`config` of the JSON line: the workload only (identical in both arms);
+    how each arm executes it goes under `executor`."""
+    def s(p):
+        st = p.strategy
+        return f"(pp{st.pp},dp{st.dp},tp{st.tp})"
+    return {"workload": w.name, "description": w.description,
+            "model": "data" if w.data_bytes else w.model.name, "plan_devices": w.devices,
+            "phases": [f"{s(a)}->{s(b)}" for a, b in w.phases],
+            "l2": "inputs larger than L2 (multi-GB shards); no flush needed",
+            "weights": "hash-initialised bf16 (seed 1); every destination shard checked after timing"}
+
+
+def host_info() -> dict:
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), model)
+    except OSError:
+        pass
+    return {"cpu_model": model, "cores": os.cpu_count() or 1, "mem_available_gb": round(mem_available() / 1e9, 1)}
+
+
+def mem_available() -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable:"):
+                    return int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def cpu_realloc(w, steps: int, warmup: int, threads: int, budget_s: float = None) -> dict:
+    """The reference path on the host: the oracle's CPU reallocation
+    (oracle/liboracle.so, SPEC.md:541-611 restated; the reference itself
+    moves no bytes) of the WHOLE workload `w` (plain objects),
+    every phase per step, all shards in host RAM, `threads` worker threads.
+    Steps run until both `steps` and (if given) `budget_s` are reached. The
+    result is checked against the oracle's expected shards afterwards: the
+    last phase's destinations byte for byte, earlier ones on 64 MiB windows."""
     import numpy as np
     from oracle import oracle as O
-    from paper_2406_14088_b200.workloads import truncated
-    if workload.data_bytes:  # already small: the whole batch
-        return cpu_sample_data(workload, steps, warmup, threads, budget_s)
-    w = truncated(workload, layers)
-    c = w.cluster()
-    n = c.device_count()
+    c = w.cluster
+    n = c.n_nodes * c.gpus_per_node
+    if w.data_bytes:
+        return cpu_data(w, steps, warmup, threads, budget_s)
     phases = []
     bufs = {}
     for (src, dst) in w.phases:
-        ops, loc, _tb, _et = O.plan(w.model, src, dst, c, 1)
+        ops, loc, _tb, _et = O.plan(w.model, src, dst, c, 1)  # 1 = balanced sources, as the B200 arm
         phases.append((src, dst, ops + loc))
-    # Phase i+1's source shards are phase i's destination shards (round trip).
-    def shards(p):
-        key = (p.strategy, p.qkv_layout, p.gate_up_layout)
-        if key not in bufs:
-            bufs[key] = [np.zeros(O.shard_bytes(w.model, p, c, d) // 2, np.uint16) for d in range(n)]
-        return bufs[key]
-    first_src = phases[0][0]
+
+    def key(p):
+        return (p.strategy.pp, p.strategy.dp, p.strategy.tp, p.qkv_layout, p.gate_up_layout, p.kv_layout,
+                p.mesh.gpu_offset, p.mesh.gpu_count)
+    sets = {}
+    for src, dst, _ops in phases:
+        for p in (src, dst):
+            sets.setdefault(key(p), p)
+    need = sum(O.shard_bytes(w.model, p, c, d) for p in sets.values() for d in range(n))
+    if need > 0.85 * mem_available():
+        raise MemoryError(f"{w.name}: {need / 1e9:.1f} GB of shards, {mem_available() / 1e9:.1f} GB available")
+    for k, p in sets.items():  # calloc'd: padding stays zero, pages fault in during warm-up
+        bufs[k] = [np.zeros(O.shard_bytes(w.model, p, c, d) // 2, np.uint16) for d in range(n)]
+    first = phases[0][0]
     for d in range(n):
-        shards(first_src)[d][:] = O.fill(w.model, first_src, c, d, 1)
-    delivered = 0
-    for (src, dst, ops) in phases:
-        for (s, dsts, _payload, b) in ops:
-            delivered += b * len(dsts)
+        if bufs[key(first)][d].size:
+            O.fill_range_into(w.model, first, c, d, 1, 0, bufs[key(first)][d].nbytes,
+                              bufs[key(first)][d].ctypes.data, threads)
+    delivered = sum(b * len(dsts) for (_s, _d, ops) in phases for (_src, dsts, _p, b) in ops)
 
     def step():
         for (src, dst, ops) in phases:
-            O.execute(w.model, src, dst, c, ops, shards(src), shards(dst), threads)
+            O.execute(w.model, src, dst, c, ops, bufs[key(src)], bufs[key(dst)], threads)
 
     for _ in range(warmup):
         step()
     t0 = time.perf_counter()
     done = 0
-    while done < steps or (budget_s is not None and time.perf_counter() - t0 < budget_s and done < 100):
+    while True:
         step()
         done += 1
-        if budget_s is not None and done >= steps and time.perf_counter() - t0 >= budget_s:
+        el = time.perf_counter() - t0
+        if done >= steps and (budget_s is None or el >= budget_s or done >= 100):
             break
     dt = (time.perf_counter() - t0) / done
-    # Check the sample (the CPU arm must be correct too).
-    last_dst = phases[-1][1]
-    ok = all(np.array_equal(shards(last_dst)[d], O.fill(w.model, last_dst, c, d, 1)) for d in range(n)
-             if O.shard_bytes(w.model, last_dst, c, d))
-    return delivered / dt / 1e9, dt, delivered, ok, w
+    bad = 0
+    for i, (_src, dst, _ops) in enumerate(phases):
+        for d, b in enumerate(bufs[key(dst)]):
+            if not b.size:
+                continue
+            n_check = b.nbytes if i == len(phases) - 1 else min(b.nbytes, 64 << 20)
+            bad += O.check_range(w.model, dst, c, d, 1, 0, n_check, b.ctypes.data, threads)[0]
+    return {"gbs": delivered / dt / 1e9, "s_per_step": dt, "delivered": delivered, "correct": bad == 0,
+            "steps": done, "shard_gb": need / 1e9}
 
 
-def cpu_sample_data(w, steps: int, warmup: int, threads: int, budget_s: float = None):
-    """cpu_sample_run for a data workload: the oracle's plan_data_transfer
+def cpu_data(w, steps: int, warmup: int, threads: int, budget_s: float = None) -> dict:
+    """cpu_realloc for a data workload: the oracle's plan_data_transfer
     restatement executed on host buffers with `threads` threads."""
     import numpy as np
     from oracle import oracle as O
-    c = w.cluster()
-    n = c.device_count()
+    c = w.cluster
+    n = c.n_nodes * c.gpus_per_node
     (prod, cons), = w.phases
     total = w.data_bytes * prod.strategy.dp
     ops, loc = O.plan_data(prod, cons, c, w.data_bytes, 1)[:2]
@@ -175,8 +247,49 @@ def cpu_sample_data(w, steps: int, warmup: int, threads: int, budget_s: float = 
             break
     dt = (time.perf_counter() - t0) / done
     ok = all(np.array_equal(dst[d], O.data_fill(cons, c, d, False, total, 1)) for d in range(n) if dst[d].size)
-    return delivered / dt / 1e9, dt, delivered, ok, w
+    return {"gbs": delivered / dt / 1e9, "s_per_step": dt, "delivered": delivered, "correct": ok, "steps": done,
+            "shard_gb": sum(x.nbytes for x in dst) / 1e9}
 
+
+def cpu_sample_text(w, r: dict, threads: int) -> str:
+    return (f"the whole workload ({w.description}), all phases per step, shards in host RAM "
+            f"({r['shard_gb']:.1f} GB); oracle CPU reallocation (oracle/liboracle.so) with {threads} threads; "
+            f"{r['delivered'] / 1e9:.2f} GB delivered per step; {r['steps']} timed steps; "
+            f"checked against the oracle: {r['correct']}")
+
+
+def run_reference(args) -> None:
+    """--impl reference: the reference path (its CPU reallocation) on the
+    box's host cores. Rank 0 only; imports nothing from the product."""
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    if args.config:
+        print(json.dumps({"impl": "reference", "unavailable": "--config workloads: the reference arm runs the "
+                                                              "named workloads of workloads.json"}), flush=True)
+        return
+    w = plain_workload(args.workload)
+    threads = os.cpu_count() or 1
+    r = cpu_realloc(w, args.steps, max(args.warmup, 1), threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(r["gbs"], 3), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": r["steps"], "warmup": args.warmup, "ms_per_step": round(r["s_per_step"] * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": workload_config(w),
+        "executor": {"impl": "oracle CPU reallocation (oracle/liboracle.so: SPEC.md:541-611 restated; the "
+                             "reference moves no bytes itself, SPEC.md:607)", "threads": threads},
+        "host": host_info(),
+        "cpu_baseline": {"value": round(r["gbs"], 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": cpu_sample_text(w, r, threads)},
+        "e2e": {"value": round(r["gbs"], 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "verified": r["correct"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
 
 def load_workload(args):
     from paper_2406_14088_b200.workloads import WORKLOADS, from_config
@@ -185,32 +298,6 @@ def load_workload(args):
             return from_config(json.load(f), name=os.path.splitext(os.path.basename(args.config))[0])
     return WORKLOADS[args.workload]
 
-
-def run_reference(args) -> None:
-    rank, world, _ = env_rank()
-    if rank != 0:
-        return
-    from paper_2406_14088_b200.workloads import WORKLOADS
-    w = load_workload(args)
-    threads = os.cpu_count() or 1
-    gbs, dt, delivered, ok, ws = cpu_sample_run(w, args.cpu_layers, args.steps, max(args.warmup, 1), threads)
-    sample = (f"{ws.description}; all phases; oracle CPU reallocation (oracle/liboracle.so) with {threads} "
-              f"threads; {delivered / 1e9:.2f} GB delivered per step; correct={ok}")
-    line = {
-        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": w.name, "description": w.description, "sample_layers": args.cpu_layers},
-        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": sample},
-        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-# ---------------------------------------------------------------------------
-# B200 arm
-# ---------------------------------------------------------------------------
 
 def run_b200(args) -> None:
     import torch
@@ -421,17 +508,32 @@ def run_b200(args) -> None:
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_ms, 3),
                "timing": "host wall clock around stream-synchronised steps, max over ranks",
                "path": "public API: RankRealloc.run_phase_onload (H2D chunks pipelined with the copy kernels)",
+               "results": "the resharded weights stay in HBM for the engine that uses them next (generation / "
+                          "training); d2h reads back a 4 KiB sample of every destination shard per step. Copying "
+                          "every result to the host would bound e2e by the same host link as the onload",
                "verified": e2e_bad == 0}
         for hb in list(host.values()) + list(res_host.values()):
             hb.free()
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    oracle_checked, oracle_bad = False, None
+    if rank == 0 and world == 1 and not args.no_cpu and not args.config and not args.layers:
+        # the reference path on this box's host cores, same workload (plain
+        # objects from workloads.json), after the GPU arm has released its
+        # pinned host buffers
         threads = os.cpu_count() or 1
-        gbs, dt, delivered, ok, ws = cpu_sample_run(w, args.cpu_layers, 1, 1, threads, budget_s=args.cpu_budget)
-        cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-               "sample": f"{ws.description}; all phases; oracle CPU reallocation, {delivered / 1e9:.2f} GB "
-                         f"delivered per step, correct={ok}"}
+        pw = plain_workload(w.name)
+        # the oracle as the checker of the GPU arm: every byte of every
+        # destination shard of every phase against its expected shard
+        oracle_bad = oracle_check(rr, bind, plans, pw, seed, threads)
+        oracle_checked = True
+        verified = verified and oracle_bad == 0
+        try:
+            r = cpu_realloc(pw, 1, 1, threads, budget_s=args.cpu_budget)
+            cpu = {"value": round(r["gbs"], 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                   "sample": cpu_sample_text(pw, r, threads)}
+        except MemoryError as e:
+            cpu = {"value": None, "unit": "GB/s", "cores": threads, "kind": "port", "sample": f"not run: {e}"}
 
     if rank == 0:
         peaks = measured_peaks()
@@ -442,6 +544,8 @@ def run_b200(args) -> None:
             achieved = dom_hbm / (dom_ms * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": profile_traffic(w.name),
+                    "traffic_source": (f"profiles/{w.name}.ncu.json: dram__bytes_read+write of this kernel per "
+                                       "launch from a committed ncu --set full capture, not measured in this run"),
                     "kernel": kname, "phase": dom, "peak_source": peaks["source"],
                     "algorithmic_bytes_per_launch": int(dom_hbm)}
         else:
@@ -492,17 +596,17 @@ def run_b200(args) -> None:
                              "on other GPUs over NVLink (900 GB/s per direction vs ~6.5 TB/s HBM), so time "
                              "need not fall with N; compare each N against its own roofline"),
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": w.name, "description": w.description, "plan_devices": w.devices,
-                       "plan_devices_per_gpu": w.devices // world, "phases": len(plans),
-                       "policy": args.policy, "mode": args.mode, "multicast_sets": rr.multicast,
-                       "relay_phases": rr.relay_phases, "overlap_phases": rr.overlap_phases,
-                       "copy_kernel": kname,
-                       "ce_runs": [list(e.ce_runs()) for e in rr.executors],
-                       "staged_phases": rr.staged_phases, "bulk_variants": {"plain": 1 if kernel is None else kernel,
-                                                                      "flag_synchronised": flag_kernel},
-                       "chunk_kib": args.chunk_kib or "library default (256; smaller for phases too small for it)", "ctas": args.ctas or "resident capacity",
-                       "l2": "inputs larger than L2 (multi-GB shards); no flush needed",
-                       "weights": "hash-initialised bf16 (seed 1), verified after timing"},
+            "config": (workload_config(plain_workload(w.name)) if not (args.config or args.layers)
+                       else workload_config(w)),
+            "executor": {"plan_devices_per_gpu": w.devices // world, "policy": args.policy, "mode": args.mode,
+                         "multicast_sets": rr.multicast, "relay_phases": rr.relay_phases,
+                         "overlap_phases": rr.overlap_phases, "copy_kernel": kname,
+                         "ce_runs": [list(e.ce_runs()) for e in rr.executors], "staged_phases": rr.staged_phases,
+                         "bulk_variants": {"plain": 1 if kernel is None else kernel, "flag_synchronised": flag_kernel},
+                         "chunk_kib": args.chunk_kib or "library default (256; smaller for phases too small for it)",
+                         "ctas": args.ctas or "resident capacity",
+                         "policy_probe": getattr(rr, "probe_log", None)},
+            "host": host_info(),
             "phase_ms": [round(float(x), 4) for x in ph_ms_all.max(axis=0)],
             "step_ms": {"median": round(step_ms[len(step_ms) // 2], 4), "best": round(step_ms[0], 4),
                         "worst": round(step_ms[-1], 4), "of": "rank 0's timed steps (CUDA events)"},
@@ -523,6 +627,11 @@ def run_b200(args) -> None:
             # lowering, and rank 0's buffer allocation + executor binding/upload
             "host_ms": {"plan_and_lower": round(plan_ms, 3), "allocate_and_bind": round(bind_ms, 1)},
             "verified": verified,
+            "verified_by": ("device regenerate-and-compare of every destination shard (product fill function)"
+                            + ("; and every byte of every destination shard against the oracle's expected shards "
+                               f"(oracle/liboracle.so orc_check_range, in the cpu_baseline leg): "
+                               f"{'0' if not oracle_bad else oracle_bad} mismatching elements"
+                               if oracle_checked else "")),
         }
         if oversub:
             line["oversubscribed"] = f"{world} ranks on {gpus} GPUs: correctness run, not a measurement"
@@ -531,6 +640,36 @@ def run_b200(args) -> None:
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def oracle_check(rr, bind, plans, pw, seed: int, threads: int) -> int:
+    """Compare every destination shard the GPU arm wrote with the oracle's
+    expected shard (streamed 256 MiB windows, D2H of window k + 1 overlapped
+    with the check of window k). Returns the mismatching elements."""
+    from oracle import oracle as O
+    from paper_2406_14088_b200 import runtime as R
+    window = 256 << 20
+    hosts = [R.HostBuffer(window), R.HostBuffer(window)]
+    bad = 0
+    try:
+        for i, (_sname, dname) in enumerate(bind):
+            dst = pw.phases[i][1]
+            for d, b in sorted(rr.buffers[dname].items()):
+                offs = list(range(0, b.nbytes, window))
+                if offs:
+                    R.memcpy_async(hosts[0].ptr, b.ptr, min(window, b.nbytes), 1)
+                for k, off in enumerate(offs):
+                    R.stream_sync()
+                    if k + 1 < len(offs):
+                        R.memcpy_async(hosts[(k + 1) % 2].ptr, b.ptr + offs[k + 1],
+                                       min(window, b.nbytes - offs[k + 1]), 1)
+                    bad += O.check_range(pw.model, dst, pw.cluster, d, seed, off, min(window, b.nbytes - off),
+                                         hosts[k % 2].ptr, threads)[0]
+                R.stream_sync()
+    finally:
+        for h in hosts:
+            h.free()
+    return bad
 
 
 def profile_traffic(workload: str):
@@ -573,8 +712,8 @@ def main() -> None:
     ap.add_argument("--chunk-kib", type=int, default=0, help="work-item size in KiB (0 = library default)")
     ap.add_argument("--layers", type=int, default=0, help="truncate the model (profiling only)")
     ap.add_argument("--kernel", type=int, default=-1, help="copy engine: 0 LDG/STG, 1..5 TMA bulk (-1 default)")
-    ap.add_argument("--cpu-layers", type=int, default=2)
-    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--cpu-budget", type=float, default=10.0,
+                    help="seconds of timed CPU reallocation in the cpu_baseline leg (whole workload, >= 1 step)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

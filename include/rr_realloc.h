@@ -31,7 +31,8 @@
 extern "C" {
 #endif
 
-#define RR_ABI_VERSION 4 /* 2: rr_placement.kv_layout, rr_shard.part; 3: rr_exec_options.ce_min_run_bytes; 4: staged gather */
+#define RR_ABI_VERSION 5 /* 2: rr_placement.kv_layout, rr_shard.part; 3: rr_exec_options.ce_min_run_bytes; 4: staged gather;
+                            5: rr_exec_options.ce_transport */
 
 typedef enum {
   RR_OK = 0,
@@ -311,6 +312,18 @@ typedef struct {
   int32_t n_hosts;
   void* const* stage_remote;
   void* const* stage_flags;
+  /* Copy-engine transport (ABI v5; push mode): every remote destination of
+   * the plain phase-0 work moves by copy engine straight into the
+   * destination shard — the per-layer pieces of one tensor kind merged into
+   * one cudaMemcpy2DAsync (contiguous pieces, rows = layers) or one
+   * cudaMemcpy3DAsync (row-parallel pieces) per (source, destination) —
+   * issued on a side stream in rotation rounds (round r to the host r places
+   * after this one), beside the SM kernel that does the local copies. No
+   * staging, no unpack pass. Copy engines carry more payload per NVLink byte
+   * than SM stores (~780 vs ~710 GB/s). Excludes relay / overlapped fan-out
+   * jobs (they stay on SM stores); copy-engine runs are not used with it.
+   * 0 = off. */
+  int32_t ce_transport;
 } rr_exec_options;
 /* Length of the relay flag array for this host map, chunk size and scheme
  * switches (identical on every rank). */
@@ -324,9 +337,17 @@ rr_status rr_plan_stage_slots(const rr_plan* plan, const int32_t* host_of, int64
  * offset, dst byte offset, bytes}; pass out5 = NULL to query *n. */
 rr_status rr_plan_ce_runs(const rr_plan* plan, int n_local, const int32_t* local, const int32_t* host_of,
                           int64_t min_run_bytes, int64_t* out5, int cap, int* n);
+/* Copy-engine transport copies a push executor driving `local` (with
+ * `host_of`) would issue, host only, in issue order: 11 int64 per copy {src
+ * device, dst device, src offset, dst offset, width, height, depth, src
+ * pitch, dst pitch, src slice stride, dst slice stride}; out11 = NULL
+ * queries *n. */
+rr_status rr_plan_ce_copies(const rr_plan* plan, int n_local, const int32_t* local, const int32_t* host_of,
+                            int64_t* out11, int cap, int* n);
 /* Staged-gather pieces this executor pushes per launch, and their bytes. */
 rr_status rr_exec_stage_pushes(const rr_exec* ex, int* n_pushes, int64_t* bytes);
-/* Copy-engine runs phase 0 issues (see rr_exec_options.ce_min_run_bytes). */
+/* Copy-engine submissions phase 0 issues (copy-engine runs, see
+ * rr_exec_options.ce_min_run_bytes, or copy-engine transport copies). */
 rr_status rr_exec_ce_runs(const rr_exec* ex, int* n_runs, int64_t* bytes);
 /* Relay waits that timed out (bounded spins) since the executor was created. */
 rr_status rr_exec_relay_timeouts(rr_exec* ex, int64_t* timeouts);
@@ -352,7 +373,11 @@ void rr_mcast_destroy(rr_mcast* m);
 
 /* ---- deterministic weights (test/bench infrastructure) ----
  * Fill or check a device's shard under one side of a plan with
- * bf16 value = hash(seed, tensor_id, logical_index). */
+ * bf16 value = hash(seed, tensor_id, logical_index). Seeds with
+ * RR_SEED_SPECIAL set draw special bf16 words instead (signed zeros,
+ * infinities, quiet and signalling NaNs with payloads, subnormals, extreme
+ * normals, arbitrary 16-bit patterns). */
+#define RR_SEED_SPECIAL (1ull << 62)
 rr_status rr_fill_shard(const rr_plan* plan, int side, int32_t device, void* buf, uint64_t seed,
                         void* stream);
 /* Synchronous; *mismatches = number of differing elements, *first = buffer

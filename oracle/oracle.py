@@ -146,6 +146,46 @@ def fill(model, placement, cluster, dev: int, seed: int) -> np.ndarray:
     return buf
 
 
+_lib.orc_fill_range.argtypes = [POINTER(OrcModel), POINTER(OrcPlacement), POINTER(OrcCluster), c_int, c_uint64,
+                                c_int64, c_int64, c_void_p, c_int]
+_lib.orc_check_range.argtypes = [POINTER(OrcModel), POINTER(OrcPlacement), POINTER(OrcCluster), c_int, c_uint64,
+                                 c_int64, c_int64, c_void_p, c_int, POINTER(c_int64), POINTER(c_int64)]
+SEED_SPECIAL = 1 << 62  # special-value mode (ORC_SEED_SPECIAL)
+
+
+def fill_range_into(model, placement, cluster, dev: int, seed: int, offset: int, nbytes: int, ptr: int,
+                    threads: int = 0) -> None:
+    """Write bytes [offset, offset + nbytes) of the expected shard of `dev` to
+    host address `ptr` (padding zero), with `threads` threads (0 = all)."""
+    rc = _lib.orc_fill_range(ctypes.byref(_model(model)), ctypes.byref(_placement(placement)),
+                             ctypes.byref(_cluster(cluster)), dev, seed, offset, nbytes, ptr,
+                             threads or (os.cpu_count() or 1))
+    assert rc == 0, "orc_fill_range: bad window"
+
+
+def fill_mt(model, placement, cluster, dev: int, seed: int, threads: int = 0) -> np.ndarray:
+    """fill() computed with several threads (multi-GB shards)."""
+    n = shard_bytes(model, placement, cluster, dev)
+    buf = np.empty(n // 2, dtype=np.uint16)
+    if n:
+        fill_range_into(model, placement, cluster, dev, seed, 0, n, buf.ctypes.data, threads)
+    return buf
+
+
+def check_range(model, placement, cluster, dev: int, seed: int, offset: int, nbytes: int, ptr: int,
+                threads: int = 0) -> Tuple[int, int]:
+    """Compare nbytes at host address `ptr` with the expected shard window at
+    `offset`: (mismatching bf16 elements, first mismatching element of the
+    window or -1). Runs without the GIL (ctypes), so a caller may overlap it
+    with a device->host copy of the next window."""
+    bad, first = c_int64(), c_int64()
+    rc = _lib.orc_check_range(ctypes.byref(_model(model)), ctypes.byref(_placement(placement)),
+                              ctypes.byref(_cluster(cluster)), dev, seed, offset, nbytes, ptr,
+                              threads or (os.cpu_count() or 1), ctypes.byref(bad), ctypes.byref(first))
+    assert rc == 0, "orc_check_range: bad window"
+    return bad.value, first.value
+
+
 def _ops_array(ops: Sequence[OpTuple]):
     arr = (OrcOp * max(1, len(ops)))()
     for i, (s, d, (lo, hi, k, G, rep, part), b) in enumerate(ops):

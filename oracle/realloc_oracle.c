@@ -476,11 +476,29 @@ int64_t orc_shard_bytes(const orc_model* m, const orc_placement* p, const orc_cl
 
 /* ---- weights: DESIGN.md §4 value function (splitmix64) ------------------- */
 
+/* Special-value mode (seed bit 62): class c = bits 24..27 of the hash picks
+ * one of seven bf16 special classes (c < 7) or the raw low 16 bits; bit 16 is
+ * the sign, bits 17..23 a 7-bit field m for payloads / denormal mantissas. */
+static uint16_t orc_special(uint64_t z) {
+  const unsigned cls = (unsigned)((z >> 24) & 15u);
+  const unsigned s = (unsigned)((z >> 16) & 1u) ? 0x8000u : 0u;
+  const unsigned m = (unsigned)((z >> 17) & 0x7fu);
+  if (cls == 0) return (uint16_t)s;                                   /* signed zero */
+  if (cls == 1) return (uint16_t)(s + 0x7f80u);                       /* infinity */
+  if (cls == 2) return (uint16_t)(s + 0x7f80u + 0x40u + (m % 64u));   /* quiet NaN + payload */
+  if (cls == 3) return (uint16_t)(s + 0x7f80u + 1u + (m % 63u));      /* signalling NaN */
+  if (cls == 4) return (uint16_t)(s + (m | 1u));                      /* subnormal */
+  if (cls == 5) return (uint16_t)(s + 0x7f7fu);                       /* largest finite */
+  if (cls == 6) return (uint16_t)(s + 0x80u);                         /* smallest normal */
+  return (uint16_t)(z & 0xffffu);
+}
+
 uint16_t orc_value(uint64_t seed, int64_t tensor, int64_t index) {
   uint64_t z = (seed ^ ((uint64_t)tensor << 40) ^ (uint64_t)index) + 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   z ^= z >> 31;
+  if ((seed >> 62) & 1u) return orc_special(z);
   const uint32_t sign = (uint32_t)(z >> 63), expo = 117u + (uint32_t)((z >> 8) & 7u);
   return (uint16_t)((sign << 15) | (expo << 7) | (uint32_t)(z & 0x7fu));
 }
@@ -502,6 +520,140 @@ int orc_fill(const orc_model* m, const orc_placement* p, const orc_cluster* c, i
   }
   free(L.loc);
   return 0;
+}
+
+/* ---- streamed windows of a shard ------------------------------------------ *
+ * Expected bytes [off, off + len) of a device's shard, computed per element
+ * through the same address function as orc_fill, without materialising the
+ * shard: the full-size parity tests compare every destination byte of
+ * multi-GB shards window by window, and the CPU baseline fills its sources
+ * with several threads. */
+
+/* Local rows of a tensor as laid out: count, column range, and whether row i
+ * is logical row first + i at base + i * row_bytes (all modes but grouped). */
+static int64_t local_rows(const orc_model* m, const tensor_loc* t, int64_t id, int64_t* c0, int64_t* c1,
+                          int64_t* first) {
+  const tensor_shape s = shape_of(m, id);
+  *c0 = t->mode == MODE_COLS ? t->lo : 0;
+  *c1 = t->mode == MODE_COLS ? t->hi : s.cols;
+  *first = t->mode == MODE_COLS || t->mode == MODE_FULL ? 0 : t->lo;
+  return t->mode == MODE_COLS || t->mode == MODE_FULL ? s.rows : t->hi - t->lo;
+}
+
+static void fill_window(const orc_model* m, const dev_layout* L, uint64_t seed, int64_t off, int64_t len,
+                        uint16_t* buf) {
+  const int64_t pb = m->param_bytes, end = off + len;
+  memset(buf, 0, (size_t)len);
+  for (int64_t id = 0; id < n_tensors(m); ++id) {
+    const tensor_loc* t = &L->loc[id];
+    if (t->mode == MODE_NONE) continue;
+    const tensor_shape s = shape_of(m, id);
+    int64_t c0, c1, first;
+    const int64_t n = local_rows(m, t, id, &c0, &c1, &first);
+    const int64_t row_bytes = (c1 - c0) * pb;
+    int64_t i0 = 0, i1 = n;
+    if (t->mode != MODE_GROUPED) { /* rows are consecutive: clip to the window */
+      if (t->base >= end || t->base + n * row_bytes <= off) continue;
+      if (off > t->base) i0 = (off - t->base) / row_bytes;
+      if (end < t->base + n * row_bytes) i1 = (end - t->base + row_bytes - 1) / row_bytes;
+    }
+    for (int64_t i = i0; i < i1; ++i) {
+      const int64_t r = first + i;
+      const int64_t a = addr_of(m, L, id, r, c0);
+      if (a >= end || a + row_bytes <= off) continue;
+      int64_t ca = c0, cb = c1;
+      if (a < off) ca = c0 + (off - a) / pb;
+      if (a + row_bytes > end) cb = c0 + (end - a) / pb;
+      const int64_t at = (a - off) / pb - c0; /* window element of column 0 of this row */
+      for (int64_t col = ca; col < cb; ++col) buf[at + col] = orc_value(seed, id, r * s.cols + col);
+    }
+  }
+}
+
+typedef struct {
+  const orc_model* m;
+  const dev_layout* L;
+  uint64_t seed;
+  int64_t off, len, piece;
+  uint16_t* out;         /* fill target (NULL when checking) */
+  const uint16_t* got;   /* bytes to check (NULL when filling) */
+  int64_t next;          /* next piece (atomic) */
+  int64_t bad, first;    /* mismatching elements, first mismatching element index of the window */
+  pthread_mutex_t mu;
+} window_job;
+
+static void* window_worker(void* arg) {
+  window_job* j = (window_job*)arg;
+  uint16_t* scratch = j->got ? malloc((size_t)j->piece) : NULL;
+  int64_t bad = 0, first = -1;
+  for (;;) {
+    const int64_t k = __atomic_fetch_add(&j->next, 1, __ATOMIC_RELAXED);
+    const int64_t a = k * j->piece;
+    if (a >= j->len) break;
+    const int64_t n = a + j->piece < j->len ? j->piece : j->len - a;
+    if (j->out) {
+      fill_window(j->m, j->L, j->seed, j->off + a, n, j->out + a / 2);
+      continue;
+    }
+    fill_window(j->m, j->L, j->seed, j->off + a, n, scratch);
+    const uint16_t* g = j->got + a / 2;
+    if (memcmp(scratch, g, (size_t)n) == 0) continue;
+    for (int64_t e = 0; e < n / 2; ++e)
+      if (scratch[e] != g[e]) {
+        if (first < 0 || a / 2 + e < first) first = a / 2 + e;
+        ++bad;
+      }
+  }
+  free(scratch);
+  pthread_mutex_lock(&j->mu);
+  j->bad += bad;
+  if (first >= 0 && (j->first < 0 || first < j->first)) j->first = first;
+  pthread_mutex_unlock(&j->mu);
+  return NULL;
+}
+
+static int run_window(const orc_model* m, const orc_placement* p, const orc_cluster* c, int dev, uint64_t seed,
+                      int64_t off, int64_t len, uint16_t* out, const uint16_t* got, int threads, int64_t* bad,
+                      int64_t* first) {
+  dev_layout L;
+  if (!build_layout(m, p, c, dev, &L) || off < 0 || len < 0 || off + len > L.bytes || (off | len) & 1) {
+    free(L.loc);
+    return -1;
+  }
+  window_job j;
+  memset(&j, 0, sizeof(j));
+  j.m = m;
+  j.L = &L;
+  j.seed = seed;
+  j.off = off;
+  j.len = len;
+  j.piece = 4 << 20;
+  j.out = out;
+  j.got = got;
+  j.first = -1;
+  pthread_mutex_init(&j.mu, NULL);
+  if (threads < 1) threads = 1;
+  if ((int64_t)threads > len / j.piece + 1) threads = (int)(len / j.piece + 1);
+  pthread_t* th = malloc(sizeof(pthread_t) * (size_t)threads);
+  for (int i = 0; i < threads; ++i) pthread_create(&th[i], NULL, window_worker, &j);
+  for (int i = 0; i < threads; ++i) pthread_join(th[i], NULL);
+  free(th);
+  pthread_mutex_destroy(&j.mu);
+  free(L.loc);
+  if (bad) *bad = j.bad;
+  if (first) *first = j.first;
+  return 0;
+}
+
+int orc_fill_range(const orc_model* m, const orc_placement* p, const orc_cluster* c, int dev, uint64_t seed,
+                   int64_t offset, int64_t len, uint16_t* buf, int threads) {
+  return run_window(m, p, c, dev, seed, offset, len, buf, NULL, threads, NULL, NULL);
+}
+
+int orc_check_range(const orc_model* m, const orc_placement* p, const orc_cluster* c, int dev, uint64_t seed,
+                    int64_t offset, int64_t len, const uint16_t* got, int threads, int64_t* mismatches,
+                    int64_t* first) {
+  return run_window(m, p, c, dev, seed, offset, len, NULL, got, threads, mismatches, first);
 }
 
 /* ---- CPU reallocation ------------------------------------------------------ */

@@ -75,10 +75,25 @@ int orc_plan(const orc_model* m, const orc_placement* src, const orc_placement* 
              const orc_cluster* c, int policy, orc_op* ops, int cap, int* n_ops, orc_op* local,
              int cap_local, int* n_local, int64_t* total_bytes, double* est_time);
 int64_t orc_shard_bytes(const orc_model* m, const orc_placement* p, const orc_cluster* c, int dev);
+/* bf16 bits of logical element `index` of `tensor`. Seed bit 62 selects the
+ * special-value mode (signed zeros, infinities, quiet/signalling NaNs with
+ * payloads, subnormals, extreme normals, arbitrary 16-bit words). */
+#define ORC_SEED_SPECIAL (1ull << 62)
 uint16_t orc_value(uint64_t seed, int64_t tensor, int64_t index);
 /* Fill a device's shard (all held elements; padding untouched). */
 int orc_fill(const orc_model* m, const orc_placement* p, const orc_cluster* c, int dev,
              uint64_t seed, uint16_t* buf);
+/* Bytes [offset, offset + len) of a device's expected shard (padding zero),
+ * element by element like orc_fill, with `threads` threads; offset and len
+ * even and inside the shard. 0 ok, -1 invalid. */
+int orc_fill_range(const orc_model* m, const orc_placement* p, const orc_cluster* c, int dev, uint64_t seed,
+                   int64_t offset, int64_t len, uint16_t* buf, int threads);
+/* Compare `got` (len bytes) with that window: *mismatches = differing bf16
+ * elements (padding included), *first = first differing element index
+ * within the window or -1. */
+int orc_check_range(const orc_model* m, const orc_placement* p, const orc_cluster* c, int dev, uint64_t seed,
+                    int64_t offset, int64_t len, const uint16_t* got, int threads, int64_t* mismatches,
+                    int64_t* first);
 /* CPU reallocation: run ops and local ops on host buffers indexed by device. */
 int orc_execute(const orc_model* m, const orc_placement* src, const orc_placement* dst,
                 const orc_cluster* c, const orc_op* ops, int n_ops, void* const* src_bufs,

@@ -55,7 +55,8 @@ class RrExecOptions(Structure):
     _fields_ = [("mode", c_int32), ("chunk_bytes", c_int64), ("host_of", POINTER(c_int32)),
                 ("mc_bufs", POINTER(c_void_p)), ("relay_flags", POINTER(c_void_p)), ("relay_chain", c_int32),
                 ("overlap_fanout", c_int32), ("ce_min_run_bytes", c_int64), ("stage_chunk_bytes", c_int64),
-                ("n_hosts", c_int32), ("stage_remote", POINTER(c_void_p)), ("stage_flags", POINTER(c_void_p))]
+                ("n_hosts", c_int32), ("stage_remote", POINTER(c_void_p)), ("stage_flags", POINTER(c_void_p)),
+                ("ce_transport", c_int32)]
 
 
 _P = c_void_p
@@ -71,6 +72,8 @@ _SIGNATURES = {
     "rr_plan_stage_slots": (c_int, [_P, POINTER(c_int32), c_int64, POINTER(c_int64)]),
     "rr_plan_ce_runs": (c_int, [_P, c_int, POINTER(c_int32), POINTER(c_int32), c_int64, POINTER(c_int64), c_int,
                                 POINTER(c_int)]),
+    "rr_plan_ce_copies": (c_int, [_P, c_int, POINTER(c_int32), POINTER(c_int32), POINTER(c_int64), c_int,
+                                  POINTER(c_int)]),
     "rr_mcast_supported": (c_int, [c_int, POINTER(c_int)]),
     "rr_mcast_create": (c_int, [c_int, c_size_t, c_int, POINTER(c_int), POINTER(c_size_t), POINTER(_P)]),
     "rr_mcast_import": (c_int, [c_int, c_int, c_size_t, c_int, POINTER(_P)]),

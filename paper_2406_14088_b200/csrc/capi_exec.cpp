@@ -111,12 +111,15 @@ struct rr_exec {
 
   // Copy-engine runs of phase 0 (rr::CeRun): issued on ce_stream, forked
   // from and joined back into the launching stream around the kernels.
+  // A copy-engine submission: a contiguous run (height = depth = 1), or a
+  // copy-engine transport copy (2D / 3D, rr::CeCopy).
   struct CeCopy {
-    void* dst;
-    const void* src;
-    size_t bytes;
-    DeviceId src_dev;  // source plan device and byte offset in its shard (onload pipelining)
-    int64_t src_off;
+    char* dst;
+    const char* src;
+    int64_t width, height, depth, src_pitch, dst_pitch, src_slice, dst_slice;
+    DeviceId src_dev;  // source plan device and byte offsets in its shard (onload pipelining)
+    int64_t src_off, src_end;
+    int64_t bytes() const { return width * height * depth; }
   };
   std::vector<CeCopy> ce;
   int64_t ce_bytes = 0;
@@ -300,6 +303,28 @@ std::vector<rr::CeRun> ce_runs(const rr_plan* plan, const std::vector<rr::Job>& 
   return out;
 }
 
+void issue_copy(const rr_exec::CeCopy& c, cudaStream_t stream) {
+  if (c.depth > 1) {
+    cudaMemcpy3DParms p = {};
+    p.srcPtr = make_cudaPitchedPtr(const_cast<char*>(c.src), static_cast<size_t>(c.src_pitch),
+                                   static_cast<size_t>(c.width), static_cast<size_t>(c.src_slice / c.src_pitch));
+    p.dstPtr = make_cudaPitchedPtr(c.dst, static_cast<size_t>(c.dst_pitch), static_cast<size_t>(c.width),
+                                   static_cast<size_t>(c.dst_slice / c.dst_pitch));
+    p.extent = make_cudaExtent(static_cast<size_t>(c.width), static_cast<size_t>(c.height),
+                               static_cast<size_t>(c.depth));
+    p.kind = cudaMemcpyDeviceToDevice;
+    check_cuda(cudaMemcpy3DAsync(&p, stream), "copy-engine transport (3D)");
+  } else if (c.height > 1) {
+    check_cuda(cudaMemcpy2DAsync(c.dst, static_cast<size_t>(c.dst_pitch), c.src, static_cast<size_t>(c.src_pitch),
+                                 static_cast<size_t>(c.width), static_cast<size_t>(c.height), cudaMemcpyDeviceToDevice,
+                                 stream),
+               "copy-engine transport (2D)");
+  } else {
+    check_cuda(cudaMemcpyAsync(c.dst, c.src, static_cast<size_t>(c.width), cudaMemcpyDeviceToDevice, stream),
+               "copy-engine copy");
+  }
+}
+
 // Copy-engine runs: start them on ce_stream once the work already queued on
 // `after` (or, with an event, that event) is done; join them back into
 // `into` so that whatever follows there (barrier, next phase) sees them.
@@ -309,12 +334,18 @@ void ce_issue(rr_exec* ex, cudaStream_t after, cudaEvent_t after_event = nullptr
     after_event = ex->ce_fork;
   }
   check_cuda(cudaStreamWaitEvent(ex->ce_stream, after_event, 0), "cudaStreamWaitEvent(ce fork)");
-  for (const auto& c : ex->ce)
-    check_cuda(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "copy-engine run");
+  for (const auto& c : ex->ce) issue_copy(c, ex->ce_stream);
   for (const auto& p : ex->stage) {
     check_cuda(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "staged push");
     signal_piece(ex->ce_stream, p.flag, ex->epoch);
   }
+}
+
+// Largest row pitch a 2D / 3D copy accepts on this device.
+int64_t max_pitch(int cuda_device) {
+  int v = 0;
+  check_cuda(cudaDeviceGetAttribute(&v, cudaDevAttrMaxPitch, cuda_device), "cudaDevAttrMaxPitch");
+  return v;
 }
 
 // The first n uint32 of a flag array (mapped in this process) must be zero.
@@ -396,6 +427,27 @@ rr_status rr_plan_ce_runs(const rr_plan* plan, int n_local, const int32_t* local
   });
 }
 
+rr_status rr_plan_ce_copies(const rr_plan* plan, int n_local, const int32_t* local, const int32_t* host_of,
+                            int64_t* out11, int cap, int* n) {
+  return guarded([&] {
+    need(plan != nullptr && n != nullptr, "null plan/output");
+    rr::HostMap hm = host_map(plan, n_local, local, host_of);
+    hm.ce_remote = true;
+    const auto jobs = rr::build_jobs(plan->lowered, hm, 0);
+    // host only: the pitch limit of B200 (cudaDevAttrMaxPitch = 2^31 - 1)
+    const auto copies = rr::ce_transport_copies(jobs, hm, (int64_t{1} << 31) - 1);
+    *n = static_cast<int>(copies.size());
+    if (out11 == nullptr) return;
+    need(cap >= *n, "output table too small");
+    for (size_t i = 0; i < copies.size(); ++i) {
+      const auto& c = copies[i];
+      const int64_t v[11] = {c.src,   c.dst,       c.src_off,   c.dst_off,   c.width,    c.height,
+                             c.depth, c.src_pitch, c.dst_pitch, c.src_slice, c.dst_slice};
+      std::copy(v, v + 11, out11 + 11 * i);
+    }
+  });
+}
+
 rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, void* const* src_bufs,
                          void* const* dst_bufs, int n_local, const int32_t* local, const int32_t* host_of,
                          int mode, int64_t chunk_bytes, rr_exec** out) {
@@ -412,6 +464,7 @@ rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, vo
   opt.n_hosts = 0;
   opt.stage_remote = nullptr;
   opt.stage_flags = nullptr;
+  opt.ce_transport = 0;
   return rr_exec_create_ex(plan, cuda_device, n_devices, src_bufs, dst_bufs, n_local, local, &opt, out);
 }
 
@@ -459,14 +512,24 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       hm.stage_flags = reinterpret_cast<uint64_t>(options->stage_flags[hm.me]);
       need(n_stage_slots == 0 || hm.stage_flags != 0, "missing this host's stage flag array");
     }
+    if (options->ce_transport) {
+      need(mode == 0, "copy-engine transport is a push-mode path");
+      need(!staged && options->mc_bufs == nullptr, "copy-engine transport excludes the staged gather and multicast");
+      hm.ce_remote = true;
+    }
     check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
     int per_sm = 0, sms = 0;
     check_cuda(rr::copy_max_ctas(&per_sm, &sms), "occupancy query");
     const auto jobs = rr::build_jobs(plan->lowered, hm, mode);
     const int64_t ce_min = options->ce_min_run_bytes == 0 ? kDefaultCeRunBytes : options->ce_min_run_bytes;
     const std::vector<rr::CeRun> runs =
-        (mode == 0 && ce_min > 0 && src_bufs && dst_bufs) ? ce_runs(plan, jobs, hm, ce_min)
-                                                          : std::vector<rr::CeRun>{};
+        (mode == 0 && ce_min > 0 && src_bufs && dst_bufs && !hm.ce_remote) ? ce_runs(plan, jobs, hm, ce_min)
+                                                                           : std::vector<rr::CeRun>{};
+    std::vector<rr::CeCopy> transport;
+    if (hm.ce_remote) {
+      need(src_bufs != nullptr && dst_bufs != nullptr, "copy-engine transport needs buffer tables");
+      transport = rr::ce_transport_copies(jobs, hm, max_pitch(cuda_device));
+    }
     auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes, &runs);
     auto b = rr::build_items(jobs, 1, hm, src_bufs, dst_bufs, chunk_bytes);
     if (options->chunk_bytes <= 0) {
@@ -500,9 +563,17 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
     upload(a, ex->phase[0]);
     upload(b, ex->phase[1]);
     for (const auto& u : runs) {
-      ex->ce.push_back({static_cast<char*>(dst_bufs[u.dst]) + u.dst_off, static_cast<const char*>(src_bufs[u.src]) + u.src_off,
-                        static_cast<size_t>(u.bytes), u.src, u.src_off});
+      ex->ce.push_back({static_cast<char*>(dst_bufs[u.dst]) + u.dst_off,
+                        static_cast<const char*>(src_bufs[u.src]) + u.src_off, u.bytes, 1, 1, u.bytes, u.bytes, 0, 0,
+                        u.src, u.src_off, u.src_off + u.bytes});
       ex->ce_bytes += u.bytes;
+    }
+    for (const auto& c : transport) {
+      need(dst_bufs[c.dst] != nullptr && src_bufs[c.src] != nullptr, "missing a copy-engine transport buffer");
+      ex->ce.push_back({static_cast<char*>(dst_bufs[c.dst]) + c.dst_off,
+                        static_cast<const char*>(src_bufs[c.src]) + c.src_off, c.width, c.height, c.depth,
+                        c.src_pitch, c.dst_pitch, c.src_slice, c.dst_slice, c.src, c.src_off, c.src_end()});
+      ex->ce_bytes += c.bytes();
     }
     if (staged) {
       ex->stage_ctas = sms;
@@ -722,8 +793,7 @@ rr_status rr_exec_enable_onload(rr_exec* ex, int n_src, const int32_t* src_devic
     for (const auto& c : ex->ce)
       for (int k = 0; k < n_src; ++k)
         if (src_devices[k] == c.src_dev)
-          need(c.src_off + static_cast<int64_t>(c.bytes) <= src_bytes[k],
-               "a copy-engine run reads beyond the onloaded bytes of its source");
+          need(c.src_end <= src_bytes[k], "a copy-engine copy reads beyond the onloaded bytes of its source");
     // So must every staged push: it sends source bytes as they stand.
     for (const auto& p : ex->stage)
       for (int k = 0; k < n_src; ++k)
@@ -843,31 +913,41 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
       }
     }
     if (!ex->ce.empty()) {
-      // Copy-engine runs follow the onload: the part of a run that reads
-      // chunk c starts once chunk c has landed; runs over sources that are
-      // not onloaded start right away.
+      // Copy-engine copies follow the onload: the part of a contiguous run
+      // that reads chunk c starts once chunk c has landed; a 2D / 3D
+      // transport copy starts once the chunk holding its last source byte
+      // has; copies over sources that are not onloaded start right away.
       auto onloaded = [&](DeviceId d) {
         return std::any_of(ex->chunks.begin(), ex->chunks.end(), [&](const rr_exec::Chunk& ch) { return ch.device == d; });
       };
+      auto flat = [](const rr_exec::CeCopy& c) { return c.height == 1 && c.depth == 1; };
       auto piece = [&](const rr_exec::CeCopy& c, int64_t lo, int64_t hi) {  // source bytes [lo, hi) of the shard
-        const int64_t a = std::max(lo, c.src_off), b = std::min(hi, c.src_off + static_cast<int64_t>(c.bytes));
+        const int64_t a = std::max(lo, c.src_off), b = std::min(hi, c.src_end);
         if (a >= b) return;
-        check_cuda(cudaMemcpyAsync(static_cast<char*>(c.dst) + (a - c.src_off),
-                                   static_cast<const char*>(c.src) + (a - c.src_off), static_cast<size_t>(b - a),
-                                   cudaMemcpyDeviceToDevice, ex->ce_stream),
-                   "copy-engine run");
+        rr_exec::CeCopy p = c;
+        p.dst += a - c.src_off;
+        p.src += a - c.src_off;
+        p.width = b - a;
+        issue_copy(p, ex->ce_stream);
       };
       for (const auto& c : ex->ce)
-        if (!onloaded(c.src_dev)) piece(c, c.src_off, c.src_off + static_cast<int64_t>(c.bytes));
+        if (!onloaded(c.src_dev)) issue_copy(c, ex->ce_stream);
       for (size_t k = 0; k < ex->chunks.size(); ++k) {
         const auto& ch = ex->chunks[k];
-        bool any = false;
-        for (const auto& c : ex->ce) any = any || (c.src_dev == ch.device && c.src_off < ch.offset + ch.bytes &&
-                                                  c.src_off + static_cast<int64_t>(c.bytes) > ch.offset);
-        if (!any) continue;
+        const int64_t lo = ch.offset, hi = ch.offset + ch.bytes;
+        auto in_chunk = [&](const rr_exec::CeCopy& c) {
+          if (c.src_dev != ch.device) return false;
+          return flat(c) ? (c.src_off < hi && c.src_end > lo) : (c.src_end > lo && c.src_end <= hi);
+        };
+        if (!std::any_of(ex->ce.begin(), ex->ce.end(), in_chunk)) continue;
         check_cuda(cudaStreamWaitEvent(ex->ce_stream, ex->events[k], 0), "cudaStreamWaitEvent(ce chunk)");
-        for (const auto& c : ex->ce)
-          if (c.src_dev == ch.device) piece(c, ch.offset, ch.offset + ch.bytes);
+        for (const auto& c : ex->ce) {
+          if (!in_chunk(c)) continue;
+          if (flat(c))
+            piece(c, lo, hi);
+          else
+            issue_copy(c, ex->ce_stream);
+        }
       }
     }
     auto segment_phase = [&](const rr_exec::Segment& sg) {

@@ -370,6 +370,12 @@ std::vector<CeRun> matching_runs(const rlplan::ShardLayout& s, const rlplan::Sha
 
 namespace {
 
+// A job whose remote destinations the copy-engine transport (or a copy-engine
+// run) may take: plain phase-0 work reading a real source shard.
+bool plain_push(const Job& j, int phase) {
+  return phase == 0 && !j.multicast && !j.src_is_dst_buffer && !j.relay_wait && !j.relay_signal;
+}
+
 bool ce_covered(const std::vector<CeRun>& runs, DeviceId src, DeviceId dst, const CopyRect& r) {
   for (const auto& u : runs)
     if (u.src == src && u.dst == dst && r.dst_off >= u.dst_off && rect_dst_end(r) <= u.dst_off + u.bytes) return true;
@@ -481,9 +487,8 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
       int64_t relay_slot = j.relay_base;
       if ((j.relay_wait || j.relay_signal) && j.dsts.size() > static_cast<size_t>(kMaxFan))
         throw rlplan::ValidationError("relay job with more than kMaxFan destinations");
-      // Copy-engine runs: plain jobs that read a real source shard
-      const bool ce_job = ce && !ce->empty() && phase == 0 && !mc0 && !j.src_is_dst_buffer && !j.relay_wait &&
-                          !j.relay_signal;
+      // Copy-engine runs / transport: plain jobs that read a real source shard
+      const bool ce_job = ((ce && !ce->empty()) || hm.ce_remote) && plain_push(j, phase);
       std::vector<uint64_t> kept;
       for (CopyRect r : j.op->rects) {
         if (j.src_is_dst_buffer) {  // fan-out reads the leader's copy: destination geometry
@@ -493,8 +498,11 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
         const std::vector<uint64_t>* to = &dsts;
         if (ce_job) {
           kept.clear();
-          for (size_t k = 0; k < dsts.size(); ++k)
-            if (!ce_covered(*ce, j.src, devs[k], r)) kept.push_back(dsts[k]);
+          for (size_t k = 0; k < dsts.size(); ++k) {
+            if (hm.ce_remote && hm.host[static_cast<size_t>(devs[k])] != hm.me) continue;
+            if (ce && ce_covered(*ce, j.src, devs[k], r)) continue;
+            kept.push_back(dsts[k]);
+          }
           if (kept.empty()) continue;
           if (kept.size() != dsts.size()) to = &kept;
         }
@@ -580,6 +588,144 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
     acc.src_is_dst.push_back(t->src_is_dst);
   }
   return acc;
+}
+
+namespace {
+
+// Longest arithmetic chain of unused copies starting at i: copy k of the
+// chain sits at (src_off, dst_off) + k * (ds, dd). Candidates are the same
+// shape, sorted by src_off; ok(ds, dd) says whether a stride pair can be
+// expressed (non-overlapping rows, pitch limits, 3D divisibility).
+template <class Ok>
+std::vector<size_t> best_chain(const std::vector<CeCopy>& c, const std::vector<bool>& used, size_t i, Ok ok) {
+  std::map<std::pair<int64_t, int64_t>, size_t> at;  // (src_off, dst_off) -> index
+  for (size_t k = i; k < c.size(); ++k)
+    if (!used[k]) at.emplace(std::make_pair(c[k].src_off, c[k].dst_off), k);
+  std::vector<size_t> best{i};
+  size_t tried = 0;
+  for (size_t j = i + 1; j < c.size() && tried < 64; ++j) {
+    if (used[j]) continue;
+    ++tried;
+    const int64_t ds = c[j].src_off - c[i].src_off, dd = c[j].dst_off - c[i].dst_off;
+    if (ds <= 0 || dd <= 0 || !ok(ds, dd)) continue;
+    std::vector<size_t> chain{i, j};
+    for (;;) {
+      const auto it = at.find({c[i].src_off + ds * static_cast<int64_t>(chain.size()),
+                               c[i].dst_off + dd * static_cast<int64_t>(chain.size())});
+      if (it == at.end()) break;
+      chain.push_back(it->second);
+    }
+    if (chain.size() > best.size()) best = std::move(chain);
+  }
+  return best;
+}
+
+// Merge the elementary copies of one (source, destination) pair.
+std::vector<CeCopy> merge_pair(std::vector<CeCopy> flat, std::vector<CeCopy> strided, int64_t max_pitch) {
+  std::vector<CeCopy> out;
+  // contiguous pieces: coalesce neighbours, then chain equal widths into 2D
+  std::sort(flat.begin(), flat.end(), [](const CeCopy& a, const CeCopy& b) { return a.src_off < b.src_off; });
+  std::vector<CeCopy> co;
+  for (const auto& c : flat) {
+    if (!co.empty() && co.back().src_off + co.back().width == c.src_off &&
+        co.back().dst_off + co.back().width == c.dst_off)
+      co.back().width += c.width;
+    else
+      co.push_back(c);
+  }
+  std::map<int64_t, std::vector<CeCopy>> by_width;
+  for (const auto& c : co) by_width[c.width].push_back(c);
+  for (auto& [w, list] : by_width) {
+    std::vector<bool> used(list.size(), false);
+    for (size_t i = 0; i < list.size(); ++i) {
+      if (used[i]) continue;
+      const auto chain = best_chain(list, used, i, [&, w = w](int64_t ds, int64_t dd) {
+        return ds >= w && dd >= w && ds <= max_pitch && dd <= max_pitch;
+      });
+      for (size_t k : chain) used[k] = true;
+      CeCopy m = list[i];
+      if (chain.size() > 1) {
+        m.height = static_cast<int64_t>(chain.size());
+        m.src_pitch = list[chain[1]].src_off - list[i].src_off;
+        m.dst_pitch = list[chain[1]].dst_off - list[i].dst_off;
+      } else {
+        m.src_pitch = m.dst_pitch = m.width;
+      }
+      out.push_back(m);
+    }
+  }
+  // row-parallel pieces: chain equal shapes into 3D
+  using Shape = std::tuple<int64_t, int64_t, int64_t, int64_t>;
+  std::map<Shape, std::vector<CeCopy>> by_shape;
+  for (const auto& c : strided) by_shape[{c.width, c.height, c.src_pitch, c.dst_pitch}].push_back(c);
+  for (auto& [shape, list] : by_shape) {
+    std::sort(list.begin(), list.end(), [](const CeCopy& a, const CeCopy& b) { return a.src_off < b.src_off; });
+    std::vector<bool> used(list.size(), false);
+    const auto [w, h, sp, dp] = shape;
+    for (size_t i = 0; i < list.size(); ++i) {
+      if (used[i]) continue;
+      const auto chain = best_chain(list, used, i, [&, h = h, sp = sp, dp = dp](int64_t ds, int64_t dd) {
+        return ds % sp == 0 && dd % dp == 0 && ds / sp >= h && dd / dp >= h;
+      });
+      for (size_t k : chain) used[k] = true;
+      CeCopy m = list[i];
+      if (chain.size() > 1) {
+        m.depth = static_cast<int64_t>(chain.size());
+        m.src_slice = list[chain[1]].src_off - list[i].src_off;
+        m.dst_slice = list[chain[1]].dst_off - list[i].dst_off;
+      }
+      out.push_back(m);
+    }
+  }
+  std::sort(out.begin(), out.end(), [](const CeCopy& a, const CeCopy& b) { return a.dst_off < b.dst_off; });
+  return out;
+}
+
+}  // namespace
+
+std::vector<CeCopy> ce_transport_copies(const std::vector<Job>& jobs, const HostMap& hm, int64_t max_pitch) {
+  std::map<std::pair<DeviceId, DeviceId>, std::pair<std::vector<CeCopy>, std::vector<CeCopy>>> pairs;
+  for (const auto& j : jobs) {
+    if (!plain_push(j, j.phase) || hm.host[static_cast<size_t>(j.src)] != hm.me) continue;
+    for (DeviceId d : j.dsts) {
+      if (hm.host[static_cast<size_t>(d)] == hm.me) continue;
+      auto& [flat, strided] = pairs[{j.src, d}];
+      for (const auto& r : j.op->rects) {
+        CeCopy c;
+        c.src = j.src;
+        c.dst = d;
+        c.src_off = r.src_off;
+        c.dst_off = r.dst_off;
+        if (r.rows == 1 || (r.src_pitch == r.row_bytes && r.dst_pitch == r.row_bytes)) {
+          c.width = r.row_bytes * r.rows;
+          flat.push_back(c);
+        } else {
+          c.width = r.row_bytes;
+          c.height = r.rows;
+          c.src_pitch = r.src_pitch;
+          c.dst_pitch = r.dst_pitch;
+          strided.push_back(c);
+        }
+      }
+    }
+  }
+  // rotation rounds over the hosts (ascending ids)
+  std::vector<int> hosts(hm.host.begin(), hm.host.end());
+  hosts.push_back(hm.me);
+  std::sort(hosts.begin(), hosts.end());
+  hosts.erase(std::unique(hosts.begin(), hosts.end()), hosts.end());
+  const int H = static_cast<int>(hosts.size());
+  const int pos = static_cast<int>(std::find(hosts.begin(), hosts.end(), hm.me) - hosts.begin());
+  std::vector<CeCopy> out;
+  for (int r = 1; r < H; ++r) {
+    const int h = hosts[static_cast<size_t>((pos + r) % H)];
+    for (auto& [sd, lists] : pairs) {
+      if (hm.host[static_cast<size_t>(sd.second)] != h) continue;
+      auto merged = merge_pair(std::move(lists.first), std::move(lists.second), max_pitch);
+      out.insert(out.end(), merged.begin(), merged.end());
+    }
+  }
+  return out;
 }
 
 }  // namespace rr

@@ -61,6 +61,9 @@ struct HostMap {
   int64_t stage_chunk = 0;               // 0 = off
   uint64_t stage_flags = 0;
   std::vector<int64_t> stage_slot0;      // per plan device: its first slot here, -1 = not staged
+  // Copy-engine transport (push): every remote destination of a plain
+  // phase-0 job is left out of the SM items; ce_transport_copies moves it.
+  bool ce_remote = false;
 };
 
 // Staged gather: the remote sources host `h` reads, in arrival order. Round
@@ -102,6 +105,30 @@ struct CeRun {
 // offset relative to the run start).
 std::vector<CeRun> matching_runs(const rlplan::ShardLayout& s, const rlplan::ShardLayout& d, rlplan::DeviceId sd,
                                  rlplan::DeviceId dd, int64_t min_bytes);
+
+// Copy-engine transport: one copy-engine submission of a (local source,
+// remote destination) pair — width bytes x height rows x depth slices, rows
+// at the pitches, slices at the slice strides (multiples of the pitches).
+// depth > 1 is a cudaMemcpy3DAsync, height > 1 a cudaMemcpy2DAsync.
+struct CeCopy {
+  rlplan::DeviceId src = -1, dst = -1;
+  int64_t src_off = 0, dst_off = 0;
+  int64_t width = 0, height = 1, depth = 1;
+  int64_t src_pitch = 0, dst_pitch = 0;
+  int64_t src_slice = 0, dst_slice = 0;
+  int64_t bytes() const { return width * height * depth; }
+  int64_t src_end() const { return src_off + (depth - 1) * src_slice + (height - 1) * src_pitch + width; }
+};
+
+// The copies that move every remote destination of the plain phase-0 push
+// jobs in `jobs` (hm.ce_remote). The per-layer rects of one tensor kind sit
+// at a constant layer stride in both shards, so they merge into one 2D copy
+// (contiguous pieces: rows = layers) or one 3D copy (row-parallel pieces,
+// when the layer strides are whole multiples of the row pitches); pitches
+// stay <= max_pitch. Ordered in rotation rounds: round r sends to the host r
+// places after this one (ids ascending), so while every host follows its
+// order each receives from one sender at a time.
+std::vector<CeCopy> ce_transport_copies(const std::vector<Job>& jobs, const HostMap& hm, int64_t max_pitch);
 
 // Byte extent [first, last) a rect writes in its destination shard.
 inline int64_t rect_dst_end(const rlplan::CopyRect& r) {

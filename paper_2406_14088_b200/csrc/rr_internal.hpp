@@ -65,10 +65,34 @@ __host__ __device__ inline uint64_t mix64(uint64_t x) {
   return z ^ (z >> 31);
 }
 
+// Seed flag of the special-value fill (DESIGN.md §3 "Weights"): bf16 words
+// that a value-preserving copy must not disturb — ±0, ±Inf, quiet NaNs with
+// payloads, signalling NaNs, denormals, ±max / ±min normals — interleaved
+// with arbitrary 16-bit patterns. Shards are opaque bytes; this
+// mode proves every copy path moves them as such.
+constexpr uint64_t kSeedSpecial = uint64_t{1} << 62;
+
+__host__ __device__ inline uint16_t special_value(uint64_t h) {
+  const uint32_t r = static_cast<uint32_t>(h >> 16);
+  const uint32_t sign = (r & 1u) << 15;
+  const uint32_t m7 = (r >> 1) & 0x7fu;
+  switch ((r >> 8) & 15u) {
+    case 0: return static_cast<uint16_t>(sign);                            // +-0
+    case 1: return static_cast<uint16_t>(sign | 0x7f80u);                  // +-Inf
+    case 2: return static_cast<uint16_t>(sign | 0x7fc0u | (m7 & 0x3fu));   // quiet NaN, payload
+    case 3: return static_cast<uint16_t>(sign | 0x7f80u | (1u + m7 % 63u));  // signalling NaN
+    case 4: return static_cast<uint16_t>(sign | m7 | 1u);                  // denormal
+    case 5: return static_cast<uint16_t>(sign | 0x7f7fu);                  // +-max normal
+    case 6: return static_cast<uint16_t>(sign | 0x0080u);                  // +-min normal
+    default: return static_cast<uint16_t>(h);                              // any 16-bit pattern
+  }
+}
+
 // bf16 bits: random sign, exponent in [2^-10, 2^-3], random 7-bit mantissa
-// (never NaN/Inf/denormal).
+// (never NaN/Inf/denormal); with kSeedSpecial in the seed, special_value.
 __host__ __device__ inline uint16_t weight_value(uint64_t seed, uint64_t tensor, uint64_t idx) {
   const uint64_t h = mix64(seed ^ (tensor << 40) ^ idx);
+  if (seed & kSeedSpecial) return special_value(h);
   const uint32_t sign = static_cast<uint32_t>(h >> 63);
   const uint32_t expo = 117u + static_cast<uint32_t>((h >> 8) & 7u);
   const uint32_t mant = static_cast<uint32_t>(h & 0x7fu);

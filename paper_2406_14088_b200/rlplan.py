@@ -384,6 +384,20 @@ class ReallocPlan:
         check(lib.rr_plan_ce_runs(self._h, len(local), arr, hosts, min_run_bytes, out, cnt.value, ctypes.byref(cnt)))
         return [tuple(out[5 * i:5 * i + 5]) for i in range(cnt.value)]
 
+    def ce_copies(self, local: Sequence[int], host_of: Optional[Sequence[int]] = None) -> List[Tuple[int, ...]]:
+        """Copy-engine transport copies a push executor driving `local` would
+        issue, in issue order (host only): (src device, dst device, src offset,
+        dst offset, width, height, depth, src pitch, dst pitch, src slice
+        stride, dst slice stride)."""
+        arr = (ctypes.c_int32 * max(1, len(local)))(*local)
+        n = self.cluster.device_count()
+        hosts = (ctypes.c_int32 * n)(*host_of) if host_of is not None else None
+        cnt = ctypes.c_int()
+        check(lib.rr_plan_ce_copies(self._h, len(local), arr, hosts, None, 0, ctypes.byref(cnt)))
+        out = (ctypes.c_int64 * (11 * max(1, cnt.value)))()
+        check(lib.rr_plan_ce_copies(self._h, len(local), arr, hosts, out, cnt.value, ctypes.byref(cnt)))
+        return [tuple(out[11 * i:11 * i + 11]) for i in range(cnt.value)]
+
     def devices(self, side: int) -> List[int]:
         p = self.src if side == 0 else self.dst
         return p.mesh.devices(self.cluster)

@@ -145,7 +145,7 @@ class Executor:
                  relay_flags: Optional[Dict[int, int]] = None, relay_chain: bool = True,
                  overlap_fanout: bool = False, ce_min_run_bytes: int = 0, stage_chunk_bytes: int = 0,
                  n_hosts: int = 0, stage_remote: Optional[Dict[Tuple[int, int], int]] = None,
-                 stage_flags: Optional[Dict[int, int]] = None):
+                 stage_flags: Optional[Dict[int, int]] = None, ce_transport: bool = False):
         n = plan.cluster.device_count()
         self.plan = plan
         sp, dp = (ctypes.c_void_p * n)(), (ctypes.c_void_p * n)()
@@ -175,7 +175,7 @@ class Executor:
             for h, p in (stage_flags or {}).items():
                 sfl[h] = p
         opt = RrExecOptions(mode, chunk_bytes, hosts, mcs, rfl, int(relay_chain), int(overlap_fanout),
-                            ce_min_run_bytes, stage_chunk_bytes, n_hosts, srem, sfl)
+                            ce_min_run_bytes, stage_chunk_bytes, n_hosts, srem, sfl, int(ce_transport))
         h = ctypes.c_void_p()
         check(lib.rr_exec_create_ex(plan.handle, cuda_device, n, sp, dp, len(loc), arr, ctypes.byref(opt),
                                     ctypes.byref(h)))
@@ -210,7 +210,8 @@ class Executor:
         return a.value, b.value
 
     def ce_runs(self) -> Tuple[int, int]:
-        """(copy-engine runs, their bytes) that launch() issues beside the kernels."""
+        """(copy-engine submissions — runs or transport copies —, their bytes)
+        that launch() issues beside the kernels."""
         n, b = ctypes.c_int(), ctypes.c_int64()
         check(lib.rr_exec_ce_runs(self._h, ctypes.byref(n), ctypes.byref(b)))
         return n.value, b.value

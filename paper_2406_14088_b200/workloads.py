@@ -7,17 +7,14 @@ written (pp, dp, tp) as in BASELINE.json.
 from __future__ import annotations
 
 import dataclasses
+import json
+import os
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Tuple
 
-from .rlplan import (BALANCED, GATE_UP_CONCAT, GATE_UP_SEPARATE, MODELS, QKV_CONCAT, QKV_GROUPED,
-                     QKV_SEPARATE, ClusterSpec, DeviceMesh, ModelSpec, ParallelStrategy, Placement,
-                     ReallocPlan, b200_cluster, plan_data_transfer, plan_param_realloc)
-
-
-def layout(devices: int, pp: int, dp: int, tp: int, qkv: int = QKV_SEPARATE,
-           gate_up: int = GATE_UP_SEPARATE) -> Placement:
-    return Placement(DeviceMesh(0, 1, 0, devices), ParallelStrategy(dp=dp, tp=tp, pp=pp), qkv, gate_up)
+from .rlplan import (BALANCED, GATE_UP_SEPARATE, MODELS, QKV_SEPARATE, ClusterSpec, DeviceMesh, ModelSpec,
+                     ParallelStrategy, Placement, ReallocPlan, b200_cluster, plan_data_transfer,
+                     plan_param_realloc)
 
 
 @dataclass(frozen=True)
@@ -47,53 +44,36 @@ def _pp(p: Placement) -> str:
     return f"(pp{s.pp},dp{s.dp},tp{s.tp})"
 
 
-def _make(name: str, model: str, devices: int, src: Placement, dst: Placement, back: bool,
-          desc: str) -> Workload:
-    phases = ((src, dst), (dst, src)) if back else ((src, dst),)
-    return Workload(name, desc, MODELS[model], devices, phases)
+# The named workloads live in workloads.json as plain data (BASELINE.json
+# configs[0..4] and companions), so that bench.py's reference arm can build
+# the very same workloads without importing this package.
+TABLE_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "workloads.json")
 
 
-WORKLOADS: Dict[str, Workload] = {}
+def _placement(d: dict) -> Placement:
+    no, nc, go, gc = d["mesh"]
+    return Placement(DeviceMesh(no, nc, go, gc), ParallelStrategy(dp=d["dp"], tp=d["tp"], pp=d["pp"]),
+                     d.get("qkv_layout", QKV_SEPARATE), d.get("gate_up_layout", GATE_UP_SEPARATE),
+                     d.get("kv_layout", 0))
 
 
-def _register(w: Workload) -> None:
-    WORKLOADS[w.name] = w
+def _load_table() -> Dict[str, Workload]:
+    with open(TABLE_PATH) as f:
+        table = json.load(f)
+    for name, dims in table["models"].items():  # the table restates rlplan.MODELS; keep them one
+        m = MODELS[name]
+        if any(getattr(m, k) != v for k, v in dims.items()):
+            raise ValueError(f"workloads.json model {name!r} differs from rlplan.MODELS")
+    out: Dict[str, Workload] = {}
+    for e in table["workloads"]:
+        src, dst = _placement(e["src"]), _placement(e["dst"])
+        phases = ((src, dst), (dst, src)) if e["back"] else ((src, dst),)
+        out[e["name"]] = Workload(e["name"], e["description"], MODELS[e["model"]], e["devices"], phases,
+                                  data_bytes=e.get("data_bytes", 0))
+    return out
 
 
-# BASELINE.json configs[0]: the CPU oracle case.
-_register(_make("tiny_tp2_to_dp2", "tiny", 2, layout(2, 1, 1, 2), layout(2, 1, 2, 1), False,
-                "tiny LLaMA (4L, h256) (pp1,dp1,tp2)->(pp1,dp2,tp1) on 2 devices"))
-# BASELINE.json configs[1]: actor train layout -> generation layout and back.
-_register(_make("llama7b_tp8_dp8_roundtrip", "llama7b", 8, layout(8, 1, 1, 8), layout(8, 1, 8, 1), True,
-                "LLaMA-7B bf16 train (pp1,dp1,tp8) -> gen (pp1,dp8,tp1) and back, 8 plan devices"))
-# BASELINE.json configs[2]: pipeline-stage remap.
-_register(_make("llama13b_pp2tp4_to_dp2tp4", "llama13b", 8, layout(8, 2, 1, 4), layout(8, 1, 2, 4), False,
-                "LLaMA-13B bf16 (pp2,dp1,tp4)->(pp1,dp2,tp4)"))
-# BASELINE.json configs[3]: critic with Megatron-grouped QKV / fused gate-up -> concat layouts.
-_register(_make("llama34b_critic_pp4tp2_to_tp8", "llama34b_critic", 8,
-                layout(8, 4, 1, 2, QKV_GROUPED, GATE_UP_CONCAT), layout(8, 1, 1, 8, QKV_CONCAT, GATE_UP_CONCAT),
-                False, "LLaMA-34B critic bf16 (pp4,dp1,tp2)->(pp1,dp1,tp8), fused QKV/gate-up reinterleave"))
-# BASELINE.json configs[4]: full-box 70B.
-_register(_make("llama70b_pp2tp4_to_tp8", "llama70b", 8, layout(8, 2, 1, 4), layout(8, 1, 1, 8), False,
-                "LLaMA-70B bf16 (pp2,dp1,tp4)->(pp1,dp1,tp8)"))
-
-
-# Parameter sync of a whole replica to a DP group (disjoint =
-# parameter sync): every op is a contiguous one-to-many broadcast.
-_register(Workload("llama7b_replicate_to_dp8", "LLaMA-7B bf16 (pp1,dp1,tp1) on device 0 -> (pp1,dp8,tp1)",
-                   MODELS["llama7b"], 8,
-                   ((Placement(DeviceMesh(0, 1, 0, 1), ParallelStrategy()), layout(8, 1, 8, 1)),)))
-
-
-# Inter-call data transfer (DP-partitioned outputs of one
-# function call redistributed to the next call's layout). 32 MiB per
-# generation DP shard is a 256 MiB batch of per-token RLHF data.
-_register(Workload("data_gen_dp8_to_train_tp8",
-                   "RLHF batch, 32 MiB per DP shard: actor generation (pp1,dp8,tp1) -> training (pp1,dp1,tp8)",
-                   MODELS["llama7b"], 8, ((layout(8, 1, 8, 1), layout(8, 1, 1, 8)),), data_bytes=32 << 20))
-_register(Workload("data_gen_dp8_to_pp2dp2tp2",
-                   "RLHF batch, 32 MiB per DP shard: generation (pp1,dp8,tp1) -> critic (pp2,dp2,tp2)",
-                   MODELS["llama7b"], 8, ((layout(8, 1, 8, 1), layout(8, 2, 2, 2)),), data_bytes=32 << 20))
+WORKLOADS: Dict[str, Workload] = _load_table()
 
 
 def truncated(w: Workload, layers: int) -> Workload:

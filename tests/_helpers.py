@@ -84,3 +84,38 @@ def random_placement(rng, model, gpus_per_node: int = 8) -> Placement:
             return p
         except P.ValidationError:
             continue
+
+
+def oracle_compare_device(model, placement, cluster, dev: int, seed: int, dev_ptr: int, nbytes: int,
+                          window: int = 256 << 20, hosts=None):
+    """Compare every byte of a device-resident shard with the oracle's
+    expected shard, window by window (orc_check_range, all host threads):
+    window k + 1 is copied device->host while the oracle checks window k.
+    Returns (mismatching bf16 elements, byte offset of the first one or -1).
+    `hosts`: two reusable pinned buffers of >= window bytes (else allocated)."""
+    from oracle import oracle as O
+    from paper_2406_14088_b200 import runtime as R
+    own = hosts is None
+    if own:
+        hosts = [R.HostBuffer(window), R.HostBuffer(window)]
+    try:
+        offs = list(range(0, nbytes, window))
+        bad, first = 0, -1
+        if offs:
+            R.memcpy_async(hosts[0].ptr, dev_ptr, min(window, nbytes), 1)
+        for k, off in enumerate(offs):
+            R.stream_sync()
+            n = min(window, nbytes - off)
+            if k + 1 < len(offs):
+                nxt = offs[k + 1]
+                R.memcpy_async(hosts[(k + 1) % 2].ptr, dev_ptr + nxt, min(window, nbytes - nxt), 1)
+            b, f = O.check_range(model, placement, cluster, dev, seed, off, n, hosts[k % 2].ptr)
+            if b and first < 0:
+                first = off + 2 * f
+            bad += b
+        R.stream_sync()
+        return bad, first
+    finally:
+        if own:
+            for h in hosts:
+                h.free()

@@ -1,13 +1,22 @@
 """Multi-process GPU parity worker (launched by tests/test_multigpu.py via
-torchrun, one process per GPU). Each rank hosts a contiguous block of the 8
-plan devices; destination shards of remote ranks are reached through CUDA
-IPC and written by NVLink peer stores. Every rank compares its hosted
-destination shards with the CPU oracle and the results are all-reduced."""
+torchrun, one process per GPU — or several per GPU, oversubscribed). Each
+rank hosts a contiguous block of the 8 plan devices; destination shards of
+remote ranks are reached through CUDA IPC and written by peer stores (NVLink
+between GPUs; the same IPC mappings within one GPU when oversubscribed).
+Every rank compares its hosted destination shards with the CPU oracle and
+the results are all-reduced.
+
+Rank 0 prints one line per case: `case <name>: ok|FAIL <seconds>`.
+Environment: RR_FUZZ_CASES (24), RR_FUZZ_SEED (2406), RR_FULL_7B=1 (full-size
+7B round trip, every byte against the oracle; distinct GPUs only)."""
 from __future__ import annotations
 
+import contextlib
 import dataclasses
 import os
+import random
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -17,7 +26,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
-from _helpers import placement  # noqa: E402
+from _helpers import oracle_compare_device, placement, random_placement  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 from paper_2406_14088_b200 import runtime as R  # noqa: E402
 from paper_2406_14088_b200.rlplan import (BALANCED, MODELS, DeviceMesh, ParallelStrategy, Placement,  # noqa: E402
@@ -26,301 +35,247 @@ from paper_2406_14088_b200.workloads import WORKLOADS  # noqa: E402
 
 TINY_GQA = dataclasses.replace(MODELS["tiny"], name="tiny_gqa", hidden_size=512, num_attention_heads=16,
                                num_kv_heads=8, intermediate_size=1024)
+TINY_MQA = dataclasses.replace(TINY_GQA, name="tiny_mqa", num_attention_heads=8, num_kv_heads=1, num_layers=3)
+SPECIAL = O.SEED_SPECIAL  # special-value bf16 words (zeros, infinities, NaN payloads, subnormals, any pattern)
 
 CASES = [
-    ((1, 1, 8, 0, 0), (1, 8, 1, 0, 0)),
-    ((4, 1, 2, 2, 1), (1, 1, 8, 1, 1)),
-    ((2, 1, 4, 0, 0), (1, 1, 8, 0, 0)),
-    ((2, 1, 4, 0, 0), (1, 2, 4, 0, 0)),
-    ((1, 8, 1, 2, 1), (4, 1, 2, 0, 0)),
+    ((1, 1, 8, 0, 0), (1, 8, 1, 0, 0)),   # tp8 -> dp8 all-gather
+    ((4, 1, 2, 2, 1), (1, 1, 8, 1, 1)),   # 34B-style grouped/concat reinterleave
+    ((2, 1, 4, 0, 0), (1, 1, 8, 0, 0)),   # 70B-style pp2 tp4 -> tp8
+    ((2, 1, 4, 0, 0), (1, 2, 4, 0, 0)),   # 13B-style stage remap
+    ((1, 8, 1, 2, 1), (4, 1, 2, 0, 0)),   # dp8 replicas -> pp4 tp2
 ]
+REPLICATE = (Placement(DeviceMesh(0, 1, 0, 1), ParallelStrategy()), placement(8, 1, 8, 1))
+
+
+def pl(spec):
+    return placement(8, *spec[:3], qkv=spec[3], gate_up=spec[4])
+
+
+class Worker:
+    def __init__(self):
+        self.rank, self.world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+        # More ranks than GPUs (world 2/4 on one GPU, world 8 on four): ranks
+        # share a GPU and their kernels time-slice; IPC, flags, copy engines
+        # and barriers behave as across GPUs. NCCL refuses two ranks per GPU,
+        # so gloo carries the host-side collectives; multicast needs distinct
+        # GPUs and is skipped.
+        gpus = torch.cuda.device_count()
+        self.local = int(os.environ["LOCAL_RANK"]) % gpus
+        self.oversub = self.world > gpus
+        torch.cuda.set_device(self.local)
+        if self.oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+        self.c = b200_cluster(8)
+        self.failures: list = []
+        self.ce_runs = 0        # copy-engine runs issued by this rank
+        self.staged_phases = 0  # staged-gather phases set up
+
+    @contextlib.contextmanager
+    def case(self, label: str):
+        n0, t0 = len(self.failures), time.time()
+        try:
+            yield
+        except Exception as e:  # a crash in one case is a failure, the others still run
+            self.failures.append(f"{label}: {type(e).__name__}: {e}")
+        if self.rank == 0:
+            ok = "ok" if len(self.failures) == n0 else "FAIL"
+            print(f"case {label}: {ok} {time.time() - t0:.2f}s", flush=True)
+
+    def run(self, label, model, src, dst, seed, reps=1, policy=BALANCED, onload_chunk=0, zero_between=True,
+            **kw):
+        """Plan src -> dst, bind RankRealloc with `kw`, launch phase 0 `reps`
+        times (epochs advance per launch), each time comparing every hosted
+        destination byte with the oracle; flag and barrier timeouts fail."""
+        with self.case(label):
+            plan = plan_param_realloc(model, src, dst, self.c, policy)
+            rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], self.rank, self.world,
+                               self.local, **kw)
+            try:
+                self.ce_runs += sum(e.ce_runs()[0] for e in rr.executors)
+                self.staged_phases += len(rr.staged_phases)
+                for d, b in rr.buffers["a"].items():
+                    R.fill_shard(plan, R.SRC, d, b.ptr, seed)
+                for rep in range(reps):
+                    if zero_between:
+                        for b in rr.buffers["b"].values():
+                            b.zero()
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    hosts = None
+                    if onload_chunk and rep % 2 == 1:  # odd reps: sources onloaded from pinned host memory
+                        hosts = {d: R.HostBuffer(b.nbytes) for d, b in rr.buffers["a"].items()}
+                        for d, hb in hosts.items():
+                            hb.array()[:] = rr.buffers["a"][d].to_host()
+                        rr.run_phase_onload(0, {d: hb.ptr for d, hb in hosts.items()}, torch.cuda.Stream(),
+                                            chunk_bytes=onload_chunk)
+                    else:
+                        rr.run_phase(0)
+                    torch.cuda.synchronize()
+                    for d, b in rr.buffers["b"].items():
+                        got = b.to_host()
+                        want = O.fill(model, dst, self.c, d, seed)
+                        if not np.array_equal(got, want):
+                            self.failures.append(f"{label} rep {rep}: device {d} differs in "
+                                                 f"{int(np.count_nonzero(got != want))} elements")
+                    for hb in (hosts or {}).values():
+                        hb.free()
+                if rr.relay_timeouts() or rr.barrier.timed_out():
+                    self.failures.append(f"{label}: flag or barrier timeouts")
+                dist.barrier()
+            finally:
+                rr.close()
+
+    # ---- sections ---------------------------------------------------------
+
+    def basic(self):
+        """Peer stores / peer loads, flat and hierarchical, both kernels."""
+        for mode in (R.PUSH, R.PULL):
+            for kernel in (0, 1):
+                for hier in (True, False):
+                    for sp, dp in CASES:
+                        seed = 21 if hier else SPECIAL | 21
+                        self.run(f"basic {sp}->{dp} mode={mode} kernel={kernel} hier={hier} seed={seed:#x}",
+                                 TINY_GQA, pl(sp), pl(dp), seed, mode=mode, kernel=kernel, hierarchical=hier)
+
+    def multicast(self):
+        """NVLS multicast (K3): one store through multimem.st reaches every GPU."""
+        if self.oversub or not R.multicast_supported(self.local):
+            if self.rank == 0:
+                print("dist_worker: NVLS multicast not supported or GPUs shared, skipped", flush=True)
+            return
+        for src, dst in (REPLICATE, (pl((1, 1, 8, 0, 0)), pl((1, 8, 1, 0, 0)))):
+            for seed in (23, SPECIAL | 23):
+                self.run(f"multicast {src.strategy}->{dst.strategy} seed={seed:#x}", TINY_GQA, src, dst, seed,
+                         multicast=["b"])
+
+    def overlap(self):
+        """Overlapped in-host fan-out (star flags), with and without the relay."""
+        for relay, kernel in ((False, 1), (True, 1), (False, 0), (True, 0)):
+            for sp, dp in CASES:
+                seed = SPECIAL | 37 if kernel else 37
+                self.run(f"overlap relay={relay} kernel={kernel} {sp}->{dp} seed={seed:#x}", TINY_GQA, pl(sp),
+                         pl(dp), seed, reps=2, relay=relay, overlap=True, kernel=kernel, flag_kernel=kernel)
+
+    def relay(self):
+        """Pipelined relay: chunks travel source -> GPU -> GPU with per-chunk flags."""
+        cases = [REPLICATE, (pl((1, 1, 8, 0, 0)), pl((1, 8, 1, 0, 0))),
+                 (placement(2, 1, 1, 2, offset=2), placement(8, 1, 4, 2))]
+        for src, dst in cases:
+            for kernel in (1, 0):
+                seed = SPECIAL | 29 if kernel else 29
+                self.run(f"relay kernel={kernel} {src.strategy}->{dst.strategy} seed={seed:#x}", TINY_GQA, src, dst,
+                         seed, reps=3, relay=True, kernel=kernel, flag_kernel=kernel)
+
+    def ce_runs_cases(self):
+        """Copy-engine runs on stage remaps (forced down to 4 KiB ranges so the
+        tiny model has some), hierarchical and flat, plain and onloaded."""
+        for sp, dp in (((2, 1, 4, 0, 0), (1, 2, 4, 0, 0)), ((2, 2, 2, 1, 1), (1, 4, 2, 1, 1)),
+                       ((1, 2, 4, 2, 1), (2, 1, 4, 2, 1))):
+            for hier in (True, False):
+                self.run(f"ce-runs {sp}->{dp} hier={hier} (+onload)", TINY_GQA, pl(sp), pl(dp), SPECIAL | 77,
+                         reps=2, onload_chunk=64 << 10, hierarchical=hier, ce_min_run_bytes=4096)
+
+    def staged(self):
+        """Staged gather (copy-engine rotation + per-piece unpack), small pieces,
+        both unpack kernels, plain / onloaded / plain again (flag epochs)."""
+        for sp, dp in (((1, 1, 8, 0, 0), (1, 8, 1, 0, 0)), ((2, 1, 4, 1, 1), (1, 1, 8, 0, 0)),
+                       ((1, 2, 4, 0, 0), (4, 1, 2, 2, 1)), ((1, 8, 1, 0, 0), (1, 1, 8, 0, 0))):
+            for kernel in (1, 0):
+                self.run(f"staged {sp}->{dp} kernel={kernel} (+onload)", TINY_GQA, pl(sp), pl(dp), SPECIAL | 91,
+                         reps=3, onload_chunk=64 << 10, staged=True, stage_chunk_bytes=64 << 10, kernel=kernel,
+                         flag_kernel=kernel)
+
+    def staged_many_items(self):
+        """A staged unpack with far more items than resident CTAs (one CTA per
+        SM, 1 KiB items): the unpack spins on piece flags while the senders'
+        copy streams raise them (no kernel takes part in signalling)."""
+        self.run("staged many-items tp8->dp8 chunk=1KiB", TINY_GQA, pl((1, 1, 8, 0, 0)), pl((1, 8, 1, 0, 0)),
+                 SPECIAL | 93, reps=2, staged=True, stage_chunk_bytes=16 << 10, chunk_bytes=1024, kernel=0,
+                 flag_kernel=0)
+
+    def fuzz(self):
+        """Random placement pairs with random delivery options (same seed on
+        every rank, so all ranks build the same plans and executors)."""
+        rng = random.Random(int(os.environ.get("RR_FUZZ_SEED", "2406")))
+        for i in range(int(os.environ.get("RR_FUZZ_CASES", "24"))):
+            fm = (TINY_GQA, TINY_MQA)[i % 2]
+            src, dst = random_placement(rng, fm), random_placement(rng, fm)
+            kw = dict(mode=rng.choice([R.PUSH, R.PULL]), hierarchical=rng.random() < 0.7,
+                      relay=rng.choice([False, True, "auto"]), overlap=rng.random() < 0.5,
+                      chunk_bytes=rng.choice([0, 8192, 65536]),
+                      ce_min_run_bytes=rng.choice([-1, 0, 4096]),  # off, default (256 MiB: none here), >= 4 KiB
+                      staged=rng.random() < 0.25, stage_chunk_bytes=32 << 10)
+            kw["kernel"] = kw["flag_kernel"] = rng.choice([0, 1, 5])
+            policy = rng.choice([0, 1])
+            seed = (SPECIAL if i % 3 == 0 else 0) | (50 + i)
+            opts = " ".join(f"{k}={v}" for k, v in kw.items() if k != "flag_kernel")
+            self.run(f"fuzz {i} {src.strategy}{src.mesh}->{dst.strategy}{dst.mesh} policy={policy} {opts}", fm,
+                     src, dst, seed, reps=2, policy=policy, **kw)
+
+    def full_7b(self):
+        """BASELINE configs[1] at full size across the GPUs: every byte of
+        every hosted shard against the oracle (streamed windows)."""
+        if os.environ.get("RR_FULL_7B") != "1" or self.oversub:
+            return
+        with self.case("full-size 7B tp8->dp8->tp8 (every byte vs oracle)"):
+            w = WORKLOADS["llama7b_tp8_dp8_roundtrip"]
+            (train, gen), _ = w.phases
+            plans = [plan_param_realloc(w.model, s, d, self.c, BALANCED) for (s, d) in w.phases]
+            rr = R.RankRealloc(plans, {"train": (0, R.SRC), "gen": (0, R.DST)},
+                               [("train", "gen"), ("gen", "train")], self.rank, self.world, self.local,
+                               overlap=True, staged="auto")
+            try:
+                seed = SPECIAL | 4
+                for d, b in rr.buffers["train"].items():
+                    R.fill_shard(plans[0], R.SRC, d, b.ptr, seed)
+                torch.cuda.synchronize()
+                dist.barrier()
+                for _ in range(2):
+                    rr.run_phase(0)
+                    rr.run_phase(1)
+                torch.cuda.synchronize()
+                for name, p in (("gen", gen), ("train", train)):
+                    for d, b in rr.buffers[name].items():
+                        bad, first = oracle_compare_device(w.model, p, self.c, d, seed, b.ptr, b.nbytes)
+                        if bad:
+                            self.failures.append(f"7B {name} shard {d}: {bad} mismatches (first byte {first})")
+                if rr.relay_timeouts() or rr.barrier.timed_out():
+                    self.failures.append("7B: flag or barrier timeouts")
+                dist.barrier()
+            finally:
+                rr.close()
+
+    def finish(self) -> int:
+        if self.world > 1 and self.staged_phases == 0:
+            self.failures.append("staged cases ran no staged phase")
+        t = torch.tensor([self.ce_runs], device="cpu" if self.oversub else "cuda")
+        dist.all_reduce(t)
+        if self.world > 1 and t.item() == 0:
+            self.failures.append("copy-engine cases issued no runs")
+        flag = torch.tensor([len(self.failures)], device="cpu" if self.oversub else "cuda")
+        dist.all_reduce(flag)
+        for f in self.failures:
+            print(f"rank {self.rank}: {f}", flush=True)
+        if self.rank == 0:
+            print(f"dist_worker: copy-engine runs {t.item()} (all ranks), staged phases on rank 0: "
+                  f"{self.staged_phases}", flush=True)
+            print(f"dist_worker world={self.world}: {'OK' if flag.item() == 0 else 'FAILED'}", flush=True)
+        dist.destroy_process_group()
+        return 0 if flag.item() == 0 else 1
 
 
 def main() -> int:
-    rank, world, lrank = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
-    # More ranks than GPUs (e.g. world 8 on a 4-GPU box, the 8-GPU code path):
-    # two processes share a GPU, their kernels time-slice, IPC and flags work
-    # as across GPUs. NCCL refuses two ranks per GPU, so gloo carries the
-    # host-side collectives; multicast needs distinct GPUs and is skipped.
-    gpus = torch.cuda.device_count()
-    local = lrank % gpus
-    oversub = world > gpus
-    torch.cuda.set_device(local)
-    if oversub:
-        dist.init_process_group("gloo")
-    else:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    c = b200_cluster(8)
-    failures = []
-    combos = [(m, k, h) for m in (R.PUSH, R.PULL) for k in (0, 1) for h in (True, False)]
-    for mode, kernel, hier in combos:
-        for sp, dp in CASES:
-            src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
-            dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
-            plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
-            rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
-                               mode=mode, kernel=kernel, hierarchical=hier)
-            for d, b in rr.buffers["a"].items():
-                R.fill_shard(plan, R.SRC, d, b.ptr, 21)
-            torch.cuda.synchronize()
-            dist.barrier()
-            rr.run_phase(0)
-            torch.cuda.synchronize()
-            if rr.barrier.timed_out():
-                failures.append(f"{sp}->{dp} mode {mode} kernel {kernel} hier {hier}: barrier timed out")
-            for d, b in rr.buffers["b"].items():
-                got = b.to_host()
-                want = O.fill(TINY_GQA, dst, c, d, 21)
-                if not np.array_equal(got, want):
-                    failures.append(f"{sp}->{dp} mode {mode} kernel {kernel} hier {hier}: device {d} differs in "
-                                    f"{int(np.count_nonzero(got != want))} elements")
-            dist.barrier()
-            rr.close()
-    # NVLS multicast (K3): one-to-many payloads stored once through multimem.st.
-    if R.multicast_supported(local) and not oversub:
-        mc_cases = [
-            (Placement(DeviceMesh(0, 1, 0, 1), ParallelStrategy()), placement(8, 1, 8, 1)),  # replicate from dev 0
-            (placement(8, 1, 1, 8), placement(8, 1, 8, 1)),                                  # tp8 -> dp8
-        ]
-        for src, dst in mc_cases:
-            plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
-            rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
-                               multicast=["b"])
-            uses_mc = sum(e.stats(0)[0] for e in rr.executors) > 0
-            for d, b in rr.buffers["a"].items():
-                R.fill_shard(plan, R.SRC, d, b.ptr, 23)
-            torch.cuda.synchronize()
-            dist.barrier()
-            rr.run_phase(0)
-            torch.cuda.synchronize()
-            for d, b in rr.buffers["b"].items():
-                got = b.to_host()
-                want = O.fill(TINY_GQA, dst, c, d, 23)
-                if not np.array_equal(got, want):
-                    failures.append(f"multicast {src.strategy}->{dst.strategy}: device {d} differs in "
-                                    f"{int(np.count_nonzero(got != want))} elements (items {uses_mc})")
-            rr.close()
-    elif rank == 0:
-        print("dist_worker: NVLS multicast not supported or GPUs shared, skipped", flush=True)
-    # Overlapped fan-out (star flags) and relay + overlap, over all parity
-    # cases, on the TMA bulk kernel (1) and the LDG/STG kernel (0).
-    for relay_opt, kernel in ((False, 1), (True, 1), (False, 0), (True, 0)):
-        for sp, dp in CASES:
-            src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
-            dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
-            plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
-            rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
-                               relay=relay_opt, overlap=True, kernel=kernel, flag_kernel=kernel)
-            for d, b in rr.buffers["a"].items():
-                R.fill_shard(plan, R.SRC, d, b.ptr, 37)
-            for rep in range(2):
-                for b in rr.buffers["b"].values():
-                    b.zero()
-                torch.cuda.synchronize()
-                dist.barrier()
-                rr.run_phase(0)
-                torch.cuda.synchronize()
-                for d, b in rr.buffers["b"].items():
-                    got = b.to_host()
-                    want = O.fill(TINY_GQA, dst, c, d, 37)
-                    if not np.array_equal(got, want):
-                        failures.append(f"overlap relay={relay_opt} kernel {kernel} {sp}->{dp} rep {rep}: device {d} differs in "
-                                        f"{int(np.count_nonzero(got != want))} elements")
-            if rr.relay_timeouts():
-                failures.append(f"overlap relay={relay_opt} kernel {kernel} {sp}->{dp}: {rr.relay_timeouts()} timeouts")
-            rr.close()
-    # Pipelined relay: chunks travel source -> GPU -> GPU with per-chunk flags.
-    relay_cases = [
-        (Placement(DeviceMesh(0, 1, 0, 1), ParallelStrategy()), placement(8, 1, 8, 1)),  # replicate from dev 0
-        (placement(8, 1, 1, 8), placement(8, 1, 8, 1)),                                  # tp8 -> dp8
-        (placement(2, 1, 1, 2, offset=2), placement(8, 1, 4, 2)),                        # 2 sources -> dp4 tp2
-    ]
-    for (src, dst), kernel in [(case, k) for case in relay_cases for k in (1, 0)]:
-        plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
-        rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
-                           relay=True, kernel=kernel, flag_kernel=kernel)
-        for d, b in rr.buffers["a"].items():
-            R.fill_shard(plan, R.SRC, d, b.ptr, 29)
-        torch.cuda.synchronize()
-        dist.barrier()
-        for rep in range(3):  # epochs advance per launch
-            for b in rr.buffers["b"].values():
-                b.zero()
-            torch.cuda.synchronize()
-            dist.barrier()
-            rr.run_phase(0)
-            torch.cuda.synchronize()
-            for d, b in rr.buffers["b"].items():
-                got = b.to_host()
-                want = O.fill(TINY_GQA, dst, c, d, 29)
-                if not np.array_equal(got, want):
-                    failures.append(f"relay kernel {kernel} {src.strategy}->{dst.strategy} rep {rep}: device {d} differs in "
-                                    f"{int(np.count_nonzero(got != want))} elements")
-        if rr.relay_timeouts():
-            failures.append(f"relay kernel {kernel} {src.strategy}->{dst.strategy}: {rr.relay_timeouts()} timeouts")
-        rr.close()
-    # Fuzz: random placement pairs with random delivery options (same seed on
-    # every rank, so all ranks build the same plans and executors).
-    import random
-
-    from _helpers import random_placement
-    rng = random.Random(int(os.environ.get("RR_FUZZ_SEED", "2406")))
-    fuzz_models = [TINY_GQA, dataclasses.replace(TINY_GQA, name="tiny_mqa", num_attention_heads=8, num_kv_heads=1,
-                                                 num_layers=3)]
-    ce_cases = 0  # fuzz cases in which this rank issued copy-engine runs
-    staged_cases = 0  # fuzz cases with a staged-gather phase
-    for i in range(int(os.environ.get("RR_FUZZ_CASES", "24"))):
-        fm = fuzz_models[i % 2]
-        src, dst = random_placement(rng, fm), random_placement(rng, fm)
-        mode = rng.choice([R.PUSH, R.PULL])
-        hier = rng.random() < 0.7
-        relay = rng.choice([False, True, "auto"])
-        overlap = rng.random() < 0.5
-        kernel = rng.choice([0, 1, 5])
-        chunk = rng.choice([0, 8192, 65536])
-        ce = rng.choice([-1, 0, 4096])  # copy-engine runs: off, default (256 MiB: none here), >= 4 KiB
-        staged = rng.random() < 0.25    # staged gather (push mode, hierarchical, no relay), 32 KiB pieces
-        plan = plan_param_realloc(fm, src, dst, c, rng.choice([0, 1]))
-        rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
-                           mode=mode, kernel=kernel, flag_kernel=kernel, hierarchical=hier, relay=relay,
-                           overlap=overlap, chunk_bytes=chunk, ce_min_run_bytes=ce, staged=staged,
-                           stage_chunk_bytes=32 << 10)
-        ce_cases += int(any(e.ce_runs()[0] for e in rr.executors))
-        staged_cases += int(bool(rr.staged_phases))
-        for d, b in rr.buffers["a"].items():
-            R.fill_shard(plan, R.SRC, d, b.ptr, 50 + i)
-        for rep in range(2):
-            for b in rr.buffers["b"].values():
-                b.zero()
-            torch.cuda.synchronize()
-            dist.barrier()
-            rr.run_phase(0)
-            torch.cuda.synchronize()
-            for d, b in rr.buffers["b"].items():
-                got = b.to_host()
-                want = O.fill(fm, dst, c, d, 50 + i)
-                if not np.array_equal(got, want):
-                    failures.append(f"fuzz {i} {src}->{dst} mode {mode} hier {hier} relay {relay} overlap {overlap} "
-                                    f"kernel {kernel} chunk {chunk} ce {ce} staged {rr.staged_phases} rep {rep}: device {d} differs in "
-                                    f"{int(np.count_nonzero(got != want))} elements")
-        if rr.relay_timeouts() or rr.barrier.timed_out():
-            failures.append(f"fuzz {i}: flag or barrier timeouts")
-        dist.barrier()
-        rr.close()
-    # Copy-engine runs on stage remaps (forced down to 4 KiB ranges so the
-    # tiny model has some), push and hierarchical/flat, with the onload path.
-    ce_total = 0
-    for sp, dp in (((2, 1, 4, 0, 0), (1, 2, 4, 0, 0)), ((2, 2, 2, 1, 1), (1, 4, 2, 1, 1)),
-                   ((1, 2, 4, 2, 1), (2, 1, 4, 2, 1))):
-        for hier in (True, False):
-            src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
-            dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
-            plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
-            rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
-                               hierarchical=hier, ce_min_run_bytes=4096)
-            ce_total += sum(e.ce_runs()[0] for e in rr.executors)
-            for d, b in rr.buffers["a"].items():
-                R.fill_shard(plan, R.SRC, d, b.ptr, 77)
-            for onload in (False, True):
-                for b in rr.buffers["b"].values():
-                    b.zero()
-                torch.cuda.synchronize()
-                dist.barrier()
-                if onload:
-                    host = {d: R.HostBuffer(plan.shard_bytes(R.SRC, d)) for d in rr.buffers["a"]}
-                    for d, hb in host.items():
-                        hb.array()[:] = rr.buffers["a"][d].to_host()
-                    copy_stream = torch.cuda.Stream()
-                    # small chunks so that runs straddle several of them
-                    rr.run_phase_onload(0, {d: hb.ptr for d, hb in host.items()}, copy_stream, chunk_bytes=64 << 10)
-                else:
-                    rr.run_phase(0)
-                torch.cuda.synchronize()
-                for d, b in rr.buffers["b"].items():
-                    bad, first = R.verify_shard(plan, R.DST, d, b.ptr, 77)
-                    if bad:
-                        failures.append(f"ce {sp}->{dp} hier {hier} onload {onload}: device {d} {bad} mismatches")
-                if onload:
-                    for hb in host.values():
-                        hb.free()
-            if rr.barrier.timed_out():
-                failures.append(f"ce {sp}->{dp}: barrier timed out")
-            dist.barrier()
-            rr.close()
-    # Staged gather (copy-engine rotation + per-piece unpack), small pieces.
-    staged_total = 0
-    for sp, dp in (((1, 1, 8, 0, 0), (1, 8, 1, 0, 0)), ((2, 1, 4, 1, 1), (1, 1, 8, 0, 0)),
-                   ((1, 2, 4, 0, 0), (4, 1, 2, 2, 1)), ((1, 8, 1, 0, 0), (1, 1, 8, 0, 0))):
-        src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
-        dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
-        plan = plan_param_realloc(TINY_GQA, src, dst, c, BALANCED)
-        rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], rank, world, local,
-                           staged=True, stage_chunk_bytes=64 << 10)
-        staged_total += len(rr.staged_phases)
-        for d, b in rr.buffers["a"].items():
-            R.fill_shard(plan, R.SRC, d, b.ptr, 91)
-        for onload in (False, True, False):  # repeated launches exercise the flag epochs
-            for b in rr.buffers["b"].values():
-                b.zero()
-            torch.cuda.synchronize()
-            dist.barrier()
-            if onload:
-                host = {d: R.HostBuffer(plan.shard_bytes(R.SRC, d)) for d in rr.buffers["a"]}
-                for d, hb in host.items():
-                    hb.array()[:] = rr.buffers["a"][d].to_host()
-                rr.run_phase_onload(0, {d: hb.ptr for d, hb in host.items()}, torch.cuda.Stream(),
-                                    chunk_bytes=64 << 10)
-            else:
-                rr.run_phase(0)
-            torch.cuda.synchronize()
-            for d, b in rr.buffers["b"].items():
-                bad, first = R.verify_shard(plan, R.DST, d, b.ptr, 91)
-                if bad:
-                    failures.append(f"staged {sp}->{dp} onload {onload}: device {d} {bad} mismatches")
-            if onload:
-                for hb in host.values():
-                    hb.free()
-        if rr.relay_timeouts() or rr.barrier.timed_out():
-            failures.append(f"staged {sp}->{dp}: flag or barrier timeouts")
-        dist.barrier()
-        rr.close()
-    if world > 1 and staged_total == 0:
-        failures.append("staged cases ran no staged phase")
-    if world > 1 and not oversub:
-        t = torch.tensor([ce_total], device="cuda")
-        dist.all_reduce(t)
-        if t.item() == 0:
-            failures.append("copy-engine cases issued no runs")
-    if os.environ.get("RR_FULL_7B") == "1" and not oversub:
-        w = WORKLOADS["llama7b_tp8_dp8_roundtrip"]
-        plans = [plan_param_realloc(w.model, s, d, c, BALANCED) for (s, d) in w.phases]
-        rr = R.RankRealloc(plans, {"train": (0, R.SRC), "gen": (0, R.DST)}, [("train", "gen"), ("gen", "train")],
-                           rank, world, local)
-        for d, b in rr.buffers["train"].items():
-            R.fill_shard(plans[0], R.SRC, d, b.ptr, 4)
-        torch.cuda.synchronize()
-        dist.barrier()
-        for _ in range(2):
-            rr.run_phase(0)
-            rr.run_phase(1)
-        torch.cuda.synchronize()
-        for name, p in (("gen", plans[0]), ("train", plans[1])):
-            for d, b in rr.buffers[name].items():
-                bad, first = R.verify_shard(p, R.DST, d, b.ptr, 4)
-                if bad:
-                    failures.append(f"7B {name} shard {d}: {bad} mismatches (first {first})")
-        dist.barrier()
-        rr.close()
-    flag = torch.tensor([len(failures)], device="cpu" if oversub else "cuda")
-    dist.all_reduce(flag)
-    for f in failures:
-        print(f"rank {rank}: {f}", flush=True)
-    if rank == 0:
-        print(f"dist_worker: fuzz cases with copy-engine runs on rank 0: {ce_cases}, staged: {staged_cases}",
-              flush=True)
-        print(f"dist_worker world={world}: {'OK' if flag.item() == 0 else 'FAILED'}", flush=True)
-    dist.destroy_process_group()
-    return 0 if flag.item() == 0 else 1
+    w = Worker()
+    sections = os.environ.get("RR_SECTIONS", "basic,multicast,overlap,relay,ce,staged,fuzz,full7b").split(",")
+    table = {"basic": w.basic, "multicast": w.multicast, "overlap": w.overlap, "relay": w.relay,
+             "ce": w.ce_runs_cases, "staged": w.staged, "staged_many": w.staged_many_items, "fuzz": w.fuzz,
+             "full7b": w.full_7b}
+    for s in sections + (["staged_many"] if "staged" in sections else []):
+        table[s]()
+    return w.finish()
 
 
 if __name__ == "__main__":

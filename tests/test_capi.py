@@ -42,7 +42,7 @@ def test_no_torch_or_cuda_types_in_signatures():
 
 
 def test_abi_version_and_error_reporting():
-    assert _lib.lib.rr_abi_version() == 4
+    assert _lib.lib.rr_abi_version() == 5
     bad = P.ModelSpec(name="x", hidden_size=100, intermediate_size=8, num_layers=1, num_attention_heads=3,
                       num_kv_heads=1, vocab_size=10, max_position_embeddings=16)
     with pytest.raises(P.ValidationError, match="ModelSpec 'x': hidden_size must be divisible by num_attention_heads"):

@@ -1,0 +1,121 @@
+"""Copy-engine transport (rr_exec_options.ce_transport), host side: the
+merged 2D / 3D copies every host would issue, applied with numpy together
+with the SM work that stays (local copies, in-host fan-out), rebuild every
+destination shard exactly as the oracle expects; they are few (one per
+tensor kind and pair, not one per layer), non-overlapping, and ordered in
+rotation rounds."""
+from __future__ import annotations
+
+import dataclasses
+import random
+
+import numpy as np
+import pytest
+
+from _helpers import placement, random_placement
+from oracle import oracle as O
+from paper_2406_14088_b200 import rlplan as P
+from paper_2406_14088_b200.rlplan import BALANCED
+
+TINY_GQA = dataclasses.replace(P.MODELS["tiny"], name="tiny_gqa", hidden_size=512, num_attention_heads=16,
+                               num_kv_heads=8, intermediate_size=1024)
+
+
+def apply_copy(c, sbufs, dbufs):
+    src, dst, so, do, w, h, dep, sp, dp, ss, ds = c
+    sb, db = sbufs[src].view(np.uint8), dbufs[dst].view(np.uint8)
+    for z in range(dep):
+        for y in range(h):
+            a, b = so + z * ss + y * sp, do + z * ds + y * dp
+            assert not db[b:b + w].any() or np.array_equal(db[b:b + w], sb[a:a + w]), "overlapping copies"
+            db[b:b + w] = sb[a:a + w]
+
+
+def emulate(plan, host_of, sbufs, dbufs):
+    hosts = sorted(set(host_of))
+    lowered = plan.lowered()
+    copies = {}
+    for h in hosts:
+        local = [d for d in range(len(host_of)) if host_of[d] == h]
+        copies[h] = plan.ce_copies(local, host_of)
+        for c in copies[h]:
+            assert host_of[c[0]] == h and host_of[c[1]] != h
+            apply_copy(c, sbufs, dbufs)
+    for s, dsts, rects in lowered:
+        groups = {}
+        for d in dsts:
+            groups.setdefault(host_of[d], []).append(d)
+        for hh, ds in groups.items():
+            ds = sorted(ds)
+            if hh == host_of[s]:  # local SM copies
+                for d in ds:
+                    for (so, do, rb, sp, dp, rows) in rects:
+                        for r in range(rows):
+                            dbufs[d].view(np.uint8)[do + r * dp: do + r * dp + rb] = \
+                                sbufs[s].view(np.uint8)[so + r * sp: so + r * sp + rb]
+            else:  # phase 1: in-host fan-out from the leader ds[0], which the copy engine filled
+                for d in ds[1:]:
+                    for (_so, do, rb, _sp, dp, rows) in rects:
+                        for r in range(rows):
+                            dbufs[d].view(np.uint8)[do + r * dp: do + r * dp + rb] = \
+                                dbufs[ds[0]].view(np.uint8)[do + r * dp: do + r * dp + rb]
+    return copies
+
+
+@pytest.mark.parametrize("sp,dp,world", [
+    ((2, 1, 4, 0, 0), (1, 1, 8, 0, 0), 2), ((2, 1, 4, 0, 0), (1, 1, 8, 0, 0), 4),
+    ((4, 1, 2, 2, 1), (1, 1, 8, 1, 1), 2), ((4, 1, 2, 2, 1), (1, 1, 8, 1, 1), 4),
+    ((2, 1, 4, 0, 0), (1, 2, 4, 0, 0), 2), ((1, 1, 8, 0, 0), (1, 8, 1, 0, 0), 4),
+])
+def test_transport_rebuilds_baseline_shapes(sp, dp, world):
+    m = dataclasses.replace(TINY_GQA, num_layers=6)
+    c = P.b200_cluster(8)
+    src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
+    dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
+    plan = P.plan_param_realloc(m, src, dst, c, BALANCED)
+    host_of = [d * world // 8 for d in range(8)]
+    sbufs = {d: O.fill(m, src, c, d, 3) for d in plan.devices(0)}
+    dbufs = {d: np.zeros(plan.shard_bytes(1, d) // 2, np.uint16) for d in plan.devices(1)}
+    copies = emulate(plan, host_of, sbufs, dbufs)
+    for d in plan.devices(1):
+        assert np.array_equal(dbufs[d], O.fill(m, dst, c, d, 3)), f"device {d}"
+    # merged across layers: per (src, dst) pair a handful of copies, not one per layer and tensor
+    pairs = {(x[0], x[1]) for h in copies for x in copies[h]}
+    n = sum(len(v) for v in copies.values())
+    assert n <= 12 * max(1, len(pairs)), (n, len(pairs))
+    assert any(x[5] > 1 or x[6] > 1 for h in copies for x in copies[h])
+    # rotation rounds: host h's copies go to h+1, h+2, ... in that order
+    for h, cs in copies.items():
+        rounds = [(host_of[x[1]] - h) % world for x in cs]
+        assert rounds == sorted(rounds)
+
+
+def test_transport_fuzz():
+    rng = random.Random(5)
+    c = P.b200_cluster(8)
+    for i in range(40):
+        m = rng.choice([TINY_GQA, dataclasses.replace(TINY_GQA, name="tiny_mqa", num_attention_heads=8,
+                                                      num_kv_heads=1, num_layers=3)])
+        src, dst = random_placement(rng, m), random_placement(rng, m)
+        plan = P.plan_param_realloc(m, src, dst, c, rng.choice([0, 1]))
+        world = rng.choice([2, 4, 8])
+        host_of = [d * world // 8 for d in range(8)]
+        sbufs = {d: O.fill(m, src, c, d, 50 + i) for d in plan.devices(0)}
+        dbufs = {d: np.zeros(plan.shard_bytes(1, d) // 2, np.uint16) for d in plan.devices(1)}
+        emulate(plan, host_of, sbufs, dbufs)
+        for d in plan.devices(1):
+            assert np.array_equal(dbufs[d], O.fill(m, dst, c, d, 50 + i)), (i, d)
+
+
+def test_transport_copy_counts_at_full_size():
+    """70B (pp2,tp4)->tp8 at 2 GPUs: each (source, destination) pair is a few
+    dozen submissions at most, not 80 layers x 9 tensors."""
+    w = P.MODELS["llama70b"]
+    c = P.b200_cluster(8)
+    plan = P.plan_param_realloc(w, placement(8, 2, 1, 4), placement(8, 1, 1, 8), c, BALANCED)
+    host_of = [d // 4 for d in range(8)]
+    cs = plan.ce_copies([0, 1, 2, 3], host_of)
+    pairs = {(x[0], x[1]) for x in cs}
+    total = sum(x[4] * x[5] * x[6] for x in cs)
+    assert total == plan.work([0, 1, 2, 3], 0, host_of)["wire_out"]
+    assert len(cs) <= 100 * len(pairs), (len(cs), len(pairs))

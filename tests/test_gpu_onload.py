@@ -22,7 +22,8 @@ TINY_GQA = dataclasses.replace(MODELS["tiny"], name="tiny_gqa", hidden_size=512,
 
 @pytest.mark.parametrize("sp,dp", [((1, 1, 8, 0, 0), (1, 8, 1, 0, 0)), ((4, 1, 2, 2, 1), (1, 1, 8, 1, 1))])
 @pytest.mark.parametrize("kernel", [0, 1])
-def test_onload_pipeline_bitexact(need_gpu, sp, dp, kernel):
+@pytest.mark.parametrize("seed", [31, O.SEED_SPECIAL | 31])
+def test_onload_pipeline_bitexact(need_gpu, sp, dp, kernel, seed):
     import torch
     c = b200_cluster(8)
     src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
@@ -33,7 +34,7 @@ def test_onload_pipeline_bitexact(need_gpu, sp, dp, kernel):
     try:
         for d, b in vc.src.items():   # parked parameters: pinned host copies of the source shards
             hb = R.HostBuffer(b.nbytes)
-            hb.array()[:] = O.fill(TINY_GQA, src, c, d, 31)
+            hb.array()[:] = O.fill(TINY_GQA, src, c, d, seed)
             hosts[d] = hb
             b.zero()
         ex = vc.executor(R.PUSH, 4096, kernel)
@@ -45,7 +46,7 @@ def test_onload_pipeline_bitexact(need_gpu, sp, dp, kernel):
             ex.launch_onload({d: h.ptr for d, h in hosts.items()}, copy, torch.cuda.current_stream())
             torch.cuda.synchronize()
             for d, b in vc.dst.items():
-                assert np.array_equal(b.to_host(), O.fill(TINY_GQA, dst, c, d, 31)), d
+                assert np.array_equal(b.to_host(), O.fill(TINY_GQA, dst, c, d, seed)), d
         ex.close()
     finally:
         vc.free()
@@ -54,7 +55,8 @@ def test_onload_pipeline_bitexact(need_gpu, sp, dp, kernel):
 
 
 @pytest.mark.parametrize("kernel", [0, 1])
-def test_offload_overlaps_reallocation_then_onload_round_trip(need_gpu, kernel):
+@pytest.mark.parametrize("seed", [17, O.SEED_SPECIAL | 17])
+def test_offload_overlaps_reallocation_then_onload_round_trip(need_gpu, kernel, seed):
     """Park the source shards in pinned host memory while the reallocation
     reads them ("host-device (e.g., offload)"), wipe them,
     then onload them back pipelined with the same reallocation: every host
@@ -67,7 +69,7 @@ def test_offload_overlaps_reallocation_then_onload_round_trip(need_gpu, kernel):
     vc = R.VirtualCluster(plan, 0)
     hosts = {}
     try:
-        vc.fill_sources(seed=17)
+        vc.fill_sources(seed=seed)
         for d, b in vc.src.items():
             hosts[d] = R.HostBuffer(b.nbytes)
             hosts[d].array()[:] = 0
@@ -78,16 +80,16 @@ def test_offload_overlaps_reallocation_then_onload_round_trip(need_gpu, kernel):
         ex.launch(cur)
         torch.cuda.synchronize()
         for d, h in hosts.items():
-            assert np.array_equal(h.array(), O.fill(TINY_GQA, src, c, d, 17)), d
+            assert np.array_equal(h.array(), O.fill(TINY_GQA, src, c, d, seed)), d
         for d, b in vc.dst.items():
-            assert np.array_equal(b.to_host(), O.fill(TINY_GQA, dst, c, d, 17)), d
+            assert np.array_equal(b.to_host(), O.fill(TINY_GQA, dst, c, d, seed)), d
         for b in list(vc.src.values()) + list(vc.dst.values()):
             b.zero()
         ex.enable_onload({d: b.nbytes for d, b in vc.src.items()}, chunk_bytes=32 << 10)
         ex.launch_onload({d: h.ptr for d, h in hosts.items()}, copy, cur)
         torch.cuda.synchronize()
         for d, b in vc.dst.items():
-            assert np.array_equal(b.to_host(), O.fill(TINY_GQA, dst, c, d, 17)), d
+            assert np.array_equal(b.to_host(), O.fill(TINY_GQA, dst, c, d, seed)), d
         ex.close()
     finally:
         vc.free()

@@ -129,6 +129,38 @@ def test_reinterleave_bitexact(need_gpu, sp, dp, mode, kernel):
     assert_same(got, expected(TINY_GQA, src, dst, c))
 
 
+@pytest.mark.parametrize("sp,dp", [
+    ((1, 1, 8, 0, 0), (1, 8, 1, 0, 0)),   # all-gather, strided row-parallel pieces
+    ((4, 1, 2, 2, 1), (1, 1, 8, 1, 1)),   # grouped -> concat reinterleave
+    ((2, 1, 4, 0, 0), (1, 2, 4, 0, 0)),   # stage remap
+    ((1, 8, 1, 0, 0), (1, 1, 8, 0, 0)),   # local slicing
+])
+@pytest.mark.parametrize("mode", [R.PUSH, R.PULL])
+@pytest.mark.parametrize("kernel", [0, 1, 5])
+def test_special_value_words_survive_every_kernel(need_gpu, sp, dp, mode, kernel):
+    """Signed zeros, infinities, quiet and signalling NaNs with payloads,
+    subnormals, extreme normals and arbitrary 16-bit words are moved as
+    opaque bytes by the LDG/STG kernel and both TMA bulk rings,
+    push and pull, whole items and 4 KiB split items."""
+    c = b200_cluster(8)
+    src = placement(8, *sp[:3], qkv=sp[3], gate_up=sp[4])
+    dst = placement(8, *dp[:3], qkv=dp[3], gate_up=dp[4])
+    for chunk in (0, 4096):
+        seed = O.SEED_SPECIAL | (40 + chunk % 7)
+        _plan, got = run_virtual(TINY_GQA, src, dst, c, BALANCED, mode, chunk=chunk, kernel=kernel, seed=seed)
+        assert_same(got, expected(TINY_GQA, src, dst, c, seed=seed))
+
+
+def test_special_value_words_2byte_path(need_gpu):
+    """The 2-byte element path (SPEC.md:47 tiny spec, 8-byte rows)."""
+    m = MODELS["spec_tiny"]
+    c = b200_cluster(2)
+    src, dst = placement(2, 1, 1, 2), placement(2, 1, 2, 1)
+    seed = O.SEED_SPECIAL | 3
+    _plan, got = run_virtual(m, src, dst, c, SPEC, seed=seed, kernel=1)
+    assert_same(got, expected(m, src, dst, c, seed=seed))
+
+
 @pytest.mark.parametrize("kernel", [0, 1])
 def test_spec_tiny_unaligned_elements(need_gpu, kernel):
     """SPEC.md:47 tiny spec (h=4): 8-byte rows take the 2-byte element path."""
