@@ -142,5 +142,30 @@ def test_data_workloads_plan_and_cpu_sample():
         (prod, cons), = w.phases
         p, ops, loc = both(prod, cons, w.cluster(), w.data_bytes, BALANCED)
         assert [op_tuple(x) for x in w.plans(BALANCED)[0].ops] == ops
-        gbs, dt, delivered, ok, _ = bench.cpu_sample_data(w, 1, 0, 1)
-        assert ok and delivered == sum(b * len(d) for (_s, d, _p, b) in ops + loc) > 0
+        pw = bench.plain_workload(name)  # the reference arm's own, product-free view of the workload
+        pw.data_bytes = 1 << 20
+        r = bench.cpu_realloc(pw, 1, 0, 1)
+        assert r["correct"] and r["delivered"] == sum(b * len(d) for (_s, d, _p, b) in ops + loc) > 0
+
+
+def test_reference_arm_workloads_match_product():
+    """bench.py's reference arm builds every named workload from
+    workloads.json without the product; the oracle plans it identically to
+    the product's workload objects, and the `config` blocks of both arms
+    agree."""
+    import importlib.util
+    import os
+    from oracle import oracle as O
+    from paper_2406_14088_b200.workloads import WORKLOADS
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for name, w in WORKLOADS.items():
+        pw = bench.plain_workload(name)
+        assert bench.workload_config(pw) == bench.workload_config(w)
+        assert len(pw.phases) == len(w.phases) and pw.devices == w.devices
+        for (ps, pd), (s, d) in zip(pw.phases, w.phases):
+            if w.data_bytes:
+                assert O.plan_data(ps, pd, pw.cluster, w.data_bytes, 1) == O.plan_data(s, d, w.cluster(), w.data_bytes, 1)
+            else:
+                assert O.plan(pw.model, ps, pd, pw.cluster, 1) == O.plan(w.model, s, d, w.cluster(), 1)
