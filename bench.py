@@ -357,7 +357,8 @@ def run_b200(args) -> None:
                        multicast=multicast, relay=relay, overlap=overlap, flag_kernel=flag_kernel,
                        chunk_bytes=args.chunk_kib << 10, ce_min_run_bytes=-1 if args.ce == "off" else 0,
                        staged={"on": True, "off": False, "auto": "auto"}[args.staged],
-                       stage_chunk_bytes=args.stage_mib << 20)
+                       stage_chunk_bytes=args.stage_mib << 20,
+                       ce_transport={"on": True, "off": False, "auto": "auto"}[args.ce_transport])
     # executor creation only: the shard allocations inside RankRealloc are
     # timed too, so this is an upper bound of binding + descriptor upload
     bind_ms = (time.perf_counter() - t_bind) * 1e3
@@ -569,13 +570,14 @@ def run_b200(args) -> None:
                                                                "~710, one copy-engine copy ~780 GB/s; "
                                                                "profiles/r01_nvlink_probe_n2.txt)",
                     "algorithmic_bytes_per_launch": int(dom_wire)}
-            if dom in rr.staged_phases or rr.executors[dom].ce_runs()[0] > 0:
+            if dom in rr.staged_phases or dom in rr.ce_phases or rr.executors[dom].ce_runs()[0] > 0:
                 # copy engines carry (most of) this phase's link bytes: the SM
                 # stores' protocol factor does not apply to them
                 roof.update({"traffic": None, "wire_frac_incl_protocol": None,
                              "traffic_source": "copy-engine transfers: no per-kernel ncu counter",
                              "kernel": ("copy engines (staged gather) + " if dom in rr.staged_phases
-                                        else "copy-engine runs + ") + kname})
+                                   else "copy-engine transport + " if dom in rr.ce_phases
+                                   else "copy-engine runs + ") + kname})
             if hbm_roof["frac"] > roof["frac"]:
                 hbm_roof.update({"traffic": None, "kernel": kname, "phase": dom,
                                  "per_gpu": "max over ranks of this GPU's reads + stores landing in its HBM",
@@ -602,6 +604,9 @@ def run_b200(args) -> None:
                          "multicast_sets": rr.multicast, "relay_phases": rr.relay_phases,
                          "overlap_phases": rr.overlap_phases, "copy_kernel": kname,
                          "ce_runs": [list(e.ce_runs()) for e in rr.executors], "staged_phases": rr.staged_phases,
+                         "ce_transport_phases": rr.ce_phases,
+                         "ce_transport_estimates_ms": {pi: [round(x * 1e3, 3) for x in v]
+                                                       for pi, v in rr.ce_estimates.items()},
                          "bulk_variants": {"plain": 1 if kernel is None else kernel, "flag_synchronised": flag_kernel},
                          "chunk_kib": args.chunk_kib or "library default (256; smaller for phases too small for it)",
                          "ctas": args.ctas or "resident capacity",
@@ -701,6 +706,10 @@ def main() -> None:
     ap.add_argument("--ce", choices=["on", "off"], default="on",
                     help="copy-engine runs for >= 256 MiB ranges laid out identically in a source and a remote "
                          "destination shard (push mode; library default)")
+    ap.add_argument("--ce-transport", choices=["auto", "on", "off"], default="auto",
+                    help="copy-engine transport of remote pieces (2D/3D copies merged across layers, rotation "
+                         "rounds, straight into the destination shards); auto = phases without in-host fan-out "
+                         "where the measured rates predict >= 5%% less link time than SM peer stores")
     ap.add_argument("--staged", choices=["auto", "on", "off"], default="auto",
                     help="staged gather for phases that read other GPUs' sources: whole source shards pushed by "
                          "copy engines in rotation rounds, unpacked per 512 MiB piece; auto = from 4 GPUs on, "

@@ -394,6 +394,58 @@ def _all_gather_shaped(plan: ReallocPlan, host_of: Sequence[int], world: int, ce
     return not any(plan.ce_runs([d for d in range(n) if host_of[d] == r], host_of, min_run) for r in range(world))
 
 
+# Measured NVLink rates (profiles/r01_nvlink_probe_n2.txt, r01_ce_probe_*):
+# SM peer stores cap at ~705 GB/s of payload per GPU, a copy engine moves
+# ~775 GB/s pairwise and costs ~4 us per submission.
+SM_LINK_GBS, CE_LINK_GBS, CE_COPY_S = 705e9, 775e9, 4e-6
+
+
+HBM_COPY_GBS = 6.5e12  # measured 1:1 device copy (MEASURED_PEAKS.json)
+PHASE_OVERHEAD_S = 30e-6  # a barrier + fan-out launch
+
+
+def fanout_bytes(plan: ReallocPlan, host_of: Sequence[int]) -> Dict[int, int]:
+    """Per host: bytes its in-host fan-out copies from leader replicas (a
+    payload reaching k >= 2 destinations on a remote host crosses once and is
+    replicated k - 1 times there)."""
+    out = {h: 0 for h in set(host_of)}
+    for s, dsts, rects in plan.lowered():
+        b = sum(r[2] * r[5] for r in rects)
+        per: Dict[int, int] = {}
+        for d in dsts:
+            if host_of[d] != host_of[s]:
+                per[host_of[d]] = per.get(host_of[d], 0) + 1
+        for h, k in per.items():
+            out[h] += (k - 1) * b
+    return out
+
+
+def ce_transport_estimate(plan: ReallocPlan, host_of: Sequence[int]) -> Tuple[float, float]:
+    """Predicted time (s) of a phase's remote traffic: (copy-engine
+    transport, SM peer stores), each the max over hosts of sending and
+    receiving at the measured rates (host only). The copy-engine side adds
+    the in-host fan-out as a separate HBM phase (the overlapped fan-out's
+    per-chunk flags ride on SM stores); the SM side assumes it overlapped."""
+    n = plan.cluster.device_count()
+    hosts = sorted(set(host_of))
+    recv = {h: 0 for h in hosts}
+    ce_send = {h: 0.0 for h in hosts}
+    sm = 0.0
+    for h in hosts:
+        local = [d for d in range(n) if host_of[d] == h]
+        copies = plan.ce_copies(local, host_of)
+        for c in copies:
+            recv[host_of[c[1]]] += c[4] * c[5] * c[6]
+        ce_send[h] = sum(c[4] * c[5] * c[6] for c in copies) / CE_LINK_GBS + len(copies) * CE_COPY_S
+        w = plan.work(local, PUSH, host_of)
+        sm = max(sm, max(w["wire_in"], w["wire_out"]) / SM_LINK_GBS)
+    fan = fanout_bytes(plan, host_of)
+    ce = max(max(ce_send[h], recv[h] / CE_LINK_GBS) for h in hosts)
+    if any(fan.values()):
+        ce += max(2 * fan[h] for h in hosts) / HBM_COPY_GBS + PHASE_OVERHEAD_S
+    return ce, sm
+
+
 def stage_slots(plan: ReallocPlan, host_of: Sequence[int], chunk_bytes: int) -> int:
     """Length of the stage flag array every host allocates for a staged gather."""
     n = plan.cluster.device_count()
@@ -552,7 +604,7 @@ class RankRealloc:
                  mode: int = PUSH, kernel: Optional[int] = DEFAULT_KERNEL, hierarchical: bool = True,
                  multicast: Sequence[str] = (), relay=False, overlap: bool = False,
                  flag_kernel: int = DEFAULT_FLAG_KERNEL, chunk_bytes: int = 0, ce_min_run_bytes: int = 0,
-                 staged=False, stage_chunk_bytes: int = 512 << 20):
+                 staged=False, stage_chunk_bytes: int = 512 << 20, ce_transport=False):
         """``multicast`` names shard sets whose per-GPU leader shards (the
         lowest-id plan device of the set on each GPU) are members of one NVLS
         multicast object: a payload bound for every GPU is then stored once
@@ -611,6 +663,26 @@ class RankRealloc:
                 if any(host_of_all[s] != host_of_all[d] for s, dsts, _r in p.lowered() for d in dsts):
                     self.staged_phases.append(pi)
             self.overlap_phases = [pi for pi in self.overlap_phases if pi not in self.staged_phases]
+        # Copy-engine transport (remote pieces by copy engine, merged across
+        # layers, rotation rounds): True = every phase with remote traffic
+        # that no other scheme took; "auto" = where the measured rates predict
+        # >= 5% less time than SM peer stores (ce_transport_estimate, which
+        # charges the copy-engine side a separate in-host fan-out phase).
+        self.ce_phases: List[int] = []
+        self.ce_estimates: Dict[int, Tuple[float, float]] = {}
+        if ce_transport and world > 1 and hierarchical and mode == PUSH:
+            for pi, (_sname, dname) in enumerate(bind):
+                if pi in self.relay_phases or pi in self.staged_phases or dname in self.multicast:
+                    continue
+                p = self.plans[pi]
+                if not any(host_of_all[s] != host_of_all[d] for s, dsts, _r in p.lowered() for d in dsts):
+                    continue
+                if ce_transport == "auto":
+                    est = self.ce_estimates[pi] = ce_transport_estimate(p, host_of_all)
+                    if est[0] >= 0.95 * est[1]:
+                        continue
+                self.ce_phases.append(pi)
+            self.overlap_phases = [pi for pi in self.overlap_phases if pi not in self.ce_phases]
         self.relay_bufs: Dict[int, DeviceBuffer] = {}
         for pi in sorted(set(self.relay_phases) | set(self.overlap_phases)):
             slots = relay_slots(self.plans[pi], host_of_all, chunk_bytes, chain=pi in self.relay_phases,
@@ -733,7 +805,8 @@ class RankRealloc:
                                                mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_tables.get(pi),
                                                relay_chain=pi in self.relay_phases,
                                                overlap_fanout=pi in self.overlap_phases,
-                                               ce_min_run_bytes=ce_min_run_bytes))
+                                               ce_min_run_bytes=ce_min_run_bytes,
+                                               ce_transport=pi in self.ce_phases))
             if kernel is not None:
                 self.executors[-1].set_kernel(kernel)
             self.executors[-1].set_flag_kernel(flag_kernel)

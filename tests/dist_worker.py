@@ -178,6 +178,16 @@ class Worker:
                 self.run(f"ce-runs {sp}->{dp} hier={hier} (+onload)", TINY_GQA, pl(sp), pl(dp), SPECIAL | 77,
                          reps=2, onload_chunk=64 << 10, hierarchical=hier, ce_min_run_bytes=4096)
 
+    def ce_transport(self):
+        """Copy-engine transport: remote pieces by copy engine as 2D / 3D copies
+        merged across layers, in rotation rounds, plain and onloaded, with the
+        fan-out phase after it where a host holds several destinations."""
+        m = dataclasses.replace(TINY_GQA, num_layers=6)
+        for sp, dp in CASES + [((1, 1, 8, 0, 0), (1, 8, 1, 0, 0))]:
+            for hier in (True,):
+                self.run(f"ce-transport {sp}->{dp} (+onload)", m, pl(sp), pl(dp), SPECIAL | 83, reps=3,
+                         onload_chunk=32 << 10, hierarchical=hier, ce_transport=True)
+
     def staged(self):
         """Staged gather (copy-engine rotation + per-piece unpack), small pieces,
         both unpack kernels, plain / onloaded / plain again (flag epochs)."""
@@ -207,7 +217,8 @@ class Worker:
                       relay=rng.choice([False, True, "auto"]), overlap=rng.random() < 0.5,
                       chunk_bytes=rng.choice([0, 8192, 65536]),
                       ce_min_run_bytes=rng.choice([-1, 0, 4096]),  # off, default (256 MiB: none here), >= 4 KiB
-                      staged=rng.random() < 0.25, stage_chunk_bytes=32 << 10)
+                      staged=rng.random() < 0.25, stage_chunk_bytes=32 << 10,
+                      ce_transport=rng.random() < 0.3)
             kw["kernel"] = kw["flag_kernel"] = rng.choice([0, 1, 5])
             policy = rng.choice([0, 1])
             seed = (SPECIAL if i % 3 == 0 else 0) | (50 + i)
@@ -269,9 +280,10 @@ class Worker:
 
 def main() -> int:
     w = Worker()
-    sections = os.environ.get("RR_SECTIONS", "basic,multicast,overlap,relay,ce,staged,fuzz,full7b").split(",")
+    sections = os.environ.get("RR_SECTIONS",
+                              "basic,multicast,overlap,relay,ce,cetransport,staged,fuzz,full7b").split(",")
     table = {"basic": w.basic, "multicast": w.multicast, "overlap": w.overlap, "relay": w.relay,
-             "ce": w.ce_runs_cases, "staged": w.staged, "staged_many": w.staged_many_items, "fuzz": w.fuzz,
+             "ce": w.ce_runs_cases, "cetransport": w.ce_transport, "staged": w.staged, "staged_many": w.staged_many_items, "fuzz": w.fuzz,
              "full7b": w.full_7b}
     for s in sections + (["staged_many"] if "staged" in sections else []):
         table[s]()
