@@ -358,7 +358,8 @@ def run_b200(args) -> None:
                        chunk_bytes=args.chunk_kib << 10, ce_min_run_bytes=-1 if args.ce == "off" else 0,
                        staged={"on": True, "off": False, "auto": "auto"}[args.staged],
                        stage_chunk_bytes=args.stage_mib << 20,
-                       ce_transport={"on": True, "off": False, "auto": "auto"}[args.ce_transport])
+                       ce_transport={"on": True, "off": False, "auto": "auto"}[args.ce_transport],
+                       probe=args.probe == "on" and world > 1)
     # executor creation only: the shard allocations inside RankRealloc are
     # timed too, so this is an upper bound of binding + descriptor upload
     bind_ms = (time.perf_counter() - t_bind) * 1e3
@@ -710,6 +711,10 @@ def main() -> None:
                     help="copy-engine transport of remote pieces (2D/3D copies merged across layers, rotation "
                          "rounds, straight into the destination shards); auto = phases without in-host fan-out "
                          "where the measured rates predict >= 5%% less link time than SM peer stores")
+    ap.add_argument("--probe", choices=["on", "off"], default="on",
+                    help="N > 1: choose each phase's delivery scheme by timing every scheme the switches allow on "
+                         "the real buffers at bind time (max over ranks; executor.policy_probe) instead of the "
+                         "cost model alone")
     ap.add_argument("--staged", choices=["auto", "on", "off"], default="auto",
                     help="staged gather for phases that read other GPUs' sources: whole source shards pushed by "
                          "copy engines in rotation rounds, unpacked per 512 MiB piece; auto = from 4 GPUs on, "

@@ -19,6 +19,7 @@ Two deployment shapes:
 from __future__ import annotations
 
 import ctypes
+from dataclasses import dataclass
 from typing import Dict, Iterable, List, Optional, Sequence, Tuple
 
 import numpy as np
@@ -587,6 +588,40 @@ class MulticastBuffer:
             self.ptr = 0
 
 
+@dataclass(frozen=True)
+class Scheme:
+    """How one phase's remote pieces travel (RankRealloc). All are bit-exact;
+    they differ in which engine carries the bytes and when in-host fan-outs
+    run."""
+    relay: bool = False         # pipelined relay chain for payloads reaching >= 2 other GPUs
+    overlap: bool = False       # per-chunk in-host fan-out inside phase 0 (star flags)
+    staged: bool = False        # copy-engine rotation of whole shards + per-piece unpack
+    ce_transport: bool = False  # copy-engine 2D/3D copies straight into the destinations
+
+    def label(self) -> str:
+        parts = [k for k in ("relay", "overlap", "staged", "ce_transport") if getattr(self, k)]
+        return "+".join(parts) or "push"
+
+
+class _Binding:
+    """One phase bound to a scheme: its executor and the flag / staging
+    buffers it needs (allocated here, exchanged through CUDA IPC)."""
+
+    def __init__(self):
+        self.executor: Optional[Executor] = None
+        self.owned: List[DeviceBuffer] = []
+        self.opened: List[int] = []
+
+    def free(self) -> None:
+        if self.executor is not None:
+            self.executor.close()
+        for p in self.opened:
+            close_ipc(p)
+        for b in self.owned:
+            b.free()
+        self.executor, self.opened, self.owned = None, [], []
+
+
 class RankRealloc:
     """One rank of a one-process-per-GPU reallocation.
 
@@ -597,6 +632,11 @@ class RankRealloc:
     telling which buffers to allocate, and ``bind``: per phase the (src name,
     dst name). Buffers of remote hosts are mapped through CUDA IPC; a barrier
     runs after every phase so the next phase reads completed shards.
+
+    Per phase a delivery scheme (Scheme) is chosen: from the switches and the
+    measured-rate cost model, or — with ``probe=True`` — by timing every
+    scheme the switches allow on the real buffers at bind time (max over
+    ranks, a few launches each) and keeping the fastest (``probe_log``).
     """
 
     def __init__(self, plans: Sequence[ReallocPlan], shards: Dict[str, Tuple[int, int]],
@@ -604,104 +644,168 @@ class RankRealloc:
                  mode: int = PUSH, kernel: Optional[int] = DEFAULT_KERNEL, hierarchical: bool = True,
                  multicast: Sequence[str] = (), relay=False, overlap: bool = False,
                  flag_kernel: int = DEFAULT_FLAG_KERNEL, chunk_bytes: int = 0, ce_min_run_bytes: int = 0,
-                 staged=False, stage_chunk_bytes: int = 512 << 20, ce_transport=False):
+                 staged=False, stage_chunk_bytes: int = 512 << 20, ce_transport=False, probe: bool = False):
         """``multicast`` names shard sets whose per-GPU leader shards (the
         lowest-id plan device of the set on each GPU) are members of one NVLS
         multicast object: a payload bound for every GPU is then stored once
         (K3) instead of once per GPU (needs world > 1, push mode,
         hierarchical delivery). ``chunk_bytes``: work-item size (0 = the
-        library default), also the relay/overlap flag granularity."""
+        library default), also the relay/overlap flag granularity.
+        ``relay`` / ``staged`` / ``ce_transport``: False, True (every phase
+        it applies to) or "auto" (cost model); ``overlap``: bool."""
         self.plans, self.rank, self.world, self.cuda_device = list(plans), rank, world, cuda_device
+        self.group, self.mode, self.kernel, self.flag_kernel = group, mode, kernel, flag_kernel
+        self.hierarchical, self.chunk_bytes, self.ce_min_run_bytes = hierarchical, chunk_bytes, ce_min_run_bytes
+        self.stage_chunk = stage_chunk_bytes
         n = plans[0].cluster.device_count()
+        self.n = n
         self.local = hosted_devices(n, rank, world)
         self.owner = {d: d // (n // world) for d in range(n)}
+        self.host_of = [self.owner[d] for d in range(n)]
+        self.bind = list(bind)
         if multicast == "auto":
             # Multicast a phase's destination set only where it lowers the
             # estimated link bottleneck by >10% (one source feeding many GPUs;
             # not all-gather patterns, where every GPU is ingress-bound).
             multicast = []
             if world > 1 and mode == PUSH and hierarchical and multicast_supported(cuda_device):
-                host_of = [self.owner[d] for d in range(n)]
                 for pi, (_sname, dname) in enumerate(bind):
                     p = self.plans[pi]
-                    if link_bottleneck(p, host_of, True) < 0.9 * link_bottleneck(p, host_of, False):
+                    if link_bottleneck(p, self.host_of, True) < 0.9 * link_bottleneck(p, self.host_of, False):
                         multicast.append(dname)
         self.multicast = list(multicast)
         if multicast and (world < 2 or mode != PUSH or not hierarchical):
             raise ValueError("multicast needs world > 1, push mode and hierarchical delivery")
-        # Pipelined relay per phase (payloads reaching >= 2 other GPUs travel
-        # source -> GPU -> GPU ... chunk by chunk): True = every phase, "auto" =
-        # where it lowers the estimated link bottleneck by >10%.
-        host_of_all = [self.owner[d] for d in range(n)]
-        # ``overlap``: in-host fan-outs start per chunk inside phase 0 (star
-        # scheme, same flag machinery) instead of after a barrier.
-        self.relay_phases: List[int] = []
-        self.overlap_phases: List[int] = []
-        flag_ok = world > 1 and mode == PUSH and hierarchical
-        for pi, (_sname, dname) in enumerate(bind):
-            if not flag_ok or dname in self.multicast:
-                continue
-            p = self.plans[pi]
-            if relay and (relay != "auto" or (link_bottleneck(p, host_of_all, relay=True) <
-                                              0.9 * link_bottleneck(p, host_of_all))):
-                self.relay_phases.append(pi)
-            if overlap:
-                self.overlap_phases.append(pi)
-        # Staged gather (copy engines in rotation rounds, pull-mode unpack per
-        # piece) for phases whose destinations read sources on other GPUs.
-        # True: every such phase; "auto": from 4 GPUs on, all-gather-shaped
-        # phases (every GPU sends and receives) that copy-engine runs do not
-        # already cover. It replaces the overlapped fan-out of that phase.
-        self.staged_phases: List[int] = []
-        if staged and world > 1 and hierarchical and mode == PUSH:
-            for pi, (_sname, dname) in enumerate(bind):
-                if pi in self.relay_phases or dname in self.multicast:
-                    continue
-                p = self.plans[pi]
-                if staged == "auto" and (world < 4 or not _all_gather_shaped(p, host_of_all, world, ce_min_run_bytes)):
-                    continue
-                if any(host_of_all[s] != host_of_all[d] for s, dsts, _r in p.lowered() for d in dsts):
-                    self.staged_phases.append(pi)
-            self.overlap_phases = [pi for pi in self.overlap_phases if pi not in self.staged_phases]
-        # Copy-engine transport (remote pieces by copy engine, merged across
-        # layers, rotation rounds): True = every phase with remote traffic
-        # that no other scheme took; "auto" = where the measured rates predict
-        # >= 5% less time than SM peer stores (ce_transport_estimate, which
-        # charges the copy-engine side a separate in-host fan-out phase).
-        self.ce_phases: List[int] = []
         self.ce_estimates: Dict[int, Tuple[float, float]] = {}
-        if ce_transport and world > 1 and hierarchical and mode == PUSH:
-            for pi, (_sname, dname) in enumerate(bind):
-                if pi in self.relay_phases or pi in self.staged_phases or dname in self.multicast:
-                    continue
-                p = self.plans[pi]
-                if not any(host_of_all[s] != host_of_all[d] for s, dsts, _r in p.lowered() for d in dsts):
-                    continue
-                if ce_transport == "auto":
-                    est = self.ce_estimates[pi] = ce_transport_estimate(p, host_of_all)
-                    if est[0] >= 0.95 * est[1]:
-                        continue
-                self.ce_phases.append(pi)
-            self.overlap_phases = [pi for pi in self.overlap_phases if pi not in self.ce_phases]
-        self.relay_bufs: Dict[int, DeviceBuffer] = {}
-        for pi in sorted(set(self.relay_phases) | set(self.overlap_phases)):
-            slots = relay_slots(self.plans[pi], host_of_all, chunk_bytes, chain=pi in self.relay_phases,
-                                overlap=pi in self.overlap_phases)
-            if slots == 0:
-                continue
-            self.relay_bufs[pi] = DeviceBuffer(cuda_device, 4 * max(slots, 64))
-            self.relay_bufs[pi].zero()
-        self.stage_bufs: Dict[int, Dict[int, DeviceBuffer]] = {}
-        self.stage_flag_bufs: Dict[int, DeviceBuffer] = {}
-        self.stage_chunk = stage_chunk_bytes
-        for pi in self.staged_phases:
-            p = self.plans[pi]
-            need = sorted({s for s, dsts, _r in p.lowered() if host_of_all[s] != rank and
-                           any(host_of_all[d] == rank for d in dsts)})
-            self.stage_bufs[pi] = {s: DeviceBuffer(cuda_device, p.shard_bytes(SRC, s)) for s in need}
-            slots = stage_slots(p, host_of_all, stage_chunk_bytes)
-            self.stage_flag_bufs[pi] = DeviceBuffer(cuda_device, 4 * max(slots, 64))
-            self.stage_flag_bufs[pi].zero()
+        switches = dict(relay=relay, overlap=overlap, staged=staged, ce_transport=ce_transport)
+        self.schemes: List[Scheme] = [self._decide(pi, switches) for pi in range(len(self.plans))]
+        self._alloc_shards(shards)
+        self.bindings: List[Optional[_Binding]] = [None] * len(self.plans)
+        self.executors: List[Executor] = []
+        self.has_fanout: List[bool] = [False] * len(self.plans)
+        self.probe_log: List[dict] = []
+        for pi in range(len(self.plans)):
+            cands = self._candidates(pi, switches) if probe else [self.schemes[pi]]
+            if len(cands) > 1:
+                self.schemes[pi] = self._probe(pi, cands)
+            self._bind_phase(pi, self.schemes[pi])
+        self.executors = [b.executor for b in self.bindings]
+
+    # ---- scheme choice ----------------------------------------------------
+
+    def _flag_ok(self) -> bool:
+        return self.world > 1 and self.mode == PUSH and self.hierarchical
+
+    def _remote(self, p: ReallocPlan) -> bool:
+        return any(self.host_of[s] != self.host_of[d] for s, dsts, _r in p.lowered() for d in dsts)
+
+    def _decide(self, pi: int, sw: dict) -> Scheme:
+        """The cost-model choice for phase pi under the switches."""
+        p, dname = self.plans[pi], self.bind[pi][1]
+        if not self._flag_ok() or dname in self.multicast or not self._remote(p):
+            return Scheme()
+        relay = bool(sw["relay"]) and (sw["relay"] != "auto" or link_bottleneck(p, self.host_of, relay=True) <
+                                       0.9 * link_bottleneck(p, self.host_of))
+        if relay:
+            return Scheme(relay=True, overlap=bool(sw["overlap"]))
+        # Staged gather: True = every phase with remote reads; "auto" = from 4
+        # GPUs on, all-gather-shaped phases that copy-engine runs do not cover.
+        if sw["staged"] and (sw["staged"] != "auto" or (
+                self.world >= 4 and _all_gather_shaped(p, self.host_of, self.world, self.ce_min_run_bytes))):
+            return Scheme(staged=True)
+        # Copy-engine transport: True = every remaining phase with remote
+        # traffic; "auto" = where the measured rates predict >= 5% less time
+        # than SM peer stores (ce_transport_estimate charges the copy-engine
+        # side a separate in-host fan-out phase).
+        if sw["ce_transport"]:
+            if sw["ce_transport"] != "auto":
+                return Scheme(ce_transport=True)
+            est = self.ce_estimates[pi] = ce_transport_estimate(p, self.host_of)
+            if est[0] < 0.95 * est[1]:
+                return Scheme(ce_transport=True)
+        return Scheme(overlap=bool(sw["overlap"]))
+
+    def _candidates(self, pi: int, sw: dict) -> List[Scheme]:
+        """Every scheme the switches allow for phase pi (probe mode)."""
+        p, dname = self.plans[pi], self.bind[pi][1]
+        if not self._flag_ok() or dname in self.multicast or not self._remote(p):
+            return [Scheme()]
+        out = [self.schemes[pi], Scheme(overlap=bool(sw["overlap"]))]
+        if sw["relay"] and any(len({self.host_of[d] for d in dsts} - {self.host_of[s]}) >= 2
+                               for s, dsts, _r in p.lowered()):
+            out.append(Scheme(relay=True, overlap=bool(sw["overlap"])))
+        if sw["staged"]:
+            out.append(Scheme(staged=True))
+        if sw["ce_transport"]:
+            out.append(Scheme(ce_transport=True))
+        uniq: List[Scheme] = []
+        for sc in out:
+            if sc not in uniq:
+                uniq.append(sc)
+        return uniq
+
+    def _probe(self, pi: int, cands: List[Scheme], reps: int = 3) -> Scheme:
+        """Bind each candidate, time `reps` launches of phase pi (after one
+        warm-up) with CUDA events, take the max over ranks of the median, keep
+        the fastest. Phase pi's destinations are overwritten (bind time: the
+        caller fills sources afterwards)."""
+        import torch
+        timings: Dict[str, float] = {}
+        best, best_ms = cands[0], float("inf")
+        stream = torch.cuda.current_stream()
+        for sc in cands:
+            self._bind_phase(pi, sc)
+            ex = self.bindings[pi].executor
+            ms = []
+            for k in range(reps + 1):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                self._collective_barrier()
+                e0.record(stream)
+                ex.launch(stream)
+                self._finish_phase(pi, stream, 0)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                if k:
+                    ms.append(e0.elapsed_time(e1))
+            med = sorted(ms)[len(ms) // 2]
+            med = self._allreduce_max(med)
+            timings[sc.label()] = round(med, 4)
+            if med < best_ms:
+                best, best_ms = sc, med
+            self._unbind_phase(pi)
+        self.probe_log.append({"phase": pi, "ms": timings, "chosen": best.label(),
+                               "cost_model": self.schemes[pi].label()})
+        return best
+
+    def _collective_barrier(self) -> None:
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier(group=self.group)
+
+    def _allreduce_max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        import torch.distributed as dist
+        out: List[float] = [None] * self.world  # type: ignore
+        dist.all_gather_object(out, v, group=self.group)
+        return max(out)
+
+    def _exchange(self, mine: dict) -> List[dict]:
+        """all_gather of small picklable tables (IPC handles)."""
+        if self.world == 1:
+            return [mine]
+        import torch.distributed as dist
+        out: List[dict] = [None] * self.world  # type: ignore
+        dist.all_gather_object(out, mine, group=self.group)
+        return out
+
+    # ---- buffers and bindings -----------------------------------------------
+
+    def _alloc_shards(self, shards: Dict[str, Tuple[int, int]]) -> None:
+        """Shard buffers of every set (multicast members for multicast sets),
+        the barrier flags, and the IPC exchange that maps every remote shard
+        and flag array here."""
+        n, rank, world = self.n, self.rank, self.world
         self.buffers: Dict[str, Dict[int, object]] = {}
         self.mc_tables: Dict[str, Dict[int, int]] = {}
         mc_leaders: Dict[str, int] = {}
@@ -709,16 +813,16 @@ class RankRealloc:
             p = self.plans[pi]
             bufs = {}
             mine = [d for d in p.devices(side) if d in self.local]
-            if name in multicast:
+            if name in self.multicast:
                 if not mine:
                     raise ValueError(f"multicast set {name!r}: rank {rank} hosts none of its devices")
                 import torch.distributed as dist
                 leader = min(mine)
                 sizes: List[int] = [None] * world  # type: ignore
-                dist.all_gather_object(sizes, p.shard_bytes(side, leader), group=group)
+                dist.all_gather_object(sizes, p.shard_bytes(side, leader), group=self.group)
                 if len(set(sizes)) != 1:
                     raise ValueError(f"multicast set {name!r}: leader shards differ in size {sizes}")
-                bufs[leader] = MulticastBuffer(cuda_device, sizes[0], rank, world, group)
+                bufs[leader] = MulticastBuffer(self.cuda_device, sizes[0], rank, world, self.group)
                 bufs[leader].zero()
                 mc_leaders[name] = leader
                 leaders = [min(d for d in p.devices(side) if d in hosted_devices(n, r, world)) for r in range(world)]
@@ -726,99 +830,145 @@ class RankRealloc:
             for d in mine:
                 if d in bufs:
                     continue
-                bufs[d] = DeviceBuffer(cuda_device, p.shard_bytes(side, d))
+                bufs[d] = DeviceBuffer(self.cuda_device, p.shard_bytes(side, d))
                 bufs[d].zero()
             self.buffers[name] = bufs
-        stream_sync()
-        # Exchange IPC handles of every local shard (and the barrier flags).
-        self.flags = DeviceBuffer(cuda_device, 4 * max(world, 64))
+        self.flags = DeviceBuffer(self.cuda_device, 4 * max(world, 64))
         self.flags.zero()
         stream_sync()
-        mine: dict = {}
+        # multicast members are VMM allocations: reached through the multicast
+        # address, not through CUDA IPC
+        mine_h: dict = {}
         if world > 1:
-            # multicast members are VMM allocations: reached through the
-            # multicast address, not through CUDA IPC
-            mine = {name: {d: b.ipc_handle() for d, b in bufs.items() if mc_leaders.get(name) != d}
-                    for name, bufs in self.buffers.items()}
-            mine["__flags__"] = {rank: self.flags.ipc_handle()}
-            for pi, b in self.relay_bufs.items():
-                mine[f"__relay{pi}__"] = {rank: b.ipc_handle()}
-            for pi, bufs in self.stage_bufs.items():
-                mine[f"__stage{pi}__"] = {s: b.ipc_handle() for s, b in bufs.items()}
-                mine[f"__sflag{pi}__"] = {rank: self.stage_flag_bufs[pi].ipc_handle()}
-        gathered: List[dict] = [None] * world  # type: ignore
-        if world > 1:
-            import torch.distributed as dist
-            dist.all_gather_object(gathered, mine, group=group)
-        else:
-            gathered[0] = mine
+            mine_h = {name: {d: b.ipc_handle() for d, b in bufs.items() if mc_leaders.get(name) != d}
+                      for name, bufs in self.buffers.items()}
+            mine_h["__flags__"] = {rank: self.flags.ipc_handle()}
+        gathered = self._exchange(mine_h)
         self.ptrs: Dict[str, Dict[int, int]] = {name: {d: b.ptr for d, b in bufs.items()}
                                                  for name, bufs in self.buffers.items()}
         self._opened: List[int] = []
         flag_ptrs = [0] * world
         flag_ptrs[rank] = self.flags.ptr
-        relay_remote: Dict[Tuple[int, int], int] = {}
-        stage_remote: Dict[int, Dict[Tuple[int, int], int]] = {pi: {} for pi in self.staged_phases}
-        stage_flags: Dict[int, Dict[int, int]] = {pi: {rank: b.ptr} for pi, b in self.stage_flag_bufs.items()}
         for r, table in enumerate(gathered):
             if r == rank:
                 continue
             for name, handles in table.items():
                 for d, h in handles.items():
-                    if name.startswith("__stage") and self.owner[d] != rank:
-                        continue  # another GPU's staging for a source not held here
-                    p = open_ipc(cuda_device, h)
-                    self._opened.append(p)
+                    ptr = open_ipc(self.cuda_device, h)
+                    self._opened.append(ptr)
                     if name == "__flags__":
-                        flag_ptrs[r] = p
-                    elif name.startswith("__relay"):
-                        relay_remote[(int(name[7:-2]), r)] = p
-                    elif name.startswith("__stage"):
-                        stage_remote[int(name[7:-2])][(d, r)] = p
-                    elif name.startswith("__sflag"):
-                        stage_flags[int(name[7:-2])][r] = p
+                        flag_ptrs[r] = ptr
                     else:
-                        self.ptrs[name][d] = p
-        self.barrier = Barrier(cuda_device, rank, world, flag_ptrs)
-        self.bind = list(bind)
-        host_of = [self.owner[d] for d in range(n)]
-        # relay flag array of every plan device's host, as mapped in this process
-        relay_tables: Dict[int, Dict[int, int]] = {}
-        for pi, b in self.relay_bufs.items():
-            relay_tables[pi] = {d: (b.ptr if self.owner[d] == rank else relay_remote[(pi, self.owner[d])])
-                                for d in range(n)}
-        self.executors: List[Executor] = []
-        for pi, (sname, dname) in enumerate(bind):
-            if pi in self.staged_phases:
-                # pull-mode unpack from local staging buffers; this GPU's own
-                # sources are pushed to the others by its copy engine
-                src = {d: ptr for d, ptr in self.ptrs[sname].items() if self.owner[d] == rank}
-                src.update({d: b.ptr for d, b in self.stage_bufs[pi].items()})
-                self.executors.append(Executor(self.plans[pi], cuda_device, src, self.ptrs[dname], self.local, PULL,
-                                               chunk_bytes, host_of=host_of, stage_chunk_bytes=self.stage_chunk,
-                                               n_hosts=world, stage_remote=stage_remote[pi],
-                                               stage_flags=stage_flags[pi]))
-            else:
-                self.executors.append(Executor(self.plans[pi], cuda_device, self.ptrs[sname], self.ptrs[dname],
-                                               self.local, mode, chunk_bytes,
-                                               host_of=host_of if hierarchical else None,
-                                               mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_tables.get(pi),
-                                               relay_chain=pi in self.relay_phases,
-                                               overlap_fanout=pi in self.overlap_phases,
-                                               ce_min_run_bytes=ce_min_run_bytes,
-                                               ce_transport=pi in self.ce_phases))
-            if kernel is not None:
-                self.executors[-1].set_kernel(kernel)
-            self.executors[-1].set_flag_kernel(flag_kernel)
+                        self.ptrs[name][d] = ptr
+        self.barrier = Barrier(self.cuda_device, rank, world, flag_ptrs)
+
+    def _bind_phase(self, pi: int, sc: Scheme) -> None:
+        """Allocate what scheme `sc` needs for phase pi (relay / overlap flag
+        array, staging buffers and their flags), exchange it through IPC
+        (collective), create the executor and agree on the fan-out step."""
+        b = _Binding()
+        rank, world, n = self.rank, self.world, self.n
+        p = self.plans[pi]
+        sname, dname = self.bind[pi]
+        mine: dict = {}
+        relay_buf = stage_flag = None
+        stage_bufs: Dict[int, DeviceBuffer] = {}
+        if sc.relay or sc.overlap:
+            slots = relay_slots(p, self.host_of, self.chunk_bytes, chain=sc.relay, overlap=sc.overlap)
+            if slots:
+                relay_buf = DeviceBuffer(self.cuda_device, 4 * max(slots, 64))
+                relay_buf.zero()
+                b.owned.append(relay_buf)
+                mine["relay"] = {rank: relay_buf.ipc_handle()} if world > 1 else {}
+        if sc.staged:
+            need = sorted({s for s, dsts, _r in p.lowered() if self.host_of[s] != rank and
+                           any(self.host_of[d] == rank for d in dsts)})
+            stage_bufs = {s: DeviceBuffer(self.cuda_device, p.shard_bytes(SRC, s)) for s in need}
+            b.owned.extend(stage_bufs.values())
+            stage_flag = DeviceBuffer(self.cuda_device, 4 * max(stage_slots(p, self.host_of, self.stage_chunk), 64))
+            stage_flag.zero()
+            b.owned.append(stage_flag)
+            mine["stage"] = {s: x.ipc_handle() for s, x in stage_bufs.items()}
+            mine["sflag"] = {rank: stage_flag.ipc_handle()}
+        stream_sync()
+        gathered = self._exchange(mine) if (sc.relay or sc.overlap or sc.staged) else [mine] * world
+        relay_remote: Dict[int, int] = {}
+        stage_remote: Dict[Tuple[int, int], int] = {}
+        stage_flags: Dict[int, int] = {rank: stage_flag.ptr} if stage_flag else {}
+        for r, table in enumerate(gathered):
+            if r == rank:
+                continue
+            for key, handles in table.items():
+                for d, h in handles.items():
+                    if key == "stage" and self.owner[d] != rank:
+                        continue  # another GPU's staging for a source not held here
+                    ptr = open_ipc(self.cuda_device, h)
+                    b.opened.append(ptr)
+                    if key == "relay":
+                        relay_remote[r] = ptr
+                    elif key == "stage":
+                        stage_remote[(d, r)] = ptr
+                    else:
+                        stage_flags[r] = ptr
+        if sc.staged:
+            # pull-mode unpack from local staging buffers; this GPU's own
+            # sources are pushed to the others by its copy engine
+            src = {d: ptr for d, ptr in self.ptrs[sname].items() if self.owner[d] == rank}
+            src.update({d: x.ptr for d, x in stage_bufs.items()})
+            ex = Executor(p, self.cuda_device, src, self.ptrs[dname], self.local, PULL, self.chunk_bytes,
+                          host_of=self.host_of, stage_chunk_bytes=self.stage_chunk, n_hosts=world,
+                          stage_remote=stage_remote, stage_flags=stage_flags)
+        else:
+            relay_table = None
+            if relay_buf is not None:
+                relay_table = {d: (relay_buf.ptr if self.owner[d] == rank else relay_remote[self.owner[d]])
+                               for d in range(n)}
+            ex = Executor(p, self.cuda_device, self.ptrs[sname], self.ptrs[dname], self.local, self.mode,
+                          self.chunk_bytes, host_of=self.host_of if self.hierarchical else None,
+                          mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_table, relay_chain=sc.relay,
+                          overlap_fanout=sc.overlap, ce_min_run_bytes=self.ce_min_run_bytes,
+                          ce_transport=sc.ce_transport)
+        if self.kernel is not None:
+            ex.set_kernel(self.kernel)
+        ex.set_flag_kernel(self.flag_kernel)
+        b.executor = ex
+        self.bindings[pi] = b
+        if self.executors and pi < len(self.executors):
+            self.executors[pi] = ex
         # Every rank must run the same barrier sequence: a phase has a fan-out
         # step if any rank has fan-out work in it.
-        counts = [e.fanout_items for e in self.executors]
-        if world > 1:
-            import torch.distributed as dist
-            allc: List[list] = [None] * world  # type: ignore
-            dist.all_gather_object(allc, counts, group=group)
-            counts = [sum(c[i] for c in allc) for i in range(len(counts))]
-        self.has_fanout = [c > 0 for c in counts]
+        counts = self._exchange({"n": ex.fanout_items}) if world > 1 else [{"n": ex.fanout_items}]
+        self.has_fanout[pi] = sum(c["n"] for c in counts) > 0
+
+    def _unbind_phase(self, pi: int) -> None:
+        stream_sync()
+        self._collective_barrier()  # no rank still reads or writes this binding's buffers
+        self.bindings[pi].free()
+        self._collective_barrier()
+        self.bindings[pi] = None
+
+    # ---- reporting (bench, tests) -------------------------------------------
+
+    def _phases_with(self, attr: str) -> List[int]:
+        return [pi for pi, sc in enumerate(self.schemes) if getattr(sc, attr)]
+
+    @property
+    def relay_phases(self) -> List[int]:
+        return self._phases_with("relay")
+
+    @property
+    def overlap_phases(self) -> List[int]:
+        return self._phases_with("overlap")
+
+    @property
+    def staged_phases(self) -> List[int]:
+        return self._phases_with("staged")
+
+    @property
+    def ce_phases(self) -> List[int]:
+        return self._phases_with("ce_transport")
+
+    # ---- execution ------------------------------------------------------------
 
     def set_kernel(self, kernel: int, flag_kernel: Optional[int] = None) -> None:
         for e in self.executors:
@@ -836,7 +986,7 @@ class RankRealloc:
         if self.world > 1:
             self.barrier.launch(stream)
             if self.has_fanout[i]:
-                self.executors[i].launch_fanout(stream, ctas)
+                self.bindings[i].executor.launch_fanout(stream, ctas)
                 self.barrier.launch(stream)
 
     def run_phase_onload(self, i: int, host_ptrs: Dict[int, int], copy_stream, stream=None, ctas: int = 0,
@@ -846,7 +996,7 @@ class RankRealloc:
         copy kernels."""
         e = self.executors[i]
         sname = self.bind[i][0]
-        key = (i, chunk_bytes)
+        key = (i, chunk_bytes, id(e))
         if getattr(self, "_onload_key", {}).get(i) != key:
             e.enable_onload({d: b.nbytes for d, b in self.buffers[sname].items()}, chunk_bytes)
             self._onload_key = {**getattr(self, "_onload_key", {}), i: key}
@@ -868,24 +1018,18 @@ class RankRealloc:
         stream_sync()
         if self.world > 1:
             import torch.distributed as dist
-            dist.barrier()  # no rank may still be storing into shared buffers
-        for e in self.executors:
-            e.close()
+            dist.barrier(group=self.group)  # no rank may still be storing into shared buffers
+        for b in self.bindings:
+            if b is not None:
+                b.free()
         self.barrier.close()
         for p in self._opened:
             close_ipc(p)
         for bufs in self.buffers.values():
             for b in bufs.values():
                 b.free()
-        for b in self.relay_bufs.values():
-            b.free()
-        for bufs in self.stage_bufs.values():
-            for b in bufs.values():
-                b.free()
-        for b in self.stage_flag_bufs.values():
-            b.free()
         self.flags.free()
 
     def relay_timeouts(self) -> int:
-        """Relay waits that gave up (bounded spins); nonzero = results invalid."""
+        """Relay / stage waits that gave up (bounded spins); nonzero = results invalid."""
         return sum(e.relay_timeouts() for e in self.executors)

@@ -188,6 +188,50 @@ class Worker:
                 self.run(f"ce-transport {sp}->{dp} (+onload)", m, pl(sp), pl(dp), SPECIAL | 83, reps=3,
                          onload_chunk=32 << 10, hierarchical=hier, ce_transport=True)
 
+    def probe(self):
+        """Bind-time probe: every scheme the switches allow is timed on the real
+        buffers (max over ranks) and the fastest kept; the chosen executor
+        must be bit-exact like any other, and every rank must agree."""
+        m = dataclasses.replace(TINY_GQA, num_layers=6)
+        for sp, dp in CASES[:3] + [((1, 1, 1, 0, 0), (1, 8, 1, 0, 0))]:
+            src = REPLICATE[0] if sp == (1, 1, 1, 0, 0) else pl(sp)
+            label = f"probe {sp}->{dp}"
+            with self.case(label):
+                plan = plan_param_realloc(m, src, pl(dp), self.c, BALANCED)
+                rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], self.rank, self.world,
+                                   self.local, relay="auto", overlap=True, staged=True, ce_transport=True,
+                                   stage_chunk_bytes=64 << 10, probe=True)
+                try:
+                    log = self._agree(rr.probe_log)
+                    if self.world > 1 and not log:
+                        self.failures.append(f"{label}: no probe ran")
+                    if self.rank == 0:
+                        print(f"  {label}: {log}", flush=True)
+                    for d, b in rr.buffers["a"].items():
+                        R.fill_shard(plan, R.SRC, d, b.ptr, SPECIAL | 61)
+                    for _rep in range(2):
+                        for b in rr.buffers["b"].values():
+                            b.zero()
+                        torch.cuda.synchronize()
+                        dist.barrier()
+                        rr.run_phase(0)
+                        torch.cuda.synchronize()
+                        for d, b in rr.buffers["b"].items():
+                            if not np.array_equal(b.to_host(), O.fill(m, pl(dp), self.c, d, SPECIAL | 61)):
+                                self.failures.append(f"{label}: device {d} differs")
+                    if rr.relay_timeouts() or rr.barrier.timed_out():
+                        self.failures.append(f"{label}: flag or barrier timeouts")
+                    dist.barrier()
+                finally:
+                    rr.close()
+
+    def _agree(self, obj):
+        out = [None] * self.world
+        dist.all_gather_object(out, [e["chosen"] for e in obj])
+        if any(o != out[0] for o in out):
+            self.failures.append(f"ranks chose different schemes: {out}")
+        return obj
+
     def staged(self):
         """Staged gather (copy-engine rotation + per-piece unpack), small pieces,
         both unpack kernels, plain / onloaded / plain again (flag epochs)."""
@@ -281,9 +325,9 @@ class Worker:
 def main() -> int:
     w = Worker()
     sections = os.environ.get("RR_SECTIONS",
-                              "basic,multicast,overlap,relay,ce,cetransport,staged,fuzz,full7b").split(",")
+                              "basic,multicast,overlap,relay,ce,cetransport,probe,staged,fuzz,full7b").split(",")
     table = {"basic": w.basic, "multicast": w.multicast, "overlap": w.overlap, "relay": w.relay,
-             "ce": w.ce_runs_cases, "cetransport": w.ce_transport, "staged": w.staged, "staged_many": w.staged_many_items, "fuzz": w.fuzz,
+             "ce": w.ce_runs_cases, "cetransport": w.ce_transport, "probe": w.probe, "staged": w.staged, "staged_many": w.staged_many_items, "fuzz": w.fuzz,
              "full7b": w.full_7b}
     for s in sections + (["staged_many"] if "staged" in sections else []):
         table[s]()
