@@ -56,7 +56,7 @@ class RrExecOptions(Structure):
                 ("mc_bufs", POINTER(c_void_p)), ("relay_flags", POINTER(c_void_p)), ("relay_chain", c_int32),
                 ("overlap_fanout", c_int32), ("ce_min_run_bytes", c_int64), ("stage_chunk_bytes", c_int64),
                 ("n_hosts", c_int32), ("stage_remote", POINTER(c_void_p)), ("stage_flags", POINTER(c_void_p)),
-                ("ce_transport", c_int32)]
+                ("ce_transport", c_int32), ("ce_flags", POINTER(c_void_p))]
 
 
 _P = c_void_p
@@ -72,6 +72,7 @@ _SIGNATURES = {
     "rr_plan_stage_slots": (c_int, [_P, POINTER(c_int32), c_int64, POINTER(c_int64)]),
     "rr_plan_ce_runs": (c_int, [_P, c_int, POINTER(c_int32), POINTER(c_int32), c_int64, POINTER(c_int64), c_int,
                                 POINTER(c_int)]),
+    "rr_plan_ce_slots": (c_int, [_P, POINTER(c_int32), POINTER(c_int64)]),
     "rr_plan_ce_copies": (c_int, [_P, c_int, POINTER(c_int32), POINTER(c_int32), POINTER(c_int64), c_int,
                                   POINTER(c_int)]),
     "rr_mcast_supported": (c_int, [c_int, POINTER(c_int)]),

@@ -119,6 +119,7 @@ struct rr_exec {
     int64_t width, height, depth, src_pitch, dst_pitch, src_slice, dst_slice;
     DeviceId src_dev;  // source plan device and byte offsets in its shard (onload pipelining)
     int64_t src_off, src_end;
+    uint32_t* flag = nullptr;  // copy-engine star: flagged on the receiving host after the copy
     int64_t bytes() const { return width * height * depth; }
   };
   std::vector<CeCopy> ce;
@@ -334,7 +335,10 @@ void ce_issue(rr_exec* ex, cudaStream_t after, cudaEvent_t after_event = nullptr
     after_event = ex->ce_fork;
   }
   check_cuda(cudaStreamWaitEvent(ex->ce_stream, after_event, 0), "cudaStreamWaitEvent(ce fork)");
-  for (const auto& c : ex->ce) issue_copy(c, ex->ce_stream);
+  for (const auto& c : ex->ce) {
+    issue_copy(c, ex->ce_stream);
+    if (c.flag) signal_piece(ex->ce_stream, c.flag, ex->epoch);
+  }
   for (const auto& p : ex->stage) {
     check_cuda(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "staged push");
     signal_piece(ex->ce_stream, p.flag, ex->epoch);
@@ -448,6 +452,23 @@ rr_status rr_plan_ce_copies(const rr_plan* plan, int n_local, const int32_t* loc
   });
 }
 
+rr_status rr_plan_ce_slots(const rr_plan* plan, const int32_t* host_of, int64_t* slots) {
+  return guarded([&] {
+    need(plan != nullptr && host_of != nullptr && slots != nullptr, "null plan/host table/output");
+    rr::HostMap hm;
+    for (int d = 0; d < plan->cluster.device_count(); ++d) hm.host.push_back(host_of[d]);
+    std::vector<int> hosts(hm.host);
+    std::sort(hosts.begin(), hosts.end());
+    hosts.erase(std::unique(hosts.begin(), hosts.end()), hosts.end());
+    int64_t best = 0;
+    for (int h : hosts) {
+      hm.me = h;
+      best = std::max(best, rr::ce_star_slots(plan->lowered, hm, h, (int64_t{1} << 31) - 1));
+    }
+    *slots = best;
+  });
+}
+
 rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, void* const* src_bufs,
                          void* const* dst_bufs, int n_local, const int32_t* local, const int32_t* host_of,
                          int mode, int64_t chunk_bytes, rr_exec** out) {
@@ -465,6 +486,7 @@ rr_status rr_exec_create(const rr_plan* plan, int cuda_device, int n_devices, vo
   opt.stage_remote = nullptr;
   opt.stage_flags = nullptr;
   opt.ce_transport = 0;
+  opt.ce_flags = nullptr;
   return rr_exec_create_ex(plan, cuda_device, n_devices, src_bufs, dst_bufs, n_local, local, &opt, out);
 }
 
@@ -516,6 +538,14 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       need(mode == 0, "copy-engine transport is a push-mode path");
       need(!staged && options->mc_bufs == nullptr, "copy-engine transport excludes the staged gather and multicast");
       hm.ce_remote = true;
+      if (options->ce_flags) {
+        need(options->host_of != nullptr && options->n_hosts > 0, "copy-engine star needs host_of and n_hosts");
+        need(options->relay_flags == nullptr, "copy-engine star excludes relay / overlap flags");
+        for (size_t d = 0; d < hm.host.size(); ++d)
+          need(hm.host[d] >= 0 && hm.host[d] < options->n_hosts, "host ids must lie in 0..n_hosts-1");
+        hm.ce_star = true;
+        hm.ce_flags = reinterpret_cast<uint64_t>(options->ce_flags[hm.me]);
+      }
     }
     check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
     int per_sm = 0, sms = 0;
@@ -526,11 +556,21 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
         (mode == 0 && ce_min > 0 && src_bufs && dst_bufs && !hm.ce_remote) ? ce_runs(plan, jobs, hm, ce_min)
                                                                            : std::vector<rr::CeRun>{};
     std::vector<rr::CeCopy> transport;
+    std::vector<int64_t> send_slots;
+    rr::CeSlotMap slot_map;
+    int64_t n_ce_slots = 0;
     if (hm.ce_remote) {
       need(src_bufs != nullptr && dst_bufs != nullptr, "copy-engine transport needs buffer tables");
-      transport = rr::ce_transport_copies(jobs, hm, max_pitch(cuda_device));
+      const int64_t mp = max_pitch(cuda_device);
+      transport = rr::ce_transport_copies(jobs, hm, mp);
+      if (hm.ce_star) {
+        send_slots = rr::ce_send_slots(plan->lowered, hm, transport, mp);
+        slot_map = rr::ce_slot_map(plan->lowered, hm, hm.me, mp);
+        n_ce_slots = static_cast<int64_t>(slot_map.copies.size());
+        need(n_ce_slots == 0 || hm.ce_flags != 0, "missing this host's copy flag array");
+      }
     }
-    auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes, &runs);
+    auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes, &runs, hm.ce_star ? &slot_map : nullptr);
     auto b = rr::build_items(jobs, 1, hm, src_bufs, dst_bufs, chunk_bytes);
     if (options->chunk_bytes <= 0) {
       int bulk_ctas = 0;
@@ -549,6 +589,7 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       require_zero_flags(options->relay_flags[local[0]], n_relay, "relay_flags");
     }
     if (staged) require_zero_flags(options->stage_flags[hm.me], n_stage_slots, "stage_flags");
+    if (hm.ce_star) require_zero_flags(options->ce_flags[hm.me], n_ce_slots, "ce_flags");
 
     auto ex = std::make_unique<rr_exec>();
     ex->cuda_device = cuda_device;
@@ -568,11 +609,18 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
                         u.src, u.src_off, u.src_off + u.bytes});
       ex->ce_bytes += u.bytes;
     }
-    for (const auto& c : transport) {
+    for (size_t k = 0; k < transport.size(); ++k) {
+      const auto& c = transport[k];
       need(dst_bufs[c.dst] != nullptr && src_bufs[c.src] != nullptr, "missing a copy-engine transport buffer");
+      uint32_t* flag = nullptr;
+      if (hm.ce_star) {
+        auto* arr = static_cast<uint32_t*>(options->ce_flags[hm.host[static_cast<size_t>(c.dst)]]);
+        need(arr != nullptr, "missing a receiver's copy flag array");
+        flag = arr + send_slots[k];
+      }
       ex->ce.push_back({static_cast<char*>(dst_bufs[c.dst]) + c.dst_off,
                         static_cast<const char*>(src_bufs[c.src]) + c.src_off, c.width, c.height, c.depth,
-                        c.src_pitch, c.dst_pitch, c.src_slice, c.dst_slice, c.src, c.src_off, c.src_end()});
+                        c.src_pitch, c.dst_pitch, c.src_slice, c.dst_slice, c.src, c.src_off, c.src_end(), flag});
       ex->ce_bytes += c.bytes();
     }
     if (staged) {
@@ -931,7 +979,10 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
         issue_copy(p, ex->ce_stream);
       };
       for (const auto& c : ex->ce)
-        if (!onloaded(c.src_dev)) issue_copy(c, ex->ce_stream);
+        if (!onloaded(c.src_dev)) {
+          issue_copy(c, ex->ce_stream);
+          if (c.flag) signal_piece(ex->ce_stream, c.flag, ex->epoch);
+        }
       for (size_t k = 0; k < ex->chunks.size(); ++k) {
         const auto& ch = ex->chunks[k];
         const int64_t lo = ch.offset, hi = ch.offset + ch.bytes;
@@ -947,6 +998,8 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
             piece(c, lo, hi);
           else
             issue_copy(c, ex->ce_stream);
+          // flagged once the copy's last source byte is in (its last piece)
+          if (c.flag && c.src_end > lo && c.src_end <= hi) signal_piece(ex->ce_stream, c.flag, ex->epoch);
         }
       }
     }

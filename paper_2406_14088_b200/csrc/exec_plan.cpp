@@ -297,7 +297,9 @@ std::vector<Job> build_jobs(const std::vector<LoweredOp>& ops, const HostMap& hm
     }
     if (hs != hm.me && mine != groups.end() && mine->second.size() > 1 && !(mode == 1 && hm.stage_chunk > 0)) {
       Job j;
-      j.phase = 1;
+      // copy-engine star: the fan-out waits per copy inside phase 0
+      j.phase = hm.ce_star && mode == 0 ? 0 : 1;
+      j.ce_wait = j.phase == 0;
       j.src = mine->second.front();
       j.src_is_dst_buffer = true;
       j.op = &op;
@@ -461,7 +463,8 @@ uint64_t base_of(void* const* bufs, DeviceId d, const char* what) {
 }  // namespace
 
 ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, void* const* src_bufs,
-                    void* const* dst_bufs, int64_t chunk_bytes, const std::vector<CeRun>* ce) {
+                    void* const* dst_bufs, int64_t chunk_bytes, const std::vector<CeRun>* ce,
+                    const CeSlotMap* ce_slots) {
   ItemSet acc;
   std::vector<std::vector<Tagged>> streams;
   const bool accounting = src_bufs == nullptr;
@@ -520,6 +523,19 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
           tags.signal_base = j.relay_signal ? flags(j.dsts.front()) : 0;
           tags.slot = &relay_slot;
           add_rect(streams.back(), acc, s, dsts, r, hm.relay_chunk, mc0, j.src, j.src_is_dst_buffer, tags);
+          continue;
+        }
+        if (j.ce_wait) {
+          // wait for the transport copy that filled these leader bytes: the
+          // item's rect lies inside one copy (copies carry whole rects)
+          if (ce_slots == nullptr) throw rlplan::ValidationError("copy-engine star without its slot map");
+          const int64_t slot = ce_slots->slot_of(j.op->src, j.src, r.dst_off);
+          if (slot < 0) throw rlplan::ValidationError("fan-out rect not covered by a transport copy");
+          RelayTags tags;
+          tags.stage_base = accounting ? 4 : hm.ce_flags;  // every item of the rect waits on one slot
+          tags.stage_slot0 = slot;
+          tags.stage_chunk = int64_t{1} << 62;
+          add_rect(streams.back(), acc, s, *to, r, chunk_bytes, mc0, j.src, j.src_is_dst_buffer, tags);
           continue;
         }
         if (hm.stage_chunk > 0 && phase == 0 && hm.host[static_cast<size_t>(j.src)] != hm.me) {
@@ -682,6 +698,83 @@ std::vector<CeCopy> merge_pair(std::vector<CeCopy> flat, std::vector<CeCopy> str
 }
 
 }  // namespace
+
+std::vector<CeCopy> ce_copies_of(const std::vector<LoweredOp>& ops, const HostMap& hm, int g, int64_t max_pitch) {
+  HostMap h = hm;
+  h.me = g;
+  h.ce_remote = true;
+  h.ce_star = false;
+  h.relay_flags.clear();
+  h.mc.clear();
+  h.stage_chunk = 0;
+  return ce_transport_copies(build_jobs(ops, h, 0), h, max_pitch);
+}
+
+namespace {
+std::vector<int> host_ids(const HostMap& hm) {
+  std::vector<int> hosts(hm.host.begin(), hm.host.end());
+  hosts.push_back(hm.me);
+  std::sort(hosts.begin(), hosts.end());
+  hosts.erase(std::unique(hosts.begin(), hosts.end()), hosts.end());
+  return hosts;
+}
+
+bool copy_has(const CeCopy& c, int64_t off) {
+  int64_t rel = off - c.dst_off;
+  if (rel < 0) return false;
+  if (c.depth > 1) {
+    const int64_t z = rel / c.dst_slice;
+    if (z >= c.depth) return false;
+    rel -= z * c.dst_slice;
+  }
+  if (c.height > 1) {
+    const int64_t y = rel / c.dst_pitch;
+    if (y >= c.height) return false;
+    rel -= y * c.dst_pitch;
+  }
+  return rel < c.width;
+}
+}  // namespace
+
+CeSlotMap ce_slot_map(const std::vector<LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch) {
+  CeSlotMap m;
+  int64_t slot = 0;
+  for (int g : host_ids(hm)) {
+    if (g == h) continue;
+    for (const auto& c : ce_copies_of(ops, hm, g, max_pitch))
+      if (hm.host[static_cast<size_t>(c.dst)] == h) m.copies.push_back({c, slot++});
+  }
+  return m;
+}
+
+int64_t CeSlotMap::slot_of(DeviceId src, DeviceId dst, int64_t dst_off) const {
+  for (const auto& [c, slot] : copies)
+    if (c.src == src && c.dst == dst && copy_has(c, dst_off)) return slot;
+  return -1;
+}
+
+int64_t ce_star_slots(const std::vector<LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch) {
+  return static_cast<int64_t>(ce_slot_map(ops, hm, h, max_pitch).copies.size());
+}
+
+std::vector<int64_t> ce_send_slots(const std::vector<LoweredOp>& ops, const HostMap& hm,
+                                   const std::vector<CeCopy>& mine, int64_t max_pitch) {
+  std::map<int, int64_t> base;  // receiver -> slots taken by lower-id senders
+  for (int h : host_ids(hm)) {
+    if (h == hm.me) continue;
+    int64_t n = 0;
+    for (int g : host_ids(hm)) {
+      if (g == h) continue;
+      if (g == hm.me) break;
+      for (const auto& c : ce_copies_of(ops, hm, g, max_pitch))
+        if (hm.host[static_cast<size_t>(c.dst)] == h) ++n;
+    }
+    base[h] = n;
+  }
+  std::vector<int64_t> out;
+  for (const auto& c : mine) out.push_back(base[hm.host[static_cast<size_t>(c.dst)]]++);
+  return out;
+}
 
 std::vector<CeCopy> ce_transport_copies(const std::vector<Job>& jobs, const HostMap& hm, int64_t max_pitch) {
   std::map<std::pair<DeviceId, DeviceId>, std::pair<std::vector<CeCopy>, std::vector<CeCopy>>> pairs;

@@ -36,6 +36,9 @@ struct Job {
   bool relay_wait = false;
   bool relay_signal = false;
   int64_t relay_base = 0;
+  // Copy-engine star: an in-host fan-out in phase 0 whose items wait for the
+  // transport copy that filled the leader bytes they read.
+  bool ce_wait = false;
 };
 
 struct HostMap {
@@ -64,6 +67,12 @@ struct HostMap {
   // Copy-engine transport (push): every remote destination of a plain
   // phase-0 job is left out of the SM items; ce_transport_copies moves it.
   bool ce_remote = false;
+  // ... with per-copy flags (copy-engine star): each transport copy is
+  // flagged in the receiving host's array (ce_flag_slot), and a host's
+  // in-host fan-out runs inside phase 0, each item waiting for the copy that
+  // filled the leader bytes it reads. ce_flags = this host's array.
+  bool ce_star = false;
+  uint64_t ce_flags = 0;
 };
 
 // Staged gather: the remote sources host `h` reads, in arrival order. Round
@@ -130,6 +139,24 @@ struct CeCopy {
 // order each receives from one sender at a time.
 std::vector<CeCopy> ce_transport_copies(const std::vector<Job>& jobs, const HostMap& hm, int64_t max_pitch);
 
+// Copy-engine star slots: host h's flag array holds one slot per transport
+// copy it receives, senders in ascending host order, each sender's copies to
+// h in its issue order. ce_copies_of(ops, hm, g) = the copies host g issues.
+std::vector<CeCopy> ce_copies_of(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm, int g,
+                                 int64_t max_pitch);
+// Slots of host h's array (the incoming copies).
+int64_t ce_star_slots(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch);
+// Slot (in host `h`'s array) of the copy that carries byte `dst_off` of
+// destination `dst` from source `src`, or -1.
+struct CeSlotMap {
+  std::vector<std::pair<CeCopy, int64_t>> copies;  // incoming copies of h with their slots
+  int64_t slot_of(rlplan::DeviceId src, rlplan::DeviceId dst, int64_t dst_off) const;
+};
+CeSlotMap ce_slot_map(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch);
+// Slot of each of this host's outgoing copies (in the receiving host's array).
+std::vector<int64_t> ce_send_slots(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm,
+                                   const std::vector<CeCopy>& mine, int64_t max_pitch);
+
 // Byte extent [first, last) a rect writes in its destination shard.
 inline int64_t rect_dst_end(const rlplan::CopyRect& r) {
   return r.dst_off + (r.rows - 1) * r.dst_pitch + r.row_bytes;
@@ -153,6 +180,7 @@ struct ItemSet {
 // Resolve jobs of `phase` into items. src_bufs/dst_bufs are indexed by plan
 // device; nullptr tables mean "accounting only" (addresses left at offsets).
 ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, void* const* src_bufs,
-                    void* const* dst_bufs, int64_t chunk_bytes, const std::vector<CeRun>* ce = nullptr);
+                    void* const* dst_bufs, int64_t chunk_bytes, const std::vector<CeRun>* ce = nullptr,
+                    const CeSlotMap* ce_slots = nullptr);
 
 }  // namespace rr

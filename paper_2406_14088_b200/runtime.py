@@ -146,7 +146,8 @@ class Executor:
                  relay_flags: Optional[Dict[int, int]] = None, relay_chain: bool = True,
                  overlap_fanout: bool = False, ce_min_run_bytes: int = 0, stage_chunk_bytes: int = 0,
                  n_hosts: int = 0, stage_remote: Optional[Dict[Tuple[int, int], int]] = None,
-                 stage_flags: Optional[Dict[int, int]] = None, ce_transport: bool = False):
+                 stage_flags: Optional[Dict[int, int]] = None, ce_transport: bool = False,
+                 ce_flags: Optional[Dict[int, int]] = None):
         n = plan.cluster.device_count()
         self.plan = plan
         sp, dp = (ctypes.c_void_p * n)(), (ctypes.c_void_p * n)()
@@ -175,8 +176,13 @@ class Executor:
             sfl = (ctypes.c_void_p * n_hosts)()
             for h, p in (stage_flags or {}).items():
                 sfl[h] = p
+        cfl = None
+        if ce_flags:
+            cfl = (ctypes.c_void_p * n_hosts)()
+            for h, p in ce_flags.items():
+                cfl[h] = p
         opt = RrExecOptions(mode, chunk_bytes, hosts, mcs, rfl, int(relay_chain), int(overlap_fanout),
-                            ce_min_run_bytes, stage_chunk_bytes, n_hosts, srem, sfl, int(ce_transport))
+                            ce_min_run_bytes, stage_chunk_bytes, n_hosts, srem, sfl, int(ce_transport), cfl)
         h = ctypes.c_void_p()
         check(lib.rr_exec_create_ex(plan.handle, cuda_device, n, sp, dp, len(loc), arr, ctypes.byref(opt),
                                     ctypes.byref(h)))
@@ -421,16 +427,17 @@ def fanout_bytes(plan: ReallocPlan, host_of: Sequence[int]) -> Dict[int, int]:
     return out
 
 
-def ce_transport_estimate(plan: ReallocPlan, host_of: Sequence[int]) -> Tuple[float, float]:
-    """Predicted time (s) of a phase's remote traffic: (copy-engine
-    transport, SM peer stores), each the max over hosts of sending and
-    receiving at the measured rates (host only). The copy-engine side adds
-    the in-host fan-out as a separate HBM phase (the overlapped fan-out's
-    per-chunk flags ride on SM stores); the SM side assumes it overlapped."""
+def ce_transport_estimate(plan: ReallocPlan, host_of: Sequence[int], star: bool = False) -> Tuple[float, float]:
+    """Predicted time (s) of a phase: (copy-engine transport, SM peer stores
+    with the in-host fan-out overlapped), each the max over hosts of link
+    time (sending and receiving at the measured rates) and HBM time (host
+    only). Without `star` the copy-engine side runs the in-host fan-out as a
+    separate phase after it; with it (copy-engine star) the fan-out overlaps."""
     n = plan.cluster.device_count()
     hosts = sorted(set(host_of))
     recv = {h: 0 for h in hosts}
     ce_send = {h: 0.0 for h in hosts}
+    hbm = {h: 0.0 for h in hosts}
     sm = 0.0
     for h in hosts:
         local = [d for d in range(n) if host_of[d] == h]
@@ -439,12 +446,25 @@ def ce_transport_estimate(plan: ReallocPlan, host_of: Sequence[int]) -> Tuple[fl
             recv[host_of[c[1]]] += c[4] * c[5] * c[6]
         ce_send[h] = sum(c[4] * c[5] * c[6] for c in copies) / CE_LINK_GBS + len(copies) * CE_COPY_S
         w = plan.work(local, PUSH, host_of)
-        sm = max(sm, max(w["wire_in"], w["wire_out"]) / SM_LINK_GBS)
+        # bytes this GPU's HBM reads and writes: local reads, stores landing
+        # here (local and incoming), the fan-out's reads and writes
+        hbm[h] = (w["read"] + w["written"] - w["wire_out"] + w["wire_in"] + w["fanout_read"] +
+                  w["fanout_written"]) / HBM_COPY_GBS
+        sm = max(sm, max(w["wire_in"], w["wire_out"]) / SM_LINK_GBS, hbm[h])
     fan = fanout_bytes(plan, host_of)
-    ce = max(max(ce_send[h], recv[h] / CE_LINK_GBS) for h in hosts)
-    if any(fan.values()):
+    ce = max(max(ce_send[h], recv[h] / CE_LINK_GBS, hbm[h]) for h in hosts)
+    if any(fan.values()) and not star:
         ce += max(2 * fan[h] for h in hosts) / HBM_COPY_GBS + PHASE_OVERHEAD_S
     return ce, sm
+
+
+def ce_slots(plan: ReallocPlan, host_of: Sequence[int]) -> int:
+    """Length of the copy flag array every host allocates (copy-engine star)."""
+    n = plan.cluster.device_count()
+    hosts = (ctypes.c_int32 * n)(*host_of)
+    out = ctypes.c_int64()
+    check(lib.rr_plan_ce_slots(plan.handle, hosts, ctypes.byref(out)))
+    return out.value
 
 
 def stage_slots(plan: ReallocPlan, host_of: Sequence[int], chunk_bytes: int) -> int:
@@ -717,12 +737,14 @@ class RankRealloc:
         # traffic; "auto" = where the measured rates predict >= 5% less time
         # than SM peer stores (ce_transport_estimate charges the copy-engine
         # side a separate in-host fan-out phase).
+        # With overlap, the fan-out rides on per-copy flags (copy-engine star).
         if sw["ce_transport"]:
+            star = bool(sw["overlap"]) and any(fanout_bytes(p, self.host_of).values())
             if sw["ce_transport"] != "auto":
-                return Scheme(ce_transport=True)
-            est = self.ce_estimates[pi] = ce_transport_estimate(p, self.host_of)
+                return Scheme(overlap=star, ce_transport=True)
+            est = self.ce_estimates[pi] = ce_transport_estimate(p, self.host_of, star)
             if est[0] < 0.95 * est[1]:
-                return Scheme(ce_transport=True)
+                return Scheme(overlap=star, ce_transport=True)
         return Scheme(overlap=bool(sw["overlap"]))
 
     def _candidates(self, pi: int, sw: dict) -> List[Scheme]:
@@ -738,6 +760,8 @@ class RankRealloc:
             out.append(Scheme(staged=True))
         if sw["ce_transport"]:
             out.append(Scheme(ce_transport=True))
+            if sw["overlap"] and any(fanout_bytes(p, self.host_of).values()):
+                out.append(Scheme(overlap=True, ce_transport=True))
         uniq: List[Scheme] = []
         for sc in out:
             if sc not in uniq:
@@ -871,9 +895,15 @@ class RankRealloc:
         p = self.plans[pi]
         sname, dname = self.bind[pi]
         mine: dict = {}
-        relay_buf = stage_flag = None
+        relay_buf = stage_flag = ce_flag = None
         stage_bufs: Dict[int, DeviceBuffer] = {}
-        if sc.relay or sc.overlap:
+        star = sc.ce_transport and sc.overlap  # copy-engine star: per-copy flags, no relay array
+        if star:
+            ce_flag = DeviceBuffer(self.cuda_device, 4 * max(ce_slots(p, self.host_of), 64))
+            ce_flag.zero()
+            b.owned.append(ce_flag)
+            mine["cflag"] = {rank: ce_flag.ipc_handle()} if world > 1 else {}
+        elif sc.relay or sc.overlap:
             slots = relay_slots(p, self.host_of, self.chunk_bytes, chain=sc.relay, overlap=sc.overlap)
             if slots:
                 relay_buf = DeviceBuffer(self.cuda_device, 4 * max(slots, 64))
@@ -893,6 +923,7 @@ class RankRealloc:
         stream_sync()
         gathered = self._exchange(mine) if (sc.relay or sc.overlap or sc.staged) else [mine] * world
         relay_remote: Dict[int, int] = {}
+        ce_flags: Dict[int, int] = {rank: ce_flag.ptr} if ce_flag else {}
         stage_remote: Dict[Tuple[int, int], int] = {}
         stage_flags: Dict[int, int] = {rank: stage_flag.ptr} if stage_flag else {}
         for r, table in enumerate(gathered):
@@ -906,6 +937,8 @@ class RankRealloc:
                     b.opened.append(ptr)
                     if key == "relay":
                         relay_remote[r] = ptr
+                    elif key == "cflag":
+                        ce_flags[r] = ptr
                     elif key == "stage":
                         stage_remote[(d, r)] = ptr
                     else:
@@ -926,8 +959,9 @@ class RankRealloc:
             ex = Executor(p, self.cuda_device, self.ptrs[sname], self.ptrs[dname], self.local, self.mode,
                           self.chunk_bytes, host_of=self.host_of if self.hierarchical else None,
                           mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_table, relay_chain=sc.relay,
-                          overlap_fanout=sc.overlap, ce_min_run_bytes=self.ce_min_run_bytes,
-                          ce_transport=sc.ce_transport)
+                          overlap_fanout=sc.overlap and not star, ce_min_run_bytes=self.ce_min_run_bytes,
+                          ce_transport=sc.ce_transport, n_hosts=world if star else 0,
+                          ce_flags=ce_flags if star else None)
         if self.kernel is not None:
             ex.set_kernel(self.kernel)
         ex.set_flag_kernel(self.flag_kernel)

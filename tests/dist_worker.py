@@ -183,10 +183,15 @@ class Worker:
         merged across layers, in rotation rounds, plain and onloaded, with the
         fan-out phase after it where a host holds several destinations."""
         m = dataclasses.replace(TINY_GQA, num_layers=6)
-        for sp, dp in CASES + [((1, 1, 8, 0, 0), (1, 8, 1, 0, 0))]:
-            for hier in (True,):
-                self.run(f"ce-transport {sp}->{dp} (+onload)", m, pl(sp), pl(dp), SPECIAL | 83, reps=3,
-                         onload_chunk=32 << 10, hierarchical=hier, ce_transport=True)
+        for sp, dp in CASES:
+            for star in (False, True):  # star: fan-out inside phase 0 on per-copy flags
+                for kernel in ((1, 0) if star else (1,)):
+                    self.run(f"ce-transport {sp}->{dp} star={star} kernel={kernel} (+onload)", m, pl(sp), pl(dp),
+                             SPECIAL | 83, reps=3, onload_chunk=32 << 10, ce_transport=True, overlap=star,
+                             kernel=kernel, flag_kernel=kernel)
+        # replicate (one source, fan-out on every GPU)
+        self.run("ce-transport replicate star=True", m, REPLICATE[0], REPLICATE[1], SPECIAL | 84, reps=2,
+                 ce_transport=True, overlap=True)
 
     def probe(self):
         """Bind-time probe: every scheme the switches allow is timed on the real
