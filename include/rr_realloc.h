@@ -324,13 +324,17 @@ typedef struct {
    * jobs (they stay on SM stores); copy-engine runs are not used with it.
    * 0 = off. */
   int32_t ce_transport;
-  /* Copy-engine star (with ce_transport; host ids 0..n_hosts-1): ce_flags[h]
-   * = host h's copy flag array (rr_plan_ce_slots uint32, mapped here; zero
-   * at create, one executor per array). Each transport copy is followed on
-   * the copy stream by a cuStreamWriteValue32 of the launch epoch into its
-   * slot on the receiving host, and a host's in-host fan-out runs inside
-   * phase 0: each fan-out item waits for the copy that filled the leader
-   * bytes it reads (no separate fan-out phase). NULL = fan-out in phase 1. */
+  /* Copy flags (with ce_transport; host ids 0..n_hosts-1): ce_flags[h] =
+   * host h's copy flag array (rr_plan_ce_slots uint32, mapped here; zero at
+   * create, one executor per array). With them the transport copies follow
+   * a global schedule (no receiver takes two senders at once): a transfer
+   * waits on this host's array (cuStreamWaitValue32) for the previous
+   * transfer into its receiver, whose sender raises it after its last copy
+   * (cuStreamWriteValue32). With overlap_fanout also set (copy-engine star),
+   * every copy raises a slot on the receiving host and that host's in-host
+   * fan-out runs inside phase 0, each item waiting for the copy that filled
+   * the leader bytes it reads. NULL = rotation order only, fan-out in
+   * phase 1. */
   void* const* ce_flags;
 } rr_exec_options;
 /* Length of the relay flag array for this host map, chunk size and scheme
@@ -352,9 +356,14 @@ rr_status rr_plan_ce_runs(const rr_plan* plan, int n_local, const int32_t* local
  * queries *n. */
 rr_status rr_plan_ce_copies(const rr_plan* plan, int n_local, const int32_t* local, const int32_t* host_of,
                             int64_t* out11, int cap, int* n);
-/* Copy-engine star: length of the copy flag array every host allocates (the
- * maximum over hosts of the transport copies it receives). */
+/* Copy flags: length of the copy flag array every host allocates (maximum
+ * over hosts of its incoming copy slots plus its schedule waits). */
 rr_status rr_plan_ce_slots(const rr_plan* plan, const int32_t* host_of, int64_t* slots);
+/* The copy-engine schedule of every host (host only): 6 doubles per
+ * transfer {sender host, receiver host, simulated start s, end s, waits for
+ * another sender (0/1), bytes}, each sender's transfers in issue order;
+ * out6 = NULL queries *n. */
+rr_status rr_plan_ce_schedule(const rr_plan* plan, const int32_t* host_of, double* out6, int cap, int* n);
 /* Staged-gather pieces this executor pushes per launch, and their bytes. */
 rr_status rr_exec_stage_pushes(const rr_exec* ex, int* n_pushes, int64_t* bytes);
 /* Copy-engine submissions phase 0 issues (copy-engine runs, see

@@ -73,6 +73,7 @@ _SIGNATURES = {
     "rr_plan_ce_runs": (c_int, [_P, c_int, POINTER(c_int32), POINTER(c_int32), c_int64, POINTER(c_int64), c_int,
                                 POINTER(c_int)]),
     "rr_plan_ce_slots": (c_int, [_P, POINTER(c_int32), POINTER(c_int64)]),
+    "rr_plan_ce_schedule": (c_int, [_P, POINTER(c_int32), POINTER(c_double), c_int, POINTER(c_int)]),
     "rr_plan_ce_copies": (c_int, [_P, c_int, POINTER(c_int32), POINTER(c_int32), POINTER(c_int64), c_int,
                                   POINTER(c_int)]),
     "rr_mcast_supported": (c_int, [c_int, POINTER(c_int)]),

@@ -50,6 +50,28 @@ WriteValue32Fn write_value32() {
   return fn;
 }
 
+using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+// Copy-engine schedule: the copy stream itself waits until a flag reaches
+// the launch epoch (cuStreamWaitValue32, GEQ: (int32)(*flag - epoch) >= 0),
+// without an SM.
+void wait_piece(cudaStream_t stream, const uint32_t* flag, uint32_t epoch) {
+  static const WaitValue32Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<WaitValue32Fn>(nullptr);
+    }
+    return reinterpret_cast<WaitValue32Fn>(p);
+  }();
+  if (fn == nullptr) rr::capi::raise(RR_EUNSUPPORTED, "cuStreamWaitValue32 unavailable (copy-engine schedule)");
+  const CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), epoch,
+                        CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) rr::capi::raise(RR_ECUDA, "cuStreamWaitValue32 (copy-engine schedule) failed: " + std::to_string(r));
+}
+
 void signal_piece(cudaStream_t stream, uint32_t* flag, uint32_t epoch) {
   const WriteValue32Fn fn = write_value32();
   if (fn == nullptr) rr::capi::raise(RR_EUNSUPPORTED, "cuStreamWriteValue32 unavailable (staged gather)");
@@ -120,6 +142,8 @@ struct rr_exec {
     DeviceId src_dev;  // source plan device and byte offsets in its shard (onload pipelining)
     int64_t src_off, src_end;
     uint32_t* flag = nullptr;  // copy-engine star: flagged on the receiving host after the copy
+    uint32_t* wait = nullptr;  // schedule: wait (>= epoch) before the copy, on this host's array
+    uint32_t* done = nullptr;  // schedule: raised after the copy (the next sender into its receiver)
     int64_t bytes() const { return width * height * depth; }
   };
   std::vector<CeCopy> ce;
@@ -336,8 +360,10 @@ void ce_issue(rr_exec* ex, cudaStream_t after, cudaEvent_t after_event = nullptr
   }
   check_cuda(cudaStreamWaitEvent(ex->ce_stream, after_event, 0), "cudaStreamWaitEvent(ce fork)");
   for (const auto& c : ex->ce) {
+    if (c.wait) wait_piece(ex->ce_stream, c.wait, ex->epoch);
     issue_copy(c, ex->ce_stream);
     if (c.flag) signal_piece(ex->ce_stream, c.flag, ex->epoch);
+    if (c.done) signal_piece(ex->ce_stream, c.done, ex->epoch);
   }
   for (const auto& p : ex->stage) {
     check_cuda(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "staged push");
@@ -463,9 +489,33 @@ rr_status rr_plan_ce_slots(const rr_plan* plan, const int32_t* host_of, int64_t*
     int64_t best = 0;
     for (int h : hosts) {
       hm.me = h;
-      best = std::max(best, rr::ce_star_slots(plan->lowered, hm, h, (int64_t{1} << 31) - 1));
+      best = std::max(best, rr::ce_flag_slots(plan->lowered, hm, h, (int64_t{1} << 31) - 1));
     }
     *slots = best;
+  });
+}
+
+rr_status rr_plan_ce_schedule(const rr_plan* plan, const int32_t* host_of, double* out6, int cap, int* n) {
+  return guarded([&] {
+    need(plan != nullptr && host_of != nullptr && n != nullptr, "null plan/host table/output");
+    rr::HostMap hm;
+    for (int d = 0; d < plan->cluster.device_count(); ++d) hm.host.push_back(host_of[d]);
+    hm.me = hm.host.front();
+    const int64_t mp = (int64_t{1} << 31) - 1;
+    const auto sched = rr::ce_schedule(plan->lowered, hm, mp);
+    *n = static_cast<int>(sched.size());
+    if (out6 == nullptr) return;
+    need(cap >= *n, "output table too small");
+    std::map<int, std::vector<rr::CeCopy>> copies;
+    for (size_t i = 0; i < sched.size(); ++i) {
+      const auto& t = sched[i];
+      if (!copies.count(t.sender)) copies[t.sender] = rr::ce_copies_of(plan->lowered, hm, t.sender, mp);
+      int64_t bytes = 0;
+      for (size_t k = t.first; k < t.first + t.count; ++k) bytes += copies[t.sender][k].bytes();
+      const double v[6] = {static_cast<double>(t.sender), static_cast<double>(t.receiver), t.start, t.end,
+                           t.wait_slot >= 0 ? 1.0 : 0.0, static_cast<double>(bytes)};
+      std::copy(v, v + 6, out6 + 6 * i);
+    }
   });
 }
 
@@ -538,13 +588,15 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       need(mode == 0, "copy-engine transport is a push-mode path");
       need(!staged && options->mc_bufs == nullptr, "copy-engine transport excludes the staged gather and multicast");
       hm.ce_remote = true;
+      need(options->relay_flags == nullptr, "copy-engine transport excludes relay flags");
       if (options->ce_flags) {
-        need(options->host_of != nullptr && options->n_hosts > 0, "copy-engine star needs host_of and n_hosts");
-        need(options->relay_flags == nullptr, "copy-engine star excludes relay / overlap flags");
+        need(options->host_of != nullptr && options->n_hosts > 0, "copy flags need host_of and n_hosts");
         for (size_t d = 0; d < hm.host.size(); ++d)
           need(hm.host[d] >= 0 && hm.host[d] < options->n_hosts, "host ids must lie in 0..n_hosts-1");
-        hm.ce_star = true;
         hm.ce_flags = reinterpret_cast<uint64_t>(options->ce_flags[hm.me]);
+        hm.ce_star = options->overlap_fanout != 0;  // fan-out on per-copy flags inside phase 0
+      } else {
+        need(options->overlap_fanout == 0, "the copy-engine star (overlap_fanout) needs ce_flags");
       }
     }
     check_cuda(cudaSetDevice(cuda_device), "cudaSetDevice");
@@ -557,6 +609,7 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
                                                                            : std::vector<rr::CeRun>{};
     std::vector<rr::CeCopy> transport;
     std::vector<int64_t> send_slots;
+    std::vector<rr::CeTransfer> schedule;  // this host's transfers, issue order (with ce_flags)
     rr::CeSlotMap slot_map;
     int64_t n_ce_slots = 0;
     if (hm.ce_remote) {
@@ -566,7 +619,11 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       if (hm.ce_star) {
         send_slots = rr::ce_send_slots(plan->lowered, hm, transport, mp);
         slot_map = rr::ce_slot_map(plan->lowered, hm, hm.me, mp);
-        n_ce_slots = static_cast<int64_t>(slot_map.copies.size());
+      }
+      if (options->ce_flags) {
+        for (const auto& t : rr::ce_schedule(plan->lowered, hm, mp))
+          if (t.sender == hm.me) schedule.push_back(t);
+        n_ce_slots = rr::ce_flag_slots(plan->lowered, hm, hm.me, mp);
         need(n_ce_slots == 0 || hm.ce_flags != 0, "missing this host's copy flag array");
       }
     }
@@ -589,7 +646,7 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       require_zero_flags(options->relay_flags[local[0]], n_relay, "relay_flags");
     }
     if (staged) require_zero_flags(options->stage_flags[hm.me], n_stage_slots, "stage_flags");
-    if (hm.ce_star) require_zero_flags(options->ce_flags[hm.me], n_ce_slots, "ce_flags");
+    if (hm.ce_remote && options->ce_flags) require_zero_flags(options->ce_flags[hm.me], n_ce_slots, "ce_flags");
 
     auto ex = std::make_unique<rr_exec>();
     ex->cuda_device = cuda_device;
@@ -609,19 +666,37 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
                         u.src, u.src_off, u.src_off + u.bytes});
       ex->ce_bytes += u.bytes;
     }
-    for (size_t k = 0; k < transport.size(); ++k) {
+    auto host_flags = [&](int h) {
+      auto* arr = static_cast<uint32_t*>(options->ce_flags[h]);
+      need(arr != nullptr, "missing a host's copy flag array");
+      return arr;
+    };
+    auto push_copy = [&](size_t k, uint32_t* wait, uint32_t* done) {
       const auto& c = transport[k];
       need(dst_bufs[c.dst] != nullptr && src_bufs[c.src] != nullptr, "missing a copy-engine transport buffer");
-      uint32_t* flag = nullptr;
-      if (hm.ce_star) {
-        auto* arr = static_cast<uint32_t*>(options->ce_flags[hm.host[static_cast<size_t>(c.dst)]]);
-        need(arr != nullptr, "missing a receiver's copy flag array");
-        flag = arr + send_slots[k];
-      }
+      uint32_t* flag = hm.ce_star ? host_flags(hm.host[static_cast<size_t>(c.dst)]) + send_slots[k] : nullptr;
       ex->ce.push_back({static_cast<char*>(dst_bufs[c.dst]) + c.dst_off,
                         static_cast<const char*>(src_bufs[c.src]) + c.src_off, c.width, c.height, c.depth,
-                        c.src_pitch, c.dst_pitch, c.src_slice, c.dst_slice, c.src, c.src_off, c.src_end(), flag});
+                        c.src_pitch, c.dst_pitch, c.src_slice, c.dst_slice, c.src, c.src_off, c.src_end(), flag,
+                        wait, done});
       ex->ce_bytes += c.bytes();
+    };
+    if (!schedule.empty()) {
+      // scheduled issue order: each transfer waits for the previous one into
+      // its receiver (if another host sent it) and releases the next
+      size_t issued = 0;
+      for (const auto& t : schedule) {
+        for (size_t k = t.first; k < t.first + t.count; ++k) {
+          uint32_t* wait = (k == t.first && t.wait_slot >= 0) ? host_flags(hm.me) + t.wait_slot : nullptr;
+          uint32_t* done = (k + 1 == t.first + t.count && t.signal_host >= 0)
+                               ? host_flags(t.signal_host) + t.signal_slot : nullptr;
+          push_copy(k, wait, done);
+          ++issued;
+        }
+      }
+      need(issued == transport.size(), "copy-engine schedule does not cover every transport copy");
+    } else {
+      for (size_t k = 0; k < transport.size(); ++k) push_copy(k, nullptr, nullptr);
     }
     if (staged) {
       ex->stage_ctas = sms;
@@ -978,10 +1053,14 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
         p.width = b - a;
         issue_copy(p, ex->ce_stream);
       };
+      // (schedule waits are skipped here: copies follow the onload's chunk
+      // order, not the schedule's, so a wait could point ahead in this
+      // stream; the done flags are still raised, no one waits on them)
       for (const auto& c : ex->ce)
         if (!onloaded(c.src_dev)) {
           issue_copy(c, ex->ce_stream);
           if (c.flag) signal_piece(ex->ce_stream, c.flag, ex->epoch);
+          if (c.done) signal_piece(ex->ce_stream, c.done, ex->epoch);
         }
       for (size_t k = 0; k < ex->chunks.size(); ++k) {
         const auto& ch = ex->chunks[k];
@@ -999,7 +1078,10 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
           else
             issue_copy(c, ex->ce_stream);
           // flagged once the copy's last source byte is in (its last piece)
-          if (c.flag && c.src_end > lo && c.src_end <= hi) signal_piece(ex->ce_stream, c.flag, ex->epoch);
+          if (c.src_end > lo && c.src_end <= hi) {
+            if (c.flag) signal_piece(ex->ce_stream, c.flag, ex->epoch);
+            if (c.done) signal_piece(ex->ce_stream, c.done, ex->epoch);
+          }
         }
       }
     }

@@ -821,4 +821,128 @@ std::vector<CeCopy> ce_transport_copies(const std::vector<Job>& jobs, const Host
   return out;
 }
 
+std::vector<CeTransfer> ce_schedule(const std::vector<LoweredOp>& ops, const HostMap& hm, int64_t max_pitch) {
+  constexpr double kRate = 775e9;                   // copy-engine payload rate per GPU, pairwise (r02 probes)
+  constexpr double kCopy = 4e-6, kCopy2d = 10e-6;  // per submission (2D copies cost more)
+  const std::vector<int> hosts = host_ids(hm);
+  const int H = static_cast<int>(hosts.size());
+  std::map<int, int> pos;
+  for (int i = 0; i < H; ++i) pos[hosts[static_cast<size_t>(i)]] = i;
+  std::map<int, std::vector<CeCopy>> copies;
+  std::map<int, int64_t> base;  // first schedule slot of each host
+  for (int g : hosts) copies[g] = ce_copies_of(ops, hm, g, max_pitch);
+  for (int h : hosts) {
+    int64_t incoming = 0;
+    for (int g : hosts)
+      if (g != h)
+        for (const auto& c : copies[g]) incoming += hm.host[static_cast<size_t>(c.dst)] == h;
+    base[h] = incoming;
+  }
+  // Transfers: each sender's copies to one receiver (its rotation round
+  // r = receiver position - sender position, mod H; ce_transport_copies
+  // already issues them in round order).
+  std::vector<CeTransfer> all;
+  std::vector<int> round;
+  std::vector<double> dur;
+  for (int g : hosts) {
+    const auto& cs = copies[g];
+    for (size_t k = 0; k < cs.size();) {
+      CeTransfer t;
+      t.sender = g;
+      t.receiver = hm.host[static_cast<size_t>(cs[k].dst)];
+      t.first = k;
+      double d = 0;
+      while (k < cs.size() && hm.host[static_cast<size_t>(cs[k].dst)] == t.receiver) {
+        d += static_cast<double>(cs[k].bytes()) / kRate + (cs[k].height > 1 && cs[k].depth == 1 ? kCopy2d : kCopy);
+        ++k;
+      }
+      t.count = k - t.first;
+      all.push_back(t);
+      round.push_back((pos[t.receiver] - pos[g] + H) % H);
+      dur.push_back(d);
+    }
+  }
+  // Candidate orders, simulated at the measured rates (a transfer starts
+  // when its sender is free and its receiver has finished the transfer
+  // before it in that receiver's order); the shortest makespan wins:
+  //   rounds: every sender in rotation order, each receiver served in round
+  //           order (the rounds stay aligned without a barrier: all-to-all);
+  //   greedy: list schedule, next the transfer that can start first (ties:
+  //           the sender with the most work left) — sparse patterns where
+  //           rotation rounds leave receivers idle (70B at 8 GPUs).
+  const size_t T = all.size();
+  std::map<int, double> load;
+  for (size_t i = 0; i < T; ++i) load[all[i].sender] += dur[i];
+  struct Sim {
+    std::vector<double> start, end;
+    std::vector<size_t> order;  // issue order (ascending start)
+    double makespan = 0;
+  };
+  auto run = [&](bool rounds) {
+    Sim sim;
+    sim.start.assign(T, 0);
+    sim.end.assign(T, 0);
+    std::map<int, double> free_s, free_r, left = load;
+    std::vector<bool> done(T, false);
+    for (size_t n = 0; n < T; ++n) {
+      size_t best = T;
+      double bs = 0;
+      for (size_t i = 0; i < T; ++i) {
+        if (done[i]) continue;
+        if (rounds) {  // strictly by round, then sender: the receiver order is the round order
+          if (best == T || round[i] < round[best] || (round[i] == round[best] && all[i].sender < all[best].sender))
+            best = i;
+          continue;
+        }
+        const double st = std::max(free_s[all[i].sender], free_r[all[i].receiver]);
+        if (best == T || st < bs - 1e-9 ||
+            (st < bs + 1e-9 && left[all[i].sender] > left[all[best].sender] + 1e-12)) {
+          best = i;
+          bs = st;
+        }
+      }
+      const CeTransfer& t = all[best];
+      sim.start[best] = std::max(free_s[t.sender], free_r[t.receiver]);
+      sim.end[best] = sim.start[best] + dur[best];
+      free_s[t.sender] = free_r[t.receiver] = sim.end[best];
+      left[t.sender] -= dur[best];
+      done[best] = true;
+      sim.order.push_back(best);
+      sim.makespan = std::max(sim.makespan, sim.end[best]);
+    }
+    return sim;
+  };
+  const Sim a = run(true), g = run(false);
+  const Sim& pick = g.makespan < a.makespan * 0.99 ? g : a;
+  // Receiver chains in the chosen order: each transfer into a host waits for
+  // the one before it (unless the same sender: stream order); every wait
+  // points to an earlier-issued transfer, so no cycles.
+  std::map<int, int64_t> waits;  // sender -> slots handed out
+  std::map<int, size_t> last_into;
+  for (size_t i : pick.order) {
+    CeTransfer& t = all[i];
+    t.start = pick.start[i];
+    t.end = pick.end[i];
+    const auto prev = last_into.find(t.receiver);
+    if (prev != last_into.end() && all[prev->second].sender != t.sender) {
+      t.wait_slot = base[t.sender] + waits[t.sender]++;
+      all[prev->second].signal_host = t.sender;
+      all[prev->second].signal_slot = t.wait_slot;
+    }
+    last_into[t.receiver] = i;
+  }
+  // each sender issues its transfers in the chosen order
+  std::vector<CeTransfer> out;
+  for (size_t i : pick.order) out.push_back(all[i]);
+  std::stable_sort(out.begin(), out.end(), [](const CeTransfer& a, const CeTransfer& b) { return a.sender < b.sender; });
+  return out;
+}
+
+int64_t ce_flag_slots(const std::vector<LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch) {
+  int64_t n = ce_star_slots(ops, hm, h, max_pitch);
+  for (const auto& t : ce_schedule(ops, hm, max_pitch))
+    if (t.sender == h && t.wait_slot >= 0) n = std::max(n, t.wait_slot + 1);
+  return n;
+}
+
 }  // namespace rr

@@ -157,6 +157,30 @@ CeSlotMap ce_slot_map(const std::vector<rlplan::LoweredOp>& ops, const HostMap& 
 std::vector<int64_t> ce_send_slots(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm,
                                    const std::vector<CeCopy>& mine, int64_t max_pitch);
 
+// Copy-engine schedule. Every host's transport copies form transfers (one
+// per receiving host); a global list schedule (each transfer starts when
+// both its sender and its receiver are free, at the measured rates) orders
+// them so that no receiver takes two senders at once — with rotation rounds
+// alone, a sender whose round is empty runs ahead into a busy receiver (70B
+// at 4 GPUs: 524 vs 745 GB/s). Each transfer waits (cuStreamWaitValue32 on
+// its sender's array) for the previous transfer into the same receiver when
+// that one has another sender, which raises the flag after its last copy.
+// Waits only point to transfers that start earlier: no cycles.
+struct CeTransfer {
+  int sender = 0, receiver = 0;
+  size_t first = 0, count = 0;  // copies [first, first + count) of the sender's ce_transport_copies list
+  double start = 0, end = 0;    // simulated seconds
+  int64_t wait_slot = -1;       // in the sender's flag array (-1 = no wait)
+  int signal_host = -1;         // after the last copy: raise signal_slot in this host's array
+  int64_t signal_slot = -1;
+};
+// All hosts' transfers, each host's in issue order (ascending start). The
+// schedule's slots of host h follow its ce_star_slots incoming-copy slots.
+std::vector<CeTransfer> ce_schedule(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm,
+                                    int64_t max_pitch);
+// Length of host h's copy flag array: incoming copy slots + schedule waits.
+int64_t ce_flag_slots(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch);
+
 // Byte extent [first, last) a rect writes in its destination shard.
 inline int64_t rect_dst_end(const rlplan::CopyRect& r) {
   return r.dst_off + (r.rows - 1) * r.dst_pitch + r.row_bytes;

@@ -398,6 +398,19 @@ class ReallocPlan:
         check(lib.rr_plan_ce_copies(self._h, len(local), arr, hosts, out, cnt.value, ctypes.byref(cnt)))
         return [tuple(out[11 * i:11 * i + 11]) for i in range(cnt.value)]
 
+    def ce_schedule(self, host_of: Sequence[int]) -> List[Tuple[int, int, float, float, bool, int]]:
+        """The copy-engine transport schedule of every host (host only):
+        (sender, receiver, simulated start s, end s, waits for another sender,
+        bytes), each sender's transfers in issue order."""
+        n = self.cluster.device_count()
+        hosts = (ctypes.c_int32 * n)(*host_of)
+        cnt = ctypes.c_int()
+        check(lib.rr_plan_ce_schedule(self._h, hosts, None, 0, ctypes.byref(cnt)))
+        out = (ctypes.c_double * (6 * max(1, cnt.value)))()
+        check(lib.rr_plan_ce_schedule(self._h, hosts, out, cnt.value, ctypes.byref(cnt)))
+        return [(int(out[6 * i]), int(out[6 * i + 1]), out[6 * i + 2], out[6 * i + 3], bool(out[6 * i + 4]),
+                 int(out[6 * i + 5])) for i in range(cnt.value)]
+
     def devices(self, side: int) -> List[int]:
         p = self.src if side == 0 else self.dst
         return p.mesh.devices(self.cluster)

@@ -452,7 +452,11 @@ def ce_transport_estimate(plan: ReallocPlan, host_of: Sequence[int], star: bool 
                   w["fanout_written"]) / HBM_COPY_GBS
         sm = max(sm, max(w["wire_in"], w["wire_out"]) / SM_LINK_GBS, hbm[h])
     fan = fanout_bytes(plan, host_of)
-    ce = max(max(ce_send[h], recv[h] / CE_LINK_GBS, hbm[h]) for h in hosts)
+    # the copy engines follow the library's schedule (receiver chains): its
+    # simulated makespan, not just each host's bytes, bounds the link time
+    sched = plan.ce_schedule(host_of)
+    makespan = max((t[3] for t in sched), default=0.0)
+    ce = max(max(ce_send[h], recv[h] / CE_LINK_GBS, hbm[h], makespan) for h in hosts)
     if any(fan.values()) and not star:
         ce += max(2 * fan[h] for h in hosts) / HBM_COPY_GBS + PHASE_OVERHEAD_S
     return ce, sm
@@ -898,7 +902,7 @@ class RankRealloc:
         relay_buf = stage_flag = ce_flag = None
         stage_bufs: Dict[int, DeviceBuffer] = {}
         star = sc.ce_transport and sc.overlap  # copy-engine star: per-copy flags, no relay array
-        if star:
+        if sc.ce_transport and world > 1:  # schedule (and star) flags
             ce_flag = DeviceBuffer(self.cuda_device, 4 * max(ce_slots(p, self.host_of), 64))
             ce_flag.zero()
             b.owned.append(ce_flag)
@@ -921,7 +925,7 @@ class RankRealloc:
             mine["stage"] = {s: x.ipc_handle() for s, x in stage_bufs.items()}
             mine["sflag"] = {rank: stage_flag.ipc_handle()}
         stream_sync()
-        gathered = self._exchange(mine) if (sc.relay or sc.overlap or sc.staged) else [mine] * world
+        gathered = self._exchange(mine) if (sc.relay or sc.overlap or sc.staged or sc.ce_transport) else [mine] * world
         relay_remote: Dict[int, int] = {}
         ce_flags: Dict[int, int] = {rank: ce_flag.ptr} if ce_flag else {}
         stage_remote: Dict[Tuple[int, int], int] = {}
@@ -959,9 +963,9 @@ class RankRealloc:
             ex = Executor(p, self.cuda_device, self.ptrs[sname], self.ptrs[dname], self.local, self.mode,
                           self.chunk_bytes, host_of=self.host_of if self.hierarchical else None,
                           mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_table, relay_chain=sc.relay,
-                          overlap_fanout=sc.overlap and not star, ce_min_run_bytes=self.ce_min_run_bytes,
-                          ce_transport=sc.ce_transport, n_hosts=world if star else 0,
-                          ce_flags=ce_flags if star else None)
+                          overlap_fanout=sc.overlap, ce_min_run_bytes=self.ce_min_run_bytes,
+                          ce_transport=sc.ce_transport, n_hosts=world if ce_flag else 0,
+                          ce_flags=ce_flags if ce_flag else None)
         if self.kernel is not None:
             ex.set_kernel(self.kernel)
         ex.set_flag_kernel(self.flag_kernel)

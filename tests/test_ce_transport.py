@@ -119,3 +119,33 @@ def test_transport_copy_counts_at_full_size():
     total = sum(x[4] * x[5] * x[6] for x in cs)
     assert total == plan.work([0, 1, 2, 3], 0, host_of)["wire_out"]
     assert len(cs) <= 100 * len(pairs), (len(cs), len(pairs))
+
+
+@pytest.mark.parametrize("name", ["llama70b_pp2tp4_to_tp8", "llama34b_critic_pp4tp2_to_tp8",
+                                  "llama13b_pp2tp4_to_dp2tp4", "llama7b_tp8_dp8_roundtrip"])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_schedule_serves_one_sender_at_a_time(name, world):
+    """The copy-engine schedule (receiver chains): no receiver overlaps two
+    incoming transfers, every sender's transfers are sequential, every copy
+    of every host is scheduled, and the makespan is within 10% of the bound
+    max(busiest sender, busiest receiver) at the measured rate."""
+    from paper_2406_14088_b200.workloads import WORKLOADS
+    plan = WORKLOADS[name].plans(BALANCED)[0]
+    host_of = [d * world // 8 for d in range(8)]
+    sched = plan.ce_schedule(host_of)
+    for key in (0, 1):  # per sender, per receiver: intervals disjoint
+        by = {}
+        for t in sched:
+            by.setdefault(t[key], []).append((t[2], t[3]))
+        for iv in by.values():
+            iv.sort()
+            assert all(a[1] <= b[0] + 1e-9 for a, b in zip(iv, iv[1:])), iv
+    sent = sum(t[5] for t in sched)
+    assert sent == sum(c[4] * c[5] * c[6] for h in range(world)
+                       for c in plan.ce_copies([d for d in range(8) if host_of[d] == h], host_of))
+    send, recv = {}, {}
+    for t in sched:
+        send[t[0]] = send.get(t[0], 0) + t[5]
+        recv[t[1]] = recv.get(t[1], 0) + t[5]
+    bound = max(max(send.values()), max(recv.values())) / 775e9
+    assert max(t[3] for t in sched) <= 1.1 * bound + 1e-3
