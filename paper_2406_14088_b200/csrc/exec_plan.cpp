@@ -592,6 +592,18 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
         return a->it.wait_flag < b->it.wait_flag;  // 0 (no wait) first
       });
     }
+  } else if (ce_slots != nullptr && !ce_slots->ready.empty()) {
+    // copy-engine star: items that can run now first, then the fan-out items
+    // in the order their copies land (a CTA spinning on a late copy must not
+    // hold up items whose copy is already in)
+    const uint64_t base = accounting ? 4 : hm.ce_flags;
+    auto ready = [&](const Tagged* t) {
+      if (!t->it.wait_flag) return -1.0;
+      const size_t slot = static_cast<size_t>((t->it.wait_flag - base) / 4);
+      return slot < ce_slots->ready.size() ? ce_slots->ready[slot] : 1e30;
+    };
+    for (auto* list : {&vec_items, &other})
+      std::stable_sort(list->begin(), list->end(), [&](const Tagged* a, const Tagged* b) { return ready(a) < ready(b); });
   }
   acc.n_vec = static_cast<int>(vec_items.size());
   vec_items.insert(vec_items.end(), other.begin(), other.end());
@@ -739,10 +751,26 @@ bool copy_has(const CeCopy& c, int64_t off) {
 CeSlotMap ce_slot_map(const std::vector<LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch) {
   CeSlotMap m;
   int64_t slot = 0;
+  std::map<int, std::vector<CeCopy>> of;
   for (int g : host_ids(hm)) {
     if (g == h) continue;
-    for (const auto& c : ce_copies_of(ops, hm, g, max_pitch))
+    of[g] = ce_copies_of(ops, hm, g, max_pitch);
+    for (const auto& c : of[g])
       if (hm.host[static_cast<size_t>(c.dst)] == h) m.copies.push_back({c, slot++});
+  }
+  // landing times: each transfer into h from its simulated start, copy by copy
+  m.ready.assign(m.copies.size(), 0.0);
+  std::map<int, int64_t> first_slot;  // sender -> slot of its first copy to h
+  for (size_t i = 0; i < m.copies.size(); ++i)  // a sender's copies to h are consecutive (one transfer)
+    first_slot.emplace(hm.host[static_cast<size_t>(m.copies[i].first.src)], static_cast<int64_t>(i));
+  for (const auto& t : ce_schedule(ops, hm, max_pitch)) {
+    if (t.receiver != h) continue;
+    double at = t.start;
+    const int64_t s0 = first_slot[t.sender];
+    for (size_t k = 0; k < t.count; ++k) {
+      at += static_cast<double>(of[t.sender][t.first + k].bytes()) / 775e9;
+      m.ready[static_cast<size_t>(s0) + k] = at;
+    }
   }
   return m;
 }

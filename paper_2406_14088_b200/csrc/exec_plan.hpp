@@ -150,6 +150,7 @@ int64_t ce_star_slots(const std::vector<rlplan::LoweredOp>& ops, const HostMap& 
 // destination `dst` from source `src`, or -1.
 struct CeSlotMap {
   std::vector<std::pair<CeCopy, int64_t>> copies;  // incoming copies of h with their slots
+  std::vector<double> ready;  // per slot: simulated landing time (ce_schedule), to order the waiting items
   int64_t slot_of(rlplan::DeviceId src, rlplan::DeviceId dst, int64_t dst_off) const;
 };
 CeSlotMap ce_slot_map(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch);
