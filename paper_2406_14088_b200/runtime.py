@@ -768,9 +768,26 @@ class RankRealloc:
                 out.append(Scheme(overlap=True, ce_transport=True))
         uniq: List[Scheme] = []
         for sc in out:
-            if sc not in uniq:
+            if sc not in uniq and self._fits(pi, sc):
                 uniq.append(sc)
-        return uniq
+        return uniq or [self.schemes[pi]]
+
+    def _fits(self, pi: int, sc: Scheme) -> bool:
+        """Whether every rank has the device memory the scheme's extra buffers
+        need (the staged gather stages whole remote source shards; 70B at 2
+        GPUs would need 70 GB more than the 180 GB). Collective: all ranks
+        agree."""
+        need = 0
+        if sc.staged:
+            p = self.plans[pi]
+            need = sum(p.shard_bytes(SRC, s) for s in {s for s, dsts, _r in p.lowered()
+                                                        if self.host_of[s] != self.rank and
+                                                        any(self.host_of[d] == self.rank for d in dsts)})
+        ok = True
+        if need:
+            import torch
+            ok = need < 0.9 * torch.cuda.mem_get_info(self.cuda_device)[0]
+        return all(self._exchange({"ok": ok})[r]["ok"] for r in range(self.world)) if self.world > 1 else ok
 
     def _probe(self, pi: int, cands: List[Scheme], reps: int = 3) -> Scheme:
         """Bind each candidate, time `reps` launches of phase pi (after one
