@@ -588,6 +588,9 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       need(mode == 0, "copy-engine transport is a push-mode path");
       need(!staged && options->mc_bufs == nullptr, "copy-engine transport excludes the staged gather and multicast");
       hm.ce_remote = true;
+      hm.ce_hybrid = options->ce_transport == 2;
+      need(options->ce_transport == 1 || options->ce_transport == 2, "ce_transport must be 0, 1 or 2 (hybrid)");
+      need(!(hm.ce_hybrid && options->overlap_fanout), "the hybrid copy-engine transport excludes the star");
       need(options->relay_flags == nullptr, "copy-engine transport excludes relay flags");
       if (options->ce_flags) {
         need(options->host_of != nullptr && options->n_hosts > 0, "copy flags need host_of and n_hosts");
@@ -603,6 +606,8 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
     int per_sm = 0, sms = 0;
     check_cuda(rr::copy_max_ctas(&per_sm, &sms), "occupancy query");
     const auto jobs = rr::build_jobs(plan->lowered, hm, mode);
+    if (hm.ce_hybrid)  // the rects the SM kernel keeps: known before the items are built
+      rr::ce_transport_copies(jobs, hm, max_pitch(cuda_device), &hm.ce_sm_rects);
     const int64_t ce_min = options->ce_min_run_bytes == 0 ? kDefaultCeRunBytes : options->ce_min_run_bytes;
     const std::vector<rr::CeRun> runs =
         (mode == 0 && ce_min > 0 && src_bufs && dst_bufs && !hm.ce_remote) ? ce_runs(plan, jobs, hm, ce_min)

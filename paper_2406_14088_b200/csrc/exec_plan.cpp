@@ -502,7 +502,9 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
         if (ce_job) {
           kept.clear();
           for (size_t k = 0; k < dsts.size(); ++k) {
-            if (hm.ce_remote && hm.host[static_cast<size_t>(devs[k])] != hm.me) continue;
+            if (hm.ce_remote && hm.host[static_cast<size_t>(devs[k])] != hm.me &&
+                !hm.ce_sm_rects.count(std::make_tuple(j.src, devs[k], r.dst_off)))
+              continue;
             if (ce && ce_covered(*ce, j.src, devs[k], r)) continue;
             kept.push_back(dsts[k]);
           }
@@ -804,7 +806,8 @@ std::vector<int64_t> ce_send_slots(const std::vector<LoweredOp>& ops, const Host
   return out;
 }
 
-std::vector<CeCopy> ce_transport_copies(const std::vector<Job>& jobs, const HostMap& hm, int64_t max_pitch) {
+std::vector<CeCopy> ce_transport_copies(const std::vector<Job>& jobs, const HostMap& hm, int64_t max_pitch,
+                                        std::set<std::tuple<DeviceId, DeviceId, int64_t>>* sm_rects) {
   std::map<std::pair<DeviceId, DeviceId>, std::pair<std::vector<CeCopy>, std::vector<CeCopy>>> pairs;
   for (const auto& j : jobs) {
     if (!plain_push(j, j.phase) || hm.host[static_cast<size_t>(j.src)] != hm.me) continue;
@@ -825,6 +828,7 @@ std::vector<CeCopy> ce_transport_copies(const std::vector<Job>& jobs, const Host
           c.height = r.rows;
           c.src_pitch = r.src_pitch;
           c.dst_pitch = r.dst_pitch;
+          c.strided = true;
           strided.push_back(c);
         }
       }
@@ -843,7 +847,13 @@ std::vector<CeCopy> ce_transport_copies(const std::vector<Job>& jobs, const Host
     for (auto& [sd, lists] : pairs) {
       if (hm.host[static_cast<size_t>(sd.second)] != h) continue;
       auto merged = merge_pair(std::move(lists.first), std::move(lists.second), max_pitch);
-      out.insert(out.end(), merged.begin(), merged.end());
+      for (const auto& c : merged) {
+        if (hm.ce_hybrid && c.strided && c.depth == 1) {
+          if (sm_rects) sm_rects->insert({c.src, c.dst, c.dst_off});  // an unmerged row-parallel rect
+          continue;
+        }
+        out.push_back(c);
+      }
     }
   }
   return out;

@@ -5,6 +5,8 @@
 #pragma once
 
 #include <cstdint>
+#include <set>
+#include <tuple>
 #include <vector>
 
 #include "rlplan/realloc.hpp"
@@ -67,6 +69,12 @@ struct HostMap {
   // Copy-engine transport (push): every remote destination of a plain
   // phase-0 job is left out of the SM items; ce_transport_copies moves it.
   bool ce_remote = false;
+  // Hybrid: row-parallel pieces whose layers do not merge into one 3D copy
+  // (per-layer 2D copies run at ~686 GB/s against ~775) stay on SM peer
+  // stores beside the copy engines; ce_sm_rects lists them as (source,
+  // destination, destination offset of the rect).
+  bool ce_hybrid = false;
+  std::set<std::tuple<rlplan::DeviceId, rlplan::DeviceId, int64_t>> ce_sm_rects;
   // ... with per-copy flags (copy-engine star): each transport copy is
   // flagged in the receiving host's array (ce_flag_slot), and a host's
   // in-host fan-out runs inside phase 0, each item waiting for the copy that
@@ -125,6 +133,7 @@ struct CeCopy {
   int64_t width = 0, height = 1, depth = 1;
   int64_t src_pitch = 0, dst_pitch = 0;
   int64_t src_slice = 0, dst_slice = 0;
+  bool strided = false;  // rows are the rows of one row-parallel rect (not layers)
   int64_t bytes() const { return width * height * depth; }
   int64_t src_end() const { return src_off + (depth - 1) * src_slice + (height - 1) * src_pitch + width; }
 };
@@ -137,7 +146,11 @@ struct CeCopy {
 // stay <= max_pitch. Ordered in rotation rounds: round r sends to the host r
 // places after this one (ids ascending), so while every host follows its
 // order each receives from one sender at a time.
-std::vector<CeCopy> ce_transport_copies(const std::vector<Job>& jobs, const HostMap& hm, int64_t max_pitch);
+// With hm.ce_hybrid the unmerged row-parallel pieces are left out and, when
+// sm_rects is given, recorded there.
+std::vector<CeCopy> ce_transport_copies(const std::vector<Job>& jobs, const HostMap& hm, int64_t max_pitch,
+                                        std::set<std::tuple<rlplan::DeviceId, rlplan::DeviceId, int64_t>>* sm_rects =
+                                            nullptr);
 
 // Copy-engine star slots: host h's flag array holds one slot per transport
 // copy it receives, senders in ascending host order, each sender's copies to

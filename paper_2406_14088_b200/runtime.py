@@ -146,7 +146,7 @@ class Executor:
                  relay_flags: Optional[Dict[int, int]] = None, relay_chain: bool = True,
                  overlap_fanout: bool = False, ce_min_run_bytes: int = 0, stage_chunk_bytes: int = 0,
                  n_hosts: int = 0, stage_remote: Optional[Dict[Tuple[int, int], int]] = None,
-                 stage_flags: Optional[Dict[int, int]] = None, ce_transport: bool = False,
+                 stage_flags: Optional[Dict[int, int]] = None, ce_transport: int = 0,
                  ce_flags: Optional[Dict[int, int]] = None):
         n = plan.cluster.device_count()
         self.plan = plan
@@ -621,9 +621,10 @@ class Scheme:
     overlap: bool = False       # per-chunk in-host fan-out inside phase 0 (star flags)
     staged: bool = False        # copy-engine rotation of whole shards + per-piece unpack
     ce_transport: bool = False  # copy-engine 2D/3D copies straight into the destinations
+    ce_hybrid: bool = False     # ... with unmerged row-parallel pieces left on SM peer stores
 
     def label(self) -> str:
-        parts = [k for k in ("relay", "overlap", "staged", "ce_transport") if getattr(self, k)]
+        parts = [k for k in ("relay", "overlap", "staged", "ce_transport", "ce_hybrid") if getattr(self, k)]
         return "+".join(parts) or "push"
 
 
@@ -766,6 +767,12 @@ class RankRealloc:
             out.append(Scheme(ce_transport=True))
             if sw["overlap"] and any(fanout_bytes(p, self.host_of).values()):
                 out.append(Scheme(overlap=True, ce_transport=True))
+            # row-parallel pieces that stay per-layer 2D copies (thousands of
+            # rows, depth 1): try them on SM stores beside the copy engines
+            # (every host's copies: all ranks must build the same list)
+            if any(c[6] == 1 and c[5] > 256 for r in range(self.world)
+                   for c in p.ce_copies([d for d in range(self.n) if self.host_of[d] == r], self.host_of)):
+                out.append(Scheme(ce_transport=True, ce_hybrid=True))
         uniq: List[Scheme] = []
         for sc in out:
             if sc not in uniq and self._fits(pi, sc):
@@ -981,7 +988,8 @@ class RankRealloc:
                           self.chunk_bytes, host_of=self.host_of if self.hierarchical else None,
                           mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_table, relay_chain=sc.relay,
                           overlap_fanout=sc.overlap, ce_min_run_bytes=self.ce_min_run_bytes,
-                          ce_transport=sc.ce_transport, n_hosts=world if ce_flag else 0,
+                          ce_transport=2 if sc.ce_hybrid else int(sc.ce_transport),
+                          n_hosts=world if ce_flag else 0,
                           ce_flags=ce_flags if ce_flag else None)
         if self.kernel is not None:
             ex.set_kernel(self.kernel)

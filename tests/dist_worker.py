@@ -189,6 +189,31 @@ class Worker:
                     self.run(f"ce-transport {sp}->{dp} star={star} kernel={kernel} (+onload)", m, pl(sp), pl(dp),
                              SPECIAL | 83, reps=3, onload_chunk=32 << 10, ce_transport=True, overlap=star,
                              kernel=kernel, flag_kernel=kernel)
+        # hybrid: unmerged row-parallel pieces on SM stores beside the copy engines
+        for sp, dp in CASES[1:3]:
+            src, dst = pl(sp), pl(dp)
+            label = f"ce-transport hybrid {sp}->{dp}"
+            with self.case(label):
+                plan = plan_param_realloc(m, src, dst, self.c, BALANCED)
+                rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], self.rank,
+                                   self.world, self.local, ce_transport=True)
+                try:
+                    rr._unbind_phase(0)
+                    rr.schemes[0] = R.Scheme(ce_transport=True, ce_hybrid=True)
+                    rr._bind_phase(0, rr.schemes[0])
+                    rr.executors = [b.executor for b in rr.bindings]
+                    for d, b in rr.buffers["a"].items():
+                        R.fill_shard(plan, R.SRC, d, b.ptr, SPECIAL | 85)
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    rr.run_phase(0)
+                    torch.cuda.synchronize()
+                    for d, b in rr.buffers["b"].items():
+                        if not np.array_equal(b.to_host(), O.fill(m, dst, self.c, d, SPECIAL | 85)):
+                            self.failures.append(f"{label}: device {d} differs")
+                    dist.barrier()
+                finally:
+                    rr.close()
         # replicate (one source, fan-out on every GPU)
         self.run("ce-transport replicate star=True", m, REPLICATE[0], REPLICATE[1], SPECIAL | 84, reps=2,
                  ce_transport=True, overlap=True)

@@ -149,3 +149,18 @@ def test_schedule_serves_one_sender_at_a_time(name, world):
         recv[t[1]] = recv.get(t[1], 0) + t[5]
     bound = max(max(send.values()), max(recv.values())) / 775e9
     assert max(t[3] for t in sched) <= 1.1 * bound + 1e-3
+
+
+def test_hybrid_keeps_unmerged_row_parallel_pieces_on_sm():
+    """ce_transport = 2: the 34B critic's down slices (layer stride not a
+    multiple of the row pitch: per-layer 2D copies) stay on SM stores; the
+    executor-side split is exercised on GPU (dist_worker); here the host
+    view: every unmerged row-parallel copy has thousands of rows, the layer
+    chains tens."""
+    from paper_2406_14088_b200.workloads import WORKLOADS
+    plan = WORKLOADS["llama34b_critic_pp4tp2_to_tp8"].plans(BALANCED)[0]
+    host_of = [d // 4 for d in range(8)]
+    cs = plan.ce_copies([0, 1, 2, 3], host_of)
+    unmerged = [c for c in cs if c[6] == 1 and c[5] > 256]
+    assert unmerged and all(c[4] < 64 << 10 for c in unmerged)
+    assert all(c[5] <= 80 for c in cs if c[6] == 1 and c[5] > 1 and c not in unmerged)
