@@ -621,13 +621,13 @@ def run_b200(args) -> None:
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            # this rank's kernels per step: copy kernels of every phase, the staged
-            # gather's per-piece flag kernels, plus the
-            # barrier(s) and the fan-out kernels when N > 1
+            # this rank's kernels in the timed region: copy kernels of every
+            # phase, plus the barrier(s) and the fan-out kernels when N > 1
+            # (copy-engine copies and their stream-written flags are not kernels)
             "gpu_launches": args.steps * sum(
                 e.kernel_count()[0] + ((1 + rr.has_fanout[i] * (1 + e.kernel_count()[1])) if world > 1 else 0)
-                + e.stage_pushes()[0]  # staged gather: one flag kernel per pushed piece
                 for i, e in enumerate(rr.executors)),
+            "copy_engine_submissions": args.steps * sum(e.ce_runs()[0] + e.stage_pushes()[0] for e in rr.executors),
             "clocks": clock_info,
             # host side, once per plan (not in the timed region): planning +
             # lowering, and rank 0's buffer allocation + executor binding/upload
