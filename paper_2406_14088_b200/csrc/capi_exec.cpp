@@ -623,6 +623,9 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       transport = rr::ce_transport_copies(jobs, hm, mp);
       if (hm.ce_star) {
         send_slots = rr::ce_send_slots(plan->lowered, hm, transport, mp);
+        const auto flagged = rr::star_flagged(transport, hm);
+        for (size_t k = 0; k < send_slots.size(); ++k)
+          if (!flagged[k]) send_slots[k] = -1;  // inside a flag group: no write after this copy
         slot_map = rr::ce_slot_map(plan->lowered, hm, hm.me, mp);
       }
       if (options->ce_flags) {
@@ -679,7 +682,8 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
     auto push_copy = [&](size_t k, uint32_t* wait, uint32_t* done) {
       const auto& c = transport[k];
       need(dst_bufs[c.dst] != nullptr && src_bufs[c.src] != nullptr, "missing a copy-engine transport buffer");
-      uint32_t* flag = hm.ce_star ? host_flags(hm.host[static_cast<size_t>(c.dst)]) + send_slots[k] : nullptr;
+      uint32_t* flag = hm.ce_star && send_slots[k] >= 0 ? host_flags(hm.host[static_cast<size_t>(c.dst)]) + send_slots[k]
+                                                         : nullptr;
       ex->ce.push_back({static_cast<char*>(dst_bufs[c.dst]) + c.dst_off,
                         static_cast<const char*>(src_bufs[c.src]) + c.src_off, c.width, c.height, c.depth,
                         c.src_pitch, c.dst_pitch, c.src_slice, c.dst_slice, c.src, c.src_off, c.src_end(), flag,

@@ -750,6 +750,21 @@ bool copy_has(const CeCopy& c, int64_t off) {
 }
 }  // namespace
 
+std::vector<bool> star_flagged(const std::vector<CeCopy>& copies, const HostMap& hm) {
+  std::vector<bool> out(copies.size(), false);
+  int64_t run = 0;
+  for (size_t k = 0; k < copies.size(); ++k) {
+    run += copies[k].bytes();
+    const bool last_to_receiver = k + 1 == copies.size() || hm.host[static_cast<size_t>(copies[k + 1].dst)] !=
+                                                                 hm.host[static_cast<size_t>(copies[k].dst)];
+    if (run >= kStarFlagBytes || last_to_receiver) {
+      out[k] = true;
+      run = 0;
+    }
+  }
+  return out;
+}
+
 CeSlotMap ce_slot_map(const std::vector<LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch) {
   CeSlotMap m;
   int64_t slot = 0;
@@ -757,8 +772,18 @@ CeSlotMap ce_slot_map(const std::vector<LoweredOp>& ops, const HostMap& hm, int 
   for (int g : host_ids(hm)) {
     if (g == h) continue;
     of[g] = ce_copies_of(ops, hm, g, max_pitch);
-    for (const auto& c : of[g])
-      if (hm.host[static_cast<size_t>(c.dst)] == h) m.copies.push_back({c, slot++});
+    const auto flagged = star_flagged(of[g], hm);
+    // a copy's items wait on the slot of the flagged copy that ends its group
+    std::vector<size_t> mine;
+    for (size_t k = 0; k < of[g].size(); ++k)
+      if (hm.host[static_cast<size_t>(of[g][k].dst)] == h) mine.push_back(k);
+    const size_t first = m.copies.size();
+    for (size_t k : mine) m.copies.push_back({of[g][k], slot++});
+    int64_t wait = -1;
+    for (size_t i = mine.size(); i-- > 0;) {
+      if (flagged[mine[i]]) wait = m.copies[first + i].second;
+      m.copies[first + i].second = wait;
+    }
   }
   // landing times: each transfer into h from its simulated start, copy by copy
   m.ready.assign(m.copies.size(), 0.0);

@@ -162,10 +162,18 @@ int64_t ce_star_slots(const std::vector<rlplan::LoweredOp>& ops, const HostMap& 
 // Slot (in host `h`'s array) of the copy that carries byte `dst_off` of
 // destination `dst` from source `src`, or -1.
 struct CeSlotMap {
-  std::vector<std::pair<CeCopy, int64_t>> copies;  // incoming copies of h with their slots
+  std::vector<std::pair<CeCopy, int64_t>> copies;  // incoming copies of h with the slot their items wait on
   std::vector<double> ready;  // per slot: simulated landing time (ce_schedule), to order the waiting items
   int64_t slot_of(rlplan::DeviceId src, rlplan::DeviceId dst, int64_t dst_off) const;
 };
+// Copy-engine star flag groups: of a sender's copies (issue order), the
+// ones followed by a flag write — the last of every >= kStarFlagBytes run and
+// the last copy to each receiver. A flag write carries a system-wide memory
+// barrier, so flagging every copy would drain the engine each time; the
+// items of a copy wait for the flag of its group. Both sides derive the
+// groups from the same copy list.
+constexpr int64_t kStarFlagBytes = int64_t{256} << 20;
+std::vector<bool> star_flagged(const std::vector<CeCopy>& copies, const HostMap& hm);
 CeSlotMap ce_slot_map(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch);
 // Slot of each of this host's outgoing copies (in the receiving host's array).
 std::vector<int64_t> ce_send_slots(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm,
