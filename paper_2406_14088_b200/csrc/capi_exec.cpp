@@ -1064,12 +1064,29 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
       };
       // (schedule waits are skipped here: copies follow the onload's chunk
       // order, not the schedule's, so a wait could point ahead in this
-      // stream; the done flags are still raised, no one waits on them)
-      for (const auto& c : ex->ce)
-        if (!onloaded(c.src_dev)) {
-          issue_copy(c, ex->ce_stream);
-          if (c.flag) signal_piece(ex->ce_stream, c.flag, ex->epoch);
-          if (c.done) signal_piece(ex->ce_stream, c.done, ex->epoch);
+      // stream; the done flags are still raised, no one waits on them.)
+      // A star flag releases its whole group (the copies since the previous
+      // flagged copy of the same stream list): it is written once the last
+      // copy of the group to be issued here has been, whatever the order.
+      std::vector<int> left(ex->ce.size(), 0);  // per flagged copy: its group's copies not yet fully issued
+      std::vector<size_t> group_of(ex->ce.size(), 0);
+      for (size_t i = ex->ce.size(); i-- > 0;) {
+        if (ex->ce[i].flag) group_of[i] = i;
+        else if (i + 1 < ex->ce.size()) group_of[i] = group_of[i + 1];
+        else group_of[i] = i;
+      }
+      for (size_t i = 0; i < ex->ce.size(); ++i)
+        if (ex->ce[group_of[i]].flag) ++left[group_of[i]];
+      auto finished = [&](size_t i) {  // copy i fully issued on ce_stream
+        const auto& c = ex->ce[i];
+        if (c.done) signal_piece(ex->ce_stream, c.done, ex->epoch);
+        const size_t g = group_of[i];
+        if (ex->ce[g].flag && --left[g] == 0) signal_piece(ex->ce_stream, ex->ce[g].flag, ex->epoch);
+      };
+      for (size_t i = 0; i < ex->ce.size(); ++i)
+        if (!onloaded(ex->ce[i].src_dev)) {
+          issue_copy(ex->ce[i], ex->ce_stream);
+          finished(i);
         }
       for (size_t k = 0; k < ex->chunks.size(); ++k) {
         const auto& ch = ex->chunks[k];
@@ -1080,17 +1097,14 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
         };
         if (!std::any_of(ex->ce.begin(), ex->ce.end(), in_chunk)) continue;
         check_cuda(cudaStreamWaitEvent(ex->ce_stream, ex->events[k], 0), "cudaStreamWaitEvent(ce chunk)");
-        for (const auto& c : ex->ce) {
+        for (size_t i = 0; i < ex->ce.size(); ++i) {
+          const auto& c = ex->ce[i];
           if (!in_chunk(c)) continue;
           if (flat(c))
             piece(c, lo, hi);
           else
             issue_copy(c, ex->ce_stream);
-          // flagged once the copy's last source byte is in (its last piece)
-          if (c.src_end > lo && c.src_end <= hi) {
-            if (c.flag) signal_piece(ex->ce_stream, c.flag, ex->epoch);
-            if (c.done) signal_piece(ex->ce_stream, c.done, ex->epoch);
-          }
+          if (c.src_end > lo && c.src_end <= hi) finished(i);  // its last piece
         }
       }
     }
