@@ -144,6 +144,7 @@ struct rr_exec {
     uint32_t* flag = nullptr;  // copy-engine star: flagged on the receiving host after the copy
     uint32_t* wait = nullptr;  // schedule: wait (>= epoch) before the copy, on this host's array
     uint32_t* done = nullptr;  // schedule: raised after the copy (the next sender into its receiver)
+    bool hard_wait = false;    // relay forward: `wait` is a data dependency (kept with an onload)
     int64_t bytes() const { return width * height * depth; }
   };
   std::vector<CeCopy> ce;
@@ -487,10 +488,12 @@ rr_status rr_plan_ce_slots(const rr_plan* plan, const int32_t* host_of, int64_t*
     std::sort(hosts.begin(), hosts.end());
     hosts.erase(std::unique(hosts.begin(), hosts.end()), hosts.end());
     int64_t best = 0;
-    for (int h : hosts) {
-      hm.me = h;
-      best = std::max(best, rr::ce_flag_slots(plan->lowered, hm, h, (int64_t{1} << 31) - 1));
-    }
+    for (int relay = 0; relay < 2; ++relay)  // with and without relay chains (ce_transport 3 / 1-2)
+      for (int h : hosts) {
+        hm.me = h;
+        hm.ce_relay = relay != 0;
+        best = std::max(best, rr::ce_flag_slots(plan->lowered, hm, h, (int64_t{1} << 31) - 1));
+      }
     *slots = best;
   });
 }
@@ -589,7 +592,10 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       need(!staged && options->mc_bufs == nullptr, "copy-engine transport excludes the staged gather and multicast");
       hm.ce_remote = true;
       hm.ce_hybrid = options->ce_transport == 2;
-      need(options->ce_transport == 1 || options->ce_transport == 2, "ce_transport must be 0, 1 or 2 (hybrid)");
+      hm.ce_relay = options->ce_transport == 3;
+      need(options->ce_transport >= 1 && options->ce_transport <= 3,
+           "ce_transport must be 0, 1, 2 (hybrid) or 3 (with relay chains)");
+      need(!hm.ce_relay || options->ce_flags != nullptr, "the copy-engine relay needs ce_flags");
       need(!(hm.ce_hybrid && options->overlap_fanout), "the hybrid copy-engine transport excludes the star");
       need(options->relay_flags == nullptr, "copy-engine transport excludes relay flags");
       if (options->ce_flags) {
@@ -635,7 +641,35 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
         need(n_ce_slots == 0 || hm.ce_flags != 0, "missing this host's copy flag array");
       }
     }
-    auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes, &runs, hm.ce_star ? &slot_map : nullptr);
+    // copy-engine relay: ops, pieces, and this host's relay slot lookup
+    std::vector<rr::CeRelayOp> relay_ops;
+    std::map<int, int64_t> relay_base;  // per host: first relay slot in its flag array
+    rr::RelaySlotFn relay_slot_fn;
+    if (hm.ce_relay) {
+      const int64_t mp = max_pitch(cuda_device);
+      relay_ops = rr::ce_relay_ops(plan->lowered, hm);
+      for (int h : std::set<int>(hm.host.begin(), hm.host.end())) relay_base[h] = rr::ce_relay_base(plan->lowered, hm, h, mp);
+      const int64_t mine = relay_base[hm.me];
+      relay_slot_fn = [&relay_ops, mine](const LoweredOp* op, int64_t byte) -> int64_t {
+        for (const auto& r : relay_ops) {
+          if (r.op != op) continue;
+          for (size_t k = 0; k < r.pieces.size(); ++k) {
+            const auto& p = r.pieces[k];
+            int64_t rel = byte - p.dst_off;
+            if (rel < 0) continue;
+            if (p.height > 1) {
+              const int64_t y = rel / p.dst_pitch;
+              if (y >= p.height) continue;
+              rel -= y * p.dst_pitch;
+            }
+            if (rel < p.width) return mine + r.slot0 + static_cast<int64_t>(k);
+          }
+        }
+        return -1;
+      };
+    }
+    auto a = rr::build_items(jobs, 0, hm, src_bufs, dst_bufs, chunk_bytes, &runs, hm.ce_star ? &slot_map : nullptr,
+                             hm.ce_relay ? &relay_slot_fn : nullptr);
     auto b = rr::build_items(jobs, 1, hm, src_bufs, dst_bufs, chunk_bytes);
     if (options->chunk_bytes <= 0) {
       int bulk_ctas = 0;
@@ -690,6 +724,49 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
                         wait, done});
       ex->ce_bytes += c.bytes();
     };
+    // Copy-engine relay actions first, in (op, piece) order on every host:
+    // a forward depends only on the same piece's previous hop, which every
+    // other stream issues after strictly earlier pieces only, so no cycle;
+    // the transport copies (their schedule waits point only to transport
+    // copies) follow.
+    for (const auto& r : relay_ops) {
+      const LoweredOp& op = *r.op;
+      const auto pos = std::find(r.chain.begin(), r.chain.end(), hm.me) - r.chain.begin();
+      const bool sender = r.src_host == hm.me;
+      const bool forwarder = pos + 1 < static_cast<std::ptrdiff_t>(r.chain.size());
+      if (!sender && !forwarder) continue;
+      const size_t next = sender ? 0 : static_cast<size_t>(pos) + 1;
+      const int to_host = r.chain[next];
+      for (size_t k = 0; k < r.pieces.size(); ++k) {
+        const auto& p = r.pieces[k];
+        const int64_t slot = r.slot0 + static_cast<int64_t>(k);
+        rr_exec::CeCopy c{};
+        c.dst = static_cast<char*>(dst_bufs[r.leader[next]]) + p.dst_off;
+        c.width = p.width;
+        c.height = p.height;
+        c.depth = 1;
+        c.dst_pitch = p.dst_pitch ? p.dst_pitch : p.width;
+        c.src_slice = c.dst_slice = 0;
+        c.flag = host_flags(to_host) + relay_base.at(to_host) + slot;
+        if (sender) {
+          need(src_bufs[op.src] != nullptr, "missing a relay source buffer");
+          c.src = static_cast<const char*>(src_bufs[op.src]) + p.src_off;
+          c.src_pitch = p.src_pitch ? p.src_pitch : p.width;
+          c.src_dev = op.src;
+          c.src_off = p.src_off;
+          c.src_end = p.src_off + (p.height - 1) * c.src_pitch + p.width;
+        } else {
+          c.src = static_cast<const char*>(dst_bufs[r.leader[static_cast<size_t>(pos)]]) + p.dst_off;
+          c.src_pitch = c.dst_pitch;
+          c.src_dev = -1;  // this host's leader replica, not an onloaded source
+          c.wait = host_flags(hm.me) + relay_base.at(hm.me) + slot;
+          c.hard_wait = true;
+        }
+        need(c.dst != nullptr && c.src != nullptr, "missing a relay leader buffer");
+        ex->ce.push_back(c);
+        ex->ce_bytes += c.bytes();
+      }
+    }
     if (!schedule.empty()) {
       // scheduled issue order: each transfer waits for the previous one into
       // its receiver (if another host sent it) and releases the next
@@ -1083,8 +1160,11 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
         const size_t g = group_of[i];
         if (ex->ce[g].flag && --left[g] == 0) signal_piece(ex->ce_stream, ex->ce[g].flag, ex->epoch);
       };
+      // Relay forwards (hard waits: the piece must have arrived) go last, in
+      // (op, piece) order: every send they wait for is issued before them
+      // on its stream and waits only for local onload chunks.
       for (size_t i = 0; i < ex->ce.size(); ++i)
-        if (!onloaded(ex->ce[i].src_dev)) {
+        if (!ex->ce[i].hard_wait && !onloaded(ex->ce[i].src_dev)) {
           issue_copy(ex->ce[i], ex->ce_stream);
           finished(i);
         }
@@ -1099,7 +1179,7 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
         check_cuda(cudaStreamWaitEvent(ex->ce_stream, ex->events[k], 0), "cudaStreamWaitEvent(ce chunk)");
         for (size_t i = 0; i < ex->ce.size(); ++i) {
           const auto& c = ex->ce[i];
-          if (!in_chunk(c)) continue;
+          if (c.hard_wait || !in_chunk(c)) continue;
           if (flat(c))
             piece(c, lo, hi);
           else
@@ -1107,6 +1187,12 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
           if (c.src_end > lo && c.src_end <= hi) finished(i);  // its last piece
         }
       }
+      for (size_t i = 0; i < ex->ce.size(); ++i)
+        if (ex->ce[i].hard_wait) {
+          wait_piece(ex->ce_stream, ex->ce[i].wait, ex->epoch);
+          issue_copy(ex->ce[i], ex->ce_stream);
+          finished(i);
+        }
     }
     auto segment_phase = [&](const rr_exec::Segment& sg) {
       rr_exec::Phase ph;

@@ -277,14 +277,17 @@ std::vector<Job> build_jobs(const std::vector<LoweredOp>& ops, const HostMap& hm
       if (hs == hm.me) {
         // One job: the source is read once for every local destination and
         // every remote host's leader (build_items splits > kMaxFan targets).
+        // A copy-engine relay payload reaches the remote hosts by the relay
+        // (ce_relay_ops), not from here.
         Job j;
         j.phase = 0;
         j.src = op.src;
         j.op = &op;
         if (mine != groups.end()) j.dsts = mine->second;
-        for (const auto& [h, list] : groups)
-          if (h != hm.me) j.dsts.push_back(list.front());
-        jobs.push_back(std::move(j));
+        if (!ce_relay_op(op, hm))
+          for (const auto& [h, list] : groups)
+            if (h != hm.me) j.dsts.push_back(list.front());
+        if (!j.dsts.empty()) jobs.push_back(std::move(j));
       }
     } else if (mine != groups.end()) {  // pull: each destination host fetches for itself
       Job j;
@@ -297,9 +300,11 @@ std::vector<Job> build_jobs(const std::vector<LoweredOp>& ops, const HostMap& hm
     }
     if (hs != hm.me && mine != groups.end() && mine->second.size() > 1 && !(mode == 1 && hm.stage_chunk > 0)) {
       Job j;
-      // copy-engine star: the fan-out waits per copy inside phase 0
-      j.phase = hm.ce_star && mode == 0 ? 0 : 1;
+      // copy-engine star / relay: the fan-out waits per copy / piece inside phase 0
+      const bool relayed = mode == 0 && ce_relay_op(op, hm);
+      j.phase = (hm.ce_star || relayed) && mode == 0 ? 0 : 1;
       j.ce_wait = j.phase == 0;
+      j.ce_relay = relayed;
       j.src = mine->second.front();
       j.src_is_dst_buffer = true;
       j.op = &op;
@@ -402,6 +407,9 @@ struct RelayTags {
   // item's last source byte)
   uint64_t stage_base = 0;
   int64_t stage_slot0 = 0, stage_chunk = 0;
+  // copy-engine relay: the slot comes from the item's last destination byte
+  const RelaySlotFn* piece_slot = nullptr;
+  const LoweredOp* op = nullptr;
 };
 
 void add_rect(std::vector<Tagged>& out, ItemSet& acc, uint64_t src, const std::vector<uint64_t>& dsts,
@@ -437,8 +445,14 @@ void add_rect(std::vector<Tagged>& out, ItemSet& acc, uint64_t src, const std::v
       if (relay.signal_base) it.signal_flag = relay.signal_base + off;
     }
     const int64_t src_end = src_begin + ((rows - 1) * sp + cols) * unit;
-    if (relay.stage_base)
+    if (relay.piece_slot) {
+      const int64_t last = r.dst_off + ((row0 + rows - 1) * dp + col0 + cols) * unit - 1;
+      const int64_t slot = (*relay.piece_slot)(relay.op, last);
+      if (slot < 0) throw rlplan::ValidationError("fan-out bytes outside every relay piece");
+      it.wait_flag = relay.stage_base + 4u * static_cast<uint64_t>(slot);
+    } else if (relay.stage_base) {
       it.wait_flag = relay.stage_base + 4u * static_cast<uint64_t>(relay.stage_slot0 + (src_end - 1) / relay.stage_chunk);
+    }
     out.push_back({it, src_dev, src_end, src_is_dst});
     const int64_t bytes = rows * cols * unit;
     acc.read += bytes;
@@ -464,7 +478,7 @@ uint64_t base_of(void* const* bufs, DeviceId d, const char* what) {
 
 ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, void* const* src_bufs,
                     void* const* dst_bufs, int64_t chunk_bytes, const std::vector<CeRun>* ce,
-                    const CeSlotMap* ce_slots) {
+                    const CeSlotMap* ce_slots, const RelaySlotFn* relay_piece_slot) {
   ItemSet acc;
   std::vector<std::vector<Tagged>> streams;
   const bool accounting = src_bufs == nullptr;
@@ -525,6 +539,17 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
           tags.signal_base = j.relay_signal ? flags(j.dsts.front()) : 0;
           tags.slot = &relay_slot;
           add_rect(streams.back(), acc, s, dsts, r, hm.relay_chunk, mc0, j.src, j.src_is_dst_buffer, tags);
+          continue;
+        }
+        if (j.ce_wait && j.ce_relay) {
+          // wait for the relay piece holding the item's last leader byte
+          // (pieces of one op land in order)
+          if (relay_piece_slot == nullptr) throw rlplan::ValidationError("copy-engine relay without its slot map");
+          RelayTags tags;
+          tags.stage_base = accounting ? 4 : hm.ce_flags;
+          tags.piece_slot = relay_piece_slot;
+          tags.op = j.op;
+          add_rect(streams.back(), acc, s, *to, r, chunk_bytes, mc0, j.src, j.src_is_dst_buffer, tags);
           continue;
         }
         if (j.ce_wait) {
@@ -594,15 +619,17 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
         return a->it.wait_flag < b->it.wait_flag;  // 0 (no wait) first
       });
     }
-  } else if (ce_slots != nullptr && !ce_slots->ready.empty()) {
-    // copy-engine star: items that can run now first, then the fan-out items
-    // in the order their copies land (a CTA spinning on a late copy must not
-    // hold up items whose copy is already in)
+  } else if ((ce_slots != nullptr && !ce_slots->ready.empty()) || relay_piece_slot != nullptr) {
+    // copy-engine star / relay: items that can run now first, then the
+    // fan-out items in the order their copies or pieces land (a CTA spinning
+    // on a late copy must not hold up items whose copy is already in); relay
+    // pieces (slots after the star's) in slot order
     const uint64_t base = accounting ? 4 : hm.ce_flags;
     auto ready = [&](const Tagged* t) {
       if (!t->it.wait_flag) return -1.0;
       const size_t slot = static_cast<size_t>((t->it.wait_flag - base) / 4);
-      return slot < ce_slots->ready.size() ? ce_slots->ready[slot] : 1e30;
+      if (ce_slots != nullptr && slot < ce_slots->ready.size()) return ce_slots->ready[slot];
+      return 1e20 + static_cast<double>(slot);
     };
     for (auto* list : {&vec_items, &other})
       std::stable_sort(list->begin(), list->end(), [&](const Tagged* a, const Tagged* b) { return ready(a) < ready(b); });
@@ -836,6 +863,7 @@ std::vector<CeCopy> ce_transport_copies(const std::vector<Job>& jobs, const Host
   std::map<std::pair<DeviceId, DeviceId>, std::pair<std::vector<CeCopy>, std::vector<CeCopy>>> pairs;
   for (const auto& j : jobs) {
     if (!plain_push(j, j.phase) || hm.host[static_cast<size_t>(j.src)] != hm.me) continue;
+    if (ce_relay_op(*j.op, hm)) continue;  // travels by the relay
     for (DeviceId d : j.dsts) {
       if (hm.host[static_cast<size_t>(d)] == hm.me) continue;
       auto& [flat, strided] = pairs[{j.src, d}];
@@ -1001,11 +1029,79 @@ std::vector<CeTransfer> ce_schedule(const std::vector<LoweredOp>& ops, const Hos
   return out;
 }
 
-int64_t ce_flag_slots(const std::vector<LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch) {
+int64_t ce_relay_base(const std::vector<LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch) {
   int64_t n = ce_star_slots(ops, hm, h, max_pitch);
   for (const auto& t : ce_schedule(ops, hm, max_pitch))
     if (t.sender == h && t.wait_slot >= 0) n = std::max(n, t.wait_slot + 1);
   return n;
+}
+
+int64_t ce_flag_slots(const std::vector<LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch) {
+  int64_t n = ce_relay_base(ops, hm, h, max_pitch);
+  if (hm.ce_relay)
+    for (const auto& r : ce_relay_ops(ops, hm)) n += static_cast<int64_t>(r.pieces.size());
+  return n;
+}
+
+bool ce_relay_op(const LoweredOp& op, const HostMap& hm) {
+  if (!hm.ce_relay || !hm.hierarchical) return false;
+  const int hs = hm.host[static_cast<size_t>(op.src)];
+  std::set<int> remote;
+  for (DeviceId d : op.dst)
+    if (hm.host[static_cast<size_t>(d)] != hs) remote.insert(hm.host[static_cast<size_t>(d)]);
+  return remote.size() >= 2;
+}
+
+std::vector<CeRelayOp> ce_relay_ops(const std::vector<LoweredOp>& ops, const HostMap& hm) {
+  std::vector<CeRelayOp> out;
+  int64_t slot = 0;
+  for (const auto& op : ops) {
+    if (!ce_relay_op(op, hm)) continue;
+    CeRelayOp r;
+    r.op = &op;
+    r.src_host = hm.host[static_cast<size_t>(op.src)];
+    const auto groups = by_host(op, hm);
+    r.chain = relay_chain(groups, r.src_host);
+    for (int h : r.chain) r.leader.push_back(groups.at(h).front());
+    // pieces: rects cut into <= kRelayPieceBytes row ranges; neighbouring 1D
+    // pieces contiguous on both sides are coalesced
+    for (const auto& rc : op.rects) {
+      const bool flat = rc.rows == 1 || (rc.src_pitch == rc.row_bytes && rc.dst_pitch == rc.row_bytes);
+      if (flat) {
+        const int64_t total = rc.row_bytes * rc.rows;
+        for (int64_t off = 0; off < total; off += kRelayPieceBytes) {
+          const int64_t w = std::min(kRelayPieceBytes, total - off);
+          auto& v = r.pieces;
+          if (!v.empty() && v.back().height == 1 && v.back().src_off + v.back().width == rc.src_off + off &&
+              v.back().dst_off + v.back().width == rc.dst_off + off && v.back().width + w <= kRelayPieceBytes) {
+            v.back().width += w;
+            continue;
+          }
+          CeRelayPiece p;
+          p.src_off = rc.src_off + off;
+          p.dst_off = rc.dst_off + off;
+          p.width = w;
+          v.push_back(p);
+        }
+      } else {
+        const int64_t per = std::max<int64_t>(1, kRelayPieceBytes / rc.row_bytes);
+        for (int64_t row = 0; row < rc.rows; row += per) {
+          CeRelayPiece p;
+          p.src_off = rc.src_off + row * rc.src_pitch;
+          p.dst_off = rc.dst_off + row * rc.dst_pitch;
+          p.width = rc.row_bytes;
+          p.height = std::min(per, rc.rows - row);
+          p.src_pitch = rc.src_pitch;
+          p.dst_pitch = rc.dst_pitch;
+          r.pieces.push_back(p);
+        }
+      }
+    }
+    r.slot0 = slot;
+    slot += static_cast<int64_t>(r.pieces.size());
+    out.push_back(std::move(r));
+  }
+  return out;
 }
 
 }  // namespace rr

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <set>
 #include <tuple>
 #include <vector>
@@ -41,6 +42,9 @@ struct Job {
   // Copy-engine star: an in-host fan-out in phase 0 whose items wait for the
   // transport copy that filled the leader bytes they read.
   bool ce_wait = false;
+  // ... of a copy-engine relay payload: the items wait for the relay piece
+  // holding the last leader byte they read.
+  bool ce_relay = false;
 };
 
 struct HostMap {
@@ -81,6 +85,11 @@ struct HostMap {
   // filled the leader bytes it reads. ce_flags = this host's array.
   bool ce_star = false;
   uint64_t ce_flags = 0;
+  // Copy-engine relay (with ce_remote): a payload reaching >= 2 other hosts
+  // travels source -> host 1 -> host 2 ... (ring order) by copy engines,
+  // piece by piece, each hop's copy stream waiting for the piece's flag
+  // before forwarding it; every host fans its pieces out inside phase 0.
+  bool ce_relay = false;
 };
 
 // Staged gather: the remote sources host `h` reads, in arrival order. Round
@@ -200,8 +209,33 @@ struct CeTransfer {
 // schedule's slots of host h follow its ce_star_slots incoming-copy slots.
 std::vector<CeTransfer> ce_schedule(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm,
                                     int64_t max_pitch);
-// Length of host h's copy flag array: incoming copy slots + schedule waits.
+// Length of host h's copy flag array: incoming copy slots + schedule waits
+// (+ relay piece slots with hm.ce_relay).
 int64_t ce_flag_slots(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch);
+
+// Copy-engine relay. A piece is a 1D run (height 1) or a row range of a
+// row-parallel rect, <= kRelayPieceBytes, in the op's rect order; hop 0
+// reads the source shard (src geometry), later hops read the previous
+// host's leader (the destination geometry on both sides). Pieces of one op
+// land in order on every hop.
+constexpr int64_t kRelayPieceBytes = int64_t{256} << 20;
+bool ce_relay_op(const rlplan::LoweredOp& op, const HostMap& hm);
+struct CeRelayPiece {
+  int64_t src_off = 0, dst_off = 0, width = 0, height = 1, src_pitch = 0, dst_pitch = 0;
+  int64_t dst_last() const { return dst_off + (height - 1) * dst_pitch + width - 1; }
+};
+struct CeRelayOp {
+  const rlplan::LoweredOp* op = nullptr;
+  int src_host = 0;
+  std::vector<int> chain;                   // destination hosts in hop order
+  std::vector<rlplan::DeviceId> leader;     // per chain host: its lowest-id destination
+  std::vector<CeRelayPiece> pieces;
+  int64_t slot0 = 0;                        // relay slot of piece 0 (same on every host)
+};
+// The relay ops of a plan (plan order) with their pieces and slots.
+std::vector<CeRelayOp> ce_relay_ops(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm);
+// First relay slot in host h's flag array (after its star and schedule slots).
+int64_t ce_relay_base(const std::vector<rlplan::LoweredOp>& ops, const HostMap& hm, int h, int64_t max_pitch);
 
 // Byte extent [first, last) a rect writes in its destination shard.
 inline int64_t rect_dst_end(const rlplan::CopyRect& r) {
@@ -225,8 +259,11 @@ struct ItemSet {
 
 // Resolve jobs of `phase` into items. src_bufs/dst_bufs are indexed by plan
 // device; nullptr tables mean "accounting only" (addresses left at offsets).
+// relay: (op, destination byte) -> relay slot in this host's array (-1: none);
+// items of ce_relay jobs wait on base + 4 * slot of their last byte.
+using RelaySlotFn = std::function<int64_t(const rlplan::LoweredOp*, int64_t)>;
 ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, void* const* src_bufs,
                     void* const* dst_bufs, int64_t chunk_bytes, const std::vector<CeRun>* ce = nullptr,
-                    const CeSlotMap* ce_slots = nullptr);
+                    const CeSlotMap* ce_slots = nullptr, const RelaySlotFn* relay_piece_slot = nullptr);
 
 }  // namespace rr

@@ -732,7 +732,8 @@ class RankRealloc:
         relay = bool(sw["relay"]) and (sw["relay"] != "auto" or link_bottleneck(p, self.host_of, relay=True) <
                                        0.9 * link_bottleneck(p, self.host_of))
         if relay:
-            return Scheme(relay=True, overlap=bool(sw["overlap"]))
+            # ce_transport=True: the relay chains run on copy engines
+            return Scheme(relay=True, overlap=bool(sw["overlap"]), ce_transport=sw["ce_transport"] is True)
         # Staged gather: True = every phase with remote reads; "auto" = from 4
         # GPUs on, all-gather-shaped phases that copy-engine runs do not cover.
         if sw["staged"] and (sw["staged"] != "auto" or (
@@ -761,6 +762,8 @@ class RankRealloc:
         if sw["relay"] and any(len({self.host_of[d] for d in dsts} - {self.host_of[s]}) >= 2
                                for s, dsts, _r in p.lowered()):
             out.append(Scheme(relay=True, overlap=bool(sw["overlap"])))
+            if sw["ce_transport"]:  # relay chains on copy engines
+                out.append(Scheme(relay=True, overlap=bool(sw["overlap"]), ce_transport=True))
         if sw["staged"]:
             out.append(Scheme(staged=True))
         if sw["ce_transport"]:
@@ -988,7 +991,8 @@ class RankRealloc:
                           self.chunk_bytes, host_of=self.host_of if self.hierarchical else None,
                           mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_table, relay_chain=sc.relay,
                           overlap_fanout=sc.overlap, ce_min_run_bytes=self.ce_min_run_bytes,
-                          ce_transport=2 if sc.ce_hybrid else int(sc.ce_transport),
+                          ce_transport=(3 if sc.relay and sc.ce_transport else 2 if sc.ce_hybrid
+                                        else int(sc.ce_transport)),
                           n_hosts=world if ce_flag else 0,
                           ce_flags=ce_flags if ce_flag else None)
         if self.kernel is not None:

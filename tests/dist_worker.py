@@ -168,6 +168,12 @@ class Worker:
                 seed = SPECIAL | 29 if kernel else 29
                 self.run(f"relay kernel={kernel} {src.strategy}->{dst.strategy} seed={seed:#x}", TINY_GQA, src, dst,
                          seed, reps=3, relay=True, kernel=kernel, flag_kernel=kernel)
+                # the same chains on copy engines (hop-by-hop pieces, stream
+                # wait/write flags), plain and onloaded, with and without star
+                for overlap in (False, True):
+                    self.run(f"ce-relay kernel={kernel} overlap={overlap} {src.strategy}->{dst.strategy} (+onload)",
+                             TINY_GQA, src, dst, SPECIAL | 30, reps=3, onload_chunk=32 << 10, relay=True,
+                             ce_transport=True, overlap=overlap, kernel=kernel, flag_kernel=kernel)
 
     def ce_runs_cases(self):
         """Copy-engine runs on stage remaps (forced down to 4 KiB ranges so the
