@@ -321,8 +321,9 @@ void host_wire_bytes(const std::vector<LoweredOp>& ops, const HostMap& hm, int64
     const int hs = hm.host[static_cast<size_t>(op.src)];
     const int64_t b = op_bytes(op);
     const auto groups = by_host(op, hm);
-    if (!hm.relay_flags.empty() && relay_eligible(op, groups, hm)) {
-      // relay: every chain host receives one copy; all but the last send one
+    if ((!hm.relay_flags.empty() && relay_eligible(op, groups, hm)) || ce_relay_op(op, hm)) {
+      // relay (SM or copy-engine): every chain host receives one copy; all
+      // but the last send one
       const std::vector<int> chain = relay_chain(groups, hs);
       if (hs == hm.me) o += b;
       const auto at = std::find(chain.begin(), chain.end(), hm.me);
