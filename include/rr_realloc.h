@@ -322,7 +322,11 @@ typedef struct {
    * staging, no unpack pass. Copy engines carry more payload per NVLink byte
    * than SM stores (~780 vs ~710 GB/s). Excludes relay / overlapped fan-out
    * jobs (they stay on SM stores); copy-engine runs are not used with it.
-   * 0 = off. */
+   * 0 = off; 1 = on; 2 = hybrid: row-parallel pieces whose layers do not
+   * merge into one 3D copy (per-layer 2D copies) stay on SM peer stores
+   * beside the copy engines; 3 = on, and payloads reaching >= 2 other hosts
+   * travel host to host by copy engines in <= 256 MiB pieces (copy-engine
+   * relay; needs ce_flags). */
   int32_t ce_transport;
   /* Copy flags (with ce_transport; host ids 0..n_hosts-1): ce_flags[h] =
    * host h's copy flag array (rr_plan_ce_slots uint32, mapped here; zero at
