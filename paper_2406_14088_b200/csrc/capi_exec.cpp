@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <vector>
@@ -286,6 +287,8 @@ void launch_phase(rr_exec* ex, const rr_exec::Phase& ph, void* stream, int ctas,
 // Flag-synchronised phases keep the slot granularity every rank agrees on.
 constexpr int64_t kItemsPerBulkCta = 16;
 constexpr int64_t kMinBulkChunk = int64_t{32} << 10;
+constexpr int64_t kWriteWindowMiB = 16;               // see refine_chunk
+constexpr int64_t kMinWindowChunk = int64_t{16} << 10;  // one ring stage
 
 rr::ItemSet refine_chunk(rr::ItemSet set, const std::vector<rr::Job>& jobs, int phase, const rr::HostMap& hm,
                          void* const* src_bufs, void* const* dst_bufs, int ldst_ctas, int bulk_ctas,
@@ -294,10 +297,25 @@ rr::ItemSet refine_chunk(rr::ItemSet set, const std::vector<rr::Job>& jobs, int 
   if (std::any_of(set.items.begin(), set.items.end(),
                   [](const rr::CopyItem& it) { return it.wait_flag || it.signal_flag; }))
     return set;
-  const int64_t chunk =
+  int64_t chunk =
       set.written < kSmallPhaseBytes
           ? std::max<int64_t>(kMinSmallChunk, (set.read / std::max(1, ldst_ctas)) & ~int64_t{15})
           : std::max<int64_t>(kMinBulkChunk, (set.read / (kItemsPerBulkCta * std::max(1, bulk_ctas))) & ~int64_t{15});
+  if (set.written >= kSmallPhaseBytes && !set.remote_stores) {
+    // Write window (HBM phases): every resident CTA stores its current item
+    // to each of the item's destinations, so CTAs x item x fan-out bytes are
+    // being written at once. Keeping that near 16 MiB keeps the DRAM write
+    // streams local: the 7B forward (a 1:8 broadcast) gets 16 KiB items, the
+    // 1:1 back phase ~37 KiB; the default step is 1.9% faster than with
+    // 256 KiB items (profiles/r02_window_sweep_n1.txt; 8 MiB starves the 1:1
+    // phase, >= 64 MiB loses the gain). Phases with peer stores keep their
+    // item size. RR_WRITE_WINDOW_MIB overrides it for sweeps (0 = off).
+    const char* env = std::getenv("RR_WRITE_WINDOW_MIB");
+    const int64_t window = (env ? std::atoll(env) : kWriteWindowMiB) << 20;
+    const double fanout = set.read > 0 ? static_cast<double>(set.written) / static_cast<double>(set.read) : 1.0;
+    const int64_t w = static_cast<int64_t>(static_cast<double>(window) / (std::max(1, bulk_ctas) * fanout)) & ~int64_t{15};
+    if (window > 0) chunk = std::min(chunk, std::max(kMinWindowChunk, w));
+  }
   if (chunk >= kDefaultChunk) return set;
   return rr::build_items(jobs, phase, hm, src_bufs, dst_bufs, chunk, ce);
 }
