@@ -5,6 +5,7 @@
 #include "exec_plan.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -604,6 +605,12 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
       all_tma = all_tma && t.it.vec == kItemVec;
     }
   }
+  const char* order_env = std::getenv("RR_ITEM_ORDER");
+  const bool sequential = order_env && std::string(order_env) == "seq" && !acc.remote_stores && !flagged;
+  if (sequential) {  // experiment: HBM-only phases claimed job by job (contiguous write windows)
+    for (const auto& st : streams)
+      for (const auto& t : st) (t.it.vec == kItemVec ? vec_items : other).push_back(&t);
+  } else
   for (size_t k = 0, seen = 0; seen < total; ++k)
     for (int waiting = 0; waiting < 2; ++waiting)
       for (const auto& st : streams)
