@@ -605,9 +605,16 @@ ItemSet build_items(const std::vector<Job>& jobs, int phase, const HostMap& hm, 
       all_tma = all_tma && t.it.vec == kItemVec;
     }
   }
+  // HBM-only 1:1 phases are claimed job by job (each CTA walks consecutive
+  // rows: contiguous read and write windows; the 7B back phase 4.72 -> 4.67
+  // ms); broadcasts (fan-out >= 2) stay interleaved, which is faster for
+  // them (forward 22.52 vs 22.31 ms; profiles/r02_order_sweep_n1.txt).
+  // RR_ITEM_ORDER=rr|seq overrides the choice for sweeps.
   const char* order_env = std::getenv("RR_ITEM_ORDER");
-  const bool sequential = order_env && std::string(order_env) == "seq" && !acc.remote_stores && !flagged;
-  if (sequential) {  // experiment: HBM-only phases claimed job by job (contiguous write windows)
+  const bool one_to_one = acc.read > 0 && acc.written < acc.read + acc.read / 2;
+  const bool sequential = !acc.remote_stores && !flagged &&
+                          (order_env ? std::string(order_env) == "seq" : one_to_one);
+  if (sequential) {
     for (const auto& st : streams)
       for (const auto& t : st) (t.it.vec == kItemVec ? vec_items : other).push_back(&t);
   } else
