@@ -128,8 +128,7 @@ def workload_config(w) -> dict:
     def s(p):
         st = p.strategy
         return f"(pp{st.pp},dp{st.dp},tp{st.tp})"
-    return {"workload": w.name, "description": w.description,
-            "model": "data" if w.data_bytes else w.model.name, "plan_devices": w.devices,
+    return {"workload": w.name, "description": w.description, "plan_devices": w.devices,
             "phases": [f"{s(a)}->{s(b)}" for a, b in w.phases],
             "l2": "inputs larger than L2 (multi-GB shards); no flush needed",
             "weights": "hash-initialised bf16 (seed 1); every destination shard checked after timing"}
