@@ -620,7 +620,7 @@ def run_b200(args) -> None:
             # step, and per phase over that phase's kernel time (the slowest rank's)
             "nvlink_gbs_per_rank": ([round(float(x) / (ms_max * 1e-3) / 1e9, 2)
                                      for x in allv[:, 3 + P:3 + 2 * P].sum(axis=1)] if world > 1 else None),
-            "nvlink_gbs_per_rank_phase": ([[round(float(allv[r, 3 + P + i]) / (float(ph_ms_all[:, i].max()) * 1e-3) / 1e9, 1)
+            "nvlink_gbs_per_rank_phase": ([[round(float(allv[r, 3 + P + i]) / (max(float(ph_ms_all[:, i].max()), 1e-6) * 1e-3) / 1e9, 1)
                                             for i in range(P)] for r in range(world)] if world > 1 else None),
             "bytes_per_step": int(total_written),
             "roofline": roof,
