@@ -478,29 +478,41 @@ int64_t orc_shard_bytes(const orc_model* m, const orc_placement* p, const orc_cl
 
 /* Special-value mode (seed bit 62): class c = bits 24..27 of the hash picks
  * one of seven bf16 special classes (c < 7) or the raw low 16 bits; bit 16 is
- * the sign, bits 17..23 a 7-bit field m for payloads / denormal mantissas. */
-static uint16_t orc_special(uint64_t z) {
-  const unsigned cls = (unsigned)((z >> 24) & 15u);
-  const unsigned s = (unsigned)((z >> 16) & 1u) ? 0x8000u : 0u;
-  const unsigned m = (unsigned)((z >> 17) & 0x7fu);
-  if (cls == 0) return (uint16_t)s;                                   /* signed zero */
-  if (cls == 1) return (uint16_t)(s + 0x7f80u);                       /* infinity */
-  if (cls == 2) return (uint16_t)(s + 0x7f80u + 0x40u + (m % 64u));   /* quiet NaN + payload */
-  if (cls == 3) return (uint16_t)(s + 0x7f80u + 1u + (m % 63u));      /* signalling NaN */
-  if (cls == 4) return (uint16_t)(s + (m | 1u));                      /* subnormal */
-  if (cls == 5) return (uint16_t)(s + 0x7f7fu);                       /* largest finite */
-  if (cls == 6) return (uint16_t)(s + 0x80u);                         /* smallest normal */
-  return (uint16_t)(z & 0xffffu);
+ * the sign, bits 17..23 a 7-bit field m for payloads / denormal mantissas.
+ * Written branch-free (selects), so the checker's row loop vectorises. */
+static inline uint64_t hash_of(uint64_t seed, uint64_t tensor, uint64_t index) {
+  uint64_t z = (seed ^ (tensor << 40) ^ index) + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static inline uint16_t normal_of(uint64_t z) {
+  const uint32_t sign = (uint32_t)(z >> 63), expo = 117u + (uint32_t)((z >> 8) & 7u);
+  return (uint16_t)((sign << 15) | (expo << 7) | (uint32_t)(z & 0x7fu));
+}
+
+static inline uint16_t special_of(uint64_t z) {
+  const uint32_t cls = (uint32_t)((z >> 24) & 15u);
+  const uint32_t s = (uint32_t)((z >> 16) & 1u) << 15;
+  const uint32_t m = (uint32_t)((z >> 17) & 0x7fu);
+  const uint32_t m63 = m - 63u * (uint32_t)(m >= 63u) - 63u * (uint32_t)(m >= 126u); /* m % 63 */
+#define ORC_PICK(k, val) v = (v & ~(0u - (uint32_t)(cls == (k)))) | ((val) & (0u - (uint32_t)(cls == (k))))
+  uint32_t v = (uint32_t)(z & 0xffffu);      /* any 16-bit pattern (classes 7..15) */
+  ORC_PICK(0u, s);                           /* signed zero */
+  ORC_PICK(1u, s + 0x7f80u);                 /* infinity */
+  ORC_PICK(2u, s + 0x7fc0u + (m & 63u));     /* quiet NaN + payload */
+  ORC_PICK(3u, s + 0x7f81u + m63);           /* signalling NaN */
+  ORC_PICK(4u, s + (m | 1u));                /* subnormal */
+  ORC_PICK(5u, s + 0x7f7fu);                 /* largest finite */
+  ORC_PICK(6u, s + 0x80u);                   /* smallest normal */
+#undef ORC_PICK
+  return (uint16_t)v;
 }
 
 uint16_t orc_value(uint64_t seed, int64_t tensor, int64_t index) {
-  uint64_t z = (seed ^ ((uint64_t)tensor << 40) ^ (uint64_t)index) + 0x9E3779B97F4A7C15ull;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  z ^= z >> 31;
-  if ((seed >> 62) & 1u) return orc_special(z);
-  const uint32_t sign = (uint32_t)(z >> 63), expo = 117u + (uint32_t)((z >> 8) & 7u);
-  return (uint16_t)((sign << 15) | (expo << 7) | (uint32_t)(z & 0x7fu));
+  const uint64_t z = hash_of(seed, (uint64_t)tensor, (uint64_t)index);
+  return (seed >> 62) & 1u ? special_of(z) : normal_of(z);
 }
 
 int orc_fill(const orc_model* m, const orc_placement* p, const orc_cluster* c, int dev,
@@ -540,6 +552,10 @@ static int64_t local_rows(const orc_model* m, const tensor_loc* t, int64_t id, i
   return t->mode == MODE_COLS || t->mode == MODE_FULL ? s.rows : t->hi - t->lo;
 }
 
+/* The checker computes every element of multi-GB shards: the row loop is
+ * compiled twice, for AVX-512 (x86-64-v4: eight 64-bit hash lanes per
+ * instruction) and baseline x86-64, and picked at load time. */
+__attribute__((target_clones("arch=x86-64-v4", "default")))
 static void fill_window(const orc_model* m, const dev_layout* L, uint64_t seed, int64_t off, int64_t len,
                         uint16_t* buf) {
   const int64_t pb = m->param_bytes, end = off + len;
@@ -565,7 +581,13 @@ static void fill_window(const orc_model* m, const dev_layout* L, uint64_t seed, 
       if (a < off) ca = c0 + (off - a) / pb;
       if (a + row_bytes > end) cb = c0 + (end - a) / pb;
       const int64_t at = (a - off) / pb - c0; /* window element of column 0 of this row */
-      for (int64_t col = ca; col < cb; ++col) buf[at + col] = orc_value(seed, id, r * s.cols + col);
+      const uint64_t row0 = (uint64_t)(r * s.cols);
+      if ((seed >> 62) & 1u)
+        for (int64_t col = ca; col < cb; ++col)
+          buf[at + col] = special_of(hash_of(seed, (uint64_t)id, row0 + (uint64_t)col));
+      else
+        for (int64_t col = ca; col < cb; ++col)
+          buf[at + col] = normal_of(hash_of(seed, (uint64_t)id, row0 + (uint64_t)col));
     }
   }
 }

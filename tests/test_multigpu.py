@@ -52,7 +52,7 @@ def _report(r, world):
 @pytest.mark.parametrize("world", [2, 4])
 def test_multiprocess_on_one_gpu(need_gpu, world):
     r = _torchrun(world, {"CUDA_VISIBLE_DEVICES": os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0],
-                          "RR_FUZZ_CASES": "16"})
+                          "RR_FUZZ_CASES": "10", "RR_QUICK": "1"})
     _report(r, world)
 
 
