@@ -34,11 +34,23 @@ def _free_port() -> int:
 
 
 def _torchrun(n: int, env_extra=None, timeout=900):
+    """Run the worker under torchrun in its own process group; on timeout the
+    whole group (launcher and every rank) is killed, so no rank is left
+    holding the GPU."""
+    import signal
     env = dict(os.environ)
     env.update(env_extra or {})
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "dist_worker.py")]
-    return subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout)
+    proc = subprocess.Popen(cmd, env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
+                            start_new_session=True)
+    try:
+        out, err = proc.communicate(timeout=timeout)
+    except subprocess.TimeoutExpired:
+        os.killpg(proc.pid, signal.SIGKILL)
+        out, err = proc.communicate()
+        pytest.fail(f"torchrun world {n} timed out after {timeout} s:\n{out[-3000:]}\n{err[-3000:]}")
+    return subprocess.CompletedProcess(cmd, proc.returncode, out, err)
 
 
 def _report(r, world):
