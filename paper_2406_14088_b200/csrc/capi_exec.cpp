@@ -152,7 +152,8 @@ struct rr_exec {
   int64_t ce_bytes = 0;
   // Staged gather, sender side: whole local source shards pushed piece by
   // piece into the other hosts' staging buffers, each piece followed by a
-  // one-thread kernel that flags it in the receiver's stage flag array.
+  // stream write (signal_piece) that flags it in the receiver's stage flag
+  // array.
   struct StagePush {
     void* dst;
     const void* src;
