@@ -1070,6 +1070,9 @@ bool ce_relay_op(const LoweredOp& op, const HostMap& hm) {
 std::vector<CeRelayOp> ce_relay_ops(const std::vector<LoweredOp>& ops, const HostMap& hm) {
   std::vector<CeRelayOp> out;
   int64_t slot = 0;
+  // RR_RELAY_PIECE_MIB overrides the piece size for sweeps (identical on every rank)
+  const char* env = std::getenv("RR_RELAY_PIECE_MIB");
+  const int64_t kRelayPieceBytes = env ? std::max<int64_t>(1, std::atoll(env)) << 20 : rr::kRelayPieceBytes;
   for (const auto& op : ops) {
     if (!ce_relay_op(op, hm)) continue;
     CeRelayOp r;
