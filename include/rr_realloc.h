@@ -346,7 +346,9 @@ typedef struct {
 rr_status rr_plan_relay_slots(const rr_plan* plan, const int32_t* host_of, int64_t chunk_bytes, int relay_chain,
                               int overlap_fanout, int64_t* slots);
 /* Staged gather: length of the stage flag array every host allocates (the
- * maximum over hosts of its pieces) for this host map and piece size. */
+ * maximum over hosts of its pieces, then one round token per host: round r's
+ * push into a receiver waits, on the copy stream, for the round r-1 sender
+ * into that receiver to finish) for this host map and piece size. */
 rr_status rr_plan_stage_slots(const rr_plan* plan, const int32_t* host_of, int64_t chunk_bytes, int64_t* slots);
 /* Copy-engine runs a push executor driving `local` (with `host_of`) would
  * issue, host only: 5 int64 per run {src device, dst device, src byte

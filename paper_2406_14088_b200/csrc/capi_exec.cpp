@@ -157,10 +157,15 @@ struct rr_exec {
   struct StagePush {
     void* dst;
     const void* src;
-    size_t bytes;
-    uint32_t* flag;
+    size_t bytes;      // 0: a round with nothing to send (it still passes the round token)
+    uint32_t* flag;    // this piece's slot in the receiver's stage flag array (null when bytes == 0)
     DeviceId src_dev;  // source plan device and byte offset in its shard (onload pipelining)
     int64_t src_off;
+    // Round alignment: the first push of round r waits until the previous
+    // round's sender into the same receiver is done (`wait`, this host's
+    // array); the last push of the round passes the token on (`done`).
+    uint32_t* wait = nullptr;
+    uint32_t* done = nullptr;
   };
   std::vector<StagePush> stage;
   int64_t stage_bytes = 0;
@@ -386,9 +391,28 @@ void ce_issue(rr_exec* ex, cudaStream_t after, cudaEvent_t after_event = nullptr
     if (c.done) signal_piece(ex->ce_stream, c.done, ex->epoch);
   }
   for (const auto& p : ex->stage) {
-    check_cuda(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "staged push");
-    signal_piece(ex->ce_stream, p.flag, ex->epoch);
+    if (p.wait) wait_piece(ex->ce_stream, p.wait, ex->epoch);
+    if (p.bytes) {
+      check_cuda(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "staged push");
+      signal_piece(ex->ce_stream, p.flag, ex->epoch);
+    }
+    if (p.done) signal_piece(ex->ce_stream, p.done, ex->epoch);
   }
+}
+
+// Staged gather: the round tokens sit after every host's piece slots, at the
+// same offset in every host's stage flag array (the largest piece count).
+int64_t stage_sched_base(const rr_plan* plan, const rr::HostMap& hm, const std::vector<int64_t>& src_bytes) {
+  std::vector<int> hosts(hm.host.begin(), hm.host.end());
+  std::sort(hosts.begin(), hosts.end());
+  hosts.erase(std::unique(hosts.begin(), hosts.end()), hosts.end());
+  int64_t best = 0;
+  for (int h : hosts) {
+    int64_t k = 0;
+    rr::stage_slots(plan->lowered, hm.host, h, src_bytes, hm.stage_chunk, &k);
+    best = std::max(best, k);
+  }
+  return best;
 }
 
 // Largest row pitch a 2D / 3D copy accepts on this device.
@@ -450,7 +474,7 @@ rr_status rr_plan_stage_slots(const rr_plan* plan, const int32_t* host_of, int64
       rr::stage_slots(plan->lowered, host, h, src_bytes, chunk_bytes, &k);
       best = std::max(best, k);
     }
-    *slots = best;
+    *slots = best + static_cast<int64_t>(hosts.size()) + 1;  // + the round tokens (stage_sched_base)
   });
 }
 
@@ -706,7 +730,14 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       const int64_t n_relay = rr::relay_slots(plan->lowered, hm);
       require_zero_flags(options->relay_flags[local[0]], n_relay, "relay_flags");
     }
-    if (staged) require_zero_flags(options->stage_flags[hm.me], n_stage_slots, "stage_flags");
+    if (staged) {
+      std::vector<int> hs(hm.host.begin(), hm.host.end());
+      std::sort(hs.begin(), hs.end());
+      hs.erase(std::unique(hs.begin(), hs.end()), hs.end());
+      require_zero_flags(options->stage_flags[hm.me],
+                         std::max(n_stage_slots, stage_sched_base(plan, hm, src_bytes) + static_cast<int64_t>(hs.size()) + 1),
+                         "stage_flags");
+    }
     if (hm.ce_remote && options->ce_flags) require_zero_flags(options->ce_flags[hm.me], n_ce_slots, "ce_flags");
 
     auto ex = std::make_unique<rr_exec>();
@@ -817,10 +848,24 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
       hosts.erase(std::unique(hosts.begin(), hosts.end()), hosts.end());
       const int H = static_cast<int>(hosts.size());
       const int pos = static_cast<int>(std::find(hosts.begin(), hosts.end(), hm.me) - hosts.begin());
+      // Rounds stay aligned without a barrier: the round-r push into host h
+      // waits for the round-(r-1) sender into h (the host one place after
+      // this one) to finish, which raises slot sched_base + r in this
+      // host's stage flag array; after its own round r this host raises slot
+      // sched_base + r + 1 in the array of the host one place before it (the
+      // round-(r+1) sender into h). Waits point only to the previous round:
+      // no cycle. Unaligned, a sender whose round ran short pushed into a
+      // receiver still taking the previous round's sender.
+      const int64_t sched_base = stage_sched_base(plan, hm, src_bytes);
+      const int prev_host = hosts[static_cast<size_t>((pos + H - 1) % H)];
+      auto* my_flags = static_cast<uint32_t*>(options->stage_flags[hm.me]);
+      auto* prev_flags = static_cast<uint32_t*>(options->stage_flags[prev_host]);
+      need(my_flags != nullptr && prev_flags != nullptr, "missing a stage flag array");
       for (int r = 1; r < H; ++r) {
         const int h = hosts[static_cast<size_t>((pos + r) % H)];
         int64_t n_slots = 0;
         const auto slot0 = rr::stage_slots(plan->lowered, hm.host, h, src_bytes, hm.stage_chunk, &n_slots);
+        const size_t first = ex->stage.size();
         for (DeviceId sdev : rr::stage_sources(plan->lowered, hm.host, h)) {
           if (hm.host[static_cast<size_t>(sdev)] != hm.me) continue;
           void* remote = options->stage_remote[static_cast<size_t>(sdev) * options->n_hosts + h];
@@ -835,6 +880,10 @@ rr_status rr_exec_create_ex(const rr_plan* plan, int cuda_device, int n_devices,
             ex->stage_bytes += nb;
           }
         }
+        if (ex->stage.size() == first)  // nothing for h this round: the token still passes
+          ex->stage.push_back({nullptr, nullptr, 0, nullptr, -1, 0});
+        if (r > 1) ex->stage[first].wait = my_flags + sched_base + r;
+        if (r + 1 < H) ex->stage.back().done = prev_flags + sched_base + r + 1;
       }
     }
     if (!ex->ce.empty() || !ex->stage.empty()) {
@@ -1136,8 +1185,13 @@ rr_status rr_exec_launch_onload(rr_exec* ex, void* const* host_bufs, void* copy_
                      "cudaStreamWaitEvent(staged push)");
           waited = last;
         }
-        check_cuda(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "staged push");
-        signal_piece(ex->ce_stream, p.flag, ex->epoch);
+        // (round waits are skipped here: pushes follow the onload's chunk
+        // order, not the rounds'; the tokens are still passed on)
+        if (p.bytes) {
+          check_cuda(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyDeviceToDevice, ex->ce_stream), "staged push");
+          signal_piece(ex->ce_stream, p.flag, ex->epoch);
+        }
+        if (p.done) signal_piece(ex->ce_stream, p.done, ex->epoch);
       }
     }
     if (!ex->ce.empty()) {

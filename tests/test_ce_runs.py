@@ -69,10 +69,11 @@ def test_stage_slots_7b_all_gather(world, expect):
     w = WORKLOADS["llama7b_tp8_dp8_roundtrip"]
     plan = plan_param_realloc(w.model, *w.phases[0], w.cluster(), BALANCED)
     host_of = _hosts(8, world)
-    assert R.stage_slots(plan, host_of, 512 << 20) == expect
+    # piece slots, then one round token per host (+1) for the aligned rounds
+    assert R.stage_slots(plan, host_of, 512 << 20) == expect + world + 1
     # the gen -> train phase reads only local replicas: nothing to stage
     back = plan_param_realloc(w.model, *w.phases[1], w.cluster(), BALANCED)
-    assert R.stage_slots(back, host_of, 512 << 20) == 0
+    assert R.stage_slots(back, host_of, 512 << 20) == world + 1
 
 
 @pytest.mark.parametrize("world", [4, 8])
