@@ -145,7 +145,7 @@ def build(config: Dict[str, Any], data: bool = False) -> Dict[str, Any]:
     host_of = [d // k for d in range(n)]
     out["device_traffic"] = {str(d): dict(zip(("wire_in", "wire_out", "local"), plan.device_traffic(d)))
                              for d in range(n)}
-    out["b200_estimate"] = costmodel.estimate_seconds(plan, host_of)
+    out["b200_estimate"] = costmodel.estimate_best(plan, host_of)
     return out
 
 

@@ -19,7 +19,11 @@ actually takes on B200, from the same lowered work the kernels run:
   pipelined onload overlaps phase 0, so that phase takes the longer of the
   two.
 
-Constants are the r01 measurements (profiles/).
+* the copy-engine transport (r02) by the library's own schedule simulation
+  (`estimate_best` picks the fastest scheme, as the bind-time probe does by
+  measurement).
+
+Constants are the r01/r02 measurements (profiles/).
 """
 from __future__ import annotations
 
@@ -48,10 +52,27 @@ def host_transfer_seconds(nbytes_per_gpu: int, profile: B200Profile = B200Profil
     return nbytes_per_gpu / (profile.host_link_gbs * 1e9)
 
 
+def estimate_best(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
+                  profile: B200Profile = B200Profile()) -> Dict[str, float]:
+    """The fastest delivery scheme by this model (what the bind-time probe
+    measures at run time): SM peer stores with copy-engine runs, the
+    pipelined relay, the staged gather, and the copy-engine transport
+    (schedule makespan, r02), with the scheme's name under "scheme"."""
+    est = {"push": estimate_seconds(plan, host_of, profile)}
+    n = plan.cluster.device_count()
+    host = list(host_of) if host_of is not None else list(range(n))
+    if len(set(host)) > 1:
+        est["relay"] = estimate_seconds(plan, host_of, profile, relay=True)
+        est["staged"] = estimate_seconds(plan, host_of, profile, staged=True)
+        est["ce_transport"] = estimate_seconds(plan, host_of, profile, ce_transport=True)
+    name = min(est, key=lambda k: est[k]["seconds"])
+    return {**est[name], "scheme": name}
+
+
 def estimate_seconds(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
                      profile: B200Profile = B200Profile(), multicast: bool = False,
                      relay: bool = False, onload: bool = False, copy_engine: bool = True,
-                     staged: bool = False) -> Dict[str, float]:
+                     staged: bool = False, ce_transport: bool = False) -> Dict[str, float]:
     """Estimated execution time of `plan` with plan device d hosted on GPU
     host_of[d] (default: one GPU per plan device). `relay`: payloads reaching
     >= 2 other GPUs use the pipelined relay (one copy in and out per GPU,
@@ -61,7 +82,19 @@ def estimate_seconds(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
     copy-engine runs (the executor default; not combined with relay or
     multicast here). `staged`: the remote bytes move as a staged gather
     (copy-engine rotation rounds into staging buffers, then an unpack that
-    reads them once more from HBM)."""
+    reads them once more from HBM). `ce_transport`: every remote piece moves
+    by copy engine as merged 2D/3D copies following the library's schedule
+    (its simulated makespan, rr_plan_ce_schedule), the in-host fan-out
+    overlapped (copy-engine star)."""
+    if ce_transport:
+        from .runtime import ce_transport_estimate
+        n = plan.cluster.device_count()
+        host = list(host_of) if host_of is not None else list(range(n))
+        if len(set(host)) > 1:
+            ce, _sm = ce_transport_estimate(plan, host, star=True)
+            fixed = (profile.launch_us + profile.barrier_us) * 1e-6
+            base = estimate_seconds(plan, host_of, profile, copy_engine=False)
+            return {**base, "seconds": ce + fixed, "phase0_s": ce, "fanout_s": 0.0}
     n = plan.cluster.device_count()
     host = list(host_of) if host_of is not None else list(range(n))
     hosts = sorted(set(host))
@@ -115,8 +148,18 @@ def estimate_seconds(plan: ReallocPlan, host_of: Optional[Sequence[int]] = None,
             ingress[h] = max(0, ingress[h] - ce_in[h])
 
     if staged and len(hosts) > 1:
+        # the staged gather moves WHOLE source shards to every host that
+        # reads any of their bytes (rr_plan_stage_slots), not just the bytes
+        # read; staging is written, then read back by the unpack, which
+        # writes every local replica
+        reads = {(s, host[d]) for s, dsts, _r in plan.lowered() for d in dsts if host[d] != host[s]}
+        ingress = {h: 0 for h in hosts}
+        egress = {h: 0 for h in hosts}
+        for s, h in reads:
+            ingress[h] += plan.shard_bytes(0, s)
+            egress[host[s]] += plan.shard_bytes(0, s)
         for h in hosts:
-            hbm[h] += 2 * ingress[h] + fan[h]  # staging written, read back; the unpack writes every replica
+            hbm[h] += 2 * ingress[h] + fan[h]
             fan[h] = 0
 
     def link_s(h: int) -> float:
