@@ -183,3 +183,19 @@ def test_realloc_plan_cli_replicated_kv_heads(tmp_path):
     p.write_text(json.dumps(cfg))
     with pytest.raises(cli.ConfigError, match="kv_layout"):
         cli.build(json.load(open(p)))
+
+
+@pytest.mark.parametrize("name,world,measured_ms,scheme", [
+    ("llama70b_pp2tp4_to_tp8", 4, 46.50, "ce_transport"),   # profiles/r02_configs_n4.jsonl
+    ("llama70b_pp2tp4_to_tp8", 2, 47.31, "ce_transport"),   # profiles/r02_configs_n2.jsonl
+    ("llama34b_critic_pp4tp2_to_tp8", 4, 19.20, "ce_transport"),
+    ("llama7b_tp8_dp8_roundtrip", 4, 16.07, "staged"),
+])
+def test_estimate_best_matches_round2_measurements(name, world, measured_ms, scheme):
+    """The cost-model twin of the bind-time probe picks the scheme the probe
+    picked on the B200s and lands within 5% of its measured phase time."""
+    from paper_2406_14088_b200.workloads import WORKLOADS
+    plan = WORKLOADS[name].plans(BALANCED)[0]
+    est = costmodel.estimate_best(plan, [d * world // 8 for d in range(8)])
+    assert est["scheme"] == scheme
+    assert est["seconds"] * 1e3 == pytest.approx(measured_ms, rel=0.05)
