@@ -52,6 +52,37 @@ def pl(spec):
     return placement(8, *spec[:3], qkv=spec[3], gate_up=spec[4])
 
 
+PAGE = 2 << 20  # rr_device_alloc pads every allocation to whole 2 MiB pages
+GUARD = 0xA5
+
+
+def guard_tails(bufs):
+    """compute-sanitizer is closed on this pool: out-of-bounds stores are
+    caught instead by a known pattern in the padding after every local
+    shard (up to 64 KiB of it), checked after each launch."""
+    from paper_2406_14088_b200._lib import check, lib
+    out = []
+    for b in bufs:
+        if not isinstance(b, R.DeviceBuffer):
+            continue
+        start = max(b.nbytes, 256)
+        tail = min((max(b.nbytes, 256) + PAGE - 1) // PAGE * PAGE - start, 64 << 10)
+        if tail > 0:
+            check(lib.rr_memset(b.ptr + start, GUARD, tail, None))
+            out.append((b, start, tail))
+    return out
+
+
+def tails_intact(guards) -> bool:
+    from paper_2406_14088_b200._lib import check, lib
+    for b, start, tail in guards:
+        h = np.empty(tail, np.uint8)
+        check(lib.rr_memcpy(h.ctypes.data, b.ptr + start, tail, 1, None, 1))
+        if not (h == GUARD).all():
+            return False
+    return True
+
+
 class Worker:
     def __init__(self):
         self.rank, self.world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -106,6 +137,7 @@ class Worker:
                     if zero_between:
                         for b in rr.buffers["b"].values():
                             b.zero()
+                    guards = guard_tails(list(rr.buffers["a"].values()) + list(rr.buffers["b"].values()))
                     torch.cuda.synchronize()
                     dist.barrier()
                     hosts = None
@@ -124,6 +156,9 @@ class Worker:
                         if not np.array_equal(got, want):
                             self.failures.append(f"{label} rep {rep}: device {d} differs in "
                                                  f"{int(np.count_nonzero(got != want))} elements")
+                    dist.barrier()  # every rank's stores are done before the guards are read
+                    if not tails_intact(guards):
+                        self.failures.append(f"{label} rep {rep}: a store landed past the end of a shard")
                     for hb in (hosts or {}).values():
                         hb.free()
                 if rr.relay_timeouts() or rr.barrier.timed_out():
