@@ -95,11 +95,12 @@ def reference_outputs() -> dict:
 def weights_kat() -> dict:
     from oracle import oracle as O
     cases = []
-    for seed in (0, 1, 5, 2**63 + 7):
+    for seed in (0, 1, 5, 2**63 + 7, O.SEED_SPECIAL | 3, O.SEED_SPECIAL | (2**63 + 9)):
         for tensor in (0, 1, 2, 100, 723):
             for idx in (0, 1, 255, 4096, 123456789, 2**39 - 1):
                 cases.append([seed, tensor, idx, O.value(seed, tensor, idx)])
-    return {"function": "splitmix64(seed ^ tensor<<40 ^ index) -> bf16 bits (DESIGN.md §4)", "cases": cases}
+    return {"function": "splitmix64(seed ^ tensor<<40 ^ index) -> bf16 bits (DESIGN.md §3; seed bit 62: special values)",
+            "cases": cases}
 
 
 def main() -> None:
