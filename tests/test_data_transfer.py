@@ -169,3 +169,25 @@ def test_reference_arm_workloads_match_product():
                 assert O.plan_data(ps, pd, pw.cluster, w.data_bytes, 1) == O.plan_data(s, d, w.cluster(), w.data_bytes, 1)
             else:
                 assert O.plan(pw.model, ps, pd, pw.cluster, 1) == O.plan(w.model, s, d, w.cluster(), 1)
+
+
+def test_reference_arm_never_loads_the_product():
+    """`bench.py --impl reference` runs the oracle's CPU reallocation on
+    product-free workload objects: the process never maps librrealloc.so
+    nor imports the package (the old reference arm did)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--workload', 'tiny_tp2_to_dp2', "
+            "'--steps', '2', '--warmup', '1']; runpy.run_path('bench.py', run_name='__main__'); "
+            "maps = open('/proc/self/maps').read(); "
+            "print('PRODUCT' if 'librrealloc' in maps or any(m.startswith('paper_2406_14088_b200') "
+            "for m in sys.modules) else 'CLEAN')")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = r.stdout.strip().splitlines()
+    assert lines[-1] == "CLEAN", r.stdout
+    import json
+    line = json.loads(lines[-2])
+    assert line["impl"] == "reference" and line["verified"] and line["cpu_baseline"]["kind"] == "port"
