@@ -337,7 +337,8 @@ class Worker:
                       chunk_bytes=rng.choice([0, 8192, 65536]),
                       ce_min_run_bytes=rng.choice([-1, 0, 4096]),  # off, default (256 MiB: none here), >= 4 KiB
                       staged=rng.random() < 0.25, stage_chunk_bytes=32 << 10,
-                      ce_transport=rng.random() < 0.3)
+                      ce_transport=rng.random() < 0.3,
+                      probe=rng.random() < 0.15)  # bind-time probe: every allowed scheme, fastest kept
             kw["kernel"] = kw["flag_kernel"] = rng.choice([0, 1, 5])
             policy = rng.choice([0, 1])
             seed = (SPECIAL if i % 3 == 0 else 0) | (50 + i)
