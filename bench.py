@@ -570,13 +570,15 @@ def run_b200(args) -> None:
                                                                "~710, one copy-engine copy ~780 GB/s; "
                                                                "profiles/r01_nvlink_probe_n2.txt)",
                     "algorithmic_bytes_per_launch": int(dom_wire)}
-            if dom in rr.staged_phases or dom in rr.ce_phases or rr.executors[dom].ce_runs()[0] > 0:
+            if (dom in rr.staged_phases or dom in rr.ce_phases or dom in rr.nccl_phases
+                    or rr.executors[dom].ce_runs()[0] > 0):
                 # copy engines carry (most of) this phase's link bytes: the SM
                 # stores' protocol factor does not apply to them
                 roof.update({"traffic": None, "wire_frac_incl_protocol": None,
-                             "traffic_source": "copy-engine transfers: no per-kernel ncu counter",
+                             "traffic_source": "copy-engine / NCCL transfers: no per-kernel ncu counter",
                              "kernel": ("copy engines (staged gather) + " if dom in rr.staged_phases
                                    else "copy-engine transport + " if dom in rr.ce_phases
+                                   else "NCCL + " if dom in rr.nccl_phases
                                    else "copy-engine runs + ") + kname})
             if hbm_roof["frac"] > roof["frac"]:
                 hbm_roof.update({"traffic": None, "kernel": kname, "phase": dom,
@@ -604,7 +606,7 @@ def run_b200(args) -> None:
                          "multicast_sets": rr.multicast, "relay_phases": rr.relay_phases,
                          "overlap_phases": rr.overlap_phases, "copy_kernel": kname,
                          "ce_runs": [list(e.ce_runs()) for e in rr.executors], "staged_phases": rr.staged_phases,
-                         "ce_transport_phases": rr.ce_phases,
+                         "ce_transport_phases": rr.ce_phases, "nccl_phases": rr.nccl_phases,
                          "ce_transport_estimates_ms": {pi: [round(x * 1e3, 3) for x in v]
                                                        for pi, v in rr.ce_estimates.items()},
                          "bulk_variants": {"plain": 1 if kernel is None else kernel, "flag_synchronised": flag_kernel},

@@ -622,10 +622,73 @@ class Scheme:
     staged: bool = False        # copy-engine rotation of whole shards + per-piece unpack
     ce_transport: bool = False  # copy-engine 2D/3D copies straight into the destinations
     ce_hybrid: bool = False     # ... with unmerged row-parallel pieces left on SM peer stores
+    nccl: bool = False          # the library baseline: NCCL moves whole source shards, then a local unpack
 
     def label(self) -> str:
-        parts = [k for k in ("relay", "overlap", "staged", "ce_transport", "ce_hybrid") if getattr(self, k)]
+        parts = [k for k in ("relay", "overlap", "staged", "ce_transport", "ce_hybrid", "nccl") if getattr(self, k)]
         return "+".join(parts) or "push"
+
+
+def _torch_bytes(ptr: int, nbytes: int):
+    """A torch uint8 tensor aliasing device memory the library allocated."""
+    import torch
+
+    class _View:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+    return torch.as_tensor(_View(), device="cuda")
+
+
+class NcclStaged:
+    """The NCCL baseline as a delivery scheme (the upstream runtime moves
+    weights with NCCL): every source shard another rank reads
+    moves whole with NCCL — `broadcast` when one source shard feeds every
+    rank, else `batch_isend_irecv` to exactly the ranks that read it — into
+    staging buffers, then the library's pull executor unpacks it locally.
+    Behaves like an Executor (launch, stats, onload) so that the bind-time
+    probe times it beside the library's own schemes on the same buffers."""
+
+    def __init__(self, inner: "Executor", group, sends, recvs, bcast, local_src: Dict[int, "DeviceBuffer"]):
+        self.inner, self.group = inner, group
+        self.sends, self.recvs, self.bcast = sends, recvs, bcast  # lists of (tensor, peer rank)
+        self.local_src = local_src
+        self._onload = None
+
+    def __getattr__(self, name):  # stats, wire, kernel_count, phase_kernels, ... of the unpack executor
+        return getattr(self.inner, name)
+
+    def _collective(self) -> None:
+        import torch.distributed as dist
+        if self.bcast is not None:
+            t, root = self.bcast
+            dist.broadcast(t, src=root, group=self.group)
+            return
+        ops = [dist.P2POp(dist.isend, t, q, group=self.group) for t, q in self.sends]
+        ops += [dist.P2POp(dist.irecv, t, q, group=self.group) for t, q in self.recvs]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+    def launch(self, stream=None, ctas: int = 0) -> None:
+        self._collective()  # ordered after the work on torch's current stream
+        self.inner.launch(stream, ctas)
+
+    def enable_onload(self, src_bytes: Dict[int, int], chunk_bytes: int = 256 << 20) -> None:
+        self._onload = dict(src_bytes)
+
+    def launch_onload(self, host_ptrs: Dict[int, int], copy_stream, stream=None, ctas: int = 0) -> None:
+        # the baseline is not pipelined: the local sources land, then NCCL, then the unpack
+        for d, nb in (self._onload or {}).items():
+            memcpy_async(self.local_src[d].ptr, host_ptrs[d], nb, 0, stream)
+        self.launch(stream, ctas)
+
+    def ce_runs(self) -> Tuple[int, int]:
+        return 0, 0
+
+    def stage_pushes(self) -> Tuple[int, int]:
+        return 0, 0
+
+    def close(self) -> None:
+        self.inner.close()
 
 
 class _Binding:
@@ -766,6 +829,8 @@ class RankRealloc:
                 out.append(Scheme(relay=True, overlap=bool(sw["overlap"]), ce_transport=True))
         if sw["staged"]:
             out.append(Scheme(staged=True))
+        if self._nccl_ok():
+            out.append(Scheme(nccl=True))  # the library baseline, timed beside the rest
         if sw["ce_transport"]:
             out.append(Scheme(ce_transport=True))
             if sw["overlap"] and any(fanout_bytes(p, self.host_of).values()):
@@ -782,17 +847,29 @@ class RankRealloc:
                 uniq.append(sc)
         return uniq or [self.schemes[pi]]
 
+    def _nccl_ok(self) -> bool:
+        if self.world < 2:
+            return False
+        import torch.distributed as dist
+        return dist.get_backend(self.group) == "nccl"
+
+    def _remote_sources(self, pi: int) -> List[int]:
+        """Source devices on other ranks whose bytes this rank reads."""
+        p = self.plans[pi]
+        return sorted({s for s, dsts, _r in p.lowered() if self.host_of[s] != self.rank and
+                       any(self.host_of[d] == self.rank for d in dsts)})
+
     def _fits(self, pi: int, sc: Scheme) -> bool:
         """Whether every rank has the device memory the scheme's extra buffers
         need (the staged gather stages whole remote source shards; 70B at 2
         GPUs would need 70 GB more than the 180 GB). Collective: all ranks
         agree."""
         need = 0
-        if sc.staged:
+        if sc.staged or sc.nccl:
             p = self.plans[pi]
-            need = sum(p.shard_bytes(SRC, s) for s in {s for s, dsts, _r in p.lowered()
-                                                        if self.host_of[s] != self.rank and
-                                                        any(self.host_of[d] == self.rank for d in dsts)})
+            need = sum(p.shard_bytes(SRC, s) for s in self._remote_sources(pi))
+            if sc.nccl:  # a broadcast receives into a scratch buffer where nothing is read
+                need += max(p.shard_bytes(SRC, s) for s in p.devices(SRC))
         ok = True
         if need:
             import torch
@@ -974,6 +1051,9 @@ class RankRealloc:
                         stage_remote[(d, r)] = ptr
                     else:
                         stage_flags[r] = ptr
+        if sc.nccl:
+            self._bind_nccl(pi, b)
+            return
         if sc.staged:
             # pull-mode unpack from local staging buffers; this GPU's own
             # sources are pushed to the others by its copy engine
@@ -1007,6 +1087,54 @@ class RankRealloc:
         counts = self._exchange({"n": ex.fanout_items}) if world > 1 else [{"n": ex.fanout_items}]
         self.has_fanout[pi] = sum(c["n"] for c in counts) > 0
 
+    def _bind_nccl(self, pi: int, b: "_Binding") -> None:
+        """Scheme(nccl=True): staging for the remote sources this rank reads,
+        the NCCL transfers, and the local pull executor that unpacks."""
+        rank, world = self.rank, self.world
+        p = self.plans[pi]
+        sname, dname = self.bind[pi]
+        need = self._remote_sources(pi)
+        staging = {s: DeviceBuffer(self.cuda_device, p.shard_bytes(SRC, s)) for s in need}
+        b.owned.extend(staging.values())
+        # who reads what, identically on every rank
+        readers: Dict[int, List[int]] = {}
+        for s, dsts, _r in p.lowered():
+            for d in dsts:
+                if self.host_of[d] != self.host_of[s] and self.host_of[d] not in readers.setdefault(s, []):
+                    readers[s].append(self.host_of[d])
+        srcs = sorted(s for s in readers if readers[s])
+        local_src = {d: buf for d, buf in self.buffers[sname].items() if self.owner[d] == rank}
+        bcast = None
+        sends, recvs = [], []
+        if len(srcs) == 1 and sorted(readers[srcs[0]]) == [r for r in range(world) if r != self.host_of[srcs[0]]]:
+            s0 = srcs[0]
+            root = self.host_of[s0]
+            if rank == root:
+                t = _torch_bytes(local_src[s0].ptr, p.shard_bytes(SRC, s0))
+            else:
+                t = _torch_bytes(staging[s0].ptr, p.shard_bytes(SRC, s0))
+            bcast = (t, root)
+        else:
+            for s in srcs:
+                nb = p.shard_bytes(SRC, s)
+                if self.host_of[s] == rank:
+                    sends += [(_torch_bytes(local_src[s].ptr, nb), q) for q in sorted(readers[s])]
+                elif rank in readers[s]:
+                    recvs.append((_torch_bytes(staging[s].ptr, nb), self.host_of[s]))
+        src = {d: buf.ptr for d, buf in local_src.items()}
+        src.update({s: buf.ptr for s, buf in staging.items()})
+        dst = {d: ptr for d, ptr in self.ptrs[dname].items() if self.owner[d] == rank}
+        # flat pull: every local destination reads its slices straight from
+        # local memory (own shards or staging), so no fan-out phase follows
+        inner = Executor(p, self.cuda_device, src, dst, self.local, PULL, self.chunk_bytes)
+        if self.kernel is not None:
+            inner.set_kernel(self.kernel)
+        b.executor = NcclStaged(inner, self.group, sends, recvs, bcast, local_src)
+        self.bindings[pi] = b
+        if self.executors and pi < len(self.executors):
+            self.executors[pi] = b.executor
+        self.has_fanout[pi] = False  # the pull executor writes every local replica itself
+
     def _unbind_phase(self, pi: int) -> None:
         stream_sync()
         self._collective_barrier()  # no rank still reads or writes this binding's buffers
@@ -1034,6 +1162,10 @@ class RankRealloc:
     @property
     def ce_phases(self) -> List[int]:
         return self._phases_with("ce_transport")
+
+    @property
+    def nccl_phases(self) -> List[int]:
+        return self._phases_with("nccl")
 
     # ---- execution ------------------------------------------------------------
 

@@ -300,6 +300,50 @@ class Worker:
                 finally:
                     rr.close()
 
+    def nccl_scheme(self):
+        """Scheme(nccl=True), the library baseline the probe times: whole
+        source shards by NCCL (broadcast for a lone source, else send/recv),
+        then a local pull unpack; plain and onloaded."""
+        if self.oversub:
+            return
+        m = dataclasses.replace(TINY_GQA, num_layers=6)
+        for src, dst in [(pl(a), pl(b)) for a, b in CASES] + [REPLICATE]:
+            label = f"nccl-scheme {src.strategy}->{dst.strategy}"
+            with self.case(label):
+                plan = plan_param_realloc(m, src, dst, self.c, BALANCED)
+                rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], self.rank, self.world,
+                                   self.local)
+                try:
+                    rr._unbind_phase(0)
+                    rr.schemes[0] = R.Scheme(nccl=True)
+                    rr._bind_phase(0, rr.schemes[0])
+                    rr.executors = [b.executor for b in rr.bindings]
+                    seed = SPECIAL | 87
+                    for d, b in rr.buffers["a"].items():
+                        R.fill_shard(plan, R.SRC, d, b.ptr, seed)
+                    for rep in range(2):
+                        for b in rr.buffers["b"].values():
+                            b.zero()
+                        torch.cuda.synchronize()
+                        dist.barrier()
+                        hosts = None
+                        if rep == 1:
+                            hosts = {d: R.HostBuffer(b.nbytes) for d, b in rr.buffers["a"].items()}
+                            for d, hb in hosts.items():
+                                hb.array()[:] = rr.buffers["a"][d].to_host()
+                            rr.run_phase_onload(0, {d: hb.ptr for d, hb in hosts.items()}, torch.cuda.Stream())
+                        else:
+                            rr.run_phase(0)
+                        torch.cuda.synchronize()
+                        for d, b in rr.buffers["b"].items():
+                            if not np.array_equal(b.to_host(), O.fill(m, dst, self.c, d, seed)):
+                                self.failures.append(f"{label} rep {rep}: device {d} differs")
+                        for hb in (hosts or {}).values():
+                            hb.free()
+                    dist.barrier()
+                finally:
+                    rr.close()
+
     def _agree(self, obj):
         out = [None] * self.world
         dist.all_gather_object(out, [e["chosen"] for e in obj])
@@ -401,9 +445,10 @@ class Worker:
 def main() -> int:
     w = Worker()
     sections = os.environ.get("RR_SECTIONS",
-                              "basic,multicast,overlap,relay,ce,cetransport,probe,staged,fuzz,full7b").split(",")
+                              "basic,multicast,overlap,relay,ce,cetransport,probe,nccl,staged,fuzz,full7b").split(",")
     table = {"basic": w.basic, "multicast": w.multicast, "overlap": w.overlap, "relay": w.relay,
-             "ce": w.ce_runs_cases, "cetransport": w.ce_transport, "probe": w.probe, "staged": w.staged, "staged_many": w.staged_many_items, "fuzz": w.fuzz,
+             "ce": w.ce_runs_cases, "cetransport": w.ce_transport, "probe": w.probe, "nccl": w.nccl_scheme,
+             "staged": w.staged, "staged_many": w.staged_many_items, "fuzz": w.fuzz,
              "full7b": w.full_7b}
     for s in sections + (["staged_many"] if "staged" in sections else []):
         table[s]()
