@@ -345,7 +345,10 @@ def run_b200(args) -> None:
     mode = R.PULL if args.mode == "pull" else R.PUSH
     # auto: peer stores, plus the pipelined relay where it lowers the link
     # bottleneck (single source feeding many GPUs); mc: NVLS multicast instead.
-    multicast = [bind[0][1]] if args.mode == "mc" else []
+    # mc: NVLS multicast for the first phase's destinations; auto: multicast
+    # sets chosen by the probe (every set a payload of which reaches every
+    # GPU is allocated as multicast members and timed) or the cost model
+    multicast = [bind[0][1]] if args.mode == "mc" else ("auto" if args.mode == "auto" else [])
     relay = {"auto": "auto", "relay": True}.get(args.mode, False)
     overlap = args.overlap == "on"
     # --kernel k: k for every phase (sweeps); default: per phase kind

@@ -396,6 +396,14 @@ rr_status rr_mcast_import(int cuda_device, int fd, size_t size, int n_devices, r
 rr_status rr_mcast_bind(rr_mcast* m, void** unicast_ptr, void** multicast_ptr);
 rr_status rr_mcast_size(const rr_mcast* m, size_t* size);
 void rr_mcast_destroy(rr_mcast* m);
+/* A bound member reached by the other GPUs through ordinary peer stores
+ * (schemes that do not use the multicast address): export its physical
+ * memory as a POSIX fd; a peer imports and maps it (read/write from
+ * cuda_device) and closes the mapping with rr_peer_mem_close. */
+typedef struct rr_peer_mem rr_peer_mem;
+rr_status rr_mcast_export_member(rr_mcast* m, int* fd_out);
+rr_status rr_peer_mem_import(int cuda_device, int fd, size_t size, void** ptr, rr_peer_mem** out);
+void rr_peer_mem_close(rr_peer_mem* p);
 
 /* ---- deterministic weights (test/bench infrastructure) ----
  * Fill or check a device's shard under one side of a plan with

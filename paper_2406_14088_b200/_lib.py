@@ -82,6 +82,9 @@ _SIGNATURES = {
     "rr_mcast_bind": (c_int, [_P, POINTER(_P), POINTER(_P)]),
     "rr_mcast_size": (c_int, [_P, POINTER(c_size_t)]),
     "rr_mcast_destroy": (None, [_P]),
+    "rr_mcast_export_member": (c_int, [_P, POINTER(c_int)]),
+    "rr_peer_mem_import": (c_int, [c_int, c_int, c_size_t, POINTER(_P), POINTER(_P)]),
+    "rr_peer_mem_close": (None, [_P]),
     "rr_last_error": (c_char_p, []),
     "rr_abi_version": (c_int, []),
     "rr_model_validate": (c_int, [POINTER(RrModel)]),

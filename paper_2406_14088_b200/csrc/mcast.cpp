@@ -260,3 +260,64 @@ rr_mcast::~rr_mcast() {
 }
 
 void rr_mcast_destroy(rr_mcast* m) { delete m; }
+
+// ---- a member's memory reached by the other GPUs with ordinary peer
+// stores (the schemes that do not use the multicast address): the member's
+// physical allocation is exported as a POSIX fd and mapped by each peer ----
+
+rr_status rr_mcast_export_member(rr_mcast* m, int* fd_out) {
+  return run([&] {
+    if (!m || !fd_out || !m->mem) throw Fail{RR_EINVAL, "multicast member not bound"};
+    int fd = -1;
+    cu(driver().exportHandle(&fd, m->mem, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),
+       "cuMemExportToShareableHandle(member)");
+    *fd_out = fd;
+  });
+}
+
+struct rr_peer_mem {
+  int cuda_device = 0;
+  size_t size = 0;
+  CUmemGenericAllocationHandle mem = 0;
+  CUdeviceptr va = 0;
+  bool mapped = false;
+  ~rr_peer_mem() {
+    const Driver& d = driver();
+    if (!d.ok) return;
+    cudaSetDevice(cuda_device);
+    if (mapped) d.memUnmap(va, size);
+    if (va) d.addrFree(va, size);
+    if (mem) d.memRelease(mem);
+  }
+};
+
+rr_status rr_peer_mem_import(int cuda_device, int fd, size_t size, void** ptr, rr_peer_mem** out) {
+  auto p = std::make_unique<rr_peer_mem>();
+  const rr_status st = run([&] {
+    if (!driver().ok) throw Fail{RR_EUNSUPPORTED, "CUDA driver lacks the VMM API"};
+    if (fd < 0 || !ptr || !out || size == 0) throw Fail{RR_EINVAL, "bad peer memory arguments"};
+    if (cudaSetDevice(cuda_device) != cudaSuccess) {
+      cudaGetLastError();
+      throw Fail{RR_ECUDA, "cudaSetDevice failed"};
+    }
+    p->cuda_device = cuda_device;
+    p->size = size;
+    cu(driver().importHandle(&p->mem, reinterpret_cast<void*>(static_cast<intptr_t>(fd)),
+                             CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
+       "cuMemImportFromShareableHandle(peer member)");
+    cu(driver().addrReserve(&p->va, size, size_t{2} << 20, 0, 0), "cuMemAddressReserve(peer member)");
+    cu(driver().memMap(p->va, size, 0, p->mem, 0), "cuMemMap(peer member)");
+    p->mapped = true;
+    CUmemAccessDesc acc;
+    std::memset(&acc, 0, sizeof(acc));
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = cuda_device;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    cu(driver().setAccess(p->va, size, &acc, 1), "cuMemSetAccess(peer member)");
+    *ptr = reinterpret_cast<void*>(p->va);
+  });
+  if (st == RR_OK) *out = p.release();
+  return st;
+}
+
+void rr_peer_mem_close(rr_peer_mem* p) { delete p; }

@@ -561,6 +561,52 @@ def _share_fd(fd: int, rank: int, world: int, tag: str, group=None) -> int:
     return fds[0]
 
 
+def _exchange_fds(fd: int, rank: int, world: int, tag: str, group=None) -> List[int]:
+    """Every rank's file descriptor to every rank (rank r serves its fd on an
+    abstract AF_UNIX socket in turn r; SCM_RIGHTS). Entry `rank` is `fd`."""
+    import socket
+
+    import torch.distributed as dist
+    out = [-1] * world
+    out[rank] = fd
+    for r in range(world):
+        name = "\0" + f"{tag}-{r}"
+        if rank == r:
+            srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            srv.bind(name)
+            srv.listen(world)
+            dist.barrier(group=group)
+            for _ in range(world - 1):
+                conn, _ = srv.accept()
+                socket.send_fds(conn, [b"fd"], [fd])
+                conn.close()
+            srv.close()
+        else:
+            dist.barrier(group=group)
+            c = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            c.connect(name)
+            _msg, fds, _flags, _addr = socket.recv_fds(c, 16, 1)
+            c.close()
+            out[r] = fds[0]
+        dist.barrier(group=group)
+    return out
+
+
+class PeerMemory:
+    """Another GPU's multicast member mapped here for ordinary peer stores
+    (rr_peer_mem_import)."""
+
+    def __init__(self, cuda_device: int, fd: int, nbytes: int):
+        p, h = ctypes.c_void_p(), ctypes.c_void_p()
+        check(lib.rr_peer_mem_import(cuda_device, fd, nbytes, ctypes.byref(p), ctypes.byref(h)))
+        self.ptr, self._h = p.value, h
+
+    def close(self) -> None:
+        if self._h and self._h.value:
+            lib.rr_peer_mem_close(self._h)
+            self._h = ctypes.c_void_p(0)
+
+
 class MulticastBuffer:
     """One rank's member buffer of an NVLS multicast object (rr_mcast_*).
 
@@ -605,6 +651,13 @@ class MulticastBuffer:
             check(lib.rr_memcpy(out.ctypes.data, self.ptr, self.nbytes, 1, None, 1))
         return out
 
+    def export_fd(self) -> int:
+        """This member's physical memory as a POSIX fd (peers map it with
+        PeerMemory for ordinary peer stores)."""
+        fd = ctypes.c_int()
+        check(lib.rr_mcast_export_member(self._h, ctypes.byref(fd)))
+        return fd.value
+
     def free(self) -> None:
         if self._h and self._h.value:
             lib.rr_mcast_destroy(self._h)
@@ -623,9 +676,11 @@ class Scheme:
     ce_transport: bool = False  # copy-engine 2D/3D copies straight into the destinations
     ce_hybrid: bool = False     # ... with unmerged row-parallel pieces left on SM peer stores
     nccl: bool = False          # the library baseline: NCCL moves whole source shards, then a local unpack
+    multicast: bool = False     # NVLS multicast: a payload for every GPU stored once through multimem.st
 
     def label(self) -> str:
-        parts = [k for k in ("relay", "overlap", "staged", "ce_transport", "ce_hybrid", "nccl") if getattr(self, k)]
+        parts = [k for k in ("relay", "overlap", "staged", "ce_transport", "ce_hybrid", "nccl", "multicast")
+                 if getattr(self, k)]
         return "+".join(parts) or "push"
 
 
@@ -751,15 +806,26 @@ class RankRealloc:
         self.owner = {d: d // (n // world) for d in range(n)}
         self.host_of = [self.owner[d] for d in range(n)]
         self.bind = list(bind)
+        # Multicast sets: destination sets whose per-GPU leaders are members of
+        # an NVLS multicast object. A list: those sets, multicast always.
+        # "auto": sets where the cost model predicts a >10% lower link
+        # bottleneck (one source feeding many GPUs), or — with the probe —
+        # every set some payload of which reaches every GPU, multicast kept
+        # only where the probe measures it fastest (the members are also
+        # mapped by the peers for the other schemes).
+        self.mc_forced = multicast != "auto"
         if multicast == "auto":
-            # Multicast a phase's destination set only where it lowers the
-            # estimated link bottleneck by >10% (one source feeding many GPUs;
-            # not all-gather patterns, where every GPU is ingress-bound).
             multicast = []
             if world > 1 and mode == PUSH and hierarchical and multicast_supported(cuda_device):
                 for pi, (_sname, dname) in enumerate(bind):
                     p = self.plans[pi]
-                    if link_bottleneck(p, self.host_of, True) < 0.9 * link_bottleneck(p, self.host_of, False):
+                    if probe:
+                        every = any({self.host_of[d] for d in dsts} == set(self.host_of) and
+                                    any(self.host_of[d] != self.host_of[s_] for d in dsts)
+                                    for s_, dsts, _r in p.lowered())
+                        if every and dname not in multicast:
+                            multicast.append(dname)
+                    elif link_bottleneck(p, self.host_of, True) < 0.9 * link_bottleneck(p, self.host_of, False):
                         multicast.append(dname)
         self.multicast = list(multicast)
         if multicast and (world < 2 or mode != PUSH or not hierarchical):
@@ -790,7 +856,9 @@ class RankRealloc:
     def _decide(self, pi: int, sw: dict) -> Scheme:
         """The cost-model choice for phase pi under the switches."""
         p, dname = self.plans[pi], self.bind[pi][1]
-        if not self._flag_ok() or dname in self.multicast or not self._remote(p):
+        if dname in self.multicast and self._remote(p):
+            return Scheme(multicast=True)
+        if not self._flag_ok() or not self._remote(p):
             return Scheme()
         relay = bool(sw["relay"]) and (sw["relay"] != "auto" or link_bottleneck(p, self.host_of, relay=True) <
                                        0.9 * link_bottleneck(p, self.host_of))
@@ -819,9 +887,13 @@ class RankRealloc:
     def _candidates(self, pi: int, sw: dict) -> List[Scheme]:
         """Every scheme the switches allow for phase pi (probe mode)."""
         p, dname = self.plans[pi], self.bind[pi][1]
-        if not self._flag_ok() or dname in self.multicast or not self._remote(p):
+        if dname in self.multicast and self.mc_forced:
+            return [self.schemes[pi]]
+        if not self._flag_ok() or not self._remote(p):
             return [Scheme()]
         out = [self.schemes[pi], Scheme(overlap=bool(sw["overlap"]))]
+        if dname in self.multicast:
+            out.append(Scheme(multicast=True))
         if sw["relay"] and any(len({self.host_of[d] for d in dsts} - {self.host_of[s]}) >= 2
                                for s, dsts, _r in p.lowered()):
             out.append(Scheme(relay=True, overlap=bool(sw["overlap"])))
@@ -993,6 +1065,35 @@ class RankRealloc:
                     else:
                         self.ptrs[name][d] = ptr
         self.barrier = Barrier(self.cuda_device, rank, world, flag_ptrs)
+        # multicast members: every peer maps every other GPU's member for the
+        # schemes that store with ordinary peer stores
+        import os
+        self._peer_mem: List[PeerMemory] = []
+        for name, leader in sorted(mc_leaders.items()):
+            b = self.buffers[name][leader]
+            fd = b.export_fd()
+            fds = _exchange_fds(fd, rank, world, f"rr-mem-{self._mc_tag()}-{name}", self.group)
+            for r in range(world):
+                if r == rank:
+                    continue
+                pm = PeerMemory(self.cuda_device, fds[r], b.padded)
+                self._peer_mem.append(pm)
+                peer_leader = min(d for d in self.plans[shards[name][0]].devices(shards[name][1])
+                                  if d in hosted_devices(n, r, world))
+                self.ptrs[name][peer_leader] = pm.ptr
+                os.close(fds[r])
+            os.close(fd)
+
+    def _mc_tag(self) -> str:
+        """A name every rank agrees on for this instance's fd sockets."""
+        import os
+        if not hasattr(self, "_tag"):
+            tag = [f"{os.getpid()}-{id(self)}"]
+            if self.world > 1:
+                import torch.distributed as dist
+                dist.broadcast_object_list(tag, src=0, group=self.group)
+            self._tag = tag[0]
+        return self._tag
 
     def _bind_phase(self, pi: int, sc: Scheme) -> None:
         """Allocate what scheme `sc` needs for phase pi (relay / overlap flag
@@ -1069,7 +1170,8 @@ class RankRealloc:
                                for d in range(n)}
             ex = Executor(p, self.cuda_device, self.ptrs[sname], self.ptrs[dname], self.local, self.mode,
                           self.chunk_bytes, host_of=self.host_of if self.hierarchical else None,
-                          mc_ptrs=self.mc_tables.get(dname), relay_flags=relay_table, relay_chain=sc.relay,
+                          mc_ptrs=self.mc_tables.get(dname) if sc.multicast else None,
+                          relay_flags=relay_table, relay_chain=sc.relay,
                           overlap_fanout=sc.overlap, ce_min_run_bytes=self.ce_min_run_bytes,
                           ce_transport=(3 if sc.relay and sc.ce_transport else 2 if sc.ce_hybrid
                                         else int(sc.ce_transport)),
@@ -1224,6 +1326,8 @@ class RankRealloc:
         self.barrier.close()
         for p in self._opened:
             close_ipc(p)
+        for pm in getattr(self, "_peer_mem", []):
+            pm.close()
         for bufs in self.buffers.values():
             for b in bufs.values():
                 b.free()

@@ -189,6 +189,35 @@ class Worker:
             for seed in (23, SPECIAL | 23):
                 self.run(f"multicast {src.strategy}->{dst.strategy} seed={seed:#x}", TINY_GQA, src, dst, seed,
                          multicast=["b"])
+            # multicast members allocated for the probe: the probe times
+            # multicast beside every other scheme (peers reach the members by
+            # mapped physical memory), and a non-multicast scheme on them
+            self.run(f"multicast-probe {src.strategy}->{dst.strategy}", TINY_GQA, src, dst, SPECIAL | 24, reps=2,
+                     multicast="auto", probe=True, overlap=True, relay="auto", staged=True, ce_transport=True)
+            with self.case(f"peer stores into multicast members {src.strategy}->{dst.strategy}"):
+                plan = plan_param_realloc(TINY_GQA, src, dst, self.c, BALANCED)
+                rr = R.RankRealloc([plan], {"a": (0, R.SRC), "b": (0, R.DST)}, [("a", "b")], self.rank,
+                                   self.world, self.local, multicast="auto", probe=True, overlap=True)
+                try:
+                    for sc in (R.Scheme(overlap=True), R.Scheme(ce_transport=True, overlap=True)):
+                        rr._unbind_phase(0)
+                        rr.schemes[0] = sc
+                        rr._bind_phase(0, sc)
+                        rr.executors = [b.executor for b in rr.bindings]
+                        for d, b in rr.buffers["a"].items():
+                            R.fill_shard(plan, R.SRC, d, b.ptr, SPECIAL | 25)
+                        for b in rr.buffers["b"].values():
+                            b.zero()
+                        torch.cuda.synchronize()
+                        dist.barrier()
+                        rr.run_phase(0)
+                        torch.cuda.synchronize()
+                        for d, b in rr.buffers["b"].items():
+                            if not np.array_equal(b.to_host(), O.fill(TINY_GQA, dst, self.c, d, SPECIAL | 25)):
+                                self.failures.append(f"{sc.label()} into multicast members: device {d} differs")
+                        dist.barrier()
+                finally:
+                    rr.close()
 
     def overlap(self):
         """Overlapped in-host fan-out (star flags), with and without the relay."""
