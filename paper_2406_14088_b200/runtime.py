@@ -816,7 +816,10 @@ class RankRealloc:
         self.mc_forced = multicast != "auto"
         if multicast == "auto":
             multicast = []
-            if world > 1 and mode == PUSH and hierarchical and multicast_supported(cuda_device):
+            # (one member per GPU: ranks sharing a GPU, as in the 8-ranks-on-4
+            # correctness runs, cannot form a multicast group)
+            if (world > 1 and mode == PUSH and hierarchical and world <= device_count() and
+                    multicast_supported(cuda_device)):
                 for pi, (_sname, dname) in enumerate(bind):
                     p = self.plans[pi]
                     if probe:
