@@ -32,7 +32,7 @@ extern "C" {
 #endif
 
 #define RR_ABI_VERSION 5 /* 2: rr_placement.kv_layout, rr_shard.part; 3: rr_exec_options.ce_min_run_bytes; 4: staged gather;
-                            5: rr_exec_options.ce_transport */
+                            5: rr_exec_options.ce_transport / ce_flags, rr_plan_ce_*, multicast member export */
 
 typedef enum {
   RR_OK = 0,
