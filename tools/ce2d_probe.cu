@@ -28,8 +28,8 @@
 
 static char* buf_src[2];
 static char* buf_dst[2];
-static cudaStream_t st[2];
-static cudaEvent_t ev0[2], ev1[2];
+static cudaStream_t st[2], st2[2];
+static cudaEvent_t ev0[2], ev1[2], evj[2];
 static const size_t kBuf = size_t(12) << 30;
 
 // Runs `issue(g, src, dst, stream)` on both GPUs at once (g pushes to 1 - g),
@@ -49,6 +49,7 @@ static void measure(const char* name, size_t bytes, const std::function<void(int
   for (int g = 0; g < 2; ++g) {
     CK(cudaSetDevice(g));
     CK(cudaEventRecord(ev0[g], st[g]));
+    CK(cudaStreamWaitEvent(st2[g], ev0[g], 0));  // the second stream (2-stream modes) starts with the first
   }
   for (int r = 0; r < reps; ++r)
     for (int g = 0; g < 2; ++g) {
@@ -57,6 +58,8 @@ static void measure(const char* name, size_t bytes, const std::function<void(int
     }
   for (int g = 0; g < 2; ++g) {
     CK(cudaSetDevice(g));
+    CK(cudaEventRecord(evj[g], st2[g]));
+    CK(cudaStreamWaitEvent(st[g], evj[g], 0));
     CK(cudaEventRecord(ev1[g], st[g]));
   }
   for (int g = 0; g < 2; ++g) {
@@ -91,6 +94,8 @@ int main() {
     CK(cudaMalloc(&buf_dst[g], kBuf));
     CK(cudaMemset(buf_src[g], 1, kBuf));
     CK(cudaStreamCreateWithFlags(&st[g], cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&st2[g], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&evj[g], cudaEventDisableTiming));
     CK(cudaEventCreate(&ev0[g]));
     CK(cudaEventCreate(&ev1[g]));
   }
@@ -109,6 +114,32 @@ int main() {
   });
   measure("2dL 16 MiB x 40 rows (pitch=stride)", q * L, [&](int, char* s, char* d, cudaStream_t t) {
     CK(cudaMemcpy2DAsync(d, stride_d, s, stride_s, q, L, cudaMemcpyDeviceToDevice, t));
+  });
+  measure("1d/40 x 16 MiB, 2 streams alternating", q * L, [&](int g, char* s, char* d, cudaStream_t t) {
+    for (int l = 0; l < L; ++l)
+      CK(cudaMemcpyAsync(d + l * stride_d, s + l * stride_s, q, cudaMemcpyDeviceToDevice, (l & 1) ? st2[g] : t));
+  });
+  // back-to-back 2D copies like the 34B / 70B transport's (one tensor kind of
+  // a stage: 16 MiB rows x 12 layers), 10 in a row, on one and on two streams
+  measure("2dL 16 MiB x 12 rows, 10 copies", q * 120, [&](int, char* s, char* d, cudaStream_t t) {
+    for (int k = 0; k < 10; ++k)
+      CK(cudaMemcpy2DAsync(d + k * q, stride_d, s + k * q, stride_s, q, 12, cudaMemcpyDeviceToDevice, t));
+  });
+  measure("2dL 16 MiB x 12 rows, 10 copies, 2 streams", q * 120, [&](int g, char* s, char* d, cudaStream_t t) {
+    for (int k = 0; k < 10; ++k)
+      CK(cudaMemcpy2DAsync(d + k * q, stride_d, s + k * q, stride_s, q, 12, cudaMemcpyDeviceToDevice,
+                           (k & 1) ? st2[g] : t));
+  });
+  measure("2dL 4 MiB x 12 rows, 40 copies", q * 120, [&](int, char* s, char* d, cudaStream_t t) {
+    const size_t w = q / 4;
+    for (int k = 0; k < 40; ++k)
+      CK(cudaMemcpy2DAsync(d + k * w, stride_d, s + k * w, stride_s, w, 12, cudaMemcpyDeviceToDevice, t));
+  });
+  measure("2dL 4 MiB x 12 rows, 40 copies, 2 streams", q * 120, [&](int g, char* s, char* d, cudaStream_t t) {
+    const size_t w = q / 4;
+    for (int k = 0; k < 40; ++k)
+      CK(cudaMemcpy2DAsync(d + k * w, stride_d, s + k * w, stride_s, w, 12, cudaMemcpyDeviceToDevice,
+                           (k & 1) ? st2[g] : t));
   });
   const size_t small = size_t(1) << 20;  // 7B k slice (1 MiB) x 32 layers
   measure("1d/32 x 1 MiB at layer stride", small * 32, [&](int, char* s, char* d, cudaStream_t t) {
