@@ -87,3 +87,25 @@ def test_world8_with_two_processes_per_gpu(n_gpus):
         pytest.skip("runs on exactly 4 GPUs")
     r = _torchrun(8, {"RR_FUZZ_CASES": "12"}, timeout=1500)
     _report(r, 8)
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_example_rank_realloc(need_gpu, world):
+    """examples/rank_realloc.py (the one-process-per-GPU API as a user calls
+    it) on GPU 0: tiny model, tp8 -> dp8 -> tp8, every shard verified."""
+    import signal
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0])
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.join(ROOT, "examples", "rank_realloc.py"), "--model", "tiny"]
+    proc = subprocess.Popen(cmd, env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
+                            start_new_session=True)
+    try:
+        out, err = proc.communicate(timeout=300)
+    except subprocess.TimeoutExpired:
+        os.killpg(proc.pid, signal.SIGKILL)
+        out, err = proc.communicate()
+        pytest.fail(f"example timed out:\n{out[-2000:]}\n{err[-2000:]}")
+    print(out)
+    assert proc.returncode == 0, out[-3000:] + err[-3000:]
+    assert "mismatches 0" in out
