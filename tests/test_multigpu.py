@@ -92,12 +92,12 @@ def test_world8_with_two_processes_per_gpu(n_gpus):
 @pytest.mark.parametrize("world", [1, 2])
 def test_example_rank_realloc(need_gpu, world):
     """examples/rank_realloc.py (the one-process-per-GPU API as a user calls
-    it) on GPU 0: tiny model, tp8 -> dp8 -> tp8, every shard verified."""
+    it) on GPU 0: tiny model (4 heads), tp4 -> dp4 -> tp4, every shard verified."""
     import signal
     env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0])
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
-           os.path.join(ROOT, "examples", "rank_realloc.py"), "--model", "tiny"]
+           os.path.join(ROOT, "examples", "rank_realloc.py"), "--model", "tiny", "--devices", "4"]
     proc = subprocess.Popen(cmd, env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
                             start_new_session=True)
     try:
