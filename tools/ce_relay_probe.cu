@@ -1,0 +1,149 @@
+// Copy-engine relay chain over NVLink (diagnostics; one process, G GPUs).
+// GPU 0 holds a `total`-byte source; GPU k (k >= 1) receives it into its
+// leader buffer from GPU k-1, piece by piece, and forwards each piece to GPU
+// k+1 once it has landed — the library's copy-engine relay (ce_transport=3)
+// without its in-host fan-out. Which part of the chain costs time?
+//   flags       each forward waits for the piece's flag (cuStreamWaitValue32
+//               GEQ), each copy raises the next GPU's flag after it
+//               (cuStreamWriteValue32, default = with a memory barrier)
+//   flags/nomb  the same, flag writes without the memory barrier (timing
+//               only: not a safe protocol)
+//   nowait      forwards issued without waiting (timing only: the bytes
+//               forwarded are stale) — the chain's pure transfer time
+//   events      waits as cross-device cudaStreamWaitEvent instead of flags
+// Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tools/ce_relay_probe tools/ce_relay_probe.cu -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#define CK(x)                                                                               \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess) {                                                                \
+      std::printf("FAIL %s:%d %s -> %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
+      std::exit(1);                                                                         \
+    }                                                                                       \
+  } while (0)
+#define CU(x)                                                    \
+  do {                                                           \
+    CUresult r_ = (x);                                           \
+    if (r_ != CUDA_SUCCESS) {                                    \
+      std::printf("FAIL %s:%d %s -> %d\n", __FILE__, __LINE__, #x, (int)r_); \
+      std::exit(1);                                              \
+    }                                                            \
+  } while (0)
+
+int G = 4;
+std::vector<char*> buf;         // GPU 0: source; others: leader
+std::vector<uint32_t*> flags;   // per GPU: one slot per piece
+std::vector<cudaStream_t> st;
+std::vector<cudaEvent_t> t0, t1;
+uint32_t epoch = 0;
+
+enum Mode { kFlags, kFlagsNoMb, kNoWait, kEvents };
+
+double run(Mode mode, size_t total, size_t piece, int reps = 3) {
+  const int P = static_cast<int>((total + piece - 1) / piece);
+  std::vector<std::vector<cudaEvent_t>> arrived(G, std::vector<cudaEvent_t>(P));
+  if (mode == kEvents)
+    for (int g = 0; g < G; ++g) {
+      CK(cudaSetDevice(g));
+      for (int p = 0; p < P; ++p) CK(cudaEventCreateWithFlags(&arrived[g][p], cudaEventDisableTiming));
+    }
+  double best = 1e30;
+  for (int r = 0; r < reps + 1; ++r) {
+    ++epoch;
+    for (int g = 0; g < G; ++g) {
+      CK(cudaSetDevice(g));
+      CK(cudaDeviceSynchronize());
+    }
+    CK(cudaSetDevice(0));
+    CK(cudaEventRecord(t0[0], st[0]));
+    for (int g = 1; g < G; ++g) {
+      CK(cudaSetDevice(g));
+      CK(cudaStreamWaitEvent(st[g], t0[0], 0));  // every stream starts with GPU 0's
+    }
+    // issue per GPU in piece order (the host issues GPU by GPU; the streams run concurrently)
+    for (int g = 0; g + 1 < G; ++g) {
+      CK(cudaSetDevice(g));
+      for (int p = 0; p < P; ++p) {
+        const size_t off = static_cast<size_t>(p) * piece, w = std::min(piece, total - off);
+        if (g > 0) {
+          if (mode == kFlags || mode == kFlagsNoMb)
+            CU(cuStreamWaitValue32(st[g], (CUdeviceptr)(flags[g] + p), epoch, CU_STREAM_WAIT_VALUE_GEQ));
+          else if (mode == kEvents)
+            CK(cudaStreamWaitEvent(st[g], arrived[g][p], 0));
+        }
+        CK(cudaMemcpyAsync(buf[g + 1] + off, buf[g] + off, w, cudaMemcpyDeviceToDevice, st[g]));
+        if (mode == kFlags)
+          CU(cuStreamWriteValue32(st[g], (CUdeviceptr)(flags[g + 1] + p), epoch, CU_STREAM_WRITE_VALUE_DEFAULT));
+        else if (mode == kFlagsNoMb)
+          CU(cuStreamWriteValue32(st[g], (CUdeviceptr)(flags[g + 1] + p), epoch,
+                                  CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER));
+        else if (mode == kEvents)
+          CK(cudaEventRecord(arrived[g + 1][p], st[g]));
+      }
+    }
+    // the chain's time: GPU 0's start to the last forwarder's end, on GPU 0's clock
+    for (int g = 1; g < G; ++g) {
+      CK(cudaSetDevice(g));
+      CK(cudaEventRecord(t1[g], st[g]));
+    }
+    CK(cudaSetDevice(0));
+    for (int g = 1; g < G; ++g) CK(cudaStreamWaitEvent(st[0], t1[g], 0));
+    CK(cudaEventRecord(t1[0], st[0]));
+    CK(cudaEventSynchronize(t1[0]));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, t0[0], t1[0]));
+    if (r > 0 && ms < best) best = ms;
+  }
+  if (mode == kEvents)
+    for (int g = 0; g < G; ++g) {
+      CK(cudaSetDevice(g));
+      for (int p = 0; p < P; ++p) CK(cudaEventDestroy(arrived[g][p]));
+    }
+  return best;
+}
+
+int main(int argc, char** argv) {
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  G = n;
+  if (G < 3) {
+    std::printf("needs >= 3 GPUs\n");
+    return 1;
+  }
+  const size_t total = size_t(16) << 30;
+  buf.resize(G);
+  flags.resize(G);
+  st.resize(G);
+  t0.resize(G);
+  t1.resize(G);
+  for (int g = 0; g < G; ++g) {
+    CK(cudaSetDevice(g));
+    for (int h = 0; h < G; ++h)
+      if (h != g) CK(cudaDeviceEnablePeerAccess(h, 0));
+    CK(cudaMalloc(&buf[g], total));
+    CK(cudaMemset(buf[g], g, total));
+    CK(cudaMalloc(&flags[g], 1 << 20));
+    CK(cudaMemset(flags[g], 0, 1 << 20));
+    CK(cudaStreamCreateWithFlags(&st[g], cudaStreamNonBlocking));
+    CK(cudaEventCreate(&t0[g]));
+    CK(cudaEventCreate(&t1[g]));  // (only GPU 0's pair is timed; the others order streams)
+  }
+  std::printf("chain 0 -> ... -> %d, %zu GiB\n", G - 1, total >> 30);
+  const char* names[] = {"flags", "flags/nomb", "nowait", "events"};
+  for (size_t piece_mib : {64, 256, 1024}) {
+    for (Mode m : {kFlags, kFlagsNoMb, kNoWait, kEvents}) {
+      const double ms = run(m, total, piece_mib << 20);
+      std::printf("%-11s piece %5zu MiB  %8.3f ms  %7.1f GB/s per link\n", names[m], piece_mib, ms,
+                  total / (ms * 1e-3) / 1e9);
+      std::fflush(stdout);
+    }
+  }
+  return 0;
+}
