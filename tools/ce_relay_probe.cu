@@ -6,8 +6,8 @@
 //   flags       each forward waits for the piece's flag (cuStreamWaitValue32
 //               GEQ), each copy raises the next GPU's flag after it
 //               (cuStreamWriteValue32, default = with a memory barrier)
-//   flags/nomb  the same, flag writes without the memory barrier (timing
-//               only: not a safe protocol)
+//   (flag writes without the memory barrier are refused on this driver:
+//   CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER -> CUDA_ERROR_INVALID_VALUE)
 //   nowait      forwards issued without waiting (timing only: the bytes
 //               forwarded are stale) — the chain's pure transfer time
 //   events      waits as cross-device cudaStreamWaitEvent instead of flags
@@ -138,7 +138,7 @@ int main(int argc, char** argv) {
   std::printf("chain 0 -> ... -> %d, %zu GiB\n", G - 1, total >> 30);
   const char* names[] = {"flags", "flags/nomb", "nowait", "events"};
   for (size_t piece_mib : {64, 256, 1024}) {
-    for (Mode m : {kFlags, kFlagsNoMb, kNoWait, kEvents}) {
+    for (Mode m : {kFlags, kNoWait, kEvents}) {
       const double ms = run(m, total, piece_mib << 20);
       std::printf("%-11s piece %5zu MiB  %8.3f ms  %7.1f GB/s per link\n", names[m], piece_mib, ms,
                   total / (ms * 1e-3) / 1e9);
