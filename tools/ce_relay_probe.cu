@@ -50,8 +50,8 @@ double run(Mode mode, size_t total, size_t piece, int reps = 3) {
   const int P = static_cast<int>((total + piece - 1) / piece);
   std::vector<std::vector<cudaEvent_t>> arrived(G, std::vector<cudaEvent_t>(P));
   if (mode == kEvents)
-    for (int g = 0; g < G; ++g) {
-      CK(cudaSetDevice(g));
+    for (int g = 1; g < G; ++g) {  // recorded by GPU g-1's stream: created on that device
+      CK(cudaSetDevice(g - 1));
       for (int p = 0; p < P; ++p) CK(cudaEventCreateWithFlags(&arrived[g][p], cudaEventDisableTiming));
     }
   double best = 1e30;
@@ -102,8 +102,8 @@ double run(Mode mode, size_t total, size_t piece, int reps = 3) {
     if (r > 0 && ms < best) best = ms;
   }
   if (mode == kEvents)
-    for (int g = 0; g < G; ++g) {
-      CK(cudaSetDevice(g));
+    for (int g = 1; g < G; ++g) {
+      CK(cudaSetDevice(g - 1));
       for (int p = 0; p < P; ++p) CK(cudaEventDestroy(arrived[g][p]));
     }
   return best;
