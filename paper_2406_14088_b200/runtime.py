@@ -808,27 +808,26 @@ class RankRealloc:
         self.bind = list(bind)
         # Multicast sets: destination sets whose per-GPU leaders are members of
         # an NVLS multicast object. A list: those sets, multicast always.
-        # "auto": sets where the cost model predicts a >10% lower link
-        # bottleneck (one source feeding many GPUs), or — with the probe —
-        # every set some payload of which reaches every GPU, multicast kept
-        # only where the probe measures it fastest (the members are also
-        # mapped by the peers for the other schemes).
+        # "auto": with the probe, every set some payload of which reaches
+        # every GPU, multicast kept only where the probe measures it fastest
+        # (the members are also mapped by the peers for the other schemes);
+        # without it, none. The link-byte model favours multicast wherever one
+        # source feeds many GPUs, but multicast stores measured slower than
+        # peer stores on every config (7B 28.0 vs 13.0 ms at
+        # 2 GPUs), so only a measurement may choose it.
         self.mc_forced = multicast != "auto"
         if multicast == "auto":
             multicast = []
             # (one member per GPU: ranks sharing a GPU, as in the 8-ranks-on-4
             # correctness runs, cannot form a multicast group)
-            if (world > 1 and mode == PUSH and hierarchical and world <= device_count() and
+            if (probe and world > 1 and mode == PUSH and hierarchical and world <= device_count() and
                     multicast_supported(cuda_device)):
                 for pi, (_sname, dname) in enumerate(bind):
                     p = self.plans[pi]
-                    if probe:
-                        every = any({self.host_of[d] for d in dsts} == set(self.host_of) and
-                                    any(self.host_of[d] != self.host_of[s_] for d in dsts)
-                                    for s_, dsts, _r in p.lowered())
-                        if every and dname not in multicast:
-                            multicast.append(dname)
-                    elif link_bottleneck(p, self.host_of, True) < 0.9 * link_bottleneck(p, self.host_of, False):
+                    every = any({self.host_of[d] for d in dsts} == set(self.host_of) and
+                                any(self.host_of[d] != self.host_of[s_] for d in dsts)
+                                for s_, dsts, _r in p.lowered())
+                    if every and dname not in multicast:
                         multicast.append(dname)
         self.multicast = list(multicast)
         if multicast and (world < 2 or mode != PUSH or not hierarchical):
@@ -859,7 +858,7 @@ class RankRealloc:
     def _decide(self, pi: int, sw: dict) -> Scheme:
         """The cost-model choice for phase pi under the switches."""
         p, dname = self.plans[pi], self.bind[pi][1]
-        if dname in self.multicast and self._remote(p):
+        if dname in self.multicast and self.mc_forced and self._remote(p):
             return Scheme(multicast=True)
         if not self._flag_ok() or not self._remote(p):
             return Scheme()
