@@ -230,24 +230,14 @@ std::vector<Job> build_jobs(const std::vector<LoweredOp>& ops, const HostMap& hm
         relay_next_slot += pieces;
       }
       if (hs == hm.me) {
-        // The first star host's push also stores our local destinations from
-        // the same read (its leader first: the signal goes to dsts.front()'s
-        // flag array), so the source is read once per star host, not once
-        // more for the local copies; single-destination remote hosts stay a
-        // plain job (copy-engine runs may carry them).
-        std::vector<DeviceId> local_dsts;
-        Job plain;
+        Job plain;  // local destinations and single-destination remote hosts
         plain.src = op.src;
         plain.op = &op;
         for (const auto& [h, list] : groups) {
           if (h == hm.me)
-            local_dsts.insert(local_dsts.end(), list.begin(), list.end());
+            plain.dsts.insert(plain.dsts.end(), list.begin(), list.end());
           else if (!base.count(h))
             plain.dsts.push_back(list.front());
-        }
-        if (static_cast<int>(local_dsts.size()) + 1 > kMaxFan) {  // too wide to ride along
-          plain.dsts.insert(plain.dsts.begin(), local_dsts.begin(), local_dsts.end());
-          local_dsts.clear();
         }
         if (!plain.dsts.empty()) jobs.push_back(std::move(plain));
         for (int h : stars) {
@@ -255,8 +245,6 @@ std::vector<Job> build_jobs(const std::vector<LoweredOp>& ops, const HostMap& hm
           j.src = op.src;
           j.op = &op;
           j.dsts = {groups.at(h).front()};
-          j.dsts.insert(j.dsts.end(), local_dsts.begin(), local_dsts.end());
-          local_dsts.clear();
           j.relay_signal = true;
           j.relay_base = base[h];
           jobs.push_back(std::move(j));
