@@ -46,6 +46,20 @@ uint32_t epoch = 0;
 
 enum Mode { kFlags, kFlagsNoMb, kNoWait, kEvents };
 
+// GPU 0's local work in the library's relay phase: the source copied to its
+// two local replicas by SMs (read once, two stores), concurrently with the
+// chain's first hop. ctas = 0: no local work.
+__global__ void local_fanout(const int4* __restrict__ src, int4* __restrict__ a, int4* __restrict__ b, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const int4 v = src[i];
+    a[i] = v;
+    b[i] = v;
+  }
+}
+int g_local_ctas = 0;
+char* g_rep[2] = {nullptr, nullptr};
+cudaStream_t g_local_stream = nullptr;
+
 double run(Mode mode, size_t total, size_t piece, int reps = 3) {
   const int P = static_cast<int>((total + piece - 1) / piece);
   std::vector<std::vector<cudaEvent_t>> arrived(G, std::vector<cudaEvent_t>(P));
@@ -66,6 +80,14 @@ double run(Mode mode, size_t total, size_t piece, int reps = 3) {
     for (int g = 1; g < G; ++g) {
       CK(cudaSetDevice(g));
       CK(cudaStreamWaitEvent(st[g], t0[0], 0));  // every stream starts with GPU 0's
+    }
+    if (g_local_ctas > 0) {
+      CK(cudaSetDevice(0));
+      CK(cudaStreamWaitEvent(g_local_stream, t0[0], 0));
+      local_fanout<<<g_local_ctas, 512, 0, g_local_stream>>>(reinterpret_cast<const int4*>(buf[0]),
+                                                              reinterpret_cast<int4*>(g_rep[0]),
+                                                              reinterpret_cast<int4*>(g_rep[1]), total / 16);
+      CK(cudaGetLastError());
     }
     // issue per GPU in piece order (the host issues GPU by GPU; the streams run concurrently)
     for (int g = 0; g + 1 < G; ++g) {
@@ -95,6 +117,13 @@ double run(Mode mode, size_t total, size_t piece, int reps = 3) {
     }
     CK(cudaSetDevice(0));
     for (int g = 1; g < G; ++g) CK(cudaStreamWaitEvent(st[0], t1[g], 0));
+    if (g_local_ctas > 0) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(cudaEventRecord(e, g_local_stream));
+      CK(cudaStreamWaitEvent(st[0], e, 0));
+      CK(cudaEventDestroy(e));
+    }
     CK(cudaEventRecord(t1[0], st[0]));
     CK(cudaEventSynchronize(t1[0]));
     float ms = 0;
@@ -137,6 +166,22 @@ int main(int argc, char** argv) {
   }
   std::printf("chain 0 -> ... -> %d, %zu GiB\n", G - 1, total >> 30);
   const char* names[] = {"flags", "flags/nomb", "nowait", "events"};
+  if (argc > 1) {  // with GPU 0's local fan-out (source -> two local replicas by SMs) at these CTA counts
+    CK(cudaSetDevice(0));
+    CK(cudaMalloc(&g_rep[0], total));
+    CK(cudaMalloc(&g_rep[1], total));
+    CK(cudaStreamCreateWithFlags(&g_local_stream, cudaStreamNonBlocking));
+    for (int a = 1; a < argc; ++a) {
+      g_local_ctas = std::atoi(argv[a]);
+      for (size_t piece_mib : {192, 256}) {
+        const double ms = run(kFlags, total, piece_mib << 20);
+        std::printf("flags + GPU0 local fan-out ctas=%4d  piece %4zu MiB  %8.3f ms  %7.1f GB/s per link\n", g_local_ctas,
+                    piece_mib, ms, total / (ms * 1e-3) / 1e9);
+        std::fflush(stdout);
+      }
+    }
+    return 0;
+  }
   for (size_t piece_mib : {64, 256, 1024}) {
     for (Mode m : {kFlags, kNoWait, kEvents}) {
       const double ms = run(m, total, piece_mib << 20);
