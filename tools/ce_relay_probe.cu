@@ -56,6 +56,28 @@ __global__ void local_fanout(const int4* __restrict__ src, int4* __restrict__ a,
     b[i] = v;
   }
 }
+// The forwarders' in-host fan-out: every CTA waits for piece p's flag, then
+// copies its share of the piece from the leader into the second replica.
+__global__ void hop_fanout(const uint32_t* flags, uint32_t epoch, const int4* __restrict__ leader,
+                           int4* __restrict__ rep, size_t piece16, size_t n16) {
+  const size_t P = (n16 + piece16 - 1) / piece16;
+  for (size_t p = 0; p < P; ++p) {
+    if (threadIdx.x == 0) {
+      uint32_t v;
+      do {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + p) : "memory");
+        if (v < epoch) __nanosleep(256);
+      } while (v < epoch);
+    }
+    __syncthreads();
+    const size_t lo = p * piece16, hi = lo + piece16 < n16 ? lo + piece16 : n16;
+    for (size_t i = lo + blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < hi; i += size_t(gridDim.x) * blockDim.x)
+      rep[i] = leader[i];
+  }
+}
+int g_hop_ctas = 0;
+std::vector<char*> g_hop_rep;
+std::vector<cudaStream_t> g_hop_stream;
 int g_local_ctas = 0;
 char* g_rep[2] = {nullptr, nullptr};
 cudaStream_t g_local_stream = nullptr;
@@ -89,6 +111,14 @@ double run(Mode mode, size_t total, size_t piece, int reps = 3) {
                                                               reinterpret_cast<int4*>(g_rep[1]), total / 16);
       CK(cudaGetLastError());
     }
+    if (g_hop_ctas > 0)
+      for (int g = 1; g < G; ++g) {
+        CK(cudaSetDevice(g));
+        CK(cudaStreamWaitEvent(g_hop_stream[g], t0[0], 0));
+        hop_fanout<<<g_hop_ctas, 512, 0, g_hop_stream[g]>>>(flags[g], epoch, reinterpret_cast<const int4*>(buf[g]),
+                                                            reinterpret_cast<int4*>(g_hop_rep[g]), piece / 16, total / 16);
+        CK(cudaGetLastError());
+      }
     // issue per GPU in piece order (the host issues GPU by GPU; the streams run concurrently)
     for (int g = 0; g + 1 < G; ++g) {
       CK(cudaSetDevice(g));
@@ -113,6 +143,10 @@ double run(Mode mode, size_t total, size_t piece, int reps = 3) {
     // the chain's time: GPU 0's start to the last forwarder's end, on GPU 0's clock
     for (int g = 1; g < G; ++g) {
       CK(cudaSetDevice(g));
+      if (g_hop_ctas > 0) {  // the hop's end includes its fan-out
+        CK(cudaEventRecord(t1[g], g_hop_stream[g]));
+        CK(cudaStreamWaitEvent(st[g], t1[g], 0));
+      }
       CK(cudaEventRecord(t1[g], st[g]));
     }
     CK(cudaSetDevice(0));
@@ -166,6 +200,25 @@ int main(int argc, char** argv) {
   }
   std::printf("chain 0 -> ... -> %d, %zu GiB\n", G - 1, total >> 30);
   const char* names[] = {"flags", "flags/nomb", "nowait", "events"};
+  if (argc > 2 && std::string(argv[1]) == "hop") {  // forwarders' fan-out kernels at these CTA counts
+    g_hop_rep.assign(G, nullptr);
+    g_hop_stream.assign(G, nullptr);
+    for (int g = 1; g < G; ++g) {
+      CK(cudaSetDevice(g));
+      CK(cudaMalloc(&g_hop_rep[g], total));
+      CK(cudaStreamCreateWithFlags(&g_hop_stream[g], cudaStreamNonBlocking));
+    }
+    for (int a = 2; a < argc; ++a) {
+      g_hop_ctas = std::atoi(argv[a]);
+      for (size_t piece_mib : {192, 256}) {
+        const double ms = run(kFlags, total, piece_mib << 20);
+        std::printf("flags + hop fan-out ctas=%4d  piece %4zu MiB  %8.3f ms  %7.1f GB/s per link\n", g_hop_ctas,
+                    piece_mib, ms, total / (ms * 1e-3) / 1e9);
+        std::fflush(stdout);
+      }
+    }
+    return 0;
+  }
   if (argc > 1) {  // with GPU 0's local fan-out (source -> two local replicas by SMs) at these CTA counts
     CK(cudaSetDevice(0));
     CK(cudaMalloc(&g_rep[0], total));
