@@ -122,15 +122,30 @@ def plain_workload(name: str):
               cluster=NS(n_nodes=1, gpus_per_node=e["devices"], intra_node_bw=900e9, inter_node_bw=50e9))
 
 
+L2_BYTES = 126 << 20  # B200 L2
+
+
 def workload_config(w) -> dict:
     """`config` of the JSON line: the workload only (identical in both arms);
     how each arm executes it goes under `executor`."""
     def s(p):
         st = p.strategy
         return f"(pp{st.pp},dp{st.dp},tp{st.tp})"
+    m = w.model
+    h, hd = m.hidden_size, m.hidden_size // m.num_attention_heads
+    params = (m.vocab_size * h * (2 if m.has_output_head else 1) + h +
+              m.num_layers * (2 * h * h + 2 * h * hd * m.num_kv_heads + 3 * h * m.intermediate_size + 2 * h))
+    nbytes = w.data_bytes * w.devices if w.data_bytes else params * m.param_bytes
+    if nbytes > 2 * L2_BYTES:
+        l2 = f"inputs larger than L2 ({nbytes / 1e9:.2f} GB of source shards per step); no flush needed"
+    elif nbytes > L2_BYTES:
+        l2 = f"{nbytes / 1e6:.1f} MB of source shards per step, under twice the 126 MB L2: partly L2-resident"
+    else:
+        l2 = (f"{nbytes / 1e6:.1f} MB of source shards: L2-resident across steps (a latency-bound parity "
+              f"case, not a bandwidth measurement)")
     return {"workload": w.name, "description": w.description, "plan_devices": w.devices,
             "phases": [f"{s(a)}->{s(b)}" for a, b in w.phases],
-            "l2": "inputs larger than L2 (multi-GB shards); no flush needed",
+            "l2": l2,
             "weights": "hash-initialised bf16 (seed 1); every destination shard checked after timing"}
 
 
